@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Throughput of the thread-safe LB hot path (BASELINE.json metric:
+"GLUPS and % of HBM roofline (D3Q19 1024^3) at 1/2/4/8 B200 vs CPU ref").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (N = 1): D3Q19 single-phase periodic Taylor-Green vortex, 1024^3
+nodes, fp32 storage, fp64 node arithmetic (the reference's float build, bit
+for bit), fused F1 step = moments kernel + stream-collide kernel.
+N > 1 (torchrun, one rank per GPU): weak scaling, one 1024^3 z slab per GPU
+of a 1024 x 1024 x (1024 N) periodic box, NCCL halo exchange overlapped with
+the interior stream-collide.
+Inputs (125 GB of state per GPU) are far larger than the 126 MB L2, so no L2
+flush is needed between steps.
+
+--impl reference times the reference's own CPU implementation
+(oracle/_ref/libtslb_ref.so = the unmodified tslb headers, WorkerPool over
+all host cores; the plain-C oracle port if that build is absent) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+METRIC = "GLUPS and % of HBM roofline (D3Q19 1024^3) at 1/2/4/8 B200 vs CPU ref"
+
+
+def peaks():
+    try:
+        with open(PEAKS) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured", p
+    except Exception:
+        return 6650.0, "fallback", {}
+
+
+def census(lat, elem_bytes):
+    from paper_2304_06437_b200 import tslb as T
+    return T.count_kernel_cost(lat, elem_bytes)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(2)
+        except Exception:
+            self.proc.kill()
+        self.t.join(1)
+        sm = [float(r[1]) for r in self.rows if len(r) > 8 and r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if len(r) > 8 and r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            if len(r) > 8:
+                for nm, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline
+# ---------------------------------------------------------------------------
+def tgv_state(dims, nz_global, z0, dtype):
+    from paper_2304_06437_b200 import tslb as T
+    nx, ny, nz = dims
+    g = T.GridDims(nx, ny, nz)
+    s = T.allocate_fields(g, T.D3Q19, dtype)
+    U = 0.03
+
+    def st(i, j, k):
+        X = 2 * np.pi * (i + 0.5) / nx
+        Y = 2 * np.pi * (j + 0.5) / ny
+        Z = 2 * np.pi * (k + z0 + 0.5) / nz_global
+        z = np.zeros(i.shape)
+        rho = 1 + 3 * (U * U / 16) * (np.cos(2 * X) + np.cos(2 * Y)) * (np.cos(2 * Z) + 2)
+        return (rho, U * np.sin(X) * np.cos(Y) * np.cos(Z), -U * np.cos(X) * np.sin(Y) * np.cos(Z), z, z, z, z, z, z, z)
+
+    T.initialize_regularized(s, None, st, T.D3Q19)
+    return s.f
+
+
+def cpu_reference(steps, warmup, sample_nz=16, workers=None):
+    """Time the reference CPU path on a 1024 x 1024 x sample_nz periodic slab
+    of the Taylor-Green workload (fp32 storage). Returns (GLUPS, info)."""
+    import ctypes as C
+
+    from oracle import oracle as O
+    workers = workers or os.cpu_count() or 1
+    dims = (1024, 1024, sample_nz)
+    f = tgv_state(dims, 1024, 0, np.float32)
+    kinds, uw = O.faces_arrays(O.periodic())
+    if os.path.exists(O.REF_SO):
+        o = O.Oracle("ref")
+        secs = C.c_double()
+        rc = o.lib.tslbref_time_steps(1, 1, *dims, 1.6, O._ptr(kinds), O._ptr(uw), O._ptr(f), int(steps),
+                                      int(warmup), int(workers), C.byref(secs))
+        o._check(rc)
+        kind, cores, t = "reference", workers, secs.value
+    else:
+        o = O.Oracle("port")
+        o.single_run("d3q19", dims, 1.6, O.periodic(), f, None, warmup, 0)
+        t0 = time.perf_counter()
+        o.single_run("d3q19", dims, 1.6, O.periodic(), f, None, steps, 0)
+        kind, cores, t = "port", 1, time.perf_counter() - t0
+    glups = dims[0] * dims[1] * dims[2] * steps / t / 1e9
+    sample = (f"D3Q19 periodic Taylor-Green slab {dims[0]}x{dims[1]}x{dims[2]} fp32 (fp64 node math), {steps} steps "
+              f"after {warmup} warm-up, WorkerPool({cores})")
+    return glups, dict(kind=kind, cores=cores, sample=sample, seconds=t)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=1024, help="edge of the per-GPU cube")
+    ap.add_argument("--lattice", default="d3q19")
+    ap.add_argument("--math", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--sample-nz", type=int, default=16)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    n = args.n
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        steps, warm = args.steps, max(1, min(args.warmup, 2))
+        glups, info = cpu_reference(steps, warm, args.sample_nz)
+        out = {"metric": METRIC, "value": round(glups, 6), "unit": "GLUPS", "n_gpus": args.gpus, "steps": steps,
+               "warmup": warm, "ms_per_step": round(info["seconds"] / steps * 1e3, 3), "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "impl": "reference",
+               "config": {"workload": f"D3Q19 periodic Taylor-Green, sample of the {n}^3 fp32 workload",
+                          "lattice": "d3q19", "storage": "f32", "sample": info["sample"]},
+               "cpu_baseline": {"value": round(glups, 6), "unit": "GLUPS", "cores": info["cores"],
+                                "kind": info["kind"], "sample": info["sample"]},
+               "e2e": {"value": round(glups, 6), "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(out))
+        return
+
+    import torch
+
+    from paper_2304_06437_b200 import _lib
+    from paper_2304_06437_b200 import tslb as T
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev_id = local if world > 1 else 0
+    torch.cuda.set_device(dev_id)
+
+    lat = T.lattice_of(args.lattice)
+    dtype = np.float32
+    nz_g = n * world
+    g = T.GridDims(n, n, nz_g)
+    spec = T.BoundarySpec.all_periodic()
+    omega = 1.6
+    slab = (rank * n, n) if world > 1 else None
+    sim = T.DeviceSolver(lat, g, omega, spec, dtype, 1, None, None, dev_id, slab=slab)
+    if args.math == "f32":
+        sim.set_math(_lib.MATH_F32)
+    if world > 1:
+        import ctypes as C
+        uid = (C.c_char * 128)()
+        if rank == 0:
+            _lib.check(_lib.load().tslb_cuda_nccl_unique_id(uid))
+        obj = [bytes(uid)]
+        dist.broadcast_object_list(obj, src=0)
+        buf = (C.c_char * 128).from_buffer_copy(obj[0])
+        _lib.check(_lib.load().tslb_cuda_attach_nccl(sim.h, buf, world, rank))
+    sim.init_analytic("taylor_green" if lat.dim == 3 else "shear", 0.03)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (untimed)
+    sim.step(args.warmup)
+    barrier()
+    launches0 = sim.launch_count()
+    clocks = Clocks() if rank == 0 else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    sim.profile(True)
+    barrier()
+    ms = sim.time_steps(args.steps)
+    barrier()
+    prof = sim.profile_read()
+    sim.profile(False)
+    launches = sim.launch_count() - launches0
+    clk = clocks.stop() if clocks else None
+    if dist:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    nodes = g.n()
+    glups = nodes * args.steps / (ms / 1e3) / 1e9
+
+    # roofline of the dominant kernel: algorithmic bytes per launch / mean
+    # launch duration (CUDA events on the solver stream, timed region)
+    es = 4
+    q, D = lat.q, lat.dim
+    nm = 1 + D + D * (D + 1) // 2
+    per_node = {"moments": (q + nm) * es, "streamcoll": (nm + q) * es}
+    dom = max(per_node, key=lambda k: prof.get(k, (0, 0))[0])
+    k_ms, k_n = prof[dom]
+    local_nodes = n * n * (n if world > 1 else nz_g)
+    achieved = per_node[dom] * local_nodes / (k_ms / k_n / 1e3) / 1e9
+    hbm, peak_kind, _ = peaks()
+    cost = census(lat, es)
+    step_bw = glups * cost.bytes / world  # per-GPU GB/s of the whole step
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+            "frac": round(achieved / hbm, 4), "traffic": None, "kernel": f"k_{dom}",
+            "peak_kind": peak_kind,
+            "per_kernel_ms": {k: round(v[0] / v[1], 4) for k, v in prof.items()},
+            "step_bytes_per_lu": cost.bytes, "step_frac": round(step_bw / hbm, 4),
+            "step_frac_of_8TBs": round(step_bw / 8000.0, 4)}
+
+    # end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e and world == 1:
+        e2e = run_e2e(sim, lat, n, args.steps, dtype)
+
+    cpu = None
+    if rank == 0 and not args.no_cpu and world == 1:
+        try:
+            cg, info = cpu_reference(max(2, min(args.steps, 5)), 1, args.sample_nz)
+            cpu = {"value": round(cg, 6), "unit": "GLUPS", "cores": info["cores"], "kind": info["kind"],
+                   "sample": info["sample"]}
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "unit": "GLUPS", "cores": 0, "kind": "unavailable", "sample": str(e)[:200]}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(glups, 4), "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
+               "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.math == "f64" else "f32",
+               "data": "synthetic",
+               "config": {"workload": f"D3Q19 periodic Taylor-Green {n}^3 per GPU"
+                          + (f" (global {n}x{n}x{nz_g}, z slabs)" if world > 1 else ""),
+                          "lattice": lat.name, "nodes": nodes, "storage": "f32",
+                          "node_math": args.math, "schedule": "F1 (moments + fused stream-collide)",
+                          "l2": "state 125 GB/GPU >> 126 MB L2, no flush needed",
+                          "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
+               "roofline": roof, "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
+        print(json.dumps(out))
+    sim.close()
+    if dist:
+        dist.destroy_process_group()
+
+
+def run_e2e(sim, lat, n, steps, dtype):
+    """The reference driver loop (tslb_main.cpp run_single) through the public
+    C-ABI with HOST buffers: upload f from pinned host memory, `steps` steps
+    each followed by a totals() sample read back to the host, then download
+    rho and u (the output frame). Host wall time around all of it."""
+    import torch
+    q = lat.q
+    nn = n * n * n
+    esz = np.dtype(dtype).itemsize
+    try:
+        host_f = torch.empty((q, nn), dtype=torch.float32, pin_memory=True)
+        out = torch.empty((1 + lat.dim, nn), dtype=torch.float32, pin_memory=True)
+    except Exception as e:
+        return {"value": None, "unit": "GLUPS", "error": f"pinned host alloc failed: {e}"[:200]}
+    import ctypes as C
+    from paper_2304_06437_b200 import _lib
+    lib = _lib.load()
+    # untimed: the host holds the initial state
+    _lib.check(lib.tslb_cuda_download_f(sim.h, 0, C.c_void_p(host_f.data_ptr())))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    _lib.check(lib.tslb_cuda_upload_f(sim.h, 0, C.c_void_p(host_f.data_ptr())))
+    mass = C.c_double()
+    mom = (C.c_double * 3)()
+    for _ in range(steps):
+        _lib.check(lib.tslb_cuda_step(sim.h, 1))
+        _lib.check(lib.tslb_cuda_totals(sim.h, C.byref(mass), mom))
+    _lib.check(lib.tslb_cuda_refresh_moments(sim.h))
+    _lib.check(lib.tslb_cuda_download_field(sim.h, 0, C.c_void_p(out.data_ptr())))
+    _lib.check(lib.tslb_cuda_download_field(sim.h, 1, C.c_void_p(out[1:].data_ptr())))
+    t = time.perf_counter() - t0
+    h2d = q * nn * esz
+    d2h = (1 + lat.dim) * nn * esz + steps * 32
+    return {"value": round(nn * steps / t / 1e9, 4), "unit": "GLUPS", "h2d_bytes_per_step": int(h2d / steps),
+            "d2h_bytes_per_step": int(d2h / steps), "seconds": round(t, 3),
+            "loop": "upload f (pinned) -> steps x (step + totals readback) -> download rho,u"}
+
+
+if __name__ == "__main__":
+    main()

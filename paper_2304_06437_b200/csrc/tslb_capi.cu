@@ -1,0 +1,1122 @@
+// C-ABI (include/tslb_cuda.h) over the sm_100a kernels: solver objects,
+// device memory, time stepping, slab halo exchange, diagnostics, profiling.
+//
+// The reference's Sim classes (solver.hpp:70-202) own host Eigen arrays and a
+// WorkerPool; here a handle owns device SoA buffers and one CUDA stream. The
+// stream order is the phase barrier. Host<->device copies happen only in the
+// explicit upload/download calls; the drop-in C++ headers (include/tslb/)
+// and the Python mirror keep the reference's host-visible semantics on top.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/tslb_cuda.h"
+#include "tslb_kernels.h"
+#include "tslb_lattice.cuh"
+
+using namespace tslb_cuda;
+
+namespace {
+
+thread_local std::string g_err;
+
+int set_err(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  std::vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                              \
+  do {                                                                        \
+    cudaError_t e_ = (call);                                                  \
+    if (e_ != cudaSuccess)                                                    \
+      return set_err(TSLB_ECUDA, "%s: %s (%s:%d)", #call,                     \
+                     cudaGetErrorString(e_), __FILE__, __LINE__);             \
+  } while (0)
+
+// ---- NCCL, loaded at run time (torch's copy if already mapped) -------------
+struct NcclApi {
+  bool ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  const char* (*ErrStr)(ncclResult_t) = nullptr;
+};
+
+NcclApi& nccl() {
+  static NcclApi api;
+  static bool tried = false;
+  if (tried) return api;
+  tried = true;
+  void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return api;
+  auto sym = [&](const char* s) { return dlsym(h, s); };
+  api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+  api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+  api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+  api.Send = (decltype(api.Send))sym("ncclSend");
+  api.Recv = (decltype(api.Recv))sym("ncclRecv");
+  api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+  api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+  api.ErrStr = (decltype(api.ErrStr))sym("ncclGetErrorString");
+  api.ok = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv &&
+           api.GroupStart && api.GroupEnd;
+  return api;
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+template <class F>
+void lattice_of(int lat, F&& f) {
+  if (lat == kD2Q9) f(D2Q9{});
+  else if (lat == kD3Q19) f(D3Q19{});
+  else f(D3Q27{});
+}
+
+}  // namespace
+
+struct tslb_cuda_sim {
+  // configuration
+  int lat = 0, scalar = 0, comps = 1, q = 0, dim = 0, np = 0, esz = 8;
+  int nx = 0, ny = 0, nzl = 0, z0 = 0, nzg = 0;
+  bool decomposed = false;
+  int device = 0;
+  int math = kMathDouble;
+  double omega = 1.0;
+  int kinds[6] = {0, 0, 0, 0, 0, 0};
+  ColorParamsDev cp{};
+  Dom d{};
+  // device memory
+  void* f[2] = {nullptr, nullptr};
+  void* mo = nullptr;     // rho, mom[D], pineq[np]
+  void* two = nullptr;    // rho_r, rho_b, phi, grad[D]
+  uint8_t* flag = nullptr;
+  uint8_t* solid = nullptr;
+  uint32_t* slow = nullptr;
+  void* scratch = nullptr;
+  double* red = nullptr;  // partials + outputs
+  uint64_t* dig = nullptr;
+  size_t dig_bytes = 0;
+  uint64_t bytes = 0;
+  uint64_t n_fluid = 0;
+  cudaStream_t s = nullptr, cs = nullptr;
+  cudaEvent_t ev_b = nullptr, ev_c = nullptr, t0 = nullptr, t1 = nullptr;
+  bool stress_pending = false;
+  long steps = 0;
+  // profiling
+  bool prof = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> rec;
+  size_t pool_used = 0;
+  int64_t launches = 0;
+  // exchange
+  int xmode = 0;  // 0 none, 1 nccl, 2 local
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1, up = -1, down = -1;
+  tslb_cuda_sim* up_peer = nullptr;
+  tslb_cuda_sim* down_peer = nullptr;
+  void* recv_lo = nullptr;  // staging (masked geometries)
+  void* recv_hi = nullptr;
+  int zp[9], zm[9], nzp = 0, nzm = 0;  // directions with c_z = +1 / -1
+  int zpx[9], zpy[9], zmx[9], zmy[9];
+
+  int64_t n() const { return int64_t(nx) * ny * nzl; }
+  int64_t plane() const { return int64_t(nx) * ny; }
+  void* fa(int sp, int a) const {
+    return static_cast<char*>(f[sp]) + size_t(a) * d.fstride * esz;
+  }
+  void* m_arr(int c) const {
+    return static_cast<char*>(mo) + size_t(c) * d.mstride * esz;
+  }
+  void* t_arr(int c) const {
+    return static_cast<char*>(two) + size_t(c) * d.mstride * esz;
+  }
+  TwoFields tf() const {
+    TwoFields t;
+    t.rho = m_arr(0);
+    t.mom = m_arr(1);
+    t.pin = m_arr(1 + dim);
+    t.rho_r = t_arr(0);
+    t.rho_b = t_arr(1);
+    t.phi = t_arr(2);
+    t.grad = t_arr(3);
+    t.flag = flag;
+    return t;
+  }
+  Dom range(int k0, int k1) const {
+    Dom r = d;
+    r.k0 = k0;
+    r.nzr = k1 - k0;
+    return r;
+  }
+};
+
+namespace {
+
+int alloc(tslb_cuda_sim* h, void** p, size_t bytes) {
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e != cudaSuccess)
+    return set_err(TSLB_ENOMEM, "cudaMalloc(%zu bytes): %s (device holds %llu already)",
+                   bytes, cudaGetErrorString(e), (unsigned long long)h->bytes);
+  h->bytes += bytes;
+  return 0;
+}
+
+// -- profiling helpers --------------------------------------------------------
+cudaEvent_t pool_event(tslb_cuda_sim* h) {
+  if (h->pool_used == h->pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    h->pool.push_back(e);
+  }
+  return h->pool[h->pool_used++];
+}
+
+struct Prof {
+  tslb_cuda_sim* h;
+  int cls;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr;
+  Prof(tslb_cuda_sim* h_, int c, cudaStream_t s_) : h(h_), cls(c), st(s_) {
+    if (h->prof) {
+      e0 = pool_event(h);
+      cudaEventRecord(e0, st);
+    }
+  }
+  ~Prof() {
+    if (h->prof) {
+      cudaEvent_t e1 = pool_event(h);
+      cudaEventRecord(e1, st);
+      h->rec.push_back({cls, {e0, e1}});
+    }
+  }
+};
+
+template <class F>
+int by_scalar(const tslb_cuda_sim* h, F&& f) {
+  if (h->scalar == TSLB_F64) return f(double(0));
+  return f(float(0));
+}
+
+// -- phases -------------------------------------------------------------------
+int ph_moments(tslb_cuda_sim* h, cudaStream_t st) {
+  Prof p(h, TSLB_K_MOMENTS, st);
+  ++h->launches;
+  return by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_moments<T>(h->lat, h->math, h->range(0, h->nzl),
+                             static_cast<const T*>(h->f[0]), static_cast<T*>(h->mo),
+                             h->solid, st);
+  });
+}
+
+int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
+  if (k1 <= k0) return 0;
+  Prof p(h, TSLB_K_STREAMCOLL, st);
+  ++h->launches;
+  return by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_streamcoll<T>(h->lat, h->math, h->range(k0, k1),
+                                static_cast<T*>(h->f[0]), static_cast<const T*>(h->mo),
+                                h->solid, h->slow, h->omega, st);
+  });
+}
+
+int ph_cg_moments(tslb_cuda_sim* h, cudaStream_t st) {
+  Prof p(h, TSLB_K_CG_MOMENTS, st);
+  ++h->launches;
+  h->stress_pending = false;
+  return by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_cg_moments<T>(h->lat, h->range(0, h->nzl),
+                                static_cast<const T*>(h->f[0]),
+                                static_cast<const T*>(h->f[1]), h->tf(), h->solid, st);
+  });
+}
+
+int ph_cg_gradient(tslb_cuda_sim* h, cudaStream_t st) {
+  Prof p(h, TSLB_K_CG_GRADIENT, st);
+  ++h->launches;
+  return by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_cg_gradient<T>(h->lat, h->range(0, h->nzl), h->tf(), h->solid,
+                                 h->slow, h->cp, st);
+  });
+}
+
+int ph_cg_prepare(tslb_cuda_sim* h, cudaStream_t st) {
+  ++h->launches;
+  h->stress_pending = false;
+  return by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_cg_prepare_stress<T>(h->lat, h->range(0, h->nzl), h->tf(),
+                                       h->solid, h->omega, h->cp, st);
+  });
+}
+
+int ph_cg_streamcoll(tslb_cuda_sim* h, int fold, cudaStream_t st) {
+  Prof p(h, TSLB_K_CG_STREAMCOLL, st);
+  ++h->launches;
+  return by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_cg_streamcoll<T>(h->lat, h->range(0, h->nzl),
+                                   static_cast<T*>(h->f[0]), static_cast<T*>(h->f[1]),
+                                   h->tf(), h->solid, h->slow, h->omega, h->cp, fold, st);
+  });
+}
+
+// -- slab exchange ------------------------------------------------------------
+// plane k (-1 .. nzl) of population array a, species 0
+void* plane_ptr(const tslb_cuda_sim* h, int a, int k) {
+  return static_cast<char*>(h->fa(0, a)) +
+         size_t((int64_t(k) + h->d.ghost) * h->plane()) * h->esz;
+}
+
+// destination for a received plane: in place, or the staging buffer
+void* recv_ptr(const tslb_cuda_sim* h, bool from_below, int e, int a) {
+  if (h->d.has_solid) {
+    void* base = from_below ? h->recv_lo : h->recv_hi;
+    return static_cast<char*>(base) + size_t(e) * h->plane() * h->esz;
+  }
+  return plane_ptr(h, a, from_below ? 0 : h->nzl - 1);
+}
+
+int unpack(tslb_cuda_sim* h, cudaStream_t st) {
+  if (!h->d.has_solid) return 0;
+  return by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    if (h->d.mode[ZMin] == kGhost) {
+      ++h->launches;
+      launch_unpack<T>(h->d, static_cast<T*>(h->f[0]), static_cast<const T*>(h->recv_lo),
+                       h->solid, h->nzp, h->zp, h->zpx, h->zpy, 0, -1, st);
+    }
+    if (h->d.mode[ZMax] == kGhost) {
+      ++h->launches;
+      launch_unpack<T>(h->d, static_cast<T*>(h->f[0]), static_cast<const T*>(h->recv_hi),
+                       h->solid, h->nzm, h->zm, h->zmx, h->zmy, h->nzl - 1, h->nzl, st);
+    }
+    return 0;
+  });
+}
+
+int exchange_nccl(tslb_cuda_sim* h, cudaStream_t st) {
+  NcclApi& N = nccl();
+  const ncclDataType_t ty = h->scalar == TSLB_F64 ? ncclFloat64 : ncclFloat32;
+  const size_t cnt = size_t(h->plane());
+  Prof p(h, TSLB_K_EXCHANGE, st);
+  N.GroupStart();
+  if (h->up >= 0)
+    for (int e = 0; e < h->nzp; ++e) N.Send(plane_ptr(h, h->zp[e], h->nzl), cnt, ty, h->up, h->comm, st);
+  if (h->down >= 0)
+    for (int e = 0; e < h->nzp; ++e) N.Recv(recv_ptr(h, true, e, h->zp[e]), cnt, ty, h->down, h->comm, st);
+  if (h->down >= 0)
+    for (int e = 0; e < h->nzm; ++e) N.Send(plane_ptr(h, h->zm[e], -1), cnt, ty, h->down, h->comm, st);
+  if (h->up >= 0)
+    for (int e = 0; e < h->nzm; ++e) N.Recv(recv_ptr(h, false, e, h->zm[e]), cnt, ty, h->up, h->comm, st);
+  ncclResult_t r = N.GroupEnd();
+  if (r != ncclSuccess)
+    return set_err(TSLB_ECUDA, "NCCL halo exchange: %s", N.ErrStr ? N.ErrStr(r) : "error");
+  return 0;
+}
+
+// local transport: this slab's ghost planes -> neighbours' boundary planes
+int exchange_local(tslb_cuda_sim* h, cudaStream_t st) {
+  const size_t bytes = size_t(h->plane()) * h->esz;
+  Prof p(h, TSLB_K_EXCHANGE, st);
+  if (h->up_peer)
+    for (int e = 0; e < h->nzp; ++e)
+      CK(cudaMemcpyAsync(recv_ptr(h->up_peer, true, e, h->zp[e]),
+                         plane_ptr(h, h->zp[e], h->nzl), bytes,
+                         cudaMemcpyDeviceToDevice, st));
+  if (h->down_peer)
+    for (int e = 0; e < h->nzm; ++e)
+      CK(cudaMemcpyAsync(recv_ptr(h->down_peer, false, e, h->zm[e]),
+                         plane_ptr(h, h->zm[e], -1), bytes,
+                         cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+// One fused step (fused_step / two_fluid_step) enqueued on h->s.
+int enqueue_step(tslb_cuda_sim* h) {
+  int rc;
+  if (h->comps == 2) {
+    if ((rc = ph_cg_moments(h, h->s))) return rc;
+    if ((rc = ph_cg_gradient(h, h->s))) return rc;
+    if ((rc = ph_cg_streamcoll(h, 1, h->s))) return rc;
+    h->stress_pending = true;
+    ++h->steps;
+    return 0;
+  }
+  if ((rc = ph_moments(h, h->s))) return rc;
+  if (h->xmode != 1) {
+    if ((rc = ph_streamcoll(h, 0, h->nzl, h->s))) return rc;
+  } else {
+    // boundary planes first, halo exchange on the comm stream overlapped
+    // with the interior planes, then join before the next moments pass
+    if ((rc = ph_streamcoll(h, 0, 1, h->s))) return rc;
+    if (h->nzl > 1 && (rc = ph_streamcoll(h, h->nzl - 1, h->nzl, h->s))) return rc;
+    CK(cudaEventRecord(h->ev_b, h->s));
+    CK(cudaStreamWaitEvent(h->cs, h->ev_b, 0));
+    if ((rc = exchange_nccl(h, h->cs))) return rc;
+    CK(cudaEventRecord(h->ev_c, h->cs));
+    if ((rc = ph_streamcoll(h, 1, h->nzl - 1, h->s))) return rc;
+    CK(cudaStreamWaitEvent(h->s, h->ev_c, 0));
+    if ((rc = unpack(h, h->s))) return rc;
+  }
+  ++h->steps;
+  return 0;
+}
+
+int check_axes(const int* kinds) {
+  for (int ax = 0; ax < 3; ++ax) {
+    const bool lo = kinds[2 * ax] == TSLB_FACE_PERIODIC;
+    const bool hi = kinds[2 * ax + 1] == TSLB_FACE_PERIODIC;
+    if (lo != hi)
+      return set_err(TSLB_EINVAL,
+                     "classify_nodes: axis %d mixes a periodic face with a wall", ax);
+  }
+  return 0;
+}
+
+int run_classify(tslb_cuda_sim* h, uint32_t* slow_dst) {
+  unsigned long long* cnt;
+  CK(cudaMallocAsync(&cnt, sizeof(unsigned long long), h->s));
+  CK(cudaMemsetAsync(cnt, 0, sizeof(unsigned long long), h->s));
+  ++h->launches;
+  if (launch_classify(h->lat, h->range(0, h->nzl), h->solid, slow_dst, cnt, h->s))
+    return set_err(TSLB_EINVAL, "classify: bad lattice");
+  unsigned long long v = 0;
+  CK(cudaMemcpyAsync(&v, cnt, sizeof v, cudaMemcpyDeviceToHost, h->s));
+  CK(cudaFreeAsync(cnt, h->s));
+  CK(cudaStreamSynchronize(h->s));
+  h->n_fluid = v;
+  return 0;
+}
+
+int create_impl(int lattice, int scalar, int components, int nx, int ny,
+                int nz, int z0, int nzl, double omega, const int* kinds,
+                const double* uw, const uint8_t* solid, const double* color,
+                const int* color_i, int device, tslb_cuda_handle* out) {
+  if (!out) return set_err(TSLB_EINVAL, "null output handle");
+  *out = nullptr;
+  if (lattice < 0 || lattice > 2) return set_err(TSLB_EINVAL, "unknown lattice %d", lattice);
+  if (scalar != TSLB_F64 && scalar != TSLB_F32) return set_err(TSLB_EINVAL, "unknown scalar %d", scalar);
+  if (components != 1 && components != 2)
+    return set_err(TSLB_EINVAL, "components must be 1 or 2");
+  if (nx <= 0 || ny <= 0 || nz <= 0 || nzl <= 0 || z0 < 0 || z0 + nzl > nz)
+    return set_err(TSLB_EINVAL, "allocate_fields: bad dims");
+  if (lattice == kD2Q9 && nz != 1) return set_err(TSLB_EINVAL, "allocate_fields: d2q9 needs nz = 1");
+  if (!kinds || !uw) return set_err(TSLB_EINVAL, "face arrays are required");
+  if (int rc = check_axes(kinds)) return rc;
+  const bool decomposed = nzl != nz;
+  if (decomposed && components == 2)
+    return set_err(TSLB_EINVAL, "two-fluid slab decomposition is not supported");
+  CK(cudaSetDevice(device));
+
+  auto* h = new tslb_cuda_sim();
+  h->lat = lattice;
+  h->scalar = scalar;
+  h->comps = components;
+  h->esz = scalar == TSLB_F64 ? 8 : 4;
+  lattice_of(lattice, [&](auto L) {
+    using Lat = decltype(L);
+    h->q = Lat::q;
+    h->dim = Lat::dim;
+    for (int a = 0; a < Lat::q; ++a) {
+      if (Lat::c[a][2] == 1) {
+        h->zpx[h->nzp] = Lat::c[a][0];
+        h->zpy[h->nzp] = Lat::c[a][1];
+        h->zp[h->nzp++] = a;
+      }
+      if (Lat::c[a][2] == -1) {
+        h->zmx[h->nzm] = Lat::c[a][0];
+        h->zmy[h->nzm] = Lat::c[a][1];
+        h->zm[h->nzm++] = a;
+      }
+    }
+  });
+  h->np = h->dim * (h->dim + 1) / 2;
+  h->nx = nx;
+  h->ny = ny;
+  h->nzl = nzl;
+  h->z0 = z0;
+  h->nzg = nz;
+  h->decomposed = decomposed;
+  h->device = device;
+  h->omega = omega;
+  std::memcpy(h->kinds, kinds, sizeof h->kinds);
+  if (color) {
+    h->cp.sigma = color[0];
+    h->cp.beta = color[1];
+    h->cp.nci_strength = color[2];
+    h->cp.eps_bulk = color[3];
+    h->cp.grad_threshold = color[4];
+  } else {
+    h->cp.sigma = 0.01;
+    h->cp.beta = 0.7;
+    h->cp.nci_strength = 0;
+    h->cp.eps_bulk = 0.02;
+    h->cp.grad_threshold = 1e-6;
+  }
+  h->cp.nci_reach = color_i ? color_i[0] : 3;
+  h->cp.linear = color_i ? color_i[1] : 0;
+
+  Dom& d = h->d;
+  d.nx = nx;
+  d.ny = ny;
+  d.nz = nzl;
+  d.ghost = decomposed ? 1 : 0;
+  d.plane = h->plane();
+  d.n = h->n();
+  d.fstride = round_up(d.plane * (nzl + 2 * d.ghost), 64);
+  d.mstride = round_up(d.n, 64);
+  for (int fc = 0; fc < 6; ++fc) {
+    d.mode[fc] = kinds[fc] == TSLB_FACE_PERIODIC ? kWrap : kWall;
+    for (int c = 0; c < 3; ++c)
+      d.uw[fc][c] = scalar == TSLB_F32 ? double(float(uw[3 * fc + c])) : uw[3 * fc + c];
+  }
+  if (decomposed) {
+    if (!(z0 == 0 && kinds[ZMin] != TSLB_FACE_PERIODIC)) d.mode[ZMin] = kGhost;
+    if (!(z0 + nzl == nz && kinds[ZMax] != TSLB_FACE_PERIODIC)) d.mode[ZMax] = kGhost;
+  }
+  d.has_solid = 0;
+  if (solid)
+    for (int64_t t = 0, N = int64_t(nx) * ny * nz; t < N; ++t)
+      if (solid[t]) {
+        d.has_solid = 1;
+        break;
+      }
+  d.xblocks = (nx + 127) / 128;
+  d.k0 = 0;
+  d.nzr = nzl;
+
+  int rc = 0;
+  auto fail = [&](int r) {
+    tslb_cuda_destroy(h);
+    return r;
+  };
+  CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&h->ev_c, cudaEventDisableTiming));
+  CK(cudaEventCreate(&h->t0));
+  CK(cudaEventCreate(&h->t1));
+
+  const size_t fbytes = size_t(d.fstride) * h->q * h->esz;
+  for (int sp = 0; sp < components; ++sp) {
+    if ((rc = alloc(h, &h->f[sp], fbytes))) return fail(rc);
+    CK(cudaMemsetAsync(h->f[sp], 0, fbytes, h->s));
+  }
+  const size_t mbytes = size_t(d.mstride) * (1 + h->dim + h->np) * h->esz;
+  if ((rc = alloc(h, &h->mo, mbytes))) return fail(rc);
+  CK(cudaMemsetAsync(h->mo, 0, mbytes, h->s));
+  if (components == 2) {
+    const size_t tb = size_t(d.mstride) * (3 + h->dim) * h->esz;
+    if ((rc = alloc(h, &h->two, tb))) return fail(rc);
+    CK(cudaMemsetAsync(h->two, 0, tb, h->s));
+    if ((rc = alloc(h, reinterpret_cast<void**>(&h->flag), size_t(d.mstride)))) return fail(rc);
+    CK(cudaMemsetAsync(h->flag, 0, size_t(d.mstride), h->s));
+  }
+  // solid mask with ghost planes (always present: 1 B/node)
+  const size_t sbytes = size_t(d.fstride);
+  if ((rc = alloc(h, reinterpret_cast<void**>(&h->solid), sbytes))) return fail(rc);
+  CK(cudaMemsetAsync(h->solid, 0, sbytes, h->s));
+  if (d.has_solid) {
+    // owned planes + ghost planes (z wraps for periodic global boundaries)
+    std::vector<uint8_t> hs(size_t(d.plane) * (nzl + 2 * d.ghost), 0);
+    for (int k = -d.ghost; k < nzl + d.ghost; ++k) {
+      int kg = z0 + k;
+      if (kg < 0 || kg >= nz) {
+        if (kinds[ZMin] != TSLB_FACE_PERIODIC) continue;
+        kg = (kg + nz) % nz;
+      }
+      std::memcpy(hs.data() + size_t(k + d.ghost) * d.plane,
+                  solid + size_t(kg) * d.plane, size_t(d.plane));
+    }
+    CK(cudaMemcpyAsync(h->solid, hs.data(), hs.size(), cudaMemcpyHostToDevice, h->s));
+    CK(cudaStreamSynchronize(h->s));
+  }
+  if (d.has_solid || components == 2) {
+    if ((rc = alloc(h, reinterpret_cast<void**>(&h->slow), size_t(d.mstride) * 4))) return fail(rc);
+    if ((rc = run_classify(h, h->slow))) return fail(rc);
+  } else {
+    // box geometry: every non-solid node is fluid
+    h->n_fluid = uint64_t(d.n);
+  }
+  if (decomposed && d.has_solid) {
+    const size_t pb = size_t(d.plane) * 9 * h->esz;
+    if ((rc = alloc(h, &h->recv_lo, pb))) return fail(rc);
+    if ((rc = alloc(h, &h->recv_hi, pb))) return fail(rc);
+  }
+  if ((rc = alloc(h, reinterpret_cast<void**>(&h->red),
+                  (reduce_partial_count() + 16) * sizeof(double))))
+    return fail(rc);
+  CK(cudaStreamSynchronize(h->s));
+  *out = h;
+  return 0;
+}
+
+int sync(tslb_cuda_sim* h) {
+  CK(cudaStreamSynchronize(h->s));
+  CK(cudaGetLastError());
+  return 0;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int tslb_cuda_abi_version(void) { return TSLB_CUDA_ABI_VERSION; }
+const char* tslb_cuda_last_error(void) { return g_err.c_str(); }
+
+int tslb_cuda_device_count(int* count) {
+  CK(cudaGetDeviceCount(count));
+  return 0;
+}
+
+int tslb_cuda_create(int lattice, int scalar, int components, int nx, int ny,
+                     int nz, double omega, const int* face_kind,
+                     const double* face_uwall, const uint8_t* solid,
+                     const double* color, const int* color_i, int device,
+                     tslb_cuda_handle* out) {
+  return create_impl(lattice, scalar, components, nx, ny, nz, 0, nz, omega,
+                     face_kind, face_uwall, solid, color, color_i, device, out);
+}
+
+int tslb_cuda_create_slab(int lattice, int scalar, int components, int nx,
+                          int ny, int nz, int z0, int nz_local, double omega,
+                          const int* face_kind, const double* face_uwall,
+                          const uint8_t* solid, const double* color,
+                          const int* color_i, int device,
+                          tslb_cuda_handle* out) {
+  return create_impl(lattice, scalar, components, nx, ny, nz, z0, nz_local,
+                     omega, face_kind, face_uwall, solid, color, color_i,
+                     device, out);
+}
+
+int tslb_cuda_destroy(tslb_cuda_handle h) {
+  if (!h) return 0;
+  cudaSetDevice(h->device);
+  if (h->s) cudaStreamSynchronize(h->s);
+  if (h->cs) cudaStreamSynchronize(h->cs);
+  if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
+  void* bufs[] = {h->f[0], h->f[1], h->mo, h->two, h->flag, h->solid, h->slow,
+                  h->scratch, h->red, h->dig, h->recv_lo, h->recv_hi};
+  for (void* b : bufs)
+    if (b) cudaFree(b);
+  for (auto e : h->pool) cudaEventDestroy(e);
+  cudaEvent_t evs[] = {h->ev_b, h->ev_c, h->t0, h->t1};
+  for (auto e : evs)
+    if (e) cudaEventDestroy(e);
+  if (h->s) cudaStreamDestroy(h->s);
+  if (h->cs) cudaStreamDestroy(h->cs);
+  delete h;
+  return 0;
+}
+
+int tslb_cuda_set_math(tslb_cuda_handle h, int math) {
+  if (math != kMathDouble && math != kMathFloat) return set_err(TSLB_EINVAL, "bad math mode");
+  h->math = math;
+  return 0;
+}
+
+int tslb_cuda_describe(tslb_cuda_handle h, int* dims, int* info) {
+  if (dims) {
+    dims[0] = h->nx;
+    dims[1] = h->ny;
+    dims[2] = h->nzl;
+    dims[3] = h->z0;
+    dims[4] = h->nzg;
+  }
+  if (info) {
+    info[0] = h->q;
+    info[1] = h->dim;
+    info[2] = h->np;
+    info[3] = h->esz;
+  }
+  return 0;
+}
+
+int tslb_cuda_memory_bytes(tslb_cuda_handle h, uint64_t* bytes) {
+  *bytes = h->bytes;
+  return 0;
+}
+
+int tslb_cuda_upload_f(tslb_cuda_handle h, int species, const void* host) {
+  if (species < 0 || species >= h->comps) return set_err(TSLB_EINVAL, "bad species");
+  CK(cudaSetDevice(h->device));
+  const size_t pb = size_t(h->n()) * h->esz;
+  for (int a = 0; a < h->q; ++a)
+    CK(cudaMemcpyAsync(static_cast<char*>(h->fa(species, a)) +
+                           size_t(h->d.ghost * h->plane()) * h->esz,
+                       static_cast<const char*>(host) + a * pb, pb,
+                       cudaMemcpyHostToDevice, h->s));
+  return sync(h);
+}
+
+int tslb_cuda_download_f(tslb_cuda_handle h, int species, void* host) {
+  if (species < 0 || species >= h->comps) return set_err(TSLB_EINVAL, "bad species");
+  CK(cudaSetDevice(h->device));
+  const size_t pb = size_t(h->n()) * h->esz;
+  for (int a = 0; a < h->q; ++a)
+    CK(cudaMemcpyAsync(static_cast<char*>(host) + a * pb,
+                       static_cast<const char*>(h->fa(species, a)) +
+                           size_t(h->d.ghost * h->plane()) * h->esz,
+                       pb, cudaMemcpyDeviceToHost, h->s));
+  return sync(h);
+}
+
+namespace {
+// (device base, number of arrays, element bytes) for a field id
+int field_desc(tslb_cuda_sim* h, int field, void** base, int* count, int* eb,
+               int64_t* stride, bool upload) {
+  *eb = h->esz;
+  *stride = h->d.mstride;
+  const bool two = h->comps == 2;
+  switch (field) {
+    case TSLB_FIELD_RHO: *base = h->m_arr(0); *count = 1; return 0;
+    case TSLB_FIELD_MOM: *base = h->m_arr(1); *count = h->dim; return 0;
+    case TSLB_FIELD_PINEQ: *base = h->m_arr(1 + h->dim); *count = h->np; return 0;
+    case TSLB_FIELD_RHO_R: if (!two) break; *base = h->t_arr(0); *count = 1; return 0;
+    case TSLB_FIELD_RHO_B: if (!two) break; *base = h->t_arr(1); *count = 1; return 0;
+    case TSLB_FIELD_PHI: if (!two) break; *base = h->t_arr(2); *count = 1; return 0;
+    case TSLB_FIELD_GRADPHI: if (!two) break; *base = h->t_arr(3); *count = h->dim; return 0;
+    case TSLB_FIELD_NCI_FLAG: if (!two) break; *base = h->flag; *count = 1; *eb = 1; return 0;
+    case TSLB_FIELD_SOLID:
+      if (upload) break;
+      *base = static_cast<char*>(static_cast<void*>(h->solid)) + h->d.ghost * h->plane();
+      *count = 1; *eb = 1; return 0;
+    case TSLB_FIELD_SLOW_MASK:
+      if (upload || !h->slow) break;
+      *base = h->slow; *count = 1; *eb = 4; return 0;
+    default: break;
+  }
+  return set_err(TSLB_EINVAL, "field %d not available for this solver%s", field,
+                 upload ? " (or read-only)" : "");
+}
+}  // namespace
+
+int tslb_cuda_upload_field(tslb_cuda_handle h, int field, const void* host) {
+  void* base; int cnt, eb; int64_t stride;
+  if (int rc = field_desc(h, field, &base, &cnt, &eb, &stride, true)) return rc;
+  CK(cudaSetDevice(h->device));
+  const size_t pb = size_t(h->n()) * eb;
+  for (int c = 0; c < cnt; ++c)
+    CK(cudaMemcpyAsync(static_cast<char*>(base) + size_t(c) * stride * eb,
+                       static_cast<const char*>(host) + c * pb, pb,
+                       cudaMemcpyHostToDevice, h->s));
+  if (field == TSLB_FIELD_MOM || field == TSLB_FIELD_PINEQ) h->stress_pending = false;
+  return sync(h);
+}
+
+int tslb_cuda_download_field(tslb_cuda_handle h, int field, void* host) {
+  CK(cudaSetDevice(h->device));
+  // two-fluid: after a step the host-visible mom/pineq are u_eq / Pi^neq
+  // (prepare_stress output, multicomponent.hpp:271-309); the fused step keeps
+  // the raw values on the device, so finish the phase lazily here.
+  if (h->comps == 2 && h->stress_pending &&
+      (field == TSLB_FIELD_MOM || field == TSLB_FIELD_PINEQ)) {
+    if (int rc = ph_cg_prepare(h, h->s)) return rc;
+  }
+  if (field == TSLB_FIELD_SLOW_MASK && !h->slow) {
+    uint32_t* tmp;
+    CK(cudaMalloc(&tmp, size_t(h->d.mstride) * 4));
+    if (int rc = run_classify(h, tmp)) { cudaFree(tmp); return rc; }
+    CK(cudaMemcpy(host, tmp, size_t(h->n()) * 4, cudaMemcpyDeviceToHost));
+    cudaFree(tmp);
+    return 0;
+  }
+  void* base; int cnt, eb; int64_t stride;
+  if (int rc = field_desc(h, field, &base, &cnt, &eb, &stride, false)) return rc;
+  const size_t pb = size_t(h->n()) * eb;
+  for (int c = 0; c < cnt; ++c)
+    CK(cudaMemcpyAsync(static_cast<char*>(host) + c * pb,
+                       static_cast<const char*>(base) + size_t(c) * stride * eb, pb,
+                       cudaMemcpyDeviceToHost, h->s));
+  return sync(h);
+}
+
+int tslb_cuda_download_geometry(tslb_cuda_handle h, uint8_t* solid,
+                                uint32_t* slow_mask, uint64_t* n_fluid) {
+  if (solid)
+    if (int rc = tslb_cuda_download_field(h, TSLB_FIELD_SOLID, solid)) return rc;
+  if (slow_mask)
+    if (int rc = tslb_cuda_download_field(h, TSLB_FIELD_SLOW_MASK, slow_mask)) return rc;
+  if (n_fluid) *n_fluid = h->n_fluid;
+  return 0;
+}
+
+int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
+                            double radius) {
+  CK(cudaSetDevice(h->device));
+  InitSpec s{};
+  s.kind = kind;
+  s.nx_g = h->nx;
+  s.ny_g = h->ny;
+  s.nz_g = h->nzg;
+  s.z0 = h->z0;
+  s.amp = amplitude;
+  s.cx = 0.5 * h->nx - 0.5;
+  s.cy = 0.5 * h->ny - 0.5;
+  s.cz = 0.5 * h->nzg - 0.5;
+  s.radius = radius;
+  s.width = 1.0;
+  ++h->launches;
+  int rc = by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    if (kind == TSLB_INIT_DROPLET) {
+      if (h->comps != 2) return set_err(TSLB_EINVAL, "droplet init needs two components");
+      return launch_init_colors<T>(h->lat, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
+                                   static_cast<T*>(h->f[1]), h->solid, s, h->s);
+    }
+    if (h->comps != 1) return set_err(TSLB_EINVAL, "analytic init %d needs one component", kind);
+    return launch_init_analytic<T>(h->lat, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
+                                   h->d.has_solid ? h->solid : nullptr, s, h->s);
+  });
+  if (rc) return rc;
+  return sync(h);
+}
+
+int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
+  if (h->xmode == 2) return set_err(TSLB_ESTATE, "locally linked slabs step with tslb_cuda_group_step");
+  if (h->decomposed && h->xmode == 0)
+    return set_err(TSLB_ESTATE, "slab solver has no halo transport attached");
+  CK(cudaSetDevice(h->device));
+  for (long k = 0; k < nsteps; ++k)
+    if (int rc = enqueue_step(h)) return rc;
+  CK(cudaGetLastError());
+  return 0;
+}
+
+int tslb_cuda_step(tslb_cuda_handle h, long nsteps) {
+  if (int rc = tslb_cuda_step_async(h, nsteps)) return rc;
+  return sync(h);
+}
+
+int tslb_cuda_synchronize(tslb_cuda_handle h) {
+  CK(cudaSetDevice(h->device));
+  return sync(h);
+}
+
+int tslb_cuda_steps_done(tslb_cuda_handle h, long* steps) {
+  *steps = h->steps;
+  return 0;
+}
+
+int tslb_cuda_time_steps(tslb_cuda_handle h, long nsteps, double* ms) {
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->s));
+  CK(cudaEventRecord(h->t0, h->s));
+  if (int rc = tslb_cuda_step_async(h, nsteps)) return rc;
+  CK(cudaEventRecord(h->t1, h->s));
+  CK(cudaEventSynchronize(h->t1));
+  float f = 0;
+  CK(cudaEventElapsedTime(&f, h->t0, h->t1));
+  *ms = f;
+  return sync(h);
+}
+
+int tslb_cuda_compute_moments(tslb_cuda_handle h) {
+  if (h->comps != 1) return set_err(TSLB_EINVAL, "compute_moments is single-fluid");
+  CK(cudaSetDevice(h->device));
+  if (int rc = ph_moments(h, h->s)) return rc;
+  return sync(h);
+}
+
+int tslb_cuda_stream_collide(tslb_cuda_handle h) {
+  if (h->comps != 1) return set_err(TSLB_EINVAL, "stream_collide_fused is single-fluid");
+  if (h->decomposed) return set_err(TSLB_ESTATE, "use step() on slab solvers");
+  CK(cudaSetDevice(h->device));
+  if (int rc = ph_streamcoll(h, 0, h->nzl, h->s)) return rc;
+  return sync(h);
+}
+
+namespace {
+int ensure_scratch(tslb_cuda_sim* h) {
+  if (h->scratch) return 0;
+  const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
+  if (int rc = alloc(h, &h->scratch, fbytes)) return rc;
+  CK(cudaMemcpyAsync(h->scratch, h->f[0], fbytes, cudaMemcpyDeviceToDevice, h->s));
+  return 0;
+}
+}  // namespace
+
+int tslb_cuda_reference_step(tslb_cuda_handle h, long nsteps) {
+  if (h->comps != 1 || h->decomposed)
+    return set_err(TSLB_EINVAL, "reference_step: single-fluid, single domain only");
+  CK(cudaSetDevice(h->device));
+  if (int rc = ensure_scratch(h)) return rc;
+  for (long s = 0; s < nsteps; ++s) {
+    if (int rc = ph_moments(h, h->s)) return rc;
+    h->launches += 2;
+    int rc = by_scalar(h, [&](auto z) {
+      using T = decltype(z);
+      launch_collide<T>(h->lat, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
+                        static_cast<const T*>(h->mo), h->solid, h->omega, h->s);
+      return launch_stream_only<T>(h->lat, h->range(0, h->nzl),
+                                   static_cast<const T*>(h->f[0]),
+                                   static_cast<T*>(h->scratch), h->solid, h->slow, h->s);
+    });
+    if (rc) return rc;
+    std::swap(h->f[0], h->scratch);
+    ++h->steps;
+  }
+  return sync(h);
+}
+
+int tslb_cuda_stream_only(tslb_cuda_handle h) {
+  if (h->comps != 1 || h->decomposed)
+    return set_err(TSLB_EINVAL, "stream_only: single-fluid, single domain only");
+  CK(cudaSetDevice(h->device));
+  if (int rc = ensure_scratch(h)) return rc;
+  const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
+  CK(cudaMemsetAsync(h->scratch, 0, fbytes, h->s));
+  ++h->launches;
+  int rc = by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_stream_only<T>(h->lat, h->range(0, h->nzl),
+                                 static_cast<const T*>(h->f[0]),
+                                 static_cast<T*>(h->scratch), h->solid, h->slow, h->s);
+  });
+  if (rc) return rc;
+  std::swap(h->f[0], h->scratch);
+  return sync(h);
+}
+
+int tslb_cuda_color_moments(tslb_cuda_handle h) {
+  if (h->comps != 2) return set_err(TSLB_EINVAL, "color_moments is two-fluid");
+  CK(cudaSetDevice(h->device));
+  if (int rc = ph_cg_moments(h, h->s)) return rc;
+  return sync(h);
+}
+
+int tslb_cuda_gradient_and_nci(tslb_cuda_handle h) {
+  if (h->comps != 2) return set_err(TSLB_EINVAL, "gradient_and_nci is two-fluid");
+  CK(cudaSetDevice(h->device));
+  if (int rc = ph_cg_gradient(h, h->s)) return rc;
+  return sync(h);
+}
+
+int tslb_cuda_prepare_stress(tslb_cuda_handle h) {
+  if (h->comps != 2) return set_err(TSLB_EINVAL, "prepare_stress is two-fluid");
+  CK(cudaSetDevice(h->device));
+  if (int rc = ph_cg_prepare(h, h->s)) return rc;
+  return sync(h);
+}
+
+int tslb_cuda_stream_collide_recolor(tslb_cuda_handle h) {
+  if (h->comps != 2) return set_err(TSLB_EINVAL, "stream_collide_recolor is two-fluid");
+  CK(cudaSetDevice(h->device));
+  if (int rc = ph_cg_streamcoll(h, 0, h->s)) return rc;
+  return sync(h);
+}
+
+int tslb_cuda_refresh_moments(tslb_cuda_handle h) {
+  CK(cudaSetDevice(h->device));
+  if (h->comps == 1) {
+    if (int rc = ph_moments(h, h->s)) return rc;
+  } else {
+    if (int rc = ph_cg_moments(h, h->s)) return rc;
+    if (int rc = ph_cg_gradient(h, h->s)) return rc;
+  }
+  return sync(h);
+}
+
+int tslb_cuda_totals(tslb_cuda_handle h, double* mass, double* momentum3) {
+  CK(cudaSetDevice(h->device));
+  double* part = h->red;
+  double* out = h->red + reduce_partial_count();
+  h->launches += 2;
+  by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_totals<T>(h->range(0, h->nzl), h->dim, static_cast<const T*>(h->m_arr(0)),
+                            static_cast<const T*>(h->m_arr(1)), h->solid, part, out, h->s);
+  });
+  double v[4];
+  CK(cudaMemcpyAsync(v, out, sizeof v, cudaMemcpyDeviceToHost, h->s));
+  if (int rc = sync(h)) return rc;
+  *mass = v[0];
+  for (int c = 0; c < 3; ++c) momentum3[c] = c < h->dim ? v[1 + c] : 0.0;
+  return 0;
+}
+
+int tslb_cuda_stability(tslb_cuda_handle h, int* finite, double* max_speed,
+                        double* min_rho, double* max_rho, int64_t* first_bad) {
+  CK(cudaSetDevice(h->device));
+  if (h->comps == 2 && h->stress_pending)
+    if (int rc = ph_cg_prepare(h, h->s)) return rc;
+  double* part = h->red;
+  double* out = h->red + reduce_partial_count();
+  h->launches += 2;
+  by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_stability<T>(h->range(0, h->nzl), h->dim, static_cast<const T*>(h->m_arr(0)),
+                               static_cast<const T*>(h->m_arr(1)), h->solid, part, out, h->s);
+  });
+  double v[5];
+  CK(cudaMemcpyAsync(v, out, sizeof v, cudaMemcpyDeviceToHost, h->s));
+  if (int rc = sync(h)) return rc;
+  if (finite) *finite = v[0] > 0.5;
+  if (max_speed) *max_speed = v[1];
+  if (min_rho) *min_rho = v[2];
+  if (max_rho) *max_rho = v[3];
+  if (first_bad) *first_bad = int64_t(v[4]);
+  return 0;
+}
+
+int tslb_cuda_color_masses(tslb_cuda_handle h, double* red, double* blue) {
+  if (h->comps != 2) return set_err(TSLB_EINVAL, "color_masses is two-fluid");
+  CK(cudaSetDevice(h->device));
+  double* part = h->red;
+  double* out = h->red + reduce_partial_count();
+  h->launches += 2;
+  by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    // rho_r as "rho", rho_b as a one-component "mom"
+    return launch_totals<T>(h->range(0, h->nzl), 1, static_cast<const T*>(h->t_arr(0)),
+                            static_cast<const T*>(h->t_arr(1)), h->solid, part, out, h->s);
+  });
+  double v[4];
+  CK(cudaMemcpyAsync(v, out, sizeof v, cudaMemcpyDeviceToHost, h->s));
+  if (int rc = sync(h)) return rc;
+  *red = v[0];
+  *blue = v[1];
+  return 0;
+}
+
+int tslb_cuda_plane_digests(tslb_cuda_handle h, uint64_t* out) {
+  CK(cudaSetDevice(h->device));
+  const int64_t plane_bytes = h->plane() * h->esz;
+  const int64_t cpp = (plane_bytes + 16383) / 16384;
+  const size_t need = size_t(h->q) * h->nzl * (cpp + 1) * sizeof(uint64_t);
+  if (h->dig_bytes < need) {
+    if (h->dig) cudaFree(h->dig);
+    CK(cudaMalloc(&h->dig, need));
+    h->dig_bytes = need;
+  }
+  uint64_t* chunk = h->dig;
+  uint64_t* planes = h->dig + size_t(h->q) * h->nzl * cpp;
+  for (int sp = 0; sp < h->comps; ++sp) {
+    h->launches += 2;
+    launch_plane_digest(h->range(0, h->nzl), h->f[sp], h->q, h->d.fstride,
+                        int64_t(h->d.ghost) * h->plane(), h->esz, chunk, planes, h->s);
+    CK(cudaMemcpyAsync(out + size_t(sp) * h->q * h->nzl, planes,
+                       size_t(h->q) * h->nzl * sizeof(uint64_t),
+                       cudaMemcpyDeviceToHost, h->s));
+    if (int rc = sync(h)) return rc;
+  }
+  return 0;
+}
+
+int tslb_cuda_profile(tslb_cuda_handle h, int enable) {
+  h->prof = enable != 0;
+  h->rec.clear();
+  h->pool_used = 0;
+  return 0;
+}
+
+int tslb_cuda_profile_read(tslb_cuda_handle h, double* ms, int64_t* launches) {
+  CK(cudaSetDevice(h->device));
+  CK(cudaStreamSynchronize(h->s));
+  CK(cudaStreamSynchronize(h->cs));
+  for (int c = 0; c < TSLB_K_COUNT; ++c) {
+    if (ms) ms[c] = 0;
+    if (launches) launches[c] = 0;
+  }
+  for (auto& r : h->rec) {
+    float t = 0;
+    CK(cudaEventElapsedTime(&t, r.second.first, r.second.second));
+    if (ms) ms[r.first] += t;
+    if (launches) launches[r.first] += 1;
+  }
+  h->rec.clear();
+  h->pool_used = 0;
+  return 0;
+}
+
+int tslb_cuda_launch_count(tslb_cuda_handle h, int64_t* launches) {
+  *launches = h->launches;
+  return 0;
+}
+
+int tslb_cuda_nccl_unique_id(void* id128) {
+  NcclApi& N = nccl();
+  if (!N.ok) return set_err(TSLB_ECUDA, "libnccl.so.2 could not be loaded");
+  ncclUniqueId id;
+  ncclResult_t r = N.GetUniqueId(&id);
+  if (r != ncclSuccess) return set_err(TSLB_ECUDA, "ncclGetUniqueId: %s", N.ErrStr(r));
+  std::memcpy(id128, &id, sizeof id);
+  return 0;
+}
+
+int tslb_cuda_attach_nccl(tslb_cuda_handle h, const void* id128, int nranks,
+                          int rank) {
+  NcclApi& N = nccl();
+  if (!N.ok) return set_err(TSLB_ECUDA, "libnccl.so.2 could not be loaded");
+  if (!h->decomposed) return set_err(TSLB_ESTATE, "attach_nccl needs a slab solver");
+  CK(cudaSetDevice(h->device));
+  ncclUniqueId id;
+  std::memcpy(&id, id128, sizeof id);
+  ncclResult_t r = N.CommInitRank(&h->comm, nranks, id, rank);
+  if (r != ncclSuccess) return set_err(TSLB_ECUDA, "ncclCommInitRank: %s", N.ErrStr(r));
+  h->rank = rank;
+  h->nranks = nranks;
+  h->up = h->d.mode[ZMax] == kGhost ? (rank + 1) % nranks : -1;
+  h->down = h->d.mode[ZMin] == kGhost ? (rank - 1 + nranks) % nranks : -1;
+  h->xmode = 1;
+  return 0;
+}
+
+int tslb_cuda_link_local(tslb_cuda_handle* slabs, int count) {
+  if (count < 2) return set_err(TSLB_EINVAL, "link_local needs at least two slabs");
+  for (int r = 0; r < count; ++r) {
+    tslb_cuda_sim* h = slabs[r];
+    if (!h->decomposed) return set_err(TSLB_ESTATE, "link_local needs slab solvers");
+    h->up_peer = h->d.mode[ZMax] == kGhost ? slabs[(r + 1) % count] : nullptr;
+    h->down_peer = h->d.mode[ZMin] == kGhost ? slabs[(r - 1 + count) % count] : nullptr;
+    h->xmode = 2;
+  }
+  return 0;
+}
+
+int tslb_cuda_group_step(tslb_cuda_handle* slabs, int count, long nsteps) {
+  // Same schedule as the NCCL path, serialised on the first slab's stream
+  // (single-device verification transport).
+  cudaStream_t st = slabs[0]->s;
+  CK(cudaSetDevice(slabs[0]->device));
+  for (long s = 0; s < nsteps; ++s) {
+    for (int r = 0; r < count; ++r)
+      if (int rc = ph_moments(slabs[r], st)) return rc;
+    for (int r = 0; r < count; ++r)
+      if (int rc = ph_streamcoll(slabs[r], 0, slabs[r]->nzl, st)) return rc;
+    for (int r = 0; r < count; ++r)
+      if (int rc = exchange_local(slabs[r], st)) return rc;
+    for (int r = 0; r < count; ++r) {
+      if (int rc = unpack(slabs[r], st)) return rc;
+      ++slabs[r]->steps;
+    }
+  }
+  CK(cudaStreamSynchronize(st));
+  CK(cudaGetLastError());
+  return 0;
+}
+
+}  // extern "C"

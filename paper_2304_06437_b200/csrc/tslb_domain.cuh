@@ -1,0 +1,61 @@
+// Device-side domain description and HBM layout.
+//
+// Layout: structure of arrays, x fastest (reference
+// fields.hpp:26-29). Population arrays carry `ghost` (0 or 1) extra z planes
+// below and above the owned slab so a z-slab-decomposed run can push
+// straight into its neighbour's boundary slots; moment/phase arrays hold only
+// owned planes. Every array starts on a 256-byte boundary (stride padded).
+#pragma once
+
+#include <cstdint>
+
+namespace tslb_cuda {
+
+// Face behaviour as seen by ONE domain (a whole box, or one z slab).
+enum FaceMode : int {
+  kWrap = 0,   // periodic inside this domain: index wraps to the far side
+  kWall = 1,   // half-way bounce-back, optional wall velocity
+  kGhost = 2,  // slab interface: push lands in the ghost plane, exchanged later
+};
+
+enum FaceId : int { XMin = 0, XMax = 1, YMin = 2, YMax = 3, ZMin = 4, ZMax = 5 };
+
+struct Dom {
+  int nx, ny, nz;        // owned extent (nz = local slab depth)
+  int ghost;             // ghost planes on each z side of population arrays
+  int64_t plane;         // nx * ny
+  int64_t n;             // owned nodes = plane * nz
+  int64_t fstride;       // elements between consecutive population arrays
+  int64_t mstride;       // elements between consecutive moment arrays
+  int mode[6];           // FaceMode per face
+  double uw[6][3];       // wall velocity per face, already rounded to T
+  int has_solid;         // solid mask / slow mask present
+  int xblocks;           // blocks per x row in the row-tiled launch
+  int k0, nzr;           // launch range: planes [k0, k0 + nzr)
+};
+
+/// Row-tiled launch geometry: block (xb, row) covers nodes
+/// [xb*BX, xb*BX+BX) of row `row` = j + ny*k; returns false past the row end.
+template <int BX>
+__device__ __forceinline__ bool node_coords(const Dom& d, int& i, int& j,
+                                            int& k) {
+  const unsigned bid = blockIdx.x;
+  const unsigned row = bid / unsigned(d.xblocks);
+  const unsigned xb = bid - row * unsigned(d.xblocks);
+  i = int(xb * BX + threadIdx.x);
+  j = int(row % unsigned(d.ny));
+  k = int(row / unsigned(d.ny)) + d.k0;
+  return i < d.nx;
+}
+
+__device__ __forceinline__ int64_t midx(const Dom& d, int i, int j, int k) {
+  return int64_t(i) + int64_t(d.nx) * (int64_t(j) + int64_t(d.ny) * k);
+}
+
+/// population-array index (shifted by the ghost plane)
+__device__ __forceinline__ int64_t fidx(const Dom& d, int i, int j, int k) {
+  return int64_t(i) +
+         int64_t(d.nx) * (int64_t(j) + int64_t(d.ny) * (int64_t(k) + d.ghost));
+}
+
+}  // namespace tslb_cuda

@@ -1,0 +1,105 @@
+// Internal launcher declarations shared by the kernel TUs and the C-ABI TU.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tslb_domain.cuh"
+
+namespace tslb_cuda {
+
+enum MathMode : int { kMathDouble = 0, kMathFloat = 1 };
+
+enum InitKind : int { kInitRest = 0, kInitShear = 1, kInitTaylorGreen = 2, kInitDroplet = 3 };
+
+struct InitSpec {
+  int kind;
+  int nx_g, ny_g, nz_g;  // global extents (for slabs)
+  int z0;                // global z of local plane 0
+  double amp;            // shear / Taylor-Green velocity amplitude
+  double cx, cy, cz, radius, width;  // droplet
+};
+
+struct ColorParamsDev {
+  double sigma, beta, nci_strength, eps_bulk, grad_threshold;
+  int nci_reach, linear;
+};
+
+// ---- single fluid (tslb_single.cu)
+template <typename T>
+int launch_moments(int lat, int math, const Dom& d, const T* f, T* mo,
+                   const uint8_t* solid, cudaStream_t st);
+template <typename T>
+int launch_streamcoll(int lat, int math, const Dom& d, T* f, const T* mo,
+                      const uint8_t* solid, const uint32_t* slow, double omega,
+                      cudaStream_t st);
+template <typename T>
+int launch_collide(int lat, const Dom& d, T* f, const T* mo,
+                   const uint8_t* solid, double omega, cudaStream_t st);
+template <typename T>
+int launch_stream_only(int lat, const Dom& d, const T* f, T* dst,
+                       const uint8_t* solid, const uint32_t* slow,
+                       cudaStream_t st);
+int launch_classify(int lat, const Dom& d, const uint8_t* solid,
+                    uint32_t* slow, unsigned long long* n_fluid,
+                    cudaStream_t st);
+template <typename T>
+int launch_init_analytic(int lat, const Dom& d, T* f, const uint8_t* solid,
+                         const InitSpec& s, cudaStream_t st);
+
+// ---- two fluid (tslb_two.cu)
+struct TwoFields {
+  void *rho_r, *rho_b, *rho, *mom, *pin, *phi, *grad;  // each mstride-strided
+  uint8_t* flag;
+};
+template <typename T>
+int launch_cg_moments(int lat, const Dom& d, const T* fr, const T* fb,
+                      const TwoFields& s, const uint8_t* solid,
+                      cudaStream_t st);
+template <typename T>
+int launch_cg_gradient(int lat, const Dom& d, const TwoFields& s,
+                       const uint8_t* solid, const uint32_t* slow,
+                       const ColorParamsDev& cp, cudaStream_t st);
+template <typename T>
+int launch_cg_prepare_stress(int lat, const Dom& d, const TwoFields& s,
+                             const uint8_t* solid, double omega,
+                             const ColorParamsDev& cp, cudaStream_t st);
+template <typename T>
+int launch_cg_streamcoll(int lat, const Dom& d, T* fr, T* fb,
+                         const TwoFields& s, const uint8_t* solid,
+                         const uint32_t* slow, double omega,
+                         const ColorParamsDev& cp, int fold_prepare,
+                         cudaStream_t st);
+template <typename T>
+int launch_init_colors(int lat, const Dom& d, T* fr, T* fb,
+                       const uint8_t* solid, const InitSpec& s,
+                       cudaStream_t st);
+
+// ---- reductions / digest (tslb_reduce.cu)
+// totals: out[0] = mass, out[1..3] = momentum (fp64 deterministic tree)
+template <typename T>
+int launch_totals(const Dom& d, int dim, const T* rho, const T* mom,
+                  const uint8_t* solid, double* partial, double* out,
+                  cudaStream_t st);
+// stability: out = {finite(0/1), max_speed, min_rho, max_rho}
+template <typename T>
+int launch_stability(const Dom& d, int dim, const T* rho, const T* mom,
+                     const uint8_t* solid, double* partial, double* out,
+                     cudaStream_t st);
+// per-plane FNV-1a digests of `narrays` arrays (stride elements apart,
+// first owned plane at offset `base`): out[a * nz + k]
+int launch_plane_digest(const Dom& d, const void* arr, int narrays,
+                        int64_t stride, int64_t base, int elem_bytes,
+                        uint64_t* chunk_scratch, uint64_t* out,
+                        cudaStream_t st);
+
+size_t reduce_partial_count();
+
+// ---- slab exchange (tslb_exchange.cu)
+template <typename T>
+int launch_unpack(const Dom& d, T* f, const T* recv, const uint8_t* solid,
+                  int ndirs, const int* a, const int* cx, const int* cy,
+                  int kdst, int ksrc_ghost, cudaStream_t st);
+
+}  // namespace tslb_cuda

@@ -1,0 +1,512 @@
+// Two-component colour-gradient kernels for sm_100a.
+//
+//   k_cg_moments     color_moments          multicomponent.hpp:55-119
+//   k_cg_gradient    gradient_and_nci       multicomponent.hpp:154-242
+//   k_cg_prepare     prepare_stress         multicomponent.hpp:271-309
+//   k_cg_streamcoll  stream_collide_recolor multicomponent.hpp:315-401
+//                    (optionally with prepare_stress folded into its
+//                    prologue: the hot schedule is 3 kernels per step)
+//
+// All arithmetic in T, as in the reference; with --fmad=false and IEEE
+// div/sqrt the results are bit-identical for float and double storage.
+// NCI flags are set-only byte stores of the value 1 -- concurrent writers
+// store the same byte, so the result is launch-shape independent, mirroring
+// the reference's relaxed atomic_ref stores (multicomponent.hpp:233-236).
+#include <cstdint>
+
+#include "tslb_collision.cuh"
+#include "tslb_domain.cuh"
+#include "tslb_kernels.h"
+
+namespace tslb_cuda {
+
+constexpr int BX2 = 128;
+
+template <typename T>
+struct TF {
+  T *rho_r, *rho_b, *rho, *mom, *pin, *phi, *grad;
+  uint8_t* flag;
+};
+
+template <typename T>
+__host__ TF<T> tf_of(const TwoFields& s) {
+  return TF<T>{static_cast<T*>(s.rho_r), static_cast<T*>(s.rho_b),
+               static_cast<T*>(s.rho),   static_cast<T*>(s.mom),
+               static_cast<T*>(s.pin),   static_cast<T*>(s.phi),
+               static_cast<T*>(s.grad),  s.flag};
+}
+
+// ---------------------------------------------------------------------------
+template <class L, typename T>
+__global__ void __launch_bounds__(BX2)
+    k_cg_moments(Dom d, const T* __restrict__ fr, const T* __restrict__ fb,
+                 TF<T> s, const uint8_t* __restrict__ solid) {
+  int i, j, k;
+  if (!node_coords<BX2>(d, i, j, k)) return;
+  const int64_t fi = fidx(d, i, j, k);
+  const int64_t mi = midx(d, i, j, k);
+  s.flag[mi] = 0;
+  if (solid[fi]) return;
+  T rr = 0, rb = 0;
+  T r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pzz = 0, pxy = 0,
+    pxz = 0, pyz = 0;
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    using dd = Dir<L, a>;
+    const T fra = __ldg(fr + a * d.fstride + fi);
+    const T fba = __ldg(fb + a * d.fstride + fi);
+    const T ga = fra + fba;
+    rr += fra;
+    rb += fba;
+    r += ga;
+    if constexpr (dd::x == 1) jx += ga;
+    if constexpr (dd::x == -1) jx -= ga;
+    if constexpr (dd::y == 1) jy += ga;
+    if constexpr (dd::y == -1) jy -= ga;
+    if constexpr (dd::z == 1) jz += ga;
+    if constexpr (dd::z == -1) jz -= ga;
+    if constexpr (dd::x != 0) pxx += ga;
+    if constexpr (dd::y != 0) pyy += ga;
+    if constexpr (dd::z != 0) pzz += ga;
+    if constexpr (dd::x * dd::y == 1) pxy += ga;
+    if constexpr (dd::x * dd::y == -1) pxy -= ga;
+    if constexpr (dd::x * dd::z == 1) pxz += ga;
+    if constexpr (dd::x * dd::z == -1) pxz -= ga;
+    if constexpr (dd::y * dd::z == 1) pyz += ga;
+    if constexpr (dd::y * dd::z == -1) pyz -= ga;
+  });
+  const int64_t ms = d.mstride;
+  s.rho_r[mi] = rr;
+  s.rho_b[mi] = rb;
+  s.rho[mi] = r;
+  s.phi[mi] = (rr - rb) / r;
+  s.mom[mi] = jx;
+  s.mom[ms + mi] = jy;
+  if constexpr (L::dim == 3) {
+    s.mom[2 * ms + mi] = jz;
+    s.pin[mi] = pxx;
+    s.pin[ms + mi] = pyy;
+    s.pin[2 * ms + mi] = pzz;
+    s.pin[3 * ms + mi] = pxy;
+    s.pin[4 * ms + mi] = pxz;
+    s.pin[5 * ms + mi] = pyz;
+  } else {
+    s.pin[mi] = pxx;
+    s.pin[ms + mi] = pyy;
+    s.pin[2 * ms + mi] = pxy;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Neighbour (pull) lookup with the reference's rule: wall or solid
+// neighbours read phi(x) itself (multicomponent.hpp:178-186).
+__device__ __forceinline__ bool nb_index(const Dom& d,
+                                         const uint8_t* __restrict__ solid,
+                                         int cx, int cy, int cz, int i, int j,
+                                         int k, int64_t& mi_out) {
+  int tc[3] = {i + cx, j + cy, k + cz};
+  const int nd[3] = {d.nx, d.ny, d.nz};
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    if (tc[ax] < 0 || tc[ax] >= nd[ax]) {
+      const int face = 2 * ax + (tc[ax] < 0 ? 0 : 1);
+      if (d.mode[face] != kWrap) return false;
+      tc[ax] = tc[ax] < 0 ? tc[ax] + nd[ax] : tc[ax] - nd[ax];
+    }
+  }
+  if (solid[fidx(d, tc[0], tc[1], tc[2])]) return false;
+  mi_out = midx(d, tc[0], tc[1], tc[2]);
+  return true;
+}
+
+template <class L, typename T>
+__global__ void __launch_bounds__(BX2)
+    k_cg_gradient(Dom d, TF<T> s, const uint8_t* __restrict__ solid,
+                  const uint32_t* __restrict__ slow, ColorParamsDev cp) {
+  int i, j, k;
+  if (!node_coords<BX2>(d, i, j, k)) return;
+  const int64_t fi = fidx(d, i, j, k);
+  const int64_t mi = midx(d, i, j, k);
+  if (solid[fi]) return;
+  const uint32_t sm = slow[mi];
+  const T phi0 = s.phi[mi];
+  T gx = 0, gy = 0, gz = 0;
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    using dd = Dir<L, a>;
+    if constexpr (a > 0) {
+      T pn;
+      if ((sm >> a) & 1u) {
+        int64_t t;
+        pn = nb_index(d, solid, dd::x, dd::y, dd::z, i, j, k, t) ? s.phi[t]
+                                                                 : phi0;
+      } else {
+        const int64_t off = int64_t(dd::x) +
+                            int64_t(d.nx) * (int64_t(dd::y) + int64_t(d.ny) * dd::z);
+        pn = s.phi[mi + off];
+      }
+      constexpr T w = dd::template t<T>();
+      const T tp = w * pn;
+      if constexpr (dd::x == 1) gx += tp;
+      if constexpr (dd::x == -1) gx -= tp;
+      if constexpr (dd::y == 1) gy += tp;
+      if constexpr (dd::y == -1) gy -= tp;
+      if constexpr (dd::z == 1) gz += tp;
+      if constexpr (dd::z == -1) gz -= tp;
+    }
+  });
+  const int64_t ms = d.mstride;
+  s.grad[mi] = T(3) * gx;
+  s.grad[ms + mi] = T(3) * gy;
+  if constexpr (L::dim == 3) s.grad[2 * ms + mi] = T(3) * gz;
+
+  // near-contact scan (multicomponent.hpp:202-238), only when enabled
+  const T bulk_cut = T(-1) + T(cp.eps_bulk);
+  if (T(cp.nci_strength) != T(0) && phi0 < bulk_cut) {
+    unroll<L::q>([&](auto A) {
+      constexpr int a = decltype(A)::value;
+      using dd = Dir<L, a>;
+      if constexpr (a > 0 && dd::opp > a) {
+        int64_t hit_p = 0, hit_m = 0;
+        bool found_p = false, found_m = false;
+        int ci = i, cj = j, ck = k;
+        for (int st = 0; st < cp.nci_reach; ++st) {
+          int64_t t;
+          if (!nb_index(d, solid, dd::x, dd::y, dd::z, ci, cj, ck, t)) break;
+          // advance (wrap) the probe position
+          ci += dd::x; cj += dd::y; ck += dd::z;
+          if (ci < 0) ci += d.nx; if (ci >= d.nx) ci -= d.nx;
+          if (cj < 0) cj += d.ny; if (cj >= d.ny) cj -= d.ny;
+          if (ck < 0) ck += d.nz; if (ck >= d.nz) ck -= d.nz;
+          if (s.phi[t] >= bulk_cut) {
+            hit_p = t;
+            found_p = true;
+            break;
+          }
+        }
+        if (found_p) {
+          ci = i; cj = j; ck = k;
+          for (int st = 0; st < cp.nci_reach; ++st) {
+            int64_t t;
+            if (!nb_index(d, solid, -dd::x, -dd::y, -dd::z, ci, cj, ck, t)) break;
+            ci -= dd::x; cj -= dd::y; ck -= dd::z;
+            if (ci < 0) ci += d.nx; if (ci >= d.nx) ci -= d.nx;
+            if (cj < 0) cj += d.ny; if (cj >= d.ny) cj -= d.ny;
+            if (ck < 0) ck += d.nz; if (ck >= d.nz) ck -= d.nz;
+            if (s.phi[t] >= bulk_cut) {
+              hit_m = t;
+              found_m = true;
+              break;
+            }
+          }
+          if (found_m) {
+            s.flag[hit_p] = 1;
+            s.flag[hit_m] = 1;
+          }
+        }
+      }
+    });
+  }
+}
+
+// ---------------------------------------------------------------------------
+// prepare_stress body (multicomponent.hpp:249-309) for one node; returns the
+// shifted velocity and Pi^neq in registers.
+template <class L, typename T>
+__device__ __forceinline__ void prepare_node_stress(
+    const Dom& d, const TF<T>& s, int64_t mi, T tau, const ColorParamsDev& cp,
+    T& ux, T& uy, T& uz, T p[6]) {
+  const int64_t ms = d.mstride;
+  T F0 = 0, F1 = 0, F2 = 0;
+  if (s.flag[mi]) {  // nci_force_at
+    const T gx = s.grad[mi];
+    const T gy = s.grad[ms + mi];
+    const T gz = L::dim == 3 ? s.grad[2 * ms + mi] : T(0);
+    const T gn = sqrt(gx * gx + gy * gy + gz * gz);
+    if (!(gn <= T(cp.grad_threshold))) {
+      const T scale = T(cp.nci_strength) * s.rho_r[mi] / gn;
+      F0 = scale * gx;
+      F1 = scale * gy;
+      F2 = scale * gz;
+    }
+  }
+  ux = s.mom[mi] + tau * F0;
+  uy = s.mom[ms + mi] + tau * F1;
+  uz = L::dim == 3 ? s.mom[2 * ms + mi] + tau * F2 : T(0);
+  const T r = s.rho[mi];
+  const T c3 = cs2<T>();
+  if constexpr (L::dim == 3) {
+    p[0] = s.pin[mi] + (-c3 * r - ux * ux);
+    p[1] = s.pin[ms + mi] + (-c3 * r - uy * uy);
+    p[2] = s.pin[2 * ms + mi] + (-c3 * r - uz * uz);
+    p[3] = s.pin[3 * ms + mi] - ux * uy;
+    p[4] = s.pin[4 * ms + mi] - ux * uz;
+    p[5] = s.pin[5 * ms + mi] - uy * uz;
+  } else {
+    p[0] = s.pin[mi] + (-c3 * r - ux * ux);
+    p[1] = s.pin[ms + mi] + (-c3 * r - uy * uy);
+    p[2] = s.pin[2 * ms + mi] - ux * uy;
+  }
+}
+
+template <class L, typename T>
+__global__ void __launch_bounds__(BX2)
+    k_cg_prepare(Dom d, TF<T> s, const uint8_t* __restrict__ solid, T tau,
+                 ColorParamsDev cp) {
+  int i, j, k;
+  if (!node_coords<BX2>(d, i, j, k)) return;
+  const int64_t mi = midx(d, i, j, k);
+  if (solid[fidx(d, i, j, k)]) return;
+  T ux, uy, uz, p[6];
+  prepare_node_stress<L, T>(d, s, mi, tau, cp, ux, uy, uz, p);
+  const int64_t ms = d.mstride;
+  s.mom[mi] = ux;
+  s.mom[ms + mi] = uy;
+  if constexpr (L::dim == 3) s.mom[2 * ms + mi] = uz;
+  constexpr int np = L::dim * (L::dim + 1) / 2;
+#pragma unroll
+  for (int c = 0; c < np; ++c) s.pin[c * ms + mi] = p[c];
+}
+
+// inv_cnorm (multicomponent.hpp:35-48), constants pre-rounded to T exactly as
+// T(long double literal) does on the host.
+template <typename T, int N2>
+__device__ __forceinline__ T inv_cnorm() {
+  if constexpr (N2 == 0) return T(0);
+  if constexpr (N2 == 1) return T(1);
+  if constexpr (N2 == 2) {
+    if constexpr (sizeof(T) == 4) return __int_as_float(0x3f3504f3);
+    else return __longlong_as_double(0x3fe6a09e667f3bcdLL);
+  }
+  if constexpr (sizeof(T) == 4) return __int_as_float(0x3f13cd3a);
+  else return __longlong_as_double(0x3fe279a74590331cLL);
+}
+
+template <class L, typename T, bool FOLD>
+__global__ void __launch_bounds__(BX2)
+    k_cg_streamcoll(Dom d, T* __restrict__ fr, T* __restrict__ fb, TF<T> s,
+                    const uint8_t* __restrict__ solid,
+                    const uint32_t* __restrict__ slow, T omega, T tau,
+                    ColorParamsDev cp) {
+  int i, j, k;
+  if (!node_coords<BX2>(d, i, j, k)) return;
+  const int64_t fi = fidx(d, i, j, k);
+  const int64_t mi = midx(d, i, j, k);
+  if (solid[fi]) return;
+  const int64_t ms = d.mstride;
+  T ux, uy, uz, p[6];
+  if constexpr (FOLD) {
+    prepare_node_stress<L, T>(d, s, mi, tau, cp, ux, uy, uz, p);
+  } else {
+    ux = s.mom[mi];
+    uy = s.mom[ms + mi];
+    uz = L::dim == 3 ? s.mom[2 * ms + mi] : T(0);
+    constexpr int np = L::dim * (L::dim + 1) / 2;
+#pragma unroll
+    for (int c = 0; c < np; ++c) p[c] = s.pin[c * ms + mi];
+  }
+  const T r = s.rho[mi];
+  NodeMoments<T> m;
+  if constexpr (L::dim == 3)
+    m = prepare_node<T>(r, ux, uy, uz, p[0], p[1], p[2], p[3], p[4], p[5]);
+  else
+    m = prepare_node<T>(r, ux, uy, T(0), p[0], p[1], T(0), p[2], T(0), T(0));
+  const T om1 = T(1) - omega;
+  const T pert_coef = T(2.25) * T(cp.sigma) * omega;
+  const T rr = s.rho_r[mi];
+  const T rb = s.rho_b[mi];
+  const T red_frac = rr / r;
+  const T rec_amp = T(cp.beta) * (rr * rb / r);
+  const T gx = s.grad[mi];
+  const T gy = s.grad[ms + mi];
+  const T gz = L::dim == 3 ? s.grad[2 * ms + mi] : T(0);
+  const T gn = sqrt(gx * gx + gy * gy + gz * gz);
+  const bool interface = gn > T(cp.grad_threshold);
+  const T pert_amp = interface ? pert_coef * gn : T(0);
+  const T inv_gn = interface ? T(1) / gn : T(0);
+  const T nhx = gx * inv_gn, nhy = gy * inv_gn, nhz = gz * inv_gn;
+  const uint32_t sm = slow[mi];
+  const bool linear = cp.linear != 0;
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    using dd = Dir<L, a>;
+    constexpr T t = dd::template t<T>();
+    constexpr T b = dd::template b<T>();
+    T g_out = post_collision<L, a, T>(m, om1);
+    T fr_out;
+    if (interface) {
+      const T cn = dot_c<dd::x, dd::y, dd::z>(nhx, nhy, nhz);
+      const T shape = !linear ? t * cn * cn - b : t * cn - b;
+      g_out += pert_amp * shape;
+      fr_out = red_frac * g_out + rec_amp * t * cn * inv_cnorm<T, dd::norm2>();
+    } else {
+      fr_out = red_frac * g_out;
+    }
+    const T fb_out = g_out - fr_out;
+    if ((sm >> a) & 1u) {
+      int tc[3] = {i + dd::x, j + dd::y, k + dd::z};
+      const int nd[3] = {d.nx, d.ny, d.nz};
+      bool bounce = false;
+      T wx = T(0), wy = T(0), wz = T(0);
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (tc[ax] < 0 || tc[ax] >= nd[ax]) {
+          const int face = 2 * ax + (tc[ax] < 0 ? 0 : 1);
+          const int mode = d.mode[face];
+          if (mode == kWrap) {
+            tc[ax] = tc[ax] < 0 ? tc[ax] + nd[ax] : tc[ax] - nd[ax];
+          } else if (mode == kWall) {
+            bounce = true;
+            wx += T(d.uw[face][0]);
+            wy += T(d.uw[face][1]);
+            wz += T(d.uw[face][2]);
+          }
+        }
+      }
+      int64_t target = 0;
+      if (!bounce) {
+        target = fidx(d, tc[0], tc[1], tc[2]);
+        if (solid[target]) bounce = true;
+      }
+      if (bounce) {
+        const T corr = bounce_correction<L, a, T>(wx, wy, wz);
+        const T corr_r = red_frac * corr;
+        fr[dd::opp * d.fstride + fi] = fr_out - corr_r;
+        fb[dd::opp * d.fstride + fi] = fb_out - (corr - corr_r);
+      } else {
+        fr[a * d.fstride + target] = fr_out;
+        fb[a * d.fstride + target] = fb_out;
+      }
+    } else {
+      const int64_t off = int64_t(dd::x) +
+                          int64_t(d.nx) * (int64_t(dd::y) + int64_t(d.ny) * dd::z);
+      fr[a * d.fstride + fi + off] = fr_out;
+      fb[a * d.fstride + fi + off] = fb_out;
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
+// device droplet initialiser (initialize_colors, multicomponent.hpp:427-449,
+// with the tslb_main droplet profile 0.5 (1 + tanh(R - r)))
+template <class L, typename T>
+__global__ void __launch_bounds__(BX2)
+    k_init_colors(Dom d, T* __restrict__ fr, T* __restrict__ fb,
+                  const uint8_t* __restrict__ solid, InitSpec sp) {
+  int i, j, k;
+  if (!node_coords<BX2>(d, i, j, k)) return;
+  const int64_t fi = fidx(d, i, j, k);
+  if (solid[fi]) return;
+  const double kg = double(k + sp.z0);
+  const double dz2 = L::dim == 3 ? (kg - sp.cz) * (kg - sp.cz) : 0.0;
+  const double dist = sp.radius - sqrt((i - sp.cx) * (i - sp.cx) +
+                                       (j - sp.cy) * (j - sp.cy) + dz2);
+  const double prof = 0.5 * (1.0 + tanh(dist / sp.width));
+  const T rr = T(prof), rb = T(1.0 - prof);
+  const T r = rr + rb;
+  const NodeMoments<T> m =
+      prepare_node<T>(r, T(0), T(0), T(0), T(0), T(0), T(0), T(0), T(0), T(0));
+  const T frac = rr / r;
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    const T fe = equilibrium<L, a, T>(m);
+    fr[a * d.fstride + fi] = frac * fe;
+    fb[a * d.fstride + fi] = fe - frac * fe;
+  });
+}
+
+// ---------------------------------------------------------------------------
+namespace {
+inline dim3 grid2(const Dom& d) {
+  return dim3(unsigned(int64_t(d.xblocks) * d.ny * d.nzr));
+}
+template <class F>
+int with_lat2(int lat, F&& f) {
+  switch (lat) {
+    case kD2Q9: f(D2Q9{}); return 0;
+    case kD3Q19: f(D3Q19{}); return 0;
+    case kD3Q27: f(D3Q27{}); return 0;
+    default: return 1;
+  }
+}
+}  // namespace
+
+template <typename T>
+int launch_cg_moments(int lat, const Dom& d, const T* fr, const T* fb,
+                      const TwoFields& s, const uint8_t* solid,
+                      cudaStream_t st) {
+  return with_lat2(lat, [&](auto L) {
+    k_cg_moments<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), solid);
+  });
+}
+
+template <typename T>
+int launch_cg_gradient(int lat, const Dom& d, const TwoFields& s,
+                       const uint8_t* solid, const uint32_t* slow,
+                       const ColorParamsDev& cp, cudaStream_t st) {
+  return with_lat2(lat, [&](auto L) {
+    k_cg_gradient<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s), solid, slow, cp);
+  });
+}
+
+template <typename T>
+int launch_cg_prepare_stress(int lat, const Dom& d, const TwoFields& s,
+                             const uint8_t* solid, double omega,
+                             const ColorParamsDev& cp, cudaStream_t st) {
+  const T tau = T(1) / T(omega);
+  return with_lat2(lat, [&](auto L) {
+    k_cg_prepare<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s), solid, tau, cp);
+  });
+}
+
+template <typename T>
+int launch_cg_streamcoll(int lat, const Dom& d, T* fr, T* fb,
+                         const TwoFields& s, const uint8_t* solid,
+                         const uint32_t* slow, double omega,
+                         const ColorParamsDev& cp, int fold_prepare,
+                         cudaStream_t st) {
+  const T om = T(omega);
+  const T tau = T(1) / om;
+  return with_lat2(lat, [&](auto L) {
+    if (fold_prepare)
+      k_cg_streamcoll<decltype(L), T, true>
+          <<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), solid, slow, om, tau, cp);
+    else
+      k_cg_streamcoll<decltype(L), T, false>
+          <<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), solid, slow, om, tau, cp);
+  });
+}
+
+template <typename T>
+int launch_init_colors(int lat, const Dom& d, T* fr, T* fb,
+                       const uint8_t* solid, const InitSpec& sp,
+                       cudaStream_t st) {
+  return with_lat2(lat, [&](auto L) {
+    k_init_colors<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, fr, fb, solid, sp);
+  });
+}
+
+#define TSLB_INST2(T)                                                         \
+  template int launch_cg_moments<T>(int, const Dom&, const T*, const T*,      \
+                                    const TwoFields&, const uint8_t*,         \
+                                    cudaStream_t);                            \
+  template int launch_cg_gradient<T>(int, const Dom&, const TwoFields&,       \
+                                     const uint8_t*, const uint32_t*,         \
+                                     const ColorParamsDev&, cudaStream_t);    \
+  template int launch_cg_prepare_stress<T>(int, const Dom&, const TwoFields&, \
+                                           const uint8_t*, double,            \
+                                           const ColorParamsDev&,             \
+                                           cudaStream_t);                     \
+  template int launch_cg_streamcoll<T>(int, const Dom&, T*, T*,               \
+                                       const TwoFields&, const uint8_t*,      \
+                                       const uint32_t*, double,               \
+                                       const ColorParamsDev&, int,            \
+                                       cudaStream_t);                         \
+  template int launch_init_colors<T>(int, const Dom&, T*, T*,                 \
+                                     const uint8_t*, const InitSpec&,         \
+                                     cudaStream_t);
+TSLB_INST2(float)
+TSLB_INST2(double)
+#undef TSLB_INST2
+
+}  // namespace tslb_cuda

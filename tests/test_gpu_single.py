@@ -1,0 +1,264 @@
+"""GPU parity of the single-fluid hot path (fused_step and its phases)
+against the CPU oracle, through the C-ABI. Bar: bit-exact (node-local
+arithmetic in double, --fmad=false), for double AND float storage, as the
+reference's own fused-vs-two-buffer check (unit_collision_stream.cpp:269-330,
+acceptance.cpp:101-135)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2304_06437_b200 import tslb as T
+
+from helpers import assert_bitwise, block_solid, corner_box_3d, mixed_2d, random_solid, spec_of, zwalls_3d
+
+pytestmark = pytest.mark.gpu
+
+DT = [np.float64, np.float32]
+
+CASES_2D = [
+    ("periodic", (16, 16, 1), O.periodic(), None),
+    ("box", (16, 12, 1), O.closed_box(), None),
+    ("lid", (20, 16, 1), O.lid_cavity(0.05), None),
+    ("mixed+block", (16, 16, 1), mixed_2d(), block_solid((16, 16, 1), (6, 5, 0), (10, 8, 1))),
+    ("periodic+random", (24, 20, 1), O.periodic(), random_solid((24, 20, 1), 0.1, 4)),
+    ("odd-x", (131, 9, 1), O.lid_cavity(0.03), None),
+]
+CASES_3D = [
+    ("periodic", (8, 7, 6), O.periodic(), None),
+    ("zwalls", (8, 7, 6), zwalls_3d(), None),
+    ("box-corners", (9, 8, 7), corner_box_3d(), None),
+    ("box+random", (10, 9, 8), O.closed_box(), random_solid((10, 9, 8), 0.08, 7)),
+    ("periodic+block", (12, 10, 9), O.periodic(), block_solid((12, 10, 9), (3, 2, 2), (7, 6, 5))),
+    ("wide-x", (200, 4, 3), zwalls_3d(), None),
+]
+
+
+def _gpu_single(lat, dims, omega, faces, f, steps, solid, phase="step", moments=None):
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), omega, spec_of(faces), f.dtype, 1, solid)
+    try:
+        dev.upload_f(f)
+        if moments is not None:
+            L = T.lattice_of(lat)
+            dev.upload_field("rho", moments[0])
+            dev.upload_field("mom", moments[1:1 + L.dim])
+            dev.upload_field("pineq", moments[1 + L.dim:])
+        if phase == "step":
+            dev.step(steps)
+        elif phase == "reference":
+            dev.phase("reference_step", steps)
+        else:
+            for _ in range(steps):
+                dev.phase(phase)
+        L = T.lattice_of(lat)
+        mo = np.concatenate([dev.download_field("rho")[None], dev.download_field("mom").reshape(L.dim, -1),
+                             dev.download_field("pineq").reshape(L.npineq, -1)])
+        return dev.download_f(0), mo
+    finally:
+        dev.close()
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("lat,case", [("d2q9", c) for c in CASES_2D] + [("d3q19", c) for c in CASES_3D]
+                         + [("d3q27", c) for c in CASES_3D[:4]])
+def test_fused_step_bitwise(gpu, oracle_port, lat, case, dtype):
+    name, dims, faces, solid = case
+    f0 = O.random_state(lat, dims, 2024, dtype, solid)
+    omega = 1.31 if lat == "d2q9" else 0.77
+    fo, mo = f0.copy(), np.zeros((O.moments_layout(lat), f0.shape[1]), dtype)
+    oracle_port.single_run(lat, dims, omega, faces, fo, mo, 5, 0, solid)
+    fg, mg = _gpu_single(lat, dims, omega, faces, f0, 5, solid)
+    fluid = np.ones(f0.shape[1], bool) if solid is None else solid == 0
+    assert_bitwise(fg, fo, f"{lat}/{name} f", fluid)
+    # lagged moment semantics: arrays hold m(t) of the last step (solver.hpp:68-69)
+    assert_bitwise(mg, mo, f"{lat}/{name} moments", fluid)
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("lat,case", [("d2q9", CASES_2D[3]), ("d3q19", CASES_3D[2]), ("d3q19", CASES_3D[3])])
+def test_matches_reference_build(gpu, oracle_ref, lat, case, dtype):
+    """Directly against the UNMODIFIED reference headers (oracle/_ref)."""
+    name, dims, faces, solid = case
+    f0 = O.random_state(lat, dims, 55, dtype, solid)
+    fr = f0.copy()
+    oracle_ref.single_run(lat, dims, 1.1, faces, fr, None, 4, 0, solid)
+    fg, _ = _gpu_single(lat, dims, 1.1, faces, f0, 4, solid)
+    fluid = np.ones(f0.shape[1], bool) if solid is None else solid == 0
+    assert_bitwise(fg, fr, f"{lat}/{name} vs reference build", fluid)
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("mode,phase", [(1, "reference"), (2, "compute_moments"), (3, "stream_collide"),
+                                        (4, "stream_only")])
+@pytest.mark.parametrize("lat,case", [("d2q9", CASES_2D[3]), ("d3q19", CASES_3D[3])])
+def test_phases_bitwise(gpu, oracle_port, lat, case, dtype, mode, phase):
+    name, dims, faces, solid = case
+    f0 = O.random_state(lat, dims, 91, dtype, solid)
+    nm = O.moments_layout(lat)
+    m0 = np.random.default_rng(5).uniform(-0.01, 0.01, (nm, f0.shape[1])).astype(dtype)
+    m0[0] += 1
+    fo, mo = f0.copy(), m0.copy()
+    steps = 3 if mode in (1, 4) else 1
+    oracle_port.single_run(lat, dims, 1.2, faces, fo, mo, steps, mode, solid)
+    fg, mg = _gpu_single(lat, dims, 1.2, faces, f0, steps, solid, phase, m0)
+    fluid = np.ones(f0.shape[1], bool) if solid is None else solid == 0
+    assert_bitwise(fg, fo, f"{phase} f", fluid)
+    if mode in (1, 2):
+        assert_bitwise(mg, mo, f"{phase} moments", fluid)
+
+
+@pytest.mark.parametrize("lat,case", [("d2q9", c) for c in CASES_2D] + [("d3q19", c) for c in CASES_3D]
+                         + [("d3q27", c) for c in CASES_3D])
+def test_classify_bitwise(gpu, oracle_port, lat, case):
+    name, dims, faces, solid = case
+    so, sl, nf = oracle_port.classify(lat, dims, faces, solid)
+    geo = T.classify_nodes(lat, T.GridDims(*dims), spec_of(faces), solid)
+    assert_bitwise(geo.solid, so, "solid")
+    assert_bitwise(geo.slow_mask, sl, "slow_mask")
+    assert geo.n_fluid == nf
+
+
+def test_half_periodic_axis_rejected(gpu):
+    spec = T.BoundarySpec.all_periodic()
+    spec.faces[T.YMin] = T.Face(T.FaceKind.NoSlipWall)
+    with pytest.raises(T.InvalidArgument, match="axis 1"):
+        T.SingleFluidSim(T.D2Q9, T.GridDims(8, 8, 1), T.CollisionParams(1.0), spec)
+    with pytest.raises(T.InvalidArgument):
+        T.SingleFluidSim(T.D2Q9, T.GridDims(0, 8, 1), T.CollisionParams(1.0), T.BoundarySpec())
+    with pytest.raises(T.InvalidArgument, match="mask size"):
+        T.SingleFluidSim(T.D2Q9, T.GridDims(8, 8, 1), T.CollisionParams(1.0), T.BoundarySpec(),
+                         solid=np.zeros(10, np.uint8))
+
+
+def test_cavity_c1_bitwise(gpu, oracle_port):
+    """Config 1: D2Q9 lid-driven cavity 256^2, Re 100, 1000 steps, fp64,
+    rest init -- bitwise against the oracle."""
+    dims = (256, 256, 1)
+    omega = T.omega_from_nu(0.064)
+    faces = O.lid_cavity(0.025)
+    g = T.GridDims(*dims)
+    sim = T.SingleFluidSim(T.D2Q9, g, T.CollisionParams(omega), spec_of(faces))
+    s = sim.fields()
+    T.initialize_regularized(s, sim.geometry(), lambda i, j, k: (1.0, 0, 0, 0, 0, 0, 0, 0, 0, 0), T.D2Q9)
+    f0 = s.f.copy()
+    sim.run(1000)
+    fo = f0.copy()
+    oracle_port.single_run("d2q9", dims, omega, faces, fo, None, 1000, 0)
+    assert_bitwise(sim.view().f, fo, "cavity f after 1000 steps")
+    # reference digest of the same state (bench.hpp:93-99)
+    assert T.fnv1a(sim.view().f) == oracle_port.fnv1a(fo)
+
+
+def test_sim_host_mirror_semantics(gpu, oracle_port):
+    """fields() edits are uploaded before the next step; moments lag by one
+    step until refresh_moments() (solver.hpp:68-69, 96)."""
+    dims = (12, 10, 1)
+    sim = T.SingleFluidSim(T.D2Q9, T.GridDims(*dims), T.CollisionParams(1.1), T.BoundarySpec.all_periodic())
+    f0 = O.random_state("d2q9", dims, 17)
+    sim.fields().f[...] = f0
+    sim.run(3)
+    fo, mo = f0.copy(), np.zeros((6, f0.shape[1]))
+    oracle_port.single_run("d2q9", dims, 1.1, O.periodic(), fo, mo, 3, 0)
+    v = sim.view()
+    assert_bitwise(v.f, fo, "f")
+    assert_bitwise(v.rho, mo[0], "lagged rho")
+    sim.refresh_moments()
+    oracle_port.single_run("d2q9", dims, 1.1, O.periodic(), fo, mo, 1, 2)
+    assert_bitwise(sim.view().rho, mo[0], "refreshed rho")
+    assert sim.steps() == 3
+
+
+@pytest.mark.parametrize("dtype,tol", [(np.float64, 1e-12), (np.float32, 1e-5)])
+def test_conservation_and_totals(gpu, oracle_port, dtype, tol):
+    """Mass/momentum conservation on a periodic box (unit_collision_stream.cpp
+    :332-379) and device totals vs the serial reference sum."""
+    dims = (24, 20, 18)
+    sim = T.SingleFluidSim(T.D3Q19, T.GridDims(*dims), T.CollisionParams(1.1), T.BoundarySpec.all_periodic(),
+                           dtype=dtype)
+    sim.fields().f[...] = O.random_state("d3q19", dims, 91, dtype)
+    sim.refresh_moments()
+    m0, p0 = sim.totals()
+    v = sim.view()
+    mref, pref = oracle_port.totals(v.rho, v.mom)
+    assert abs(m0 - mref) / mref < (1e-13 if dtype == np.float64 else 1e-6)
+    sim.run(200)
+    sim.refresh_moments()
+    m1, p1 = sim.totals()
+    assert abs(m1 - m0) / m0 < tol
+    assert np.all(np.abs(p1 - p0) < (1e-10 if dtype == np.float64 else 1e-3))
+    rep = sim.stability()
+    ref = oracle_port.stability(sim.view().rho, sim.view().mom)
+    assert rep.finite and ref["finite"]
+    assert rep.max_speed == pytest.approx(ref["max_speed"], rel=1e-12)
+    assert rep.min_rho == ref["min_rho"] and rep.max_rho == ref["max_rho"]
+
+
+def test_stability_locates_nonfinite(gpu):
+    dims = (8, 8, 4)
+    sim = T.SingleFluidSim(T.D3Q19, T.GridDims(*dims), T.CollisionParams(1.0), T.BoundarySpec.all_periodic())
+    s = sim.fields()
+    s.f[...] = O.random_state("d3q19", dims, 3)
+    s.f[2, 77] = np.nan
+    sim.refresh_moments()
+    rep = sim.stability()
+    assert not rep.finite and rep.first_bad == 77
+
+
+@pytest.mark.parametrize("lat", ["d2q9", "d3q19", "d3q27"])
+def test_fp32_math_mode_within_tolerance(gpu, oracle_port, lat):
+    """Opt-in fp32 node arithmetic: tolerance parity:
+    max|drho| <= 2e-5, max|du|/|u|max <= 2e-4 after 200 steps."""
+    dims = (32, 32, 1) if lat == "d2q9" else (16, 16, 16)
+    faces = O.lid_cavity(0.05) if lat == "d2q9" else zwalls_3d()
+    f0 = O.random_state(lat, dims, 8, np.float32)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.4, spec_of(faces), np.float32)
+    dev.set_math(1)
+    dev.upload_f(f0)
+    dev.step(200)
+    dev.phase("refresh_moments")
+    rho, mom = dev.download_field("rho"), dev.download_field("mom")
+    fo, mo = f0.copy(), np.zeros((O.moments_layout(lat), f0.shape[1]), np.float32)
+    oracle_port.single_run(lat, dims, 1.4, faces, fo, mo, 200, 0)
+    oracle_port.single_run(lat, dims, 1.4, faces, fo, mo, 1, 2)
+    D = T.lattice_of(lat).dim
+    assert np.max(np.abs(rho - mo[0])) <= 2e-5
+    umax = np.max(np.abs(mo[1:1 + D]))
+    assert np.max(np.abs(mom - mo[1:1 + D])) / umax <= 2e-4
+    dev.close()
+
+
+def test_device_digest_matches_host_definition(gpu):
+    dims = (40, 36, 5)
+    sim = T.SingleFluidSim(T.D3Q19, T.GridDims(*dims), T.CollisionParams(1.0), T.BoundarySpec.all_periodic(),
+                           dtype=np.float32)
+    sim.fields().f[...] = O.random_state("d3q19", dims, 11, np.float32)
+    sim.run(2)
+    dg = sim.plane_digests()[0]
+    host = T.chunked_plane_digest(sim.view().f, T.GridDims(*dims))
+    assert np.array_equal(dg, host)
+
+
+@pytest.mark.parametrize("init", ["shear", "taylor_green", "rest"])
+def test_device_init_matches_host_formula(gpu, init):
+    """Device analytic initialisers agree with the host initialiser to
+    libm-vs-CUDA-math rounding (not a parity path: bench inits only)."""
+    dims = (32, 16, 8)
+    g = T.GridDims(*dims)
+    dev = T.DeviceSolver(T.D3Q19, g, 1.6, T.BoundarySpec.all_periodic(), np.float64)
+    dev.init_analytic(init, 0.03)
+    fdev = dev.download_f()
+    s = T.allocate_fields(g, T.D3Q19)
+
+    def st(i, j, k):
+        X, Y, Z = (2 * np.pi * (i + 0.5) / dims[0], 2 * np.pi * (j + 0.5) / dims[1], 2 * np.pi * (k + 0.5) / dims[2])
+        z = np.zeros_like(X)
+        if init == "shear":
+            return (1.0, 0.03 * np.sin(2 * np.pi * j / dims[1]), z, z, z, z, z, z, z, z)
+        if init == "rest":
+            return (1.0, z, z, z, z, z, z, z, z, z)
+        U = 0.03
+        return (1 + 3 * (U * U / 16) * (np.cos(2 * X) + np.cos(2 * Y)) * (np.cos(2 * Z) + 2),
+                U * np.sin(X) * np.cos(Y) * np.cos(Z), -U * np.cos(X) * np.sin(Y) * np.cos(Z), z, z, z, z, z, z, z)
+
+    T.initialize_regularized(s, None, st, T.D3Q19)
+    assert np.max(np.abs(fdev - s.f)) < 1e-15
+    dev.close()

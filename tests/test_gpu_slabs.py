@@ -1,0 +1,65 @@
+"""z-slab decomposition on ONE device through the local-copy transport
+(tslb_cuda_link_local / group_step): the same kernels, ghost planes and
+masked unpack as the NCCL path, checked bit for bit against the undivided
+domain -- SURVEY.md §4's "single-GPU test of the decomposition" and §8(e)'s
+GPU-count determinism."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2304_06437_b200 import _lib
+from paper_2304_06437_b200 import tslb as T
+
+from helpers import assert_bitwise, random_solid, spec_of, zwalls_3d
+
+pytestmark = pytest.mark.gpu
+
+
+def split(nz, parts):
+    return [(nz * p // parts, nz * (p + 1) // parts - nz * p // parts) for p in range(parts)]
+
+
+def run_slabs(lat, dims, omega, faces, f0, steps, parts, solid=None, dtype=np.float64):
+    g = T.GridDims(*dims)
+    plane = dims[0] * dims[1]
+    slabs = [T.DeviceSolver(lat, g, omega, spec_of(faces), dtype, 1, solid, slab=s) for s in split(dims[2], parts)]
+    for sv, (z0, nzl) in zip(slabs, split(dims[2], parts)):
+        sv.upload_f(np.ascontiguousarray(f0[:, z0 * plane:(z0 + nzl) * plane]))
+    arr = (C.c_void_p * parts)(*[s.h.value for s in slabs])
+    _lib.call("tslb_cuda_link_local", arr, parts)
+    _lib.call("tslb_cuda_group_step", arr, parts, int(steps))
+    f = np.concatenate([s.download_f() for s in slabs], axis=1)
+    dig = np.concatenate([s.plane_digests()[0] for s in slabs], axis=1)
+    for s in slabs:
+        s.close()
+    return f, dig
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("parts", [2, 3, 4])
+@pytest.mark.parametrize("lat,faces,solid_frac", [
+    ("d3q19", O.periodic(), 0.0),
+    ("d3q19", zwalls_3d(), 0.0),
+    ("d3q19", O.closed_box(), 0.0),
+    ("d3q19", O.periodic(), 0.1),
+    ("d3q27", zwalls_3d(), 0.05),
+    ("d3q27", O.periodic(), 0.0),
+])
+def test_slabs_equal_single_domain(gpu, lat, faces, solid_frac, parts, dtype):
+    dims = (12, 10, 12)
+    solid = random_solid(dims, solid_frac, 3) if solid_frac else None
+    f0 = O.random_state(lat, dims, 20240817, dtype, solid)
+    one = T.DeviceSolver(lat, T.GridDims(*dims), 0.9, spec_of(faces), dtype, 1, solid)
+    one.upload_f(f0)
+    one.step(6)
+    ref = one.download_f()
+    dig1 = one.plane_digests()[0]
+    one.close()
+    got, dig = run_slabs(lat, dims, 0.9, faces, f0, 6, parts, solid, dtype)
+    fluid = np.ones(f0.shape[1], bool) if solid is None else solid == 0
+    assert_bitwise(got, ref, f"{parts} slabs vs one domain", fluid)
+    if solid is None:
+        # decomposition-independent digest
+        assert np.array_equal(dig, dig1)

@@ -1,0 +1,174 @@
+"""GPU parity of the two-component colour-gradient path (two_fluid_step and
+its phases) against the CPU oracle. All arithmetic in T in both, so the bar
+is bit-exact for float and double (unit_multicomponent.cpp scenarios)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2304_06437_b200 import tslb as T
+
+from helpers import assert_bitwise, block_solid, droplet_state, mixed_2d, spec_of, zwalls_3d
+
+pytestmark = pytest.mark.gpu
+
+COLORS = {
+    "squared": dict(sigma=0.02),
+    "linear": dict(sigma=0.02, linear=True),
+    "nci": dict(sigma=0.03, nci_strength=0.1, eps_bulk=0.2, nci_reach=3),
+}
+
+
+def _cp(c):
+    return T.ColorParams(sigma=c.get("sigma", 0.01), beta=c.get("beta", 0.7), nci_strength=c.get("nci_strength", 0.0),
+                         nci_reach=c.get("nci_reach", 3), eps_bulk=c.get("eps_bulk", 0.02),
+                         form=T.PerturbationForm.Linear if c.get("linear") else T.PerturbationForm.Squared)
+
+
+def _gpu_two(lat, dims, omega, color, faces, fr, fb, steps, refresh, solid):
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), omega, spec_of(faces), fr.dtype, 2, solid, _cp(color))
+    try:
+        dev.upload_f(fr, 0)
+        dev.upload_f(fb, 1)
+        dev.step(steps)
+        if refresh:
+            dev.phase("refresh_moments")
+        out = {k: dev.download_field(k) for k in ("rho_r", "rho_b", "rho", "mom", "pineq", "phi", "gradphi",
+                                                   "nci_flag")}
+        out["fr"], out["fb"] = dev.download_f(0), dev.download_f(1)
+        return out
+    finally:
+        dev.close()
+
+
+CASES = [
+    ("d2q9", (24, 20, 1), O.periodic(), None),
+    ("d2q9", (24, 20, 1), O.lid_cavity(0.05), None),
+    ("d2q9", (24, 20, 1), mixed_2d(), block_solid((24, 20, 1), (3, 2, 0), (7, 5, 1))),
+    ("d3q19", (10, 9, 8), zwalls_3d(), None),
+    ("d3q19", (12, 10, 9), O.periodic(), block_solid((12, 10, 9), (1, 1, 1), (3, 3, 3))),
+]
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("color", list(COLORS))
+@pytest.mark.parametrize("refresh", [False, True])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-{c[1]}")
+def test_two_fluid_step_bitwise(gpu, oracle_port, case, color, refresh, dtype):
+    lat, dims, faces, solid = case
+    st = droplet_state(dims, min(dims[:2]) / 4, dtype, (0.01, -0.005, 0.002 if dims[2] > 1 else 0.0))
+    fr, fb = oracle_port.init_colors(lat, dims, st, solid)
+    fro, fbo = fr.copy(), fb.copy()
+    ref = oracle_port.two_run(lat, dims, 1.2, COLORS[color], faces, fro, fbo, 6, refresh, 0, solid)
+    got = _gpu_two(lat, dims, 1.2, COLORS[color], faces, fr, fb, 6, refresh, solid)
+    fluid = np.ones(fr.shape[1], bool) if solid is None else solid == 0
+    assert_bitwise(got["fr"], fro, "fr", fluid)
+    assert_bitwise(got["fb"], fbo, "fb", fluid)
+    for k in ("rho_r", "rho_b", "rho", "phi"):
+        assert_bitwise(got[k], ref[k], k, fluid)
+    D = T.lattice_of(lat).dim
+    # after step(): u_eq / Pi^neq; after refresh: bare j / raw second moment
+    assert_bitwise(np.reshape(got["mom"], (D, -1)), ref["mom"], "mom", fluid)
+    assert_bitwise(np.reshape(got["pineq"], (-1, fr.shape[1])), ref["pineq"], "pineq", fluid)
+    assert_bitwise(np.reshape(got["gradphi"], (D, -1)), ref["gradphi"], "gradphi", fluid)
+    assert_bitwise(got["nci_flag"], ref["nci_flag"], "nci_flag")
+
+
+def test_two_fluid_matches_reference_build(gpu, oracle_ref):
+    lat, dims, faces, solid = CASES[2]
+    st = droplet_state(dims, 5.0, np.float32, (0.01, 0.0, 0.0))
+    from oracle.oracle import Oracle
+    fr, fb = Oracle("port").init_colors(lat, dims, st, solid)
+    fro, fbo = fr.copy(), fb.copy()
+    oracle_ref.two_run(lat, dims, 1.3, COLORS["nci"], faces, fro, fbo, 5, False, 0, solid)
+    got = _gpu_two(lat, dims, 1.3, COLORS["nci"], faces, fr, fb, 5, False, solid)
+    fluid = solid == 0
+    assert_bitwise(got["fr"], fro, "fr", fluid)
+    assert_bitwise(got["fb"], fbo, "fb", fluid)
+
+
+@pytest.mark.parametrize("lat,dims", [("d2q9", (12, 10, 1)), ("d3q19", (8, 8, 8))])
+def test_gradient_exact_for_linear_phi(gpu, oracle_port, lat, dims):
+    """unit_multicomponent.cpp:188-231: grad phi exact for linear fields on
+    interior nodes; and bitwise equal to the oracle everywhere."""
+    g = T.GridDims(*dims)
+    i, j, k = T._coords(g)
+    a = (0.011, -0.007, 0.019)
+    phi = (0.2 + a[0] * i + a[1] * j + (a[2] * k if dims[2] > 1 else 0)).astype(np.float64)
+    dev = T.DeviceSolver(lat, g, 1.0, T.BoundarySpec.all_periodic(), np.float64, 2)
+    dev.upload_field("phi", phi)
+    dev.phase("gradient_and_nci")
+    gp = dev.download_field("gradphi")
+    ref = oracle_port.two_run(lat, dims, 1.0, {}, O.periodic(), None, None, 0, False, 1, None, phi)
+    assert_bitwise(gp, ref["gradphi"], "gradphi")
+    D = T.lattice_of(lat).dim
+    inner = (i > 0) & (i < dims[0] - 1) & (j > 0) & (j < dims[1] - 1)
+    if D == 3:
+        inner &= (k > 0) & (k < dims[2] - 1)
+    for d in range(D):
+        assert np.allclose(gp[d][inner], a[d], rtol=1e-12, atol=0)
+    dev.close()
+
+
+def test_nci_flags_thin_film(gpu):
+    """unit_multicomponent.cpp:233-266: a 2-node film flags exactly the facing
+    columns {10, 13}; a 7-node gap flags nothing."""
+    g = T.GridDims(24, 6, 1)
+    cp = T.ColorParams(nci_strength=0.01, nci_reach=3)
+
+    def scan(lo, hi):
+        i, j, _ = T._coords(g)
+        in_gap = (i >= lo) & (i <= hi)
+        in_red = (i >= 4) & (i <= 19)
+        phi = np.where(in_red & ~in_gap, 1.0, -1.0)
+        dev = T.DeviceSolver(T.D2Q9, g, 1.0, T.BoundarySpec.all_periodic(), np.float64, 2, None, cp)
+        dev.upload_field("phi", phi)
+        dev.phase("gradient_and_nci")
+        fl = dev.download_field("nci_flag")
+        dev.close()
+        return set(np.unique(i[fl.astype(bool)]).tolist())
+
+    assert scan(11, 12) == {10, 13}
+    assert scan(9, 15) == set()
+
+
+def test_colour_mass_conservation_and_stability(gpu):
+    """unit_multicomponent.cpp:130-152 at 3D size, device reductions."""
+    dims = (32, 32, 32)
+    g = T.GridDims(*dims)
+    sim = T.TwoFluidSim(T.D3Q19, g, T.CollisionParams(T.omega_from_tau(1.0)), T.ColorParams(sigma=0.02),
+                        T.BoundarySpec.all_periodic())
+    T.initialize_colors(sim.fields(), sim.geometry(),
+                        lambda i, j, k: tuple(droplet_state(dims, 8.0, np.float64)), T.D3Q19)
+    sim.refresh_moments()
+    r0, b0 = sim.color_masses()
+    sim.run(60)
+    sim.refresh_moments()
+    r1, b1 = sim.color_masses()
+    assert abs(r1 - r0) / r0 < 1e-12 and abs(b1 - b0) / b0 < 1e-12
+    assert sim.stability().stable()
+
+
+def test_all_red_tracks_single_fluid(gpu):
+    """unit_multicomponent.cpp:83-128: all-red two-fluid == single fluid to
+    1e-12 (one summation-order difference), blue stays exactly zero."""
+    g = T.GridDims(20, 16, 1)
+    prm = T.CollisionParams(1.15)
+    single = T.SingleFluidSim(T.D2Q9, g, prm, T.BoundarySpec.all_periodic())
+    two = T.TwoFluidSim(T.D2Q9, g, prm, T.ColorParams(sigma=0.01), T.BoundarySpec.all_periodic())
+
+    def state(i, j):
+        ux = 0.02 * np.sin(2 * np.pi * j / g.ny)
+        uy = 0.01 * np.cos(2 * np.pi * i / g.nx)
+        return 1 + 0.03 * np.cos(2 * np.pi * i / g.nx), ux, uy
+
+    z = lambda i: np.zeros(i.shape)
+    T.initialize_regularized(single.fields(), None,
+                             lambda i, j, k: (state(i, j)[0], state(i, j)[1], state(i, j)[2], z(i), 0, 0, 0, 0, 0, 0),
+                             T.D2Q9)
+    T.initialize_colors(two.fields(), None, lambda i, j, k: (state(i, j)[0], z(i), state(i, j)[1], state(i, j)[2], z(i)),
+                        T.D2Q9)
+    single.run(20)
+    two.run(20)
+    fs, tv = single.view().f, two.view()
+    assert np.allclose(tv.fr, fs, rtol=1e-12, atol=0)
+    assert np.all(tv.fb == 0.0)
