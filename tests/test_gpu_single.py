@@ -178,8 +178,12 @@ def test_conservation_and_totals(gpu, oracle_port, dtype, tol):
     sim.refresh_moments()
     m0, p0 = sim.totals()
     v = sim.view()
+    # the device tree sums in fp64 (deterministic); the reference sums
+    # serially in T, whose own rounding error dominates for float storage
+    exact = float(np.sum(v.rho.astype(np.float64)))
+    assert abs(m0 - exact) / exact < 1e-14
     mref, pref = oracle_port.totals(v.rho, v.mom)
-    assert abs(m0 - mref) / mref < (1e-13 if dtype == np.float64 else 1e-6)
+    assert abs(m0 - mref) / mref < (1e-13 if dtype == np.float64 else 1e-5)
     sim.run(200)
     sim.refresh_moments()
     m1, p1 = sim.totals()
