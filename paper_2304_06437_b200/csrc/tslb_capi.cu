@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -99,6 +100,7 @@ struct tslb_cuda_sim {
   bool decomposed = false;
   int device = 0;
   int math = kMathDouble;
+  bool vec_ok = true;  // vectorised stream-collide allowed (TSLB_STREAMCOLL=scalar disables)
   double omega = 1.0;
   int kinds[6] = {0, 0, 0, 0, 0, 0};
   ColorParamsDev cp{};
@@ -233,6 +235,11 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
   ++h->launches;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
+    constexpr int VX = 16 / sizeof(T);
+    if (h->vec_ok && !h->d.has_solid && h->nx % VX == 0)
+      return launch_streamcoll_vec<T>(h->lat, h->math, h->range(k0, k1),
+                                      static_cast<T*>(h->f[0]), static_cast<const T*>(h->mo),
+                                      h->omega, st);
     return launch_streamcoll<T>(h->lat, h->math, h->range(k0, k1),
                                 static_cast<T*>(h->f[0]), static_cast<const T*>(h->mo),
                                 h->solid, h->slow, h->omega, st);
@@ -461,6 +468,7 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   h->decomposed = decomposed;
   h->device = device;
   h->omega = omega;
+  if (const char* e = std::getenv("TSLB_STREAMCOLL")) h->vec_ok = std::strcmp(e, "scalar") != 0;
   std::memcpy(h->kinds, kinds, sizeof h->kinds);
   if (color) {
     h->cp.sigma = color[0];

@@ -1,0 +1,372 @@
+// Vectorised fused stream-collide for box geometries (no solid mask): the
+// throughput kernel of the F1 schedule.
+//
+// Same results, bit for bit, as k_streamcoll / the reference
+// stream_collide_fused (kernels.hpp:154-204); what changes is the shape:
+//   * each thread owns VX consecutive x nodes (VX = 16 B / sizeof(T)), so the
+//     moment loads and population stores are 128-bit and the address
+//     arithmetic is paid once per VX nodes;
+//   * pushes along c_x = +-1 land one element off the thread's aligned
+//     vector: the missing element comes from the neighbour lane by a warp
+//     shuffle, and the two ends of each warp's row segment patch their edge
+//     element with a scalar store -- every slot still has exactly one writer;
+//   * opposite directions share their work: Q_a : Pi^neq is identical for a
+//     and opp(a), and c_opp . u = -(c_a . u), so one pair costs ~20 DP ops
+//     instead of ~36. These rewrites only change the sign of intermediate
+//     zeros, which cannot reach the result unless rho == -0.0; rho from the
+//     moments pass is never -0.0 (a +0-seeded sum cannot produce it), and a
+//     thread that sees rho == -0.0 (user-written moments) takes the
+//     reference-order path instead.
+#include <cstdint>
+
+#include "tslb_collision.cuh"
+#include "tslb_domain.cuh"
+#include "tslb_kernels.h"
+
+namespace tslb_cuda {
+
+template <typename T>
+struct Vec;
+template <>
+struct Vec<float> {
+  static constexpr int N = 4;
+  using V = float4;
+  __device__ static V ld(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  __device__ static void st(float* p, const float (&v)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+  __device__ static void unpack(const V& v, float (&o)[4]) {
+    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+  }
+};
+template <>
+struct Vec<double> {
+  static constexpr int N = 2;
+  using V = double2;
+  __device__ static V ld(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+  __device__ static void st(double* p, const double (&v)[2]) {
+    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  }
+  __device__ static void unpack(const V& v, double (&o)[2]) {
+    o[0] = v.x; o[1] = v.y;
+  }
+};
+
+constexpr int BXV = 128;
+
+// c . u without the +0 seed (sign of a zero result may differ; see header)
+template <int CX, int CY, int CZ, typename C>
+__device__ __forceinline__ C dot_noseed(C x, C y, C z) {
+  C s;
+  bool first = true;
+  auto add = [&](int c, C v) {
+    if (c == 0) return;
+    if (first) {
+      s = c > 0 ? v : -v;
+      first = false;
+    } else {
+      s = c > 0 ? s + v : s - v;
+    }
+  };
+  add(CX, x);
+  add(CY, y);
+  add(CZ, z);
+  return s;
+}
+
+// Post-collision values of the pair (A, A+1 = opp(A)), A odd.
+template <class L, int A, typename C>
+__device__ __forceinline__ void post_pair(const NodeMoments<C>& m, C om1,
+                                          C& out_a, C& out_b) {
+  using d = Dir<L, A>;
+  constexpr C t = d::template t<C>();
+  const C cu = dot_noseed<d::x, d::y, d::z, C>(m.ux, m.uy, m.uz);
+  const C c3 = C(3) * cu;
+  const C q = C(4.5) * cu * cu;
+  const C ea = t * (m.rho + c3 + q - m.usq15);
+  const C eb = t * (m.rho - c3 + q - m.usq15);
+  const C r = om1 * regularized<L, A, C>(m);  // reference order, shared
+  out_a = ea + r;
+  out_b = eb + r;
+}
+
+template <class L, typename C>
+__device__ __forceinline__ C post_rest(const NodeMoments<C>& m, C om1) {
+  constexpr C t = Dir<L, 0>::template t<C>();
+  // rho + 3*(+0) + (4.5*(+0))*(+0) == rho for rho != -0
+  const C e = t * (m.rho - m.usq15);
+  return e + om1 * regularized<L, 0, C>(m);
+}
+
+template <class L, typename T, typename C, int VX>
+__device__ __forceinline__ void load_moments_vec(const Dom& d,
+                                                 const T* __restrict__ mo,
+                                                 int64_t mi,
+                                                 NodeMoments<C> (&m)[VX]) {
+  constexpr int NM = 1 + L::dim + L::dim * (L::dim + 1) / 2;
+  T v[NM][VX];
+#pragma unroll
+  for (int c = 0; c < NM; ++c) Vec<T>::unpack(Vec<T>::ld(mo + c * d.mstride + mi), v[c]);
+#pragma unroll
+  for (int x = 0; x < VX; ++x) {
+    if constexpr (L::dim == 3)
+      m[x] = prepare_node<C>(C(v[0][x]), C(v[1][x]), C(v[2][x]), C(v[3][x]), C(v[4][x]),
+                             C(v[5][x]), C(v[6][x]), C(v[7][x]), C(v[8][x]), C(v[9][x]));
+    else
+      m[x] = prepare_node<C>(C(v[0][x]), C(v[1][x]), C(v[2][x]), C(0), C(v[3][x]),
+                             C(v[4][x]), C(0), C(v[5][x]), C(0), C(0));
+  }
+}
+
+struct RowGeom {
+  int64_t dyp, dym, dzp, dzm;  // row deltas (wrapped / ghost-shifted)
+  bool byp, bym, bzp, bzm;     // y / z step bounces off a wall
+  bool xwall_lo, xwall_hi;     // x faces are walls
+};
+
+__device__ __forceinline__ RowGeom row_geom(const Dom& d, int j, int k) {
+  RowGeom g;
+  const int64_t nx = d.nx, pl = d.plane;
+  g.dyp = nx;
+  g.dym = -nx;
+  g.dzp = pl;
+  g.dzm = -pl;
+  g.byp = g.bym = g.bzp = g.bzm = false;
+  if (j == d.ny - 1) {
+    if (d.mode[YMax] == kWrap) g.dyp = -nx * (d.ny - 1);
+    else if (d.mode[YMax] == kWall) g.byp = true;
+  }
+  if (j == 0) {
+    if (d.mode[YMin] == kWrap) g.dym = nx * (d.ny - 1);
+    else if (d.mode[YMin] == kWall) g.bym = true;
+  }
+  if (k == d.nz - 1) {
+    if (d.mode[ZMax] == kWrap) g.dzp = -pl * (d.nz - 1);
+    else if (d.mode[ZMax] == kWall) g.bzp = true;
+  }
+  if (k == 0) {
+    if (d.mode[ZMin] == kWrap) g.dzm = pl * (d.nz - 1);
+    else if (d.mode[ZMin] == kWall) g.bzm = true;
+  }
+  g.xwall_lo = d.mode[XMin] == kWall;
+  g.xwall_hi = d.mode[XMax] == kWall;
+  return g;
+}
+
+// Bounce of direction A at node fi: f[opp][fi] = T(C(out) - 6 t (c.u_wall))
+// with u_wall summed in T over the crossed wall faces in axis order.
+template <class L, int A, typename T, typename C>
+__device__ __forceinline__ T bounce_value(const Dom& d, T out, bool cross_x,
+                                          bool cross_y, bool cross_z) {
+  using dd = Dir<L, A>;
+  T wx = T(0), wy = T(0), wz = T(0);
+  auto add = [&](int face) {
+    wx += T(d.uw[face][0]);
+    wy += T(d.uw[face][1]);
+    wz += T(d.uw[face][2]);
+  };
+  if (cross_x) add(dd::x > 0 ? XMax : XMin);
+  if (cross_y) add(dd::y > 0 ? YMax : YMin);
+  if (cross_z) add(dd::z > 0 ? ZMax : ZMin);
+  return T(C(out) - bounce_correction<L, A, C>(C(wx), C(wy), C(wz)));
+}
+
+// Store direction A's VX outputs of this thread.
+template <class L, int A, typename T, typename C, int VX>
+__device__ __forceinline__ void push_dir(const Dom& d, T* __restrict__ f,
+                                         const RowGeom& g, int64_t fi, int i0,
+                                         bool seg_start, bool seg_end,
+                                         const T (&o)[VX]) {
+  using dd = Dir<L, A>;
+  T* fa = f + A * d.fstride;
+  int64_t dr = 0;
+  bool by = false, bz = false;
+  if constexpr (dd::y == 1) { dr += g.dyp; by = g.byp; }
+  if constexpr (dd::y == -1) { dr += g.dym; by = g.bym; }
+  if constexpr (dd::z == 1) { dr += g.dzp; bz = g.bzp; }
+  if constexpr (dd::z == -1) { dr += g.dzm; bz = g.bzm; }
+  const unsigned lane = threadIdx.x & 31u;
+
+  if constexpr (dd::x == 0) {
+    if (i0 < 0) return;  // inactive lane
+    if (by || bz) {
+      T b[VX];
+#pragma unroll
+      for (int v = 0; v < VX; ++v) b[v] = bounce_value<L, A, T, C>(d, o[v], false, by, bz);
+      Vec<T>::st(f + dd::opp * d.fstride + fi, b);
+    } else {
+      Vec<T>::st(fa + fi + dr, o);
+    }
+    return;
+  } else {
+    // x-shifted push. Shuffles run on every lane of the warp (inactive
+    // lanes carry dummies and store nothing).
+    T carry;
+    if constexpr (dd::x == 1) carry = __shfl_up_sync(0xffffffffu, o[VX - 1], 1);
+    else carry = __shfl_down_sync(0xffffffffu, o[0], 1);
+    if (i0 < 0) return;  // inactive lane
+    if (by || bz) {
+      // the whole row segment bounces (y/z wall); x edges may add their face
+      T b[VX];
+#pragma unroll
+      for (int v = 0; v < VX; ++v) {
+        const int x = i0 + v;
+        const bool cx = dd::x == 1 ? (x == d.nx - 1 && g.xwall_hi) : (x == 0 && g.xwall_lo);
+        b[v] = bounce_value<L, A, T, C>(d, o[v], cx, by, bz);
+      }
+      Vec<T>::st(f + dd::opp * d.fstride + fi, b);
+      return;
+    }
+    T* base = fa + fi + dr;  // aligned slot of this thread's first node
+    if constexpr (dd::x == 1) {
+      // targets x0+1 .. x0+VX; aligned vector [x0 .. x0+VX-1] needs x0-1
+      if (!seg_start) {
+        T v[VX];
+        v[0] = carry;
+#pragma unroll
+        for (int e = 1; e < VX; ++e) v[e] = o[e - 1];
+        Vec<T>::st(base, v);
+      } else {
+#pragma unroll
+        for (int e = 1; e < VX; ++e) base[e] = o[e - 1];
+      }
+      if (seg_end) {
+        const int x = i0 + VX;  // target of the last node
+        if (x < d.nx) {
+          base[VX] = o[VX - 1];
+        } else if (g.xwall_hi) {
+          f[dd::opp * d.fstride + fi + VX - 1] =
+              bounce_value<L, A, T, C>(d, o[VX - 1], true, false, false);
+        } else {
+          base[VX - d.nx] = o[VX - 1];  // periodic wrap to x = 0
+        }
+      }
+    } else {
+      // targets x0-1 .. x0+VX-2; aligned vector needs x0+VX from lane+1
+      if (!seg_end) {
+        T v[VX];
+#pragma unroll
+        for (int e = 0; e < VX - 1; ++e) v[e] = o[e + 1];
+        v[VX - 1] = carry;
+        Vec<T>::st(base, v);
+      } else {
+#pragma unroll
+        for (int e = 0; e < VX - 1; ++e) base[e] = o[e + 1];
+      }
+      if (seg_start) {
+        if (i0 > 0) {
+          base[-1] = o[0];
+        } else if (g.xwall_lo) {
+          f[dd::opp * d.fstride + fi] = bounce_value<L, A, T, C>(d, o[0], true, false, false);
+        } else {
+          base[d.nx - 1] = o[0];  // periodic wrap to x = nx-1
+        }
+      }
+    }
+    (void)lane;
+  }
+}
+
+// All q directions of this thread's VX nodes. EXACT selects the reference
+// evaluation order (only needed if some rho is -0.0, see header).
+template <class L, typename T, typename C, int VX, bool EXACT>
+__device__ __forceinline__ void all_dirs(const Dom& d, T* __restrict__ f,
+                                         const RowGeom& g, int64_t fi, int i0,
+                                         bool active, bool seg_start,
+                                         bool seg_end,
+                                         const NodeMoments<C> (&m)[VX], C om1) {
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    if constexpr (a == 0) {
+      T o[VX];
+#pragma unroll
+      for (int x = 0; x < VX; ++x)
+        o[x] = EXACT ? T(post_collision<L, 0, C>(m[x], om1)) : T(post_rest<L, C>(m[x], om1));
+      if (active) push_dir<L, 0, T, C, VX>(d, f, g, fi, i0, seg_start, seg_end, o);
+    } else if constexpr (a & 1) {
+      T oa[VX], ob[VX];
+#pragma unroll
+      for (int x = 0; x < VX; ++x) {
+        if constexpr (EXACT) {
+          oa[x] = T(post_collision<L, a, C>(m[x], om1));
+          ob[x] = T(post_collision<L, a + 1, C>(m[x], om1));
+        } else {
+          C ra, rb;
+          post_pair<L, a, C>(m[x], om1, ra, rb);
+          oa[x] = T(ra);
+          ob[x] = T(rb);
+        }
+      }
+      push_dir<L, a, T, C, VX>(d, f, g, fi, i0, seg_start, seg_end, oa);
+      push_dir<L, a + 1, T, C, VX>(d, f, g, fi, i0, seg_start, seg_end, ob);
+    }
+  });
+}
+
+template <class L, typename T, typename C>
+__global__ void __launch_bounds__(BXV)
+    k_streamcoll_vec(Dom d, T* __restrict__ f, const T* __restrict__ mo, C om1) {
+  constexpr int VX = Vec<T>::N;
+  const unsigned bid = blockIdx.x;
+  const unsigned row = bid / unsigned(d.xblocks);
+  const unsigned xb = bid - row * unsigned(d.xblocks);
+  const int j = int(row % unsigned(d.ny));
+  const int k = int(row / unsigned(d.ny)) + d.k0;
+  int i0 = int((xb * BXV + threadIdx.x) * VX);
+  const bool active = i0 < d.nx;
+  // active lanes form a prefix of the warp (rows never share a warp)
+  const unsigned amask = __ballot_sync(0xffffffffu, active);
+  const unsigned lane = threadIdx.x & 31u;
+  const bool seg_start = lane == 0;
+  const bool seg_end = active && (lane == 31u || !((amask >> (lane + 1)) & 1u));
+  const int64_t mi = int64_t(d.nx) * (int64_t(j) + int64_t(d.ny) * k) + (active ? i0 : 0);
+  const int64_t fi = mi + int64_t(d.ghost) * d.plane;
+  if (!active) i0 = -1;
+
+  NodeMoments<C> m[VX];
+  if (active) {
+    load_moments_vec<L, T, C, VX>(d, mo, mi, m);
+  } else {
+#pragma unroll
+    for (int x = 0; x < VX; ++x)
+      m[x] = prepare_node<C>(C(1), C(0), C(0), C(0), C(0), C(0), C(0), C(0), C(0), C(0));
+  }
+  bool exact = false;  // rho == -0.0 anywhere: fall back to reference order
+#pragma unroll
+  for (int x = 0; x < VX; ++x) exact |= (m[x].rho == C(0)) && signbit(m[x].rho);
+  const RowGeom g = row_geom(d, j, k);
+
+  if (__any_sync(0xffffffffu, exact))
+    all_dirs<L, T, C, VX, true>(d, f, g, fi, i0, active, seg_start, seg_end, m, om1);
+  else
+    all_dirs<L, T, C, VX, false>(d, f, g, fi, i0, active, seg_start, seg_end, m, om1);
+}
+
+template <typename T>
+int launch_streamcoll_vec(int lat, int math, const Dom& d0, T* f, const T* mo,
+                          double omega, cudaStream_t st) {
+  constexpr int VX = Vec<T>::N;
+  Dom d = d0;
+  d.xblocks = (d.nx / VX + BXV - 1) / BXV;
+  const dim3 grid(unsigned(int64_t(d.xblocks) * d.ny * d.nzr));
+  const double om1d = 1.0 - double(T(omega));
+  const float om1f = 1.0f - float(omega);
+  auto go = [&](auto L) {
+    using Lat = decltype(L);
+    if (math == kMathDouble)
+      k_streamcoll_vec<Lat, T, double><<<grid, BXV, 0, st>>>(d, f, mo, om1d);
+    else
+      k_streamcoll_vec<Lat, T, float><<<grid, BXV, 0, st>>>(d, f, mo, om1f);
+  };
+  switch (lat) {
+    case kD2Q9: go(D2Q9{}); return 0;
+    case kD3Q19: go(D3Q19{}); return 0;
+    case kD3Q27: go(D3Q27{}); return 0;
+    default: return 1;
+  }
+}
+
+template int launch_streamcoll_vec<float>(int, int, const Dom&, float*, const float*, double, cudaStream_t);
+template int launch_streamcoll_vec<double>(int, int, const Dom&, double*, const double*, double, cudaStream_t);
+
+}  // namespace tslb_cuda

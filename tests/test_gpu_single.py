@@ -30,6 +30,8 @@ CASES_3D = [
     ("box+random", (10, 9, 8), O.closed_box(), random_solid((10, 9, 8), 0.08, 7)),
     ("periodic+block", (12, 10, 9), O.periodic(), block_solid((12, 10, 9), (3, 2, 2), (7, 6, 5))),
     ("wide-x", (200, 4, 3), zwalls_3d(), None),
+    ("multi-block-x-box", (1040, 3, 3), corner_box_3d(), None),
+    ("multi-block-x-zwalls", (1032, 2, 3), zwalls_3d(), None),
 ]
 
 
@@ -104,6 +106,27 @@ def test_phases_bitwise(gpu, oracle_port, lat, case, dtype, mode, phase):
     assert_bitwise(fg, fo, f"{phase} f", fluid)
     if mode in (1, 2):
         assert_bitwise(mg, mo, f"{phase} moments", fluid)
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("lat,case", [("d2q9", CASES_2D[2]), ("d3q19", CASES_3D[1]), ("d3q19", CASES_3D[7])])
+def test_signed_zero_moments_bitwise(gpu, oracle_port, lat, case, dtype):
+    """stream_collide on user-written moments with rho = -0.0 / +0.0 and zero
+    stress: the vectorised kernel must fall back to the reference order."""
+    name, dims, faces, solid = case
+    n = int(np.prod(dims))
+    nm = O.moments_layout(lat)
+    m0 = np.random.default_rng(9).uniform(-0.01, 0.01, (nm, n)).astype(dtype)
+    m0[0] += 1
+    m0[0, ::7] = -0.0
+    m0[0, 3::11] = 0.0
+    m0[:, 5::13] = 0.0
+    m0[1:, 6::17] = -0.0
+    f0 = O.random_state(lat, dims, 1, dtype)
+    fo, mo = f0.copy(), m0.copy()
+    oracle_port.single_run(lat, dims, 1.2, faces, fo, mo, 1, 3)
+    fg, _ = _gpu_single(lat, dims, 1.2, faces, f0, 1, None, "stream_collide", m0)
+    assert_bitwise(fg, fo, "f")
 
 
 @pytest.mark.parametrize("lat,case", [("d2q9", c) for c in CASES_2D] + [("d3q19", c) for c in CASES_3D]
