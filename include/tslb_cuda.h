@@ -124,7 +124,8 @@ int tslb_cuda_set_math(tslb_cuda_handle h, int math);
 int tslb_cuda_describe(tslb_cuda_handle h, int* dims, int* info);
 int tslb_cuda_memory_bytes(tslb_cuda_handle h, uint64_t* bytes);
 
-/* populations: species 0 = f (or fr), 1 = fb; q * n_local scalars */
+/* populations: species 0 = f (or fr), 1 = fb, 2 = the second buffer of
+ * reference_step / stream_only (single fluid); q * n_local scalars */
 int tslb_cuda_upload_f(tslb_cuda_handle h, int species, const void* host);
 int tslb_cuda_download_f(tslb_cuda_handle h, int species, void* host);
 int tslb_cuda_upload_field(tslb_cuda_handle h, int field, const void* host);

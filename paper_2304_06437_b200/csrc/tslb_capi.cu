@@ -101,6 +101,8 @@ struct tslb_cuda_sim {
   int device = 0;
   int math = kMathDouble;
   bool vec_ok = true;  // vectorised stream-collide allowed (TSLB_STREAMCOLL=scalar disables)
+  int vx = 0;          // nodes per thread in the vectorised kernel (0 = default; TSLB_VX)
+  bool staged = false; // slab halos received into staging + masked unpack
   double omega = 1.0;
   int kinds[6] = {0, 0, 0, 0, 0, 0};
   ColorParamsDev cp{};
@@ -235,11 +237,10 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
   ++h->launches;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
-    constexpr int VX = 16 / sizeof(T);
-    if (h->vec_ok && !h->d.has_solid && h->nx % VX == 0)
-      return launch_streamcoll_vec<T>(h->lat, h->math, h->range(k0, k1),
-                                      static_cast<T*>(h->f[0]), static_cast<const T*>(h->mo),
-                                      h->omega, st);
+    if (h->vec_ok && !h->d.has_solid &&
+        launch_streamcoll_vec<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
+                                 static_cast<const T*>(h->mo), h->omega, h->vx, st) == 0)
+      return 0;
     return launch_streamcoll<T>(h->lat, h->math, h->range(k0, k1),
                                 static_cast<T*>(h->f[0]), static_cast<const T*>(h->mo),
                                 h->solid, h->slow, h->omega, st);
@@ -298,7 +299,7 @@ void* plane_ptr(const tslb_cuda_sim* h, int a, int k) {
 
 // destination for a received plane: in place, or the staging buffer
 void* recv_ptr(const tslb_cuda_sim* h, bool from_below, int e, int a) {
-  if (h->d.has_solid) {
+  if (h->staged) {
     void* base = from_below ? h->recv_lo : h->recv_hi;
     return static_cast<char*>(base) + size_t(e) * h->plane() * h->esz;
   }
@@ -306,7 +307,7 @@ void* recv_ptr(const tslb_cuda_sim* h, bool from_below, int e, int a) {
 }
 
 int unpack(tslb_cuda_sim* h, cudaStream_t st) {
-  if (!h->d.has_solid) return 0;
+  if (!h->staged) return 0;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
     if (h->d.mode[ZMin] == kGhost) {
@@ -469,6 +470,7 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   h->device = device;
   h->omega = omega;
   if (const char* e = std::getenv("TSLB_STREAMCOLL")) h->vec_ok = std::strcmp(e, "scalar") != 0;
+  if (const char* e = std::getenv("TSLB_VX")) h->vx = std::atoi(e);
   std::memcpy(h->kinds, kinds, sizeof h->kinds);
   if (color) {
     h->cp.sigma = color[0];
@@ -568,7 +570,11 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
     // box geometry: every non-solid node is fluid
     h->n_fluid = uint64_t(d.n);
   }
-  if (decomposed && d.has_solid) {
+  // A ghost-plane slot is written by the neighbour only if its source node is
+  // fluid and the push did not cross an x/y wall; with solids or x/y walls
+  // the received planes are staged and unpacked under that mask.
+  h->staged = decomposed && (d.has_solid || d.mode[XMin] == kWall || d.mode[YMin] == kWall);
+  if (h->staged) {
     const size_t pb = size_t(d.plane) * 9 * h->esz;
     if ((rc = alloc(h, &h->recv_lo, pb))) return fail(rc);
     if ((rc = alloc(h, &h->recv_hi, pb))) return fail(rc);
@@ -584,6 +590,29 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
 int sync(tslb_cuda_sim* h) {
   CK(cudaStreamSynchronize(h->s));
   CK(cudaGetLastError());
+  return 0;
+}
+
+// Second population buffer of the two-buffer reference step / stream_only
+// (the reference's `scratch`, kernels.hpp:219-291). Created on first use as a
+// copy of f, like `auto scratch = b.f` in the reference tests.
+int ensure_scratch(tslb_cuda_sim* h) {
+  if (h->scratch) return 0;
+  const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
+  if (int rc = alloc(h, &h->scratch, fbytes)) return rc;
+  CK(cudaMemcpyAsync(h->scratch, h->f[0], fbytes, cudaMemcpyDeviceToDevice, h->s));
+  return 0;
+}
+
+// base of population species 0/1 (f / fr, fb) or 2 (scratch buffer)
+int species_base(tslb_cuda_sim* h, int species, char** base) {
+  if (species == 2 && h->comps == 1 && !h->decomposed) {
+    if (int rc = ensure_scratch(h)) return rc;
+    *base = static_cast<char*>(h->scratch);
+    return 0;
+  }
+  if (species < 0 || species >= h->comps) return set_err(TSLB_EINVAL, "bad species %d", species);
+  *base = static_cast<char*>(h->f[species]);
   return 0;
 }
 
@@ -669,26 +698,28 @@ int tslb_cuda_memory_bytes(tslb_cuda_handle h, uint64_t* bytes) {
 }
 
 int tslb_cuda_upload_f(tslb_cuda_handle h, int species, const void* host) {
-  if (species < 0 || species >= h->comps) return set_err(TSLB_EINVAL, "bad species");
   CK(cudaSetDevice(h->device));
+  char* base;
+  if (int rc = species_base(h, species, &base)) return rc;
   const size_t pb = size_t(h->n()) * h->esz;
+  const size_t off = size_t(h->d.ghost * h->plane()) * h->esz;
   for (int a = 0; a < h->q; ++a)
-    CK(cudaMemcpyAsync(static_cast<char*>(h->fa(species, a)) +
-                           size_t(h->d.ghost * h->plane()) * h->esz,
+    CK(cudaMemcpyAsync(base + size_t(a) * h->d.fstride * h->esz + off,
                        static_cast<const char*>(host) + a * pb, pb,
                        cudaMemcpyHostToDevice, h->s));
   return sync(h);
 }
 
 int tslb_cuda_download_f(tslb_cuda_handle h, int species, void* host) {
-  if (species < 0 || species >= h->comps) return set_err(TSLB_EINVAL, "bad species");
   CK(cudaSetDevice(h->device));
+  char* base;
+  if (int rc = species_base(h, species, &base)) return rc;
   const size_t pb = size_t(h->n()) * h->esz;
+  const size_t off = size_t(h->d.ghost * h->plane()) * h->esz;
   for (int a = 0; a < h->q; ++a)
     CK(cudaMemcpyAsync(static_cast<char*>(host) + a * pb,
-                       static_cast<const char*>(h->fa(species, a)) +
-                           size_t(h->d.ghost * h->plane()) * h->esz,
-                       pb, cudaMemcpyDeviceToHost, h->s));
+                       base + size_t(a) * h->d.fstride * h->esz + off, pb,
+                       cudaMemcpyDeviceToHost, h->s));
   return sync(h);
 }
 
@@ -857,16 +888,6 @@ int tslb_cuda_stream_collide(tslb_cuda_handle h) {
   return sync(h);
 }
 
-namespace {
-int ensure_scratch(tslb_cuda_sim* h) {
-  if (h->scratch) return 0;
-  const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
-  if (int rc = alloc(h, &h->scratch, fbytes)) return rc;
-  CK(cudaMemcpyAsync(h->scratch, h->f[0], fbytes, cudaMemcpyDeviceToDevice, h->s));
-  return 0;
-}
-}  // namespace
-
 int tslb_cuda_reference_step(tslb_cuda_handle h, long nsteps) {
   if (h->comps != 1 || h->decomposed)
     return set_err(TSLB_EINVAL, "reference_step: single-fluid, single domain only");
@@ -894,9 +915,9 @@ int tslb_cuda_stream_only(tslb_cuda_handle h) {
   if (h->comps != 1 || h->decomposed)
     return set_err(TSLB_EINVAL, "stream_only: single-fluid, single domain only");
   CK(cudaSetDevice(h->device));
+  // pushes f into the second buffer (its slots not reached by any push keep
+  // their contents, as in the reference), then swaps the two
   if (int rc = ensure_scratch(h)) return rc;
-  const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
-  CK(cudaMemsetAsync(h->scratch, 0, fbytes, h->s));
   ++h->launches;
   int rc = by_scalar(h, [&](auto z) {
     using T = decltype(z);

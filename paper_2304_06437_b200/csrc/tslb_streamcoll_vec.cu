@@ -25,30 +25,24 @@
 
 namespace tslb_cuda {
 
-template <typename T>
-struct Vec;
-template <>
-struct Vec<float> {
-  static constexpr int N = 4;
-  using V = float4;
-  __device__ static V ld(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-  __device__ static void st(float* p, const float (&v)[4]) {
-    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
-  }
-  __device__ static void unpack(const V& v, float (&o)[4]) {
-    o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
-  }
+// VX consecutive scalars moved as one aligned access of VX * sizeof(T) bytes
+template <typename T, int VX>
+struct alignas(sizeof(T) * VX) Pack {
+  T v[VX];
 };
-template <>
-struct Vec<double> {
-  static constexpr int N = 2;
-  using V = double2;
-  __device__ static V ld(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
-  __device__ static void st(double* p, const double (&v)[2]) {
-    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+
+template <typename T, int VX>
+struct Vec {
+  __device__ static void load(const T* p, T (&o)[VX]) {
+    const Pack<T, VX> pk = *reinterpret_cast<const Pack<T, VX>*>(p);
+#pragma unroll
+    for (int e = 0; e < VX; ++e) o[e] = pk.v[e];
   }
-  __device__ static void unpack(const V& v, double (&o)[2]) {
-    o[0] = v.x; o[1] = v.y;
+  __device__ static void st(T* p, const T (&v)[VX]) {
+    Pack<T, VX> pk;
+#pragma unroll
+    for (int e = 0; e < VX; ++e) pk.v[e] = v[e];
+    *reinterpret_cast<Pack<T, VX>*>(p) = pk;
   }
 };
 
@@ -106,7 +100,7 @@ __device__ __forceinline__ void load_moments_vec(const Dom& d,
   constexpr int NM = 1 + L::dim + L::dim * (L::dim + 1) / 2;
   T v[NM][VX];
 #pragma unroll
-  for (int c = 0; c < NM; ++c) Vec<T>::unpack(Vec<T>::ld(mo + c * d.mstride + mi), v[c]);
+  for (int c = 0; c < NM; ++c) Vec<T, VX>::load(mo + c * d.mstride + mi, v[c]);
 #pragma unroll
   for (int x = 0; x < VX; ++x) {
     if constexpr (L::dim == 3)
@@ -193,9 +187,9 @@ __device__ __forceinline__ void push_dir(const Dom& d, T* __restrict__ f,
       T b[VX];
 #pragma unroll
       for (int v = 0; v < VX; ++v) b[v] = bounce_value<L, A, T, C>(d, o[v], false, by, bz);
-      Vec<T>::st(f + dd::opp * d.fstride + fi, b);
+      Vec<T, VX>::st(f + dd::opp * d.fstride + fi, b);
     } else {
-      Vec<T>::st(fa + fi + dr, o);
+      Vec<T, VX>::st(fa + fi + dr, o);
     }
     return;
   } else {
@@ -214,7 +208,7 @@ __device__ __forceinline__ void push_dir(const Dom& d, T* __restrict__ f,
         const bool cx = dd::x == 1 ? (x == d.nx - 1 && g.xwall_hi) : (x == 0 && g.xwall_lo);
         b[v] = bounce_value<L, A, T, C>(d, o[v], cx, by, bz);
       }
-      Vec<T>::st(f + dd::opp * d.fstride + fi, b);
+      Vec<T, VX>::st(f + dd::opp * d.fstride + fi, b);
       return;
     }
     T* base = fa + fi + dr;  // aligned slot of this thread's first node
@@ -225,7 +219,7 @@ __device__ __forceinline__ void push_dir(const Dom& d, T* __restrict__ f,
         v[0] = carry;
 #pragma unroll
         for (int e = 1; e < VX; ++e) v[e] = o[e - 1];
-        Vec<T>::st(base, v);
+        Vec<T, VX>::st(base, v);
       } else {
 #pragma unroll
         for (int e = 1; e < VX; ++e) base[e] = o[e - 1];
@@ -248,7 +242,7 @@ __device__ __forceinline__ void push_dir(const Dom& d, T* __restrict__ f,
 #pragma unroll
         for (int e = 0; e < VX - 1; ++e) v[e] = o[e + 1];
         v[VX - 1] = carry;
-        Vec<T>::st(base, v);
+        Vec<T, VX>::st(base, v);
       } else {
 #pragma unroll
         for (int e = 0; e < VX - 1; ++e) base[e] = o[e + 1];
@@ -303,10 +297,9 @@ __device__ __forceinline__ void all_dirs(const Dom& d, T* __restrict__ f,
   });
 }
 
-template <class L, typename T, typename C>
+template <class L, typename T, typename C, int VX>
 __global__ void __launch_bounds__(BXV)
     k_streamcoll_vec(Dom d, T* __restrict__ f, const T* __restrict__ mo, C om1) {
-  constexpr int VX = Vec<T>::N;
   const unsigned bid = blockIdx.x;
   const unsigned row = bid / unsigned(d.xblocks);
   const unsigned xb = bid - row * unsigned(d.xblocks);
@@ -342,31 +335,43 @@ __global__ void __launch_bounds__(BXV)
     all_dirs<L, T, C, VX, false>(d, f, g, fi, i0, active, seg_start, seg_end, m, om1);
 }
 
+// vx: elements per thread (1, 2 or 4 for float; 1 or 2 for double);
+// 0 picks the default (full 16-byte vectors for fp32 node math, 8-byte for
+// fp64 node math, whose register footprint per node is twice as large).
 template <typename T>
 int launch_streamcoll_vec(int lat, int math, const Dom& d0, T* f, const T* mo,
-                          double omega, cudaStream_t st) {
-  constexpr int VX = Vec<T>::N;
-  Dom d = d0;
-  d.xblocks = (d.nx / VX + BXV - 1) / BXV;
-  const dim3 grid(unsigned(int64_t(d.xblocks) * d.ny * d.nzr));
+                          double omega, int vx, cudaStream_t st) {
+  if (vx == 0) vx = math == kMathDouble ? 8 / int(sizeof(T)) : 16 / int(sizeof(T));
+  if (vx * int(sizeof(T)) > 16 || d0.nx % vx != 0) return 1;
   const double om1d = 1.0 - double(T(omega));
   const float om1f = 1.0f - float(omega);
-  auto go = [&](auto L) {
+  auto go = [&](auto L, auto V) {
     using Lat = decltype(L);
-    if (math == kMathDouble)
-      k_streamcoll_vec<Lat, T, double><<<grid, BXV, 0, st>>>(d, f, mo, om1d);
-    else
-      k_streamcoll_vec<Lat, T, float><<<grid, BXV, 0, st>>>(d, f, mo, om1f);
+    constexpr int VX = decltype(V)::value;
+    if constexpr (VX * sizeof(T) <= 16) {
+      Dom d = d0;
+      d.xblocks = (d.nx / VX + BXV - 1) / BXV;
+      const dim3 grid(unsigned(int64_t(d.xblocks) * d.ny * d.nzr));
+      if (math == kMathDouble)
+        k_streamcoll_vec<Lat, T, double, VX><<<grid, BXV, 0, st>>>(d, f, mo, om1d);
+      else
+        k_streamcoll_vec<Lat, T, float, VX><<<grid, BXV, 0, st>>>(d, f, mo, om1f);
+    }
+  };
+  auto by_vx = [&](auto L) {
+    if (vx == 1) go(L, std::integral_constant<int, 1>{});
+    else if (vx == 2) go(L, std::integral_constant<int, 2>{});
+    else go(L, std::integral_constant<int, 4>{});
   };
   switch (lat) {
-    case kD2Q9: go(D2Q9{}); return 0;
-    case kD3Q19: go(D3Q19{}); return 0;
-    case kD3Q27: go(D3Q27{}); return 0;
+    case kD2Q9: by_vx(D2Q9{}); return 0;
+    case kD3Q19: by_vx(D3Q19{}); return 0;
+    case kD3Q27: by_vx(D3Q27{}); return 0;
     default: return 1;
   }
 }
 
-template int launch_streamcoll_vec<float>(int, int, const Dom&, float*, const float*, double, cudaStream_t);
-template int launch_streamcoll_vec<double>(int, int, const Dom&, double*, const double*, double, cudaStream_t);
+template int launch_streamcoll_vec<float>(int, int, const Dom&, float*, const float*, double, int, cudaStream_t);
+template int launch_streamcoll_vec<double>(int, int, const Dom&, double*, const double*, double, int, cudaStream_t);
 
 }  // namespace tslb_cuda
