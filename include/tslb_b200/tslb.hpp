@@ -191,6 +191,80 @@ LatticeDescriptor<T> make_descriptor(LatticeKind kind) {
   return descriptor_of<D3Q19, T>();
 }
 
+struct ValidationReport {
+  struct Check {
+    std::string name;
+    double violation = 0.0;
+    bool pass = false;
+  };
+  std::vector<Check> checks;
+  double tolerance = 1e-14;
+  bool all_pass() const {
+    for (const auto& c : checks)
+      if (!c.pass) return false;
+    return true;
+  }
+};
+
+/// validate_moments (lattice.hpp:155-244): discrete moment and isotropy
+/// conditions of t and B, opposite map, trace of Q; failures reported.
+template <typename T>
+ValidationReport validate_moments(const LatticeDescriptor<T>& d, double tol = 1e-14) {
+  ValidationReport rep;
+  rep.tolerance = tol;
+  const int D = d.dim;
+  const double cs2 = double(d.cs2), cs4 = cs2 * cs2;
+  auto cc = [&](int a, int al) { return double(d.c(al, a)); };
+  // weighted moment of weights w over the product of the listed axes
+  auto moment = [&](const auto& w, std::initializer_list<int> axes) {
+    double s = 0.0;
+    for (int a = 0; a < d.q; ++a) {
+      double term = double(w(a));
+      for (int ax : axes) term *= cc(a, ax);
+      s += term;
+    }
+    return s;
+  };
+  auto add = [&](const char* name, double v) { rep.checks.push_back({name, v, v <= tol}); };
+  auto delta = [](int x, int y) { return x == y ? 1.0 : 0.0; };
+
+  add("sum t = 1", std::abs(moment(d.t, {}) - 1.0));
+  double v1 = 0, v2 = 0, v4 = 0, b1 = 0;
+  for (int al = 0; al < D; ++al) {
+    v1 = std::max(v1, std::abs(moment(d.t, {al})));
+    b1 = std::max(b1, std::abs(moment(d.b, {al})));
+    for (int be = 0; be < D; ++be) {
+      v2 = std::max(v2, std::abs(moment(d.t, {al, be}) - cs2 * delta(al, be)));
+      for (int ga = 0; ga < D; ++ga)
+        for (int de = 0; de < D; ++de) {
+          const double want = cs4 * (delta(al, be) * delta(ga, de) + delta(al, ga) * delta(be, de) +
+                                     delta(al, de) * delta(be, ga));
+          v4 = std::max(v4, std::abs(moment(d.t, {al, be, ga, de}) - want));
+        }
+    }
+  }
+  add("sum t c = 0", v1);
+  add("sum t cc = cs2 I", v2);
+  add("4th-order isotropy", v4);
+  double vo = 0;
+  for (int a = 0; a < d.q; ++a) {
+    const int o = d.opp(a);
+    if (o < 0 || o >= d.q || d.opp(o) != a) vo = 1.0;
+    else
+      for (int al = 0; al < 3; ++al) vo = std::max(vo, std::abs(cc(o, al) + cc(a, al)));
+  }
+  add("opp involution, c[opp] = -c", vo);
+  add("sum B = cs2", std::abs(moment(d.b, {}) - cs2));
+  add("sum B c = 0", b1);
+  double vq = 0;
+  for (int a = 0; a < d.q; ++a) {
+    const double tr = double(d.q2(0, a)) + double(d.q2(1, a)) + double(d.q2(2, a));
+    vq = std::max(vq, std::abs(tr - (cc(a, 0) * cc(a, 0) + cc(a, 1) * cc(a, 1) + cc(a, 2) * cc(a, 2) - D * cs2)));
+  }
+  add("trace Q = |c|^2 - D cs2", vq);
+  return rep;
+}
+
 inline const char* lattice_name(LatticeKind k) {
   return k == LatticeKind::D2Q9 ? "d2q9" : k == LatticeKind::D3Q19 ? "d3q19" : "d3q27";
 }
@@ -255,7 +329,7 @@ struct TwoFluidFieldSet {
 namespace detail {
 template <typename T>
 std::vector<FieldArray<T>> zero_arrays(int count, Eigen::Index n) {
-  std::vector<FieldArray<T>> v(std::size_t(count));
+  std::vector<FieldArray<T>> v(static_cast<std::size_t>(count));
   for (auto& a : v) a = FieldArray<T>::Zero(n);
   return v;
 }

@@ -165,8 +165,9 @@ __device__ __forceinline__ T bounce_value(const Dom& d, T out, bool cross_x,
   return T(C(out) - bounce_correction<L, A, C>(C(wx), C(wy), C(wz)));
 }
 
-// Store direction A's VX outputs of this thread.
-template <class L, int A, typename T, typename C, int VX>
+// Store direction A's VX outputs of this thread. WALLS = false compiles out
+// every bounce path (all faces periodic or slab ghosts).
+template <class L, int A, typename T, typename C, int VX, bool WALLS>
 __device__ __forceinline__ void push_dir(const Dom& d, T* __restrict__ f,
                                          const RowGeom& g, int64_t fi, int i0,
                                          bool seg_start, bool seg_end,
@@ -179,19 +180,19 @@ __device__ __forceinline__ void push_dir(const Dom& d, T* __restrict__ f,
   if constexpr (dd::y == -1) { dr += g.dym; by = g.bym; }
   if constexpr (dd::z == 1) { dr += g.dzp; bz = g.bzp; }
   if constexpr (dd::z == -1) { dr += g.dzm; bz = g.bzm; }
-  const unsigned lane = threadIdx.x & 31u;
 
   if constexpr (dd::x == 0) {
     if (i0 < 0) return;  // inactive lane
-    if (by || bz) {
-      T b[VX];
+    if constexpr (WALLS) {
+      if (by || bz) {
+        T b[VX];
 #pragma unroll
-      for (int v = 0; v < VX; ++v) b[v] = bounce_value<L, A, T, C>(d, o[v], false, by, bz);
-      Vec<T, VX>::st(f + dd::opp * d.fstride + fi, b);
-    } else {
-      Vec<T, VX>::st(fa + fi + dr, o);
+        for (int v = 0; v < VX; ++v) b[v] = bounce_value<L, A, T, C>(d, o[v], false, by, bz);
+        Vec<T, VX>::st(f + dd::opp * d.fstride + fi, b);
+        return;
+      }
     }
-    return;
+    Vec<T, VX>::st(fa + fi + dr, o);
   } else {
     // x-shifted push. Shuffles run on every lane of the warp (inactive
     // lanes carry dummies and store nothing).
@@ -199,17 +200,19 @@ __device__ __forceinline__ void push_dir(const Dom& d, T* __restrict__ f,
     if constexpr (dd::x == 1) carry = __shfl_up_sync(0xffffffffu, o[VX - 1], 1);
     else carry = __shfl_down_sync(0xffffffffu, o[0], 1);
     if (i0 < 0) return;  // inactive lane
-    if (by || bz) {
-      // the whole row segment bounces (y/z wall); x edges may add their face
-      T b[VX];
+    if constexpr (WALLS) {
+      if (by || bz) {
+        // the whole row segment bounces (y/z wall); x edges may add their face
+        T b[VX];
 #pragma unroll
-      for (int v = 0; v < VX; ++v) {
-        const int x = i0 + v;
-        const bool cx = dd::x == 1 ? (x == d.nx - 1 && g.xwall_hi) : (x == 0 && g.xwall_lo);
-        b[v] = bounce_value<L, A, T, C>(d, o[v], cx, by, bz);
+        for (int v = 0; v < VX; ++v) {
+          const int x = i0 + v;
+          const bool cx = dd::x == 1 ? (x == d.nx - 1 && g.xwall_hi) : (x == 0 && g.xwall_lo);
+          b[v] = bounce_value<L, A, T, C>(d, o[v], cx, by, bz);
+        }
+        Vec<T, VX>::st(f + dd::opp * d.fstride + fi, b);
+        return;
       }
-      Vec<T, VX>::st(f + dd::opp * d.fstride + fi, b);
-      return;
     }
     T* base = fa + fi + dr;  // aligned slot of this thread's first node
     if constexpr (dd::x == 1) {
@@ -228,7 +231,7 @@ __device__ __forceinline__ void push_dir(const Dom& d, T* __restrict__ f,
         const int x = i0 + VX;  // target of the last node
         if (x < d.nx) {
           base[VX] = o[VX - 1];
-        } else if (g.xwall_hi) {
+        } else if (WALLS && g.xwall_hi) {
           f[dd::opp * d.fstride + fi + VX - 1] =
               bounce_value<L, A, T, C>(d, o[VX - 1], true, false, false);
         } else {
@@ -250,20 +253,19 @@ __device__ __forceinline__ void push_dir(const Dom& d, T* __restrict__ f,
       if (seg_start) {
         if (i0 > 0) {
           base[-1] = o[0];
-        } else if (g.xwall_lo) {
+        } else if (WALLS && g.xwall_lo) {
           f[dd::opp * d.fstride + fi] = bounce_value<L, A, T, C>(d, o[0], true, false, false);
         } else {
           base[d.nx - 1] = o[0];  // periodic wrap to x = nx-1
         }
       }
     }
-    (void)lane;
   }
 }
 
 // All q directions of this thread's VX nodes. EXACT selects the reference
 // evaluation order (only needed if some rho is -0.0, see header).
-template <class L, typename T, typename C, int VX, bool EXACT>
+template <class L, typename T, typename C, int VX, bool WALLS, bool EXACT>
 __device__ __forceinline__ void all_dirs(const Dom& d, T* __restrict__ f,
                                          const RowGeom& g, int64_t fi, int i0,
                                          bool active, bool seg_start,
@@ -276,7 +278,7 @@ __device__ __forceinline__ void all_dirs(const Dom& d, T* __restrict__ f,
 #pragma unroll
       for (int x = 0; x < VX; ++x)
         o[x] = EXACT ? T(post_collision<L, 0, C>(m[x], om1)) : T(post_rest<L, C>(m[x], om1));
-      if (active) push_dir<L, 0, T, C, VX>(d, f, g, fi, i0, seg_start, seg_end, o);
+      if (active) push_dir<L, 0, T, C, VX, WALLS>(d, f, g, fi, i0, seg_start, seg_end, o);
     } else if constexpr (a & 1) {
       T oa[VX], ob[VX];
 #pragma unroll
@@ -291,13 +293,31 @@ __device__ __forceinline__ void all_dirs(const Dom& d, T* __restrict__ f,
           ob[x] = T(rb);
         }
       }
-      push_dir<L, a, T, C, VX>(d, f, g, fi, i0, seg_start, seg_end, oa);
-      push_dir<L, a + 1, T, C, VX>(d, f, g, fi, i0, seg_start, seg_end, ob);
+      push_dir<L, a, T, C, VX, WALLS>(d, f, g, fi, i0, seg_start, seg_end, oa);
+      push_dir<L, a + 1, T, C, VX, WALLS>(d, f, g, fi, i0, seg_start, seg_end, ob);
     }
   });
 }
 
-template <class L, typename T, typename C, int VX>
+// Reference-order path, outlined so it stays out of the hot instruction
+// stream (taken only when some rho == -0.0, i.e. user-written moments).
+template <class L, typename T, typename C, int VX, bool WALLS>
+// Everything is passed by value and the moments are reloaded, so the hot
+// path never spills its registers to set up this call.
+__device__ __noinline__ void all_dirs_exact(Dom d, T* f, const T* mo, RowGeom g, int64_t mi, int64_t fi,
+                                            int i0, bool active, bool seg_start, bool seg_end, C om1) {
+  NodeMoments<C> m[VX];
+  if (active) {
+    load_moments_vec<L, T, C, VX>(d, mo, mi, m);
+  } else {
+#pragma unroll
+    for (int x = 0; x < VX; ++x)
+      m[x] = prepare_node<C>(C(1), C(0), C(0), C(0), C(0), C(0), C(0), C(0), C(0), C(0));
+  }
+  all_dirs<L, T, C, VX, WALLS, true>(d, f, g, fi, i0, active, seg_start, seg_end, m, om1);
+}
+
+template <class L, typename T, typename C, int VX, bool WALLS>
 __global__ void __launch_bounds__(BXV)
     k_streamcoll_vec(Dom d, T* __restrict__ f, const T* __restrict__ mo, C om1) {
   const unsigned bid = blockIdx.x;
@@ -330,9 +350,9 @@ __global__ void __launch_bounds__(BXV)
   const RowGeom g = row_geom(d, j, k);
 
   if (__any_sync(0xffffffffu, exact))
-    all_dirs<L, T, C, VX, true>(d, f, g, fi, i0, active, seg_start, seg_end, m, om1);
+    all_dirs_exact<L, T, C, VX, WALLS>(d, f, mo, g, mi, fi, i0, active, seg_start, seg_end, om1);
   else
-    all_dirs<L, T, C, VX, false>(d, f, g, fi, i0, active, seg_start, seg_end, m, om1);
+    all_dirs<L, T, C, VX, WALLS, false>(d, f, g, fi, i0, active, seg_start, seg_end, m, om1);
 }
 
 // vx: elements per thread (1, 2 or 4 for float; 1 or 2 for double);
@@ -352,10 +372,15 @@ int launch_streamcoll_vec(int lat, int math, const Dom& d0, T* f, const T* mo,
       Dom d = d0;
       d.xblocks = (d.nx / VX + BXV - 1) / BXV;
       const dim3 grid(unsigned(int64_t(d.xblocks) * d.ny * d.nzr));
-      if (math == kMathDouble)
-        k_streamcoll_vec<Lat, T, double, VX><<<grid, BXV, 0, st>>>(d, f, mo, om1d);
-      else
-        k_streamcoll_vec<Lat, T, float, VX><<<grid, BXV, 0, st>>>(d, f, mo, om1f);
+      bool walls = false;
+      for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
+      if (math == kMathDouble) {
+        if (walls) k_streamcoll_vec<Lat, T, double, VX, true><<<grid, BXV, 0, st>>>(d, f, mo, om1d);
+        else k_streamcoll_vec<Lat, T, double, VX, false><<<grid, BXV, 0, st>>>(d, f, mo, om1d);
+      } else {
+        if (walls) k_streamcoll_vec<Lat, T, float, VX, true><<<grid, BXV, 0, st>>>(d, f, mo, om1f);
+        else k_streamcoll_vec<Lat, T, float, VX, false><<<grid, BXV, 0, st>>>(d, f, mo, om1f);
+      }
     }
   };
   auto by_vx = [&](auto L) {
