@@ -100,7 +100,9 @@ struct tslb_cuda_sim {
   bool decomposed = false;
   int device = 0;
   int math = kMathDouble;
-  bool vec_ok = true;  // vectorised stream-collide allowed (TSLB_STREAMCOLL=scalar disables)
+  // box-geometry stream-collide kernel: 0 scalar, 1 vectorised, 2 lean
+  // (TSLB_STREAMCOLL=scalar|vec|lean overrides the default)
+  int variant = 1;
   int vx = 0;          // nodes per thread in the vectorised kernel (0 = default; TSLB_VX)
   bool staged = false; // slab halos received into staging + masked unpack
   double omega = 1.0;
@@ -237,7 +239,10 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
   ++h->launches;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
-    if (h->vec_ok && !h->d.has_solid &&
+    if (h->variant == 2 && !h->d.has_solid)
+      return launch_streamcoll_lean<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
+                                       static_cast<const T*>(h->mo), h->omega, st);
+    if (h->variant == 1 && !h->d.has_solid &&
         launch_streamcoll_vec<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
                                  static_cast<const T*>(h->mo), h->omega, h->vx, st) == 0)
       return 0;
@@ -469,7 +474,8 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   h->decomposed = decomposed;
   h->device = device;
   h->omega = omega;
-  if (const char* e = std::getenv("TSLB_STREAMCOLL")) h->vec_ok = std::strcmp(e, "scalar") != 0;
+  if (const char* e = std::getenv("TSLB_STREAMCOLL"))
+    h->variant = !std::strcmp(e, "scalar") ? 0 : !std::strcmp(e, "lean") ? 2 : 1;
   if (const char* e = std::getenv("TSLB_VX")) h->vx = std::atoi(e);
   std::memcpy(h->kinds, kinds, sizeof h->kinds);
   if (color) {

@@ -34,17 +34,35 @@ struct Dom {
   int k0, nzr;           // launch range: planes [k0, k0 + nzr)
 };
 
-/// Row-tiled launch geometry: block (xb, row) covers nodes
-/// [xb*BX, xb*BX+BX) of row `row` = j + ny*k; returns false past the row end.
+/// Row-tiled launch grid: blocks (x block, row j, plane k) as a 3-D grid
+/// when ny and the plane range fit the grid limits (no index divisions in
+/// the kernel), else one flattened dimension.
+inline dim3 row_grid(const Dom& d) {
+  if (d.ny <= 65535 && d.nzr <= 65535) return dim3(unsigned(d.xblocks), unsigned(d.ny), unsigned(d.nzr));
+  return dim3(unsigned(int64_t(d.xblocks) * d.ny * d.nzr));
+}
+
+/// (x block, j, k) of this block for row_grid launches.
+__device__ __forceinline__ void row_block(const Dom& d, unsigned& xb, int& j, int& k) {
+  if (gridDim.y > 1 || gridDim.z > 1) {
+    xb = blockIdx.x;
+    j = int(blockIdx.y);
+    k = int(blockIdx.z) + d.k0;
+  } else {
+    const unsigned row = blockIdx.x / unsigned(d.xblocks);
+    xb = blockIdx.x - row * unsigned(d.xblocks);
+    j = int(row % unsigned(d.ny));
+    k = int(row / unsigned(d.ny)) + d.k0;
+  }
+}
+
+/// Row-tiled node coordinates: block (xb, j, k) covers nodes
+/// [xb*BX, xb*BX+BX) of row (j, k); returns false past the row end.
 template <int BX>
-__device__ __forceinline__ bool node_coords(const Dom& d, int& i, int& j,
-                                            int& k) {
-  const unsigned bid = blockIdx.x;
-  const unsigned row = bid / unsigned(d.xblocks);
-  const unsigned xb = bid - row * unsigned(d.xblocks);
+__device__ __forceinline__ bool node_coords(const Dom& d, int& i, int& j, int& k) {
+  unsigned xb;
+  row_block(d, xb, j, k);
   i = int(xb * BX + threadIdx.x);
-  j = int(row % unsigned(d.ny));
-  k = int(row / unsigned(d.ny)) + d.k0;
   return i < d.nx;
 }
 

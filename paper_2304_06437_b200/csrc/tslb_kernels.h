@@ -38,6 +38,10 @@ int launch_streamcoll(int lat, int math, const Dom& d, T* f, const T* mo,
 template <typename T>
 int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
                           double omega, int vx, cudaStream_t st);
+// box geometry, one node per thread, precomputed interior push offsets
+template <typename T>
+int launch_streamcoll_lean(int lat, int math, const Dom& d, T* f, const T* mo,
+                           double omega, cudaStream_t st);
 template <typename T>
 int launch_collide(int lat, const Dom& d, T* f, const T* mo,
                    const uint8_t* solid, double omega, cudaStream_t st);

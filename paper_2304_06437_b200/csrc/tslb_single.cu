@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(BX)
 namespace {
 
 inline dim3 grid_of(const Dom& d) {
-  return dim3(unsigned(int64_t(d.xblocks) * d.ny * d.nzr));
+  return row_grid(d);
 }
 
 template <class F>

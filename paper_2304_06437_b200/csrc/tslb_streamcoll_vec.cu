@@ -320,11 +320,9 @@ __device__ __noinline__ void all_dirs_exact(Dom d, T* f, const T* mo, RowGeom g,
 template <class L, typename T, typename C, int VX, bool WALLS>
 __global__ void __launch_bounds__(BXV)
     k_streamcoll_vec(Dom d, T* __restrict__ f, const T* __restrict__ mo, C om1) {
-  const unsigned bid = blockIdx.x;
-  const unsigned row = bid / unsigned(d.xblocks);
-  const unsigned xb = bid - row * unsigned(d.xblocks);
-  const int j = int(row % unsigned(d.ny));
-  const int k = int(row / unsigned(d.ny)) + d.k0;
+  unsigned xb;
+  int j, k;
+  row_block(d, xb, j, k);
   int i0 = int((xb * BXV + threadIdx.x) * VX);
   const bool active = i0 < d.nx;
   // active lanes form a prefix of the warp (rows never share a warp)
@@ -371,7 +369,7 @@ int launch_streamcoll_vec(int lat, int math, const Dom& d0, T* f, const T* mo,
     if constexpr (VX * sizeof(T) <= 16) {
       Dom d = d0;
       d.xblocks = (d.nx / VX + BXV - 1) / BXV;
-      const dim3 grid(unsigned(int64_t(d.xblocks) * d.ny * d.nzr));
+      const dim3 grid = row_grid(d);
       bool walls = false;
       for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
       if (math == kMathDouble) {
@@ -398,5 +396,139 @@ int launch_streamcoll_vec(int lat, int math, const Dom& d0, T* f, const T* mo,
 
 template int launch_streamcoll_vec<float>(int, int, const Dom&, float*, const float*, double, int, cudaStream_t);
 template int launch_streamcoll_vec<double>(int, int, const Dom&, double*, const double*, double, int, cudaStream_t);
+
+
+
+// ===========================================================================
+// Lean variant: one node per thread, scalar stores at precomputed per-
+// direction offsets (interior nodes), everything else through an outlined
+// reference-order path. Fewest issued instructions per node, which is what
+// bounds the fp64-arithmetic build.
+// ===========================================================================
+constexpr int BXL = 128;
+
+struct PushOffsets {
+  int64_t off[27];  // a * fstride + c_x + nx c_y + nx ny c_z
+};
+
+// Reference-order push of one node (any face kind), moments reloaded.
+template <class L, typename T, typename C>
+__device__ __noinline__ void lean_slow_node(Dom d, T* f, const T* mo, int i, int j, int k, C om1) {
+  const int64_t mi = midx(d, i, j, k);
+  const int64_t fi = mi + int64_t(d.ghost) * d.plane;
+  const int64_t ms = d.mstride;
+  NodeMoments<C> m;
+  if constexpr (L::dim == 3)
+    m = prepare_node<C>(C(mo[mi]), C(mo[ms + mi]), C(mo[2 * ms + mi]), C(mo[3 * ms + mi]), C(mo[4 * ms + mi]),
+                        C(mo[5 * ms + mi]), C(mo[6 * ms + mi]), C(mo[7 * ms + mi]), C(mo[8 * ms + mi]),
+                        C(mo[9 * ms + mi]));
+  else
+    m = prepare_node<C>(C(mo[mi]), C(mo[ms + mi]), C(mo[2 * ms + mi]), C(0), C(mo[3 * ms + mi]),
+                        C(mo[4 * ms + mi]), C(0), C(mo[5 * ms + mi]), C(0), C(0));
+  const int c3[3] = {i, j, k};
+  const int nd[3] = {d.nx, d.ny, d.nz};
+  const int64_t unit[3] = {1, int64_t(d.nx), d.plane};
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    using dd = Dir<L, a>;
+    const T out = T(post_collision<L, a, C>(m, om1));
+    const int cv[3] = {dd::x, dd::y, dd::z};
+    int64_t delta = 0;
+    bool bounce = false;
+    T wx = T(0), wy = T(0), wz = T(0);
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      if (cv[ax] == 0) continue;
+      delta += cv[ax] * unit[ax];
+      const int t = c3[ax] + cv[ax];
+      if (t < 0 || t >= nd[ax]) {
+        const int face = 2 * ax + (t < 0 ? 0 : 1);
+        if (d.mode[face] == kWrap) {
+          delta -= cv[ax] * int64_t(nd[ax]) * unit[ax];
+        } else if (d.mode[face] == kWall) {
+          bounce = true;
+          wx += T(d.uw[face][0]);
+          wy += T(d.uw[face][1]);
+          wz += T(d.uw[face][2]);
+        }
+      }
+    }
+    if (bounce)
+      f[dd::opp * d.fstride + fi] = T(C(out) - bounce_correction<L, a, C>(C(wx), C(wy), C(wz)));
+    else
+      f[a * d.fstride + fi + delta] = out;
+  });
+}
+
+template <class L, typename T, typename C>
+__global__ void __launch_bounds__(BXL)
+    k_streamcoll_lean(Dom d, T* __restrict__ f, const T* __restrict__ mo, C om1, PushOffsets po) {
+  int i, j, k;
+  if (!node_coords<BXL>(d, i, j, k)) return;
+  const int64_t mi = midx(d, i, j, k);
+  const int64_t ms = d.mstride;
+  const T* p = mo + mi;
+  constexpr int NM = 1 + L::dim + L::dim * (L::dim + 1) / 2;
+  T v[NM];
+#pragma unroll
+  for (int c = 0; c < NM; ++c) v[c] = __ldg(p + c * ms);
+  const C rho = C(v[0]);
+  // nodes whose pushes leave the box through a wrap or a wall face, and the
+  // (never produced by the moments pass) rho == -0.0, take the outlined path
+  const bool edge = (i == 0 && d.mode[XMin] != kGhost) || (i == d.nx - 1 && d.mode[XMax] != kGhost) ||
+                    (j == 0 && d.mode[YMin] != kGhost) || (j == d.ny - 1 && d.mode[YMax] != kGhost) ||
+                    (k == 0 && d.mode[ZMin] != kGhost) || (k == d.nz - 1 && d.mode[ZMax] != kGhost);
+  if (edge || (rho == C(0) && signbit(rho))) {
+    lean_slow_node<L, T, C>(d, f, mo, i, j, k, om1);
+    return;
+  }
+  NodeMoments<C> m;
+  if constexpr (L::dim == 3)
+    m = prepare_node<C>(rho, C(v[1]), C(v[2]), C(v[3]), C(v[4]), C(v[5]), C(v[6]), C(v[7]), C(v[8]), C(v[9]));
+  else
+    m = prepare_node<C>(rho, C(v[1]), C(v[2]), C(0), C(v[3]), C(v[4]), C(0), C(v[5]), C(0), C(0));
+  T* base = f + (mi + int64_t(d.ghost) * d.plane);
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    if constexpr (a == 0) {
+      base[po.off[0]] = T(post_rest<L, C>(m, om1));
+    } else if constexpr (a & 1) {
+      C ra, rb;
+      post_pair<L, a, C>(m, om1, ra, rb);
+      base[po.off[a]] = T(ra);
+      base[po.off[a + 1]] = T(rb);
+    }
+  });
+}
+
+template <typename T>
+int launch_streamcoll_lean(int lat, int math, const Dom& d0, T* f, const T* mo, double omega,
+                           cudaStream_t st) {
+  Dom d = d0;
+  d.xblocks = (d.nx + BXL - 1) / BXL;
+  const dim3 grid = row_grid(d);
+  const double om1d = 1.0 - double(T(omega));
+  const float om1f = 1.0f - float(omega);
+  auto go = [&](auto L) {
+    using Lat = decltype(L);
+    PushOffsets po{};
+    for (int a = 0; a < Lat::q; ++a)
+      po.off[a] = int64_t(a) * d.fstride + Lat::c[a][0] +
+                  int64_t(d.nx) * (Lat::c[a][1] + int64_t(d.ny) * Lat::c[a][2]);
+    if (math == kMathDouble)
+      k_streamcoll_lean<Lat, T, double><<<grid, BXL, 0, st>>>(d, f, mo, om1d, po);
+    else
+      k_streamcoll_lean<Lat, T, float><<<grid, BXL, 0, st>>>(d, f, mo, om1f, po);
+  };
+  switch (lat) {
+    case kD2Q9: go(D2Q9{}); return 0;
+    case kD3Q19: go(D3Q19{}); return 0;
+    case kD3Q27: go(D3Q27{}); return 0;
+    default: return 1;
+  }
+}
+
+template int launch_streamcoll_lean<float>(int, int, const Dom&, float*, const float*, double, cudaStream_t);
+template int launch_streamcoll_lean<double>(int, int, const Dom&, double*, const double*, double, cudaStream_t);
 
 }  // namespace tslb_cuda

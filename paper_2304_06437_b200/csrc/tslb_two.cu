@@ -418,7 +418,7 @@ __global__ void __launch_bounds__(BX2)
 // ---------------------------------------------------------------------------
 namespace {
 inline dim3 grid2(const Dom& d) {
-  return dim3(unsigned(int64_t(d.xblocks) * d.ny * d.nzr));
+  return row_grid(d);
 }
 template <class F>
 int with_lat2(int lat, F&& f) {
