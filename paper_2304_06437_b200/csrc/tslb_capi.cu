@@ -104,6 +104,7 @@ struct tslb_cuda_sim {
   // (TSLB_STREAMCOLL=scalar|vec|lean overrides the default)
   int variant = 1;
   int vx = 0;          // nodes per thread in the vectorised kernel (0 = default; TSLB_VX)
+  int kz = 0;          // planes per block of the pipelined kernel (<= 1: off; TSLB_KZ)
   bool staged = false; // slab halos received into staging + masked unpack
   double omega = 1.0;
   int kinds[6] = {0, 0, 0, 0, 0, 0};
@@ -244,7 +245,7 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
                                        static_cast<const T*>(h->mo), h->omega, st);
     if (h->variant == 1 && !h->d.has_solid &&
         launch_streamcoll_vec<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
-                                 static_cast<const T*>(h->mo), h->omega, h->vx, st) == 0)
+                                 static_cast<const T*>(h->mo), h->omega, h->vx, h->kz, st) == 0)
       return 0;
     return launch_streamcoll<T>(h->lat, h->math, h->range(k0, k1),
                                 static_cast<T*>(h->f[0]), static_cast<const T*>(h->mo),
@@ -477,6 +478,7 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   if (const char* e = std::getenv("TSLB_STREAMCOLL"))
     h->variant = !std::strcmp(e, "scalar") ? 0 : !std::strcmp(e, "lean") ? 2 : 1;
   if (const char* e = std::getenv("TSLB_VX")) h->vx = std::atoi(e);
+  if (const char* e = std::getenv("TSLB_KZ")) h->kz = std::atoi(e);
   std::memcpy(h->kinds, kinds, sizeof h->kinds);
   if (color) {
     h->cp.sigma = color[0];

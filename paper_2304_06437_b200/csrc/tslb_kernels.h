@@ -37,7 +37,7 @@ int launch_streamcoll(int lat, int math, const Dom& d, T* f, const T* mo,
 // box geometry (no solid mask), nx % (16 / sizeof(T)) == 0
 template <typename T>
 int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
-                          double omega, int vx, cudaStream_t st);
+                          double omega, int vx, int kz, cudaStream_t st);
 // box geometry, one node per thread, precomputed interior push offsets
 template <typename T>
 int launch_streamcoll_lean(int lat, int math, const Dom& d, T* f, const T* mo,

@@ -353,12 +353,74 @@ __global__ void __launch_bounds__(BXV)
     all_dirs<L, T, C, VX, WALLS, false>(d, f, g, fi, i0, active, seg_start, seg_end, m, om1);
 }
 
+// Software-pipelined form: a block walks KZ consecutive planes of its
+// (x segment, row j) column and prefetches the next plane's moments into
+// registers while the current plane is collided and pushed, so the load
+// latency of each warp hides behind its own fp64 work (the fp64 build runs
+// at low occupancy: ~90-170 registers per thread).
+template <class L, typename T, typename C, int VX, bool WALLS>
+__global__ void __launch_bounds__(BXV)
+    k_streamcoll_pipe(Dom d, T* __restrict__ f, const T* __restrict__ mo, C om1, int kz) {
+  constexpr int NM = 1 + L::dim + L::dim * (L::dim + 1) / 2;
+  const int j = int(blockIdx.y);
+  const int kb = d.k0 + int(blockIdx.z) * kz;
+  const int ke = min(kb + kz, d.k0 + d.nzr);
+  int i0 = int((blockIdx.x * BXV + threadIdx.x) * VX);
+  const bool active = i0 < d.nx;
+  const unsigned amask = __ballot_sync(0xffffffffu, active);
+  const unsigned lane = threadIdx.x & 31u;
+  const bool seg_start = lane == 0;
+  const bool seg_end = active && (lane == 31u || !((amask >> (lane + 1)) & 1u));
+  const int64_t mrow = int64_t(d.nx) * j + (active ? i0 : 0);
+  if (!active) i0 = -1;
+
+  T cur[NM][VX], nxt[NM][VX];
+  auto fetch = [&](T (&buf)[NM][VX], int k) {
+    const int64_t mi = mrow + int64_t(k) * d.plane;
+#pragma unroll
+    for (int c = 0; c < NM; ++c) Vec<T, VX>::load(mo + c * d.mstride + mi, buf[c]);
+  };
+  if (active) fetch(cur, kb);
+#pragma unroll 1
+  for (int k = kb; k < ke; ++k) {
+    if (active && k + 1 < ke) fetch(nxt, k + 1);
+    NodeMoments<C> m[VX];
+#pragma unroll
+    for (int x = 0; x < VX; ++x) {
+      if (!active) {
+        m[x] = prepare_node<C>(C(1), C(0), C(0), C(0), C(0), C(0), C(0), C(0), C(0), C(0));
+      } else if constexpr (L::dim == 3) {
+        m[x] = prepare_node<C>(C(cur[0][x]), C(cur[1][x]), C(cur[2][x]), C(cur[3][x]), C(cur[4][x]),
+                               C(cur[5][x]), C(cur[6][x]), C(cur[7][x]), C(cur[8][x]), C(cur[9][x]));
+      } else {
+        m[x] = prepare_node<C>(C(cur[0][x]), C(cur[1][x]), C(cur[2][x]), C(0), C(cur[3][x]), C(cur[4][x]),
+                               C(0), C(cur[5][x]), C(0), C(0));
+      }
+    }
+    bool exact = false;
+#pragma unroll
+    for (int x = 0; x < VX; ++x) exact |= (m[x].rho == C(0)) && signbit(m[x].rho);
+    const RowGeom g = row_geom(d, j, k);
+    const int64_t mi = mrow + int64_t(k) * d.plane;
+    const int64_t fi = mi + int64_t(d.ghost) * d.plane;
+    if (__any_sync(0xffffffffu, exact))
+      all_dirs_exact<L, T, C, VX, WALLS>(d, f, mo, g, mi, fi, i0, active, seg_start, seg_end, om1);
+    else
+      all_dirs<L, T, C, VX, WALLS, false>(d, f, g, fi, i0, active, seg_start, seg_end, m, om1);
+#pragma unroll
+    for (int c = 0; c < NM; ++c)
+#pragma unroll
+      for (int x = 0; x < VX; ++x) cur[c][x] = nxt[c][x];
+  }
+}
+
 // vx: elements per thread (1, 2 or 4 for float; 1 or 2 for double);
 // 0 picks the default (full 16-byte vectors for fp32 node math, 8-byte for
 // fp64 node math, whose register footprint per node is twice as large).
+// kz > 1 selects the software-pipelined kernel (kz planes per block).
 template <typename T>
 int launch_streamcoll_vec(int lat, int math, const Dom& d0, T* f, const T* mo,
-                          double omega, int vx, cudaStream_t st) {
+                          double omega, int vx, int kz, cudaStream_t st) {
   if (vx == 0) vx = math == kMathDouble ? 8 / int(sizeof(T)) : 16 / int(sizeof(T));
   if (vx * int(sizeof(T)) > 16 || d0.nx % vx != 0) return 1;
   const double om1d = 1.0 - double(T(omega));
@@ -369,9 +431,21 @@ int launch_streamcoll_vec(int lat, int math, const Dom& d0, T* f, const T* mo,
     if constexpr (VX * sizeof(T) <= 16) {
       Dom d = d0;
       d.xblocks = (d.nx / VX + BXV - 1) / BXV;
-      const dim3 grid = row_grid(d);
       bool walls = false;
       for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
+      const int nzc = kz > 1 ? (d.nzr + kz - 1) / kz : 0;
+      if (kz > 1 && d.ny <= 65535 && nzc <= 65535) {
+        const dim3 grid(unsigned(d.xblocks), unsigned(d.ny), unsigned(nzc));
+        if (math == kMathDouble) {
+          if (walls) k_streamcoll_pipe<Lat, T, double, VX, true><<<grid, BXV, 0, st>>>(d, f, mo, om1d, kz);
+          else k_streamcoll_pipe<Lat, T, double, VX, false><<<grid, BXV, 0, st>>>(d, f, mo, om1d, kz);
+        } else {
+          if (walls) k_streamcoll_pipe<Lat, T, float, VX, true><<<grid, BXV, 0, st>>>(d, f, mo, om1f, kz);
+          else k_streamcoll_pipe<Lat, T, float, VX, false><<<grid, BXV, 0, st>>>(d, f, mo, om1f, kz);
+        }
+        return;
+      }
+      const dim3 grid = row_grid(d);
       if (math == kMathDouble) {
         if (walls) k_streamcoll_vec<Lat, T, double, VX, true><<<grid, BXV, 0, st>>>(d, f, mo, om1d);
         else k_streamcoll_vec<Lat, T, double, VX, false><<<grid, BXV, 0, st>>>(d, f, mo, om1d);
@@ -394,8 +468,8 @@ int launch_streamcoll_vec(int lat, int math, const Dom& d0, T* f, const T* mo,
   }
 }
 
-template int launch_streamcoll_vec<float>(int, int, const Dom&, float*, const float*, double, int, cudaStream_t);
-template int launch_streamcoll_vec<double>(int, int, const Dom&, double*, const double*, double, int, cudaStream_t);
+template int launch_streamcoll_vec<float>(int, int, const Dom&, float*, const float*, double, int, int, cudaStream_t);
+template int launch_streamcoll_vec<double>(int, int, const Dom&, double*, const double*, double, int, int, cudaStream_t);
 
 
 
