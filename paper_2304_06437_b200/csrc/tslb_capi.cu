@@ -240,6 +240,10 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
   ++h->launches;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
+    if (h->variant == 3 && !h->d.has_solid &&
+        launch_streamcoll_row<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
+                                 static_cast<const T*>(h->mo), h->omega, h->vx, h->kz, st) == 0)
+      return 0;
     if (h->variant == 2 && !h->d.has_solid)
       return launch_streamcoll_lean<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
                                        static_cast<const T*>(h->mo), h->omega, st);
@@ -476,7 +480,7 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   h->device = device;
   h->omega = omega;
   if (const char* e = std::getenv("TSLB_STREAMCOLL"))
-    h->variant = !std::strcmp(e, "scalar") ? 0 : !std::strcmp(e, "lean") ? 2 : 1;
+    h->variant = !std::strcmp(e, "scalar") ? 0 : !std::strcmp(e, "lean") ? 2 : !std::strcmp(e, "row") ? 3 : 1;
   if (const char* e = std::getenv("TSLB_VX")) h->vx = std::atoi(e);
   if (const char* e = std::getenv("TSLB_KZ")) h->kz = std::atoi(e);
   std::memcpy(h->kinds, kinds, sizeof h->kinds);

@@ -38,6 +38,11 @@ int launch_streamcoll(int lat, int math, const Dom& d, T* f, const T* mo,
 template <typename T>
 int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
                           double omega, int vx, int kz, cudaStream_t st);
+// box geometry, one CTA per x row (nx / vx threads), kz planes per CTA;
+// returns nonzero (nothing launched) if the row does not fit
+template <typename T>
+int launch_streamcoll_row(int lat, int math, const Dom& d, T* f, const T* mo,
+                          double omega, int vx, int kz, cudaStream_t st);
 // box geometry, one node per thread, precomputed interior push offsets
 template <typename T>
 int launch_streamcoll_lean(int lat, int math, const Dom& d, T* f, const T* mo,
