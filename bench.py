@@ -3,15 +3,18 @@
 "GLUPS and % of HBM roofline (D3Q19 1024^3) at 1/2/4/8 B200 vs CPU ref").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload tgv-d3q19|channel-d3q27|droplet-d3q19|cavity-d2q9]
 
-Workload (N = 1): D3Q19 single-phase periodic Taylor-Green vortex, 1024^3
-nodes, fp32 storage, fp64 node arithmetic (the reference's float build, bit
-for bit), fused F1 step = moments kernel + stream-collide kernel.
-N > 1 (torchrun, one rank per GPU): weak scaling, one 1024^3 z slab per GPU
-of a 1024 x 1024 x (1024 N) periodic box, NCCL halo exchange overlapped with
-the interior stream-collide.
-Inputs (125 GB of state per GPU) are far larger than the 126 MB L2, so no L2
-flush is needed between steps.
+Default workload (the metric's): D3Q19 single-phase periodic Taylor-Green
+vortex, 1024^3 nodes per GPU, fp32 storage, fp64 node arithmetic (the
+reference's float build, bit for bit), F1 step = moments kernel + fused
+stream-collide kernel. N > 1 (torchrun, one rank per GPU): weak scaling, one
+1024^3 z slab per GPU of a 1024 x 1024 x (1024 N) periodic box, NCCL halo
+exchange overlapped with the interior stream-collide. The state (125.6 GB
+per GPU) is far larger than the 126 MB L2, so no L2 flush is needed.
+
+The other workloads are BASELINE.json's configs 1, 3 and 4, for the record
+(DESIGN.md); the driver's headline is the default.
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libtslb_ref.so = the unmodified tslb headers, WorkerPool over
@@ -36,6 +39,23 @@ sys.path.insert(0, ROOT)
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
 METRIC = "GLUPS and % of HBM roofline (D3Q19 1024^3) at 1/2/4/8 B200 vs CPU ref"
 
+# per-GPU workloads (BASELINE.json configs)
+WORKLOADS = {
+    "tgv-d3q19": dict(lat="d3q19", dims=(1024, 1024, 1024), faces="periodic", comps=1, init="taylor_green",
+                      amp=0.03, omega=1.6, storage="f32",
+                      desc="D3Q19 periodic Taylor-Green {n}"),
+    "channel-d3q27": dict(lat="d3q27", dims=(1024, 1024, 1024), faces="couette", comps=1, init="rest", amp=0.0,
+                          omega=1.0, storage="f32",
+                          desc="D3Q27 channel {n}: walls at y, y-max moving (0.05,0,0) (Couette; the reference "
+                               "has no body force), rest init"),
+    "droplet-d3q19": dict(lat="d3q19", dims=(512, 512, 512), faces="periodic", comps=2, init="droplet",
+                          radius=512 / 6.0, omega=1 / 0.75, storage="f32", sigma=0.03, beta=0.7,
+                          desc="D3Q19 two-component colour-gradient droplet {n}, R = 85.33, sigma 0.03, beta 0.7"),
+    "cavity-d2q9": dict(lat="d2q9", dims=(256, 256, 1), faces="lid", comps=1, init="rest", amp=0.0,
+                        omega=1 / (0.064 * 3 + 0.5), storage="f64",
+                        desc="D2Q9 lid-driven cavity {n}, Re 100, fp64"),
+}
+
 
 def peaks():
     try:
@@ -44,11 +64,6 @@ def peaks():
         return float(p["hbm_gbs"]), "measured", p
     except Exception:
         return 6650.0, "fallback", {}
-
-
-def census(lat, elem_bytes):
-    from paper_2304_06437_b200 import tslb as T
-    return T.count_kernel_cost(lat, elem_bytes)
 
 
 # ---------------------------------------------------------------------------
@@ -150,14 +165,40 @@ def cpu_reference(steps, warmup, sample_nz=16, workers=None):
 
 
 # ---------------------------------------------------------------------------
+def spec_of(T, kind):
+    if kind == "periodic":
+        return T.BoundarySpec.all_periodic()
+    if kind == "lid":
+        return T.BoundarySpec.lid_cavity(0.025)
+    s = T.BoundarySpec.all_periodic()  # couette
+    s.faces[T.YMin] = T.Face(T.FaceKind.NoSlipWall)
+    s.faces[T.YMax] = T.Face(T.FaceKind.MovingWall, (0.05, 0.0, 0.0))
+    return s
+
+
+def kernel_bytes(lat, comps, es):
+    """Algorithmic bytes per node of each kernel class."""
+    q, D = lat.q, lat.dim
+    npi = D * (D + 1) // 2
+    nm = 1 + D + npi
+    if comps == 1:
+        return {"moments": (q + nm) * es, "streamcoll": (nm + q) * es}
+    return {"cg_moments": (2 * q + 3 + nm) * es, "cg_gradient": (1 + D) * es,
+            "cg_streamcoll": (3 + D + npi + D + 2 * q) * es}
+
+
+def step_bytes(lat, comps, es):
+    return sum(kernel_bytes(lat, comps, es).values())
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=1024, help="edge of the per-GPU cube")
-    ap.add_argument("--lattice", default="d3q19")
+    ap.add_argument("--workload", default="tgv-d3q19", choices=sorted(WORKLOADS))
+    ap.add_argument("--n", type=int, default=0, help="override the per-GPU cube edge (3D)")
     ap.add_argument("--math", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -167,7 +208,12 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    n = args.n
+    W = dict(WORKLOADS[args.workload])
+    dims = W["dims"]
+    if args.n and dims[2] > 1:
+        dims = (args.n, args.n, args.n)
+    default = args.workload == "tgv-d3q19"
+    metric = METRIC if default else f"GLUPS ({args.workload})"
 
     if args.impl == "reference":
         if rank != 0:
@@ -178,7 +224,7 @@ def main():
                "warmup": warm, "ms_per_step": round(info["seconds"] / steps * 1e3, 3), "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                "impl": "reference",
-               "config": {"workload": f"D3Q19 periodic Taylor-Green, sample of the {n}^3 fp32 workload",
+               "config": {"workload": f"D3Q19 periodic Taylor-Green, sample of the {dims[0]}^3 fp32 workload",
                           "lattice": "d3q19", "storage": "f32", "sample": info["sample"]},
                "cpu_baseline": {"value": round(glups, 6), "unit": "GLUPS", "cores": info["cores"],
                                 "kind": info["kind"], "sample": info["sample"]},
@@ -199,14 +245,18 @@ def main():
     dev_id = local if world > 1 else 0
     torch.cuda.set_device(dev_id)
 
-    lat = T.lattice_of(args.lattice)
-    dtype = np.float32
-    nz_g = n * world
-    g = T.GridDims(n, n, nz_g)
-    spec = T.BoundarySpec.all_periodic()
-    omega = 1.6
-    slab = (rank * n, n) if world > 1 else None
-    sim = T.DeviceSolver(lat, g, omega, spec, dtype, 1, None, None, dev_id, slab=slab)
+    lat = T.lattice_of(W["lat"])
+    dtype = np.float32 if W["storage"] == "f32" else np.float64
+    es = np.dtype(dtype).itemsize
+    if world > 1 and (lat.dim != 3 or W["comps"] != 1):
+        raise SystemExit("multi-GPU slabs: 3-D single-fluid workloads only")
+    nx, ny, nzp = dims
+    nz_g = nzp * world
+    g = T.GridDims(nx, ny, nz_g)
+    spec = spec_of(T, W["faces"])
+    color = T.ColorParams(sigma=W.get("sigma", 0.01), beta=W.get("beta", 0.7)) if W["comps"] == 2 else None
+    slab = (rank * nzp, nzp) if world > 1 else None
+    sim = T.DeviceSolver(lat, g, W["omega"], spec, dtype, W["comps"], None, color, dev_id, slab=slab)
     if args.math == "f32":
         sim.set_math(_lib.MATH_F32)
     if world > 1:
@@ -218,7 +268,10 @@ def main():
         dist.broadcast_object_list(obj, src=0)
         buf = (C.c_char * 128).from_buffer_copy(obj[0])
         _lib.check(_lib.load().tslb_cuda_attach_nccl(sim.h, buf, world, rank))
-    sim.init_analytic("taylor_green" if lat.dim == 3 else "shear", 0.03)
+    if W["init"] == "droplet":
+        sim.init_analytic("droplet", 0.0, W["radius"])
+    else:
+        sim.init_analytic(W["init"], W.get("amp", 0.0))
 
     def barrier():
         torch.cuda.synchronize()
@@ -251,31 +304,27 @@ def main():
 
     # roofline of the dominant kernel: algorithmic bytes per launch / mean
     # launch duration (CUDA events on the solver stream, timed region)
-    es = 4
-    q, D = lat.q, lat.dim
-    nm = 1 + D + D * (D + 1) // 2
-    per_node = {"moments": (q + nm) * es, "streamcoll": (nm + q) * es}
-    dom = max(per_node, key=lambda k: prof.get(k, (0, 0))[0])
+    per_node = kernel_bytes(lat, W["comps"], es)
+    dom = max((k for k in per_node if k in prof), key=lambda k: prof[k][0])
     k_ms, k_n = prof[dom]
-    local_nodes = n * n * (n if world > 1 else nz_g)
+    local_nodes = nx * ny * nzp
     achieved = per_node[dom] * local_nodes / (k_ms / k_n / 1e3) / 1e9
     hbm, peak_kind, _ = peaks()
-    cost = census(lat, es)
-    step_bw = glups * cost.bytes / world  # per-GPU GB/s of the whole step
+    sb = step_bytes(lat, W["comps"], es)
+    step_bw = glups * sb / world  # per-GPU GB/s of the whole step
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": None, "kernel": f"k_{dom}",
-            "peak_kind": peak_kind,
+            "kernel_bytes_per_node": per_node[dom], "peak_kind": peak_kind,
             "per_kernel_ms": {k: round(v[0] / v[1], 4) for k, v in prof.items()},
-            "step_bytes_per_lu": cost.bytes, "step_frac": round(step_bw / hbm, 4),
+            "step_bytes_per_lu": sb, "step_frac": round(step_bw / hbm, 4),
             "step_frac_of_8TBs": round(step_bw / 8000.0, 4)}
 
-    # end to end through the public API with host buffers
     e2e = None
-    if not args.no_e2e and world == 1:
-        e2e = run_e2e(sim, lat, n, args.steps, dtype)
+    if default and not args.no_e2e and world == 1:
+        e2e = run_e2e(sim, lat, nx * ny * nzp, args.steps, dtype)
 
     cpu = None
-    if rank == 0 and not args.no_cpu and world == 1:
+    if default and rank == 0 and not args.no_cpu and world == 1:
         try:
             cg, info = cpu_reference(max(2, min(args.steps, 5)), 1, args.sample_nz)
             cpu = {"value": round(cg, 6), "unit": "GLUPS", "cores": info["cores"], "kind": info["kind"],
@@ -284,15 +333,20 @@ def main():
             cpu = {"value": None, "unit": "GLUPS", "cores": 0, "kind": "unavailable", "sample": str(e)[:200]}
 
     if rank == 0:
-        out = {"metric": METRIC, "value": round(glups, 4), "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
+        n_desc = f"{nx}x{ny}x{nzp}" if lat.dim == 3 else f"{nx}x{ny}"
+        out = {"metric": metric, "value": round(glups, 4), "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None, "dtype": "f64" if args.math == "f64" else "f32",
+               "scaling": "weak", "vs_baseline": None,
+               "dtype": ("f64" if args.math == "f64" else "f32") if W["comps"] == 1 else W["storage"],
                "data": "synthetic",
-               "config": {"workload": f"D3Q19 periodic Taylor-Green {n}^3 per GPU"
-                          + (f" (global {n}x{n}x{nz_g}, z slabs)" if world > 1 else ""),
-                          "lattice": lat.name, "nodes": nodes, "storage": "f32",
-                          "node_math": args.math, "schedule": "F1 (moments + fused stream-collide)",
-                          "l2": "state 125 GB/GPU >> 126 MB L2, no flush needed",
+               "config": {"workload": W["desc"].format(n=n_desc) + (" per GPU" if lat.dim == 3 else "")
+                          + (f" (global {nx}x{ny}x{nz_g}, z slabs)" if world > 1 else ""),
+                          "lattice": lat.name, "nodes": nodes, "storage": W["storage"],
+                          "node_math": (args.math if W["comps"] == 1 else W["storage"] + " (as the reference)"),
+                          "schedule": "F1: moments + fused stream-collide" if W["comps"] == 1
+                          else "colour moments + gradient + fused prepare/stream-collide-recolour",
+                          "l2": "state >> 126 MB L2, no flush needed" if nodes > 10 ** 7
+                          else "L2-resident (correctness config)",
                           "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
                "roofline": roof, "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(out))
@@ -301,30 +355,32 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(sim, lat, n, steps, dtype):
+def run_e2e(sim, lat, nn, steps, dtype):
     """The reference driver loop (tslb_main.cpp run_single) through the public
     C-ABI with HOST buffers: upload f from pinned host memory, `steps` steps
-    each followed by a totals() sample read back to the host, then download
-    rho and u (the output frame). Host wall time around all of it."""
+    each followed by a totals() sample read back to the host, then refresh
+    and download rho and u (the output frame). Host wall time around it."""
+    import ctypes as C
+
     import torch
+
+    from paper_2304_06437_b200 import _lib
     q = lat.q
-    nn = n * n * n
     esz = np.dtype(dtype).itemsize
+    tdt = torch.float32 if esz == 4 else torch.float64
     try:
-        host_f = torch.empty((q, nn), dtype=torch.float32, pin_memory=True)
-        out = torch.empty((1 + lat.dim, nn), dtype=torch.float32, pin_memory=True)
+        host_f = torch.empty((q, nn), dtype=tdt, pin_memory=True)
+        out = torch.empty((1 + lat.dim, nn), dtype=tdt, pin_memory=True)
     except Exception as e:
         return {"value": None, "unit": "GLUPS", "error": f"pinned host alloc failed: {e}"[:200]}
-    import ctypes as C
-    from paper_2304_06437_b200 import _lib
     lib = _lib.load()
     # untimed: the host holds the initial state
     _lib.check(lib.tslb_cuda_download_f(sim.h, 0, C.c_void_p(host_f.data_ptr())))
+    mass = C.c_double()
+    mom = (C.c_double * 3)()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     _lib.check(lib.tslb_cuda_upload_f(sim.h, 0, C.c_void_p(host_f.data_ptr())))
-    mass = C.c_double()
-    mom = (C.c_double * 3)()
     for _ in range(steps):
         _lib.check(lib.tslb_cuda_step(sim.h, 1))
         _lib.check(lib.tslb_cuda_totals(sim.h, C.byref(mass), mom))
@@ -336,7 +392,7 @@ def run_e2e(sim, lat, n, steps, dtype):
     d2h = (1 + lat.dim) * nn * esz + steps * 32
     return {"value": round(nn * steps / t / 1e9, 4), "unit": "GLUPS", "h2d_bytes_per_step": int(h2d / steps),
             "d2h_bytes_per_step": int(d2h / steps), "seconds": round(t, 3),
-            "loop": "upload f (pinned) -> steps x (step + totals readback) -> download rho,u"}
+            "loop": "upload f (pinned) -> steps x (step + totals readback) -> refresh, download rho,u"}
 
 
 if __name__ == "__main__":

@@ -100,11 +100,12 @@ struct tslb_cuda_sim {
   bool decomposed = false;
   int device = 0;
   int math = kMathDouble;
-  // box-geometry stream-collide kernel: 0 scalar, 1 vectorised, 2 lean
-  // (TSLB_STREAMCOLL=scalar|vec|lean overrides the default)
+  // box-geometry stream-collide kernel: 0 scalar, 1 vectorised (pipelined
+  // if kz > 1), 2 TMA-staged (TSLB_STREAMCOLL=scalar|vec|tma overrides)
   int variant = 1;
   int vx = 0;          // nodes per thread in the vectorised kernel (0 = default; TSLB_VX)
   int kz = 0;          // planes per block of the pipelined kernel (<= 1: off; TSLB_KZ)
+  TmaMaps* tmaps = nullptr;  // encoded tensor maps of the TMA stream-collide
   bool staged = false; // slab halos received into staging + masked unpack
   double omega = 1.0;
   int kinds[6] = {0, 0, 0, 0, 0, 0};
@@ -125,6 +126,12 @@ struct tslb_cuda_sim {
   uint64_t n_fluid = 0;
   cudaStream_t s = nullptr, cs = nullptr;
   cudaEvent_t ev_b = nullptr, ev_c = nullptr, t0 = nullptr, t1 = nullptr;
+  // CUDA graph of `graph_steps` fused steps, replayed for small (launch-
+  // bound) domains; TSLB_GRAPHS=0 disables
+  cudaGraphExec_t graph = nullptr;
+  long graph_steps = 0;
+  int64_t graph_launches = 0;
+  bool graphs_ok = true;
   bool stress_pending = false;
   long steps = 0;
   // profiling
@@ -240,14 +247,11 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
   ++h->launches;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
-    if (h->variant == 3 && !h->d.has_solid &&
-        launch_streamcoll_row<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
-                                 static_cast<const T*>(h->mo), h->omega, h->vx, h->kz, st) == 0)
+    if (h->variant == 2 && !h->d.has_solid &&
+        launch_streamcoll_tma<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
+                                 static_cast<const T*>(h->mo), h->omega, h->kz, h->tmaps, st) == 0)
       return 0;
-    if (h->variant == 2 && !h->d.has_solid)
-      return launch_streamcoll_lean<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
-                                       static_cast<const T*>(h->mo), h->omega, st);
-    if (h->variant == 1 && !h->d.has_solid &&
+    if (h->variant >= 1 && !h->d.has_solid &&
         launch_streamcoll_vec<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
                                  static_cast<const T*>(h->mo), h->omega, h->vx, h->kz, st) == 0)
       return 0;
@@ -480,9 +484,10 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   h->device = device;
   h->omega = omega;
   if (const char* e = std::getenv("TSLB_STREAMCOLL"))
-    h->variant = !std::strcmp(e, "scalar") ? 0 : !std::strcmp(e, "lean") ? 2 : !std::strcmp(e, "row") ? 3 : 1;
+    h->variant = !std::strcmp(e, "scalar") ? 0 : !std::strcmp(e, "tma") ? 2 : 1;
   if (const char* e = std::getenv("TSLB_VX")) h->vx = std::atoi(e);
   if (const char* e = std::getenv("TSLB_KZ")) h->kz = std::atoi(e);
+  if (const char* e = std::getenv("TSLB_GRAPHS")) h->graphs_ok = std::atoi(e) != 0;
   std::memcpy(h->kinds, kinds, sizeof h->kinds);
   if (color) {
     h->cp.sigma = color[0];
@@ -605,6 +610,11 @@ int sync(tslb_cuda_sim* h) {
   return 0;
 }
 
+void drop_graph(tslb_cuda_sim* h) {
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  h->graph = nullptr;
+}
+
 // Second population buffer of the two-buffer reference step / stream_only
 // (the reference's `scratch`, kernels.hpp:219-291). Created on first use as a
 // copy of f, like `auto scratch = b.f` in the reference tests.
@@ -671,6 +681,8 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
                   h->scratch, h->red, h->dig, h->recv_lo, h->recv_hi};
   for (void* b : bufs)
     if (b) cudaFree(b);
+  if (h->graph) cudaGraphExecDestroy(h->graph);
+  free_tma_maps(h->tmaps);
   for (auto e : h->pool) cudaEventDestroy(e);
   cudaEvent_t evs[] = {h->ev_b, h->ev_c, h->t0, h->t1};
   for (auto e : evs)
@@ -684,6 +696,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
 int tslb_cuda_set_math(tslb_cuda_handle h, int math) {
   if (math != kMathDouble && math != kMathFloat) return set_err(TSLB_EINVAL, "bad math mode");
   h->math = math;
+  drop_graph(h);
   return 0;
 }
 
@@ -851,7 +864,37 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
   if (h->decomposed && h->xmode == 0)
     return set_err(TSLB_ESTATE, "slab solver has no halo transport attached");
   CK(cudaSetDevice(h->device));
-  for (long k = 0; k < nsteps; ++k)
+  long done = 0;
+  // small domains are launch bound: replay a captured graph of G steps
+  constexpr int64_t kGraphMaxNodes = int64_t(8) << 20;
+  constexpr long kGraphSteps = 32;
+  if (h->graphs_ok && !h->prof && h->xmode == 0 && h->n() <= kGraphMaxNodes && nsteps >= kGraphSteps) {
+    if (!h->graph) {
+      const long steps0 = h->steps;
+      const int64_t l0 = h->launches;
+      cudaGraph_t g = nullptr;
+      CK(cudaStreamBeginCapture(h->s, cudaStreamCaptureModeThreadLocal));
+      int rc = 0;
+      for (long k = 0; k < kGraphSteps && !rc; ++k) rc = enqueue_step(h);
+      cudaError_t ce = cudaStreamEndCapture(h->s, &g);
+      h->steps = steps0;
+      h->graph_launches = h->launches - l0;
+      h->launches = l0;
+      if (rc) return rc;
+      if (ce != cudaSuccess) return set_err(TSLB_ECUDA, "graph capture: %s", cudaGetErrorString(ce));
+      ce = cudaGraphInstantiate(&h->graph, g, 0);
+      cudaGraphDestroy(g);
+      if (ce != cudaSuccess) return set_err(TSLB_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+      h->graph_steps = kGraphSteps;
+    }
+    for (; done + h->graph_steps <= nsteps; done += h->graph_steps) {
+      CK(cudaGraphLaunch(h->graph, h->s));
+      h->steps += h->graph_steps;
+      h->launches += h->graph_launches;
+      if (h->comps == 2) h->stress_pending = true;
+    }
+  }
+  for (long k = done; k < nsteps; ++k)
     if (int rc = enqueue_step(h)) return rc;
   CK(cudaGetLastError());
   return 0;
@@ -918,6 +961,7 @@ int tslb_cuda_reference_step(tslb_cuda_handle h, long nsteps) {
     });
     if (rc) return rc;
     std::swap(h->f[0], h->scratch);
+    drop_graph(h);  // the captured graph addresses the old f buffer
     ++h->steps;
   }
   return sync(h);
@@ -939,6 +983,7 @@ int tslb_cuda_stream_only(tslb_cuda_handle h) {
   });
   if (rc) return rc;
   std::swap(h->f[0], h->scratch);
+  drop_graph(h);
   return sync(h);
 }
 

@@ -38,15 +38,15 @@ int launch_streamcoll(int lat, int math, const Dom& d, T* f, const T* mo,
 template <typename T>
 int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
                           double omega, int vx, int kz, cudaStream_t st);
-// box geometry, one CTA per x row (nx / vx threads), kz planes per CTA;
-// returns nonzero (nothing launched) if the row does not fit
+// box geometry, TMA-staged tiles (moments in by TMA loads, populations out
+// by x-shifted TMA tensor stores); `maps` caches the encoded tensor maps
+// (opaque, owned by the caller, freed with free_tma_maps). Returns nonzero
+// (nothing launched) when the shape is not supported.
+struct TmaMaps;
 template <typename T>
-int launch_streamcoll_row(int lat, int math, const Dom& d, T* f, const T* mo,
-                          double omega, int vx, int kz, cudaStream_t st);
-// box geometry, one node per thread, precomputed interior push offsets
-template <typename T>
-int launch_streamcoll_lean(int lat, int math, const Dom& d, T* f, const T* mo,
-                           double omega, cudaStream_t st);
+int launch_streamcoll_tma(int lat, int math, const Dom& d, T* f, const T* mo,
+                          double omega, int kz, TmaMaps*& maps, cudaStream_t st);
+void free_tma_maps(TmaMaps* maps);
 template <typename T>
 int launch_collide(int lat, const Dom& d, T* f, const T* mo,
                    const uint8_t* solid, double omega, cudaStream_t st);

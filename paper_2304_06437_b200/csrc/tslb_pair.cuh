@@ -1,0 +1,129 @@
+// Shared device helpers of the box-geometry stream-collide kernels:
+// vector moves, and the opposite-pair / seed-free forms of the collision
+// (exact rewrites, see tslb_streamcoll_vec.cu header for the argument).
+#pragma once
+
+#include "tslb_collision.cuh"
+
+namespace tslb_cuda {
+
+// VX consecutive scalars moved as one aligned access of VX * sizeof(T) bytes
+template <typename T, int VX>
+struct alignas(sizeof(T) * VX) Pack {
+  T v[VX];
+};
+
+template <typename T, int VX>
+struct Vec {
+  __device__ static void load(const T* p, T (&o)[VX]) {
+    const Pack<T, VX> pk = *reinterpret_cast<const Pack<T, VX>*>(p);
+#pragma unroll
+    for (int e = 0; e < VX; ++e) o[e] = pk.v[e];
+  }
+  __device__ static void st(T* p, const T (&v)[VX]) {
+    Pack<T, VX> pk;
+#pragma unroll
+    for (int e = 0; e < VX; ++e) pk.v[e] = v[e];
+    *reinterpret_cast<Pack<T, VX>*>(p) = pk;
+  }
+};
+
+
+// c . u without the +0 seed (sign of a zero result may differ; see header)
+template <int CX, int CY, int CZ, typename C>
+__device__ __forceinline__ C dot_noseed(C x, C y, C z) {
+  C s;
+  bool first = true;
+  auto add = [&](int c, C v) {
+    if (c == 0) return;
+    if (first) {
+      s = c > 0 ? v : -v;
+      first = false;
+    } else {
+      s = c > 0 ? s + v : s - v;
+    }
+  };
+  add(CX, x);
+  add(CY, y);
+  add(CZ, z);
+  return s;
+}
+
+// Post-collision values of the pair (A, A+1 = opp(A)), A odd.
+template <class L, int A, typename C>
+__device__ __forceinline__ void post_pair(const NodeMoments<C>& m, C om1,
+                                          C& out_a, C& out_b) {
+  using d = Dir<L, A>;
+  constexpr C t = d::template t<C>();
+  const C cu = dot_noseed<d::x, d::y, d::z, C>(m.ux, m.uy, m.uz);
+  const C c3 = C(3) * cu;
+  const C q = C(4.5) * cu * cu;
+  const C ea = t * (m.rho + c3 + q - m.usq15);
+  const C eb = t * (m.rho - c3 + q - m.usq15);
+  const C r = om1 * regularized<L, A, C>(m);  // reference order, shared
+  out_a = ea + r;
+  out_b = eb + r;
+}
+
+template <class L, typename C>
+__device__ __forceinline__ C post_rest(const NodeMoments<C>& m, C om1) {
+  constexpr C t = Dir<L, 0>::template t<C>();
+  // rho + 3*(+0) + (4.5*(+0))*(+0) == rho for rho != -0
+  const C e = t * (m.rho - m.usq15);
+  return e + om1 * regularized<L, 0, C>(m);
+}
+
+// regularized_dir without the +0 seed: identical whenever the first picked
+// stress component is nonzero (checked by the caller, see header).
+template <class L, int A, typename S>
+__device__ __forceinline__ S regularized_noseed(const NodeMoments<S>& m) {
+  using d = Dir<L, A>;
+  constexpr S t45 = d::template t<S>() * S(4.5);
+  S s;
+  bool first = true;
+  auto add = [&](bool on, int sign, S v) {
+    if (!on) return;
+    if (first) {
+      s = sign > 0 ? v : -v;
+      first = false;
+    } else {
+      s = sign > 0 ? s + v : s - v;
+    }
+  };
+  add(d::x != 0, 1, m.pxx);
+  add(d::y != 0, 1, m.pyy);
+  add(d::z != 0, 1, m.pzz);
+  add(d::x * d::y != 0, d::x * d::y, m.pxy2);
+  add(d::x * d::z != 0, d::x * d::z, m.pxz2);
+  add(d::y * d::z != 0, d::y * d::z, m.pyz2);
+  if (first) s = S(0);
+  return t45 * (s - m.trcs2);
+}
+
+template <class L, typename T, typename C, int VX, bool EXACT>
+__device__ __forceinline__ void row_outputs(const NodeMoments<C> (&m)[VX], C om1, T (&o)[L::q][VX]) {
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+#pragma unroll
+    for (int x = 0; x < VX; ++x) {
+      if constexpr (EXACT) {
+        o[a][x] = T(post_collision<L, a, C>(m[x], om1));
+      } else if constexpr (a == 0) {
+        o[0][x] = T(post_rest<L, C>(m[x], om1));
+      } else if constexpr (a & 1) {
+        using dd = Dir<L, a>;
+        constexpr C t = dd::template t<C>();
+        const C cu = dot_noseed<dd::x, dd::y, dd::z, C>(m[x].ux, m[x].uy, m[x].uz);
+        const C c3 = C(3) * cu;
+        const C qq = C(4.5) * cu * cu;
+        const C ea = t * (m[x].rho + c3 + qq - m[x].usq15);
+        const C eb = t * (m[x].rho - c3 + qq - m[x].usq15);
+        const C r = om1 * regularized_noseed<L, a, C>(m[x]);
+        o[a][x] = T(ea + r);
+        o[a + 1][x] = T(eb + r);
+      }
+    }
+  });
+}
+
+}  // namespace tslb_cuda

@@ -22,75 +22,11 @@
 #include "tslb_collision.cuh"
 #include "tslb_domain.cuh"
 #include "tslb_kernels.h"
+#include "tslb_pair.cuh"
 
 namespace tslb_cuda {
 
-// VX consecutive scalars moved as one aligned access of VX * sizeof(T) bytes
-template <typename T, int VX>
-struct alignas(sizeof(T) * VX) Pack {
-  T v[VX];
-};
-
-template <typename T, int VX>
-struct Vec {
-  __device__ static void load(const T* p, T (&o)[VX]) {
-    const Pack<T, VX> pk = *reinterpret_cast<const Pack<T, VX>*>(p);
-#pragma unroll
-    for (int e = 0; e < VX; ++e) o[e] = pk.v[e];
-  }
-  __device__ static void st(T* p, const T (&v)[VX]) {
-    Pack<T, VX> pk;
-#pragma unroll
-    for (int e = 0; e < VX; ++e) pk.v[e] = v[e];
-    *reinterpret_cast<Pack<T, VX>*>(p) = pk;
-  }
-};
-
 constexpr int BXV = 128;
-
-// c . u without the +0 seed (sign of a zero result may differ; see header)
-template <int CX, int CY, int CZ, typename C>
-__device__ __forceinline__ C dot_noseed(C x, C y, C z) {
-  C s;
-  bool first = true;
-  auto add = [&](int c, C v) {
-    if (c == 0) return;
-    if (first) {
-      s = c > 0 ? v : -v;
-      first = false;
-    } else {
-      s = c > 0 ? s + v : s - v;
-    }
-  };
-  add(CX, x);
-  add(CY, y);
-  add(CZ, z);
-  return s;
-}
-
-// Post-collision values of the pair (A, A+1 = opp(A)), A odd.
-template <class L, int A, typename C>
-__device__ __forceinline__ void post_pair(const NodeMoments<C>& m, C om1,
-                                          C& out_a, C& out_b) {
-  using d = Dir<L, A>;
-  constexpr C t = d::template t<C>();
-  const C cu = dot_noseed<d::x, d::y, d::z, C>(m.ux, m.uy, m.uz);
-  const C c3 = C(3) * cu;
-  const C q = C(4.5) * cu * cu;
-  const C ea = t * (m.rho + c3 + q - m.usq15);
-  const C eb = t * (m.rho - c3 + q - m.usq15);
-  const C r = om1 * regularized<L, A, C>(m);  // reference order, shared
-  out_a = ea + r;
-  out_b = eb + r;
-}
-
-template <class L, typename C>
-__device__ __forceinline__ C post_rest(const NodeMoments<C>& m, C om1) {
-  constexpr C t = Dir<L, 0>::template t<C>();
-  // rho + 3*(+0) + (4.5*(+0))*(+0) == rho for rho != -0
-  const C e = t * (m.rho - m.usq15);
-  return e + om1 * regularized<L, 0, C>(m);
-}
 
 template <class L, typename T, typename C, int VX>
 __device__ __forceinline__ void load_moments_vec(const Dom& d,
@@ -470,386 +406,5 @@ int launch_streamcoll_vec(int lat, int math, const Dom& d0, T* f, const T* mo,
 
 template int launch_streamcoll_vec<float>(int, int, const Dom&, float*, const float*, double, int, int, cudaStream_t);
 template int launch_streamcoll_vec<double>(int, int, const Dom&, double*, const double*, double, int, int, cudaStream_t);
-
-
-
-// ===========================================================================
-// Lean variant: one node per thread, scalar stores at precomputed per-
-// direction offsets (interior nodes), everything else through an outlined
-// reference-order path. Fewest issued instructions per node, which is what
-// bounds the fp64-arithmetic build.
-// ===========================================================================
-constexpr int BXL = 128;
-
-struct PushOffsets {
-  int64_t off[27];  // a * fstride + c_x + nx c_y + nx ny c_z
-};
-
-// Reference-order push of one node (any face kind), moments reloaded.
-template <class L, typename T, typename C>
-__device__ __noinline__ void lean_slow_node(Dom d, T* f, const T* mo, int i, int j, int k, C om1) {
-  const int64_t mi = midx(d, i, j, k);
-  const int64_t fi = mi + int64_t(d.ghost) * d.plane;
-  const int64_t ms = d.mstride;
-  NodeMoments<C> m;
-  if constexpr (L::dim == 3)
-    m = prepare_node<C>(C(mo[mi]), C(mo[ms + mi]), C(mo[2 * ms + mi]), C(mo[3 * ms + mi]), C(mo[4 * ms + mi]),
-                        C(mo[5 * ms + mi]), C(mo[6 * ms + mi]), C(mo[7 * ms + mi]), C(mo[8 * ms + mi]),
-                        C(mo[9 * ms + mi]));
-  else
-    m = prepare_node<C>(C(mo[mi]), C(mo[ms + mi]), C(mo[2 * ms + mi]), C(0), C(mo[3 * ms + mi]),
-                        C(mo[4 * ms + mi]), C(0), C(mo[5 * ms + mi]), C(0), C(0));
-  const int c3[3] = {i, j, k};
-  const int nd[3] = {d.nx, d.ny, d.nz};
-  const int64_t unit[3] = {1, int64_t(d.nx), d.plane};
-  unroll<L::q>([&](auto A) {
-    constexpr int a = decltype(A)::value;
-    using dd = Dir<L, a>;
-    const T out = T(post_collision<L, a, C>(m, om1));
-    const int cv[3] = {dd::x, dd::y, dd::z};
-    int64_t delta = 0;
-    bool bounce = false;
-    T wx = T(0), wy = T(0), wz = T(0);
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-      if (cv[ax] == 0) continue;
-      delta += cv[ax] * unit[ax];
-      const int t = c3[ax] + cv[ax];
-      if (t < 0 || t >= nd[ax]) {
-        const int face = 2 * ax + (t < 0 ? 0 : 1);
-        if (d.mode[face] == kWrap) {
-          delta -= cv[ax] * int64_t(nd[ax]) * unit[ax];
-        } else if (d.mode[face] == kWall) {
-          bounce = true;
-          wx += T(d.uw[face][0]);
-          wy += T(d.uw[face][1]);
-          wz += T(d.uw[face][2]);
-        }
-      }
-    }
-    if (bounce)
-      f[dd::opp * d.fstride + fi] = T(C(out) - bounce_correction<L, a, C>(C(wx), C(wy), C(wz)));
-    else
-      f[a * d.fstride + fi + delta] = out;
-  });
-}
-
-template <class L, typename T, typename C>
-__global__ void __launch_bounds__(BXL)
-    k_streamcoll_lean(Dom d, T* __restrict__ f, const T* __restrict__ mo, C om1, PushOffsets po) {
-  int i, j, k;
-  if (!node_coords<BXL>(d, i, j, k)) return;
-  const int64_t mi = midx(d, i, j, k);
-  const int64_t ms = d.mstride;
-  const T* p = mo + mi;
-  constexpr int NM = 1 + L::dim + L::dim * (L::dim + 1) / 2;
-  T v[NM];
-#pragma unroll
-  for (int c = 0; c < NM; ++c) v[c] = __ldg(p + c * ms);
-  const C rho = C(v[0]);
-  // nodes whose pushes leave the box through a wrap or a wall face, and the
-  // (never produced by the moments pass) rho == -0.0, take the outlined path
-  const bool edge = (i == 0 && d.mode[XMin] != kGhost) || (i == d.nx - 1 && d.mode[XMax] != kGhost) ||
-                    (j == 0 && d.mode[YMin] != kGhost) || (j == d.ny - 1 && d.mode[YMax] != kGhost) ||
-                    (k == 0 && d.mode[ZMin] != kGhost) || (k == d.nz - 1 && d.mode[ZMax] != kGhost);
-  if (edge || (rho == C(0) && signbit(rho))) {
-    lean_slow_node<L, T, C>(d, f, mo, i, j, k, om1);
-    return;
-  }
-  NodeMoments<C> m;
-  if constexpr (L::dim == 3)
-    m = prepare_node<C>(rho, C(v[1]), C(v[2]), C(v[3]), C(v[4]), C(v[5]), C(v[6]), C(v[7]), C(v[8]), C(v[9]));
-  else
-    m = prepare_node<C>(rho, C(v[1]), C(v[2]), C(0), C(v[3]), C(v[4]), C(0), C(v[5]), C(0), C(0));
-  T* base = f + (mi + int64_t(d.ghost) * d.plane);
-  unroll<L::q>([&](auto A) {
-    constexpr int a = decltype(A)::value;
-    if constexpr (a == 0) {
-      base[po.off[0]] = T(post_rest<L, C>(m, om1));
-    } else if constexpr (a & 1) {
-      C ra, rb;
-      post_pair<L, a, C>(m, om1, ra, rb);
-      base[po.off[a]] = T(ra);
-      base[po.off[a + 1]] = T(rb);
-    }
-  });
-}
-
-template <typename T>
-int launch_streamcoll_lean(int lat, int math, const Dom& d0, T* f, const T* mo, double omega,
-                           cudaStream_t st) {
-  Dom d = d0;
-  d.xblocks = (d.nx + BXL - 1) / BXL;
-  const dim3 grid = row_grid(d);
-  const double om1d = 1.0 - double(T(omega));
-  const float om1f = 1.0f - float(omega);
-  auto go = [&](auto L) {
-    using Lat = decltype(L);
-    PushOffsets po{};
-    for (int a = 0; a < Lat::q; ++a)
-      po.off[a] = int64_t(a) * d.fstride + Lat::c[a][0] +
-                  int64_t(d.nx) * (Lat::c[a][1] + int64_t(d.ny) * Lat::c[a][2]);
-    if (math == kMathDouble)
-      k_streamcoll_lean<Lat, T, double><<<grid, BXL, 0, st>>>(d, f, mo, om1d, po);
-    else
-      k_streamcoll_lean<Lat, T, float><<<grid, BXL, 0, st>>>(d, f, mo, om1f, po);
-  };
-  switch (lat) {
-    case kD2Q9: go(D2Q9{}); return 0;
-    case kD3Q19: go(D3Q19{}); return 0;
-    case kD3Q27: go(D3Q27{}); return 0;
-    default: return 1;
-  }
-}
-
-template int launch_streamcoll_lean<float>(int, int, const Dom&, float*, const float*, double, cudaStream_t);
-template int launch_streamcoll_lean<double>(int, int, const Dom&, double*, const double*, double, cudaStream_t);
-
-}  // namespace tslb_cuda
-
-namespace tslb_cuda {
-
-// ===========================================================================
-// Row kernel: one CTA owns a whole x row (nx / VX threads, a multiple of 32,
-// <= 1024) and walks KZ planes of it. Because the CTA holds the entire row,
-// the one-element shift of c_x = +-1 pushes is closed inside the CTA: within
-// a warp by a shuffle, across warps through shared memory, and across the
-// row ends by the periodic wrap (or, for x walls, by the bounce of the
-// opposite direction of the same node). Every population store is therefore
-// one aligned VX-wide vector -- no per-lane edge stores, no divergence.
-// Rows that touch a wrapped/walled y or z face (block-uniform) take the
-// general per-lane path (push_dir). Moments of the next plane are prefetched
-// into registers while the current plane is collided.
-// ===========================================================================
-constexpr int kMaxRowThreads = 512;  // keeps >= 128 registers per thread
-
-struct RowOffsets {
-  int64_t off[27];  // (a * fstride + nx c_y + nx ny c_z) * sizeof(T): aligned part of the push
-};
-
-// regularized_dir without the +0 seed: identical whenever the first picked
-// stress component is nonzero (checked by the caller, see header).
-template <class L, int A, typename S>
-__device__ __forceinline__ S regularized_noseed(const NodeMoments<S>& m) {
-  using d = Dir<L, A>;
-  constexpr S t45 = d::template t<S>() * S(4.5);
-  S s;
-  bool first = true;
-  auto add = [&](bool on, int sign, S v) {
-    if (!on) return;
-    if (first) {
-      s = sign > 0 ? v : -v;
-      first = false;
-    } else {
-      s = sign > 0 ? s + v : s - v;
-    }
-  };
-  add(d::x != 0, 1, m.pxx);
-  add(d::y != 0, 1, m.pyy);
-  add(d::z != 0, 1, m.pzz);
-  add(d::x * d::y != 0, d::x * d::y, m.pxy2);
-  add(d::x * d::z != 0, d::x * d::z, m.pxz2);
-  add(d::y * d::z != 0, d::y * d::z, m.pyz2);
-  if (first) s = S(0);
-  return t45 * (s - m.trcs2);
-}
-
-template <class L, typename T, typename C, int VX, bool EXACT>
-__device__ __forceinline__ void row_outputs(const NodeMoments<C> (&m)[VX], C om1, T (&o)[L::q][VX]) {
-  unroll<L::q>([&](auto A) {
-    constexpr int a = decltype(A)::value;
-#pragma unroll
-    for (int x = 0; x < VX; ++x) {
-      if constexpr (EXACT) {
-        o[a][x] = T(post_collision<L, a, C>(m[x], om1));
-      } else if constexpr (a == 0) {
-        o[0][x] = T(post_rest<L, C>(m[x], om1));
-      } else if constexpr (a & 1) {
-        using dd = Dir<L, a>;
-        constexpr C t = dd::template t<C>();
-        const C cu = dot_noseed<dd::x, dd::y, dd::z, C>(m[x].ux, m[x].uy, m[x].uz);
-        const C c3 = C(3) * cu;
-        const C qq = C(4.5) * cu * cu;
-        const C ea = t * (m[x].rho + c3 + qq - m[x].usq15);
-        const C eb = t * (m[x].rho - c3 + qq - m[x].usq15);
-        const C r = om1 * regularized_noseed<L, a, C>(m[x]);
-        o[a][x] = T(ea + r);
-        o[a + 1][x] = T(eb + r);
-      }
-    }
-  });
-}
-
-template <class L, typename T, typename C, int VX, bool XWALL>
-__global__ void __launch_bounds__(kMaxRowThreads)
-    k_streamcoll_row(Dom d, T* __restrict__ f, const T* __restrict__ mo, C om1, int kz, RowOffsets ro) {
-  constexpr int NM = 1 + L::dim + L::dim * (L::dim + 1) / 2;
-  extern __shared__ unsigned char smem_raw[];
-  T* carry_up = reinterpret_cast<T*>(smem_raw);      // [q][nwarps]: lane 31 value, c_x = +1 dirs
-  const int nwarps = int(blockDim.x) >> 5;
-  T* carry_dn = carry_up + L::q * nwarps;            // [q][nwarps]: lane 0 value, c_x = -1 dirs
-  const int j = int(blockIdx.y);
-  const int kb = d.k0 + int(blockIdx.z) * kz;
-  const int ke = min(kb + kz, d.k0 + d.nzr);
-  const int tid = int(threadIdx.x);
-  const int lane = tid & 31, warp = tid >> 5;
-  const int i0 = tid * VX;
-  const int64_t mrow = int64_t(d.nx) * j + i0;
-  const bool yedge = (j == 0 && d.mode[YMin] != kGhost) || (j == d.ny - 1 && d.mode[YMax] != kGhost);
-
-  T cur[NM][VX], nxt[NM][VX];
-  auto fetch = [&](T (&buf)[NM][VX], int k) {
-    const int64_t mi = mrow + int64_t(k) * d.plane;
-#pragma unroll
-    for (int c = 0; c < NM; ++c) Vec<T, VX>::load(mo + c * d.mstride + mi, buf[c]);
-  };
-  fetch(cur, kb);
-#pragma unroll 1
-  for (int k = kb; k < ke; ++k) {
-    if (k + 1 < ke) fetch(nxt, k + 1);
-    NodeMoments<C> m[VX];
-    bool exact = false;
-#pragma unroll
-    for (int x = 0; x < VX; ++x) {
-      if constexpr (L::dim == 3)
-        m[x] = prepare_node<C>(C(cur[0][x]), C(cur[1][x]), C(cur[2][x]), C(cur[3][x]), C(cur[4][x]),
-                               C(cur[5][x]), C(cur[6][x]), C(cur[7][x]), C(cur[8][x]), C(cur[9][x]));
-      else
-        m[x] = prepare_node<C>(C(cur[0][x]), C(cur[1][x]), C(cur[2][x]), C(0), C(cur[3][x]), C(cur[4][x]),
-                               C(0), C(cur[5][x]), C(0), C(0));
-      exact |= (m[x].rho == C(0) && signbit(m[x].rho)) || m[x].pxx == C(0) || m[x].pyy == C(0) ||
-               (L::dim == 3 && m[x].pzz == C(0));
-    }
-    const int64_t mi = mrow + int64_t(k) * d.plane;
-    const int64_t fi = mi + int64_t(d.ghost) * d.plane;
-    const bool zedge = (k == 0 && d.mode[ZMin] != kGhost) || (k == d.nz - 1 && d.mode[ZMax] != kGhost);
-    if (yedge || zedge) {
-      // general per-lane path (wrap / wall rows), reference evaluation order
-      const RowGeom g = row_geom(d, j, k);
-      const bool seg_start = lane == 0;
-      const bool seg_end = lane == 31;
-      all_dirs<L, T, C, VX, true, true>(d, f, g, fi, i0, true, seg_start, seg_end, m, om1);
-      __syncthreads();  // keep the CTA in step (smem reuse below)
-    } else {
-      T o[L::q][VX];
-      if (__syncthreads_or(exact))
-        row_outputs<L, T, C, VX, true>(m, om1, o);
-      else
-        row_outputs<L, T, C, VX, false>(m, om1, o);
-      // publish warp-edge values of the x-shifted directions
-      unroll<L::q>([&](auto A) {
-        constexpr int a = decltype(A)::value;
-        if constexpr (Dir<L, a>::x == 1) {
-          if (lane == 31) carry_up[a * nwarps + warp] = o[a][VX - 1];
-        } else if constexpr (Dir<L, a>::x == -1) {
-          if (lane == 0) carry_dn[a * nwarps + warp] = o[a][0];
-        }
-      });
-      __syncthreads();
-      unsigned char* rowp = reinterpret_cast<unsigned char*>(f + fi);
-      unroll<L::q>([&](auto A) {
-        constexpr int a = decltype(A)::value;
-        using dd = Dir<L, a>;
-        T* dst = reinterpret_cast<T*>(rowp + ro.off[a]);
-        if constexpr (dd::x == 0) {
-          Vec<T, VX>::st(dst, o[a]);
-        } else if constexpr (dd::x == 1) {
-          // slot x0 receives node x0 - 1
-          T c = __shfl_up_sync(0xffffffffu, o[a][VX - 1], 1);
-          if (lane == 0) {
-            if (warp > 0) c = carry_up[a * nwarps + warp - 1];
-            else if constexpr (XWALL)  // x = 0: bounce of opp(a) at node 0
-              c = bounce_value<L, dd::opp, T, C>(d, o[dd::opp][0], true, false, false);
-            else c = carry_up[a * nwarps + nwarps - 1];  // periodic: node nx - 1
-          }
-          T v[VX];
-          v[0] = c;
-#pragma unroll
-          for (int e = 1; e < VX; ++e) v[e] = o[a][e - 1];
-          Vec<T, VX>::st(dst, v);
-        } else {
-          // slot x0 + VX - 1 receives node x0 + VX
-          T c = __shfl_down_sync(0xffffffffu, o[a][0], 1);
-          if (lane == 31) {
-            if (warp < nwarps - 1) c = carry_dn[a * nwarps + warp + 1];
-            else if constexpr (XWALL)  // x = nx - 1: bounce of opp(a) at node nx - 1
-              c = bounce_value<L, dd::opp, T, C>(d, o[dd::opp][VX - 1], true, false, false);
-            else c = carry_dn[a * nwarps];  // periodic: node 0
-          }
-          T v[VX];
-#pragma unroll
-          for (int e = 0; e < VX - 1; ++e) v[e] = o[a][e + 1];
-          v[VX - 1] = c;
-          Vec<T, VX>::st(dst, v);
-        }
-      });
-      __syncthreads();  // carries are rewritten by the next plane
-    }
-#pragma unroll
-    for (int c = 0; c < NM; ++c)
-#pragma unroll
-      for (int x = 0; x < VX; ++x) cur[c][x] = nxt[c][x];
-  }
-}
-
-/// Returns 1 (not launched) when the row does not fit one CTA.
-template <typename T>
-int launch_streamcoll_row(int lat, int math, const Dom& d0, T* f, const T* mo, double omega, int vx, int kz,
-                          cudaStream_t st) {
-  if (vx == 0) vx = 2;
-  if (kz <= 0) kz = 8;
-  if (vx * int(sizeof(T)) > 16 || d0.nx % vx != 0) return 1;
-  const int threads = d0.nx / vx;
-  if (threads % 32 != 0 || threads > kMaxRowThreads || d0.ny > 65535) return 1;
-  // x faces: both periodic or both walls (classify rule); only no-slip x
-  // walls are folded into the carries, moving x walls use the other kernels
-  const bool xwall = d0.mode[XMin] == kWall;
-  if (xwall && (d0.uw[XMin][0] != 0 || d0.uw[XMin][1] != 0 || d0.uw[XMin][2] != 0 || d0.uw[XMax][0] != 0 ||
-                d0.uw[XMax][1] != 0 || d0.uw[XMax][2] != 0))
-    return 1;
-  const int nzc = (d0.nzr + kz - 1) / kz;
-  if (nzc > 65535) return 1;
-  const double om1d = 1.0 - double(T(omega));
-  const float om1f = 1.0f - float(omega);
-  int rc = 1;
-  auto go = [&](auto L, auto V) {
-    using Lat = decltype(L);
-    constexpr int VX = decltype(V)::value;
-    if constexpr (VX * sizeof(T) <= 16) {
-      RowOffsets ro{};
-      for (int a = 0; a < Lat::q; ++a)
-        ro.off[a] = (int64_t(a) * d0.fstride +
-                     int64_t(d0.nx) * (Lat::c[a][1] + int64_t(d0.ny) * Lat::c[a][2])) * int64_t(sizeof(T));
-      const dim3 grid(1, unsigned(d0.ny), unsigned(nzc));
-      const size_t sm = size_t(2) * Lat::q * (threads / 32) * sizeof(T);
-      auto launch = [&](auto kern, auto om) {
-        kern<<<grid, threads, sm, st>>>(d0, f, mo, om, kz, ro);
-        rc = 0;
-      };
-      if (math == kMathDouble) {
-        if (xwall) launch(k_streamcoll_row<Lat, T, double, VX, true>, om1d);
-        else launch(k_streamcoll_row<Lat, T, double, VX, false>, om1d);
-      } else {
-        if (xwall) launch(k_streamcoll_row<Lat, T, float, VX, true>, om1f);
-        else launch(k_streamcoll_row<Lat, T, float, VX, false>, om1f);
-      }
-    }
-  };
-  auto by_vx = [&](auto L) {
-    if (vx == 2) go(L, std::integral_constant<int, 2>{});
-    else if (vx == 4) go(L, std::integral_constant<int, 4>{});
-  };
-  switch (lat) {
-    case kD2Q9: by_vx(D2Q9{}); break;
-    case kD3Q19: by_vx(D3Q19{}); break;
-    case kD3Q27: by_vx(D3Q27{}); break;
-    default: return 1;
-  }
-  return rc;
-}
-
-template int launch_streamcoll_row<float>(int, int, const Dom&, float*, const float*, double, int, int, cudaStream_t);
-template int launch_streamcoll_row<double>(int, int, const Dom&, double*, const double*, double, int, int,
-                                           cudaStream_t);
 
 }  // namespace tslb_cuda

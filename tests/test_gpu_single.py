@@ -289,3 +289,52 @@ def test_device_init_matches_host_formula(gpu, init):
     T.initialize_regularized(s, None, st, T.D3Q19)
     assert np.max(np.abs(fdev - s.f)) < 1e-15
     dev.close()
+
+
+def test_graph_replay_then_reference_step(gpu, oracle_port):
+    """Graph replay (>= 32 steps on a small box), then the two-buffer step
+    (which swaps buffers and must drop the captured graph), then more
+    replays: every phase bit-exact against the oracle."""
+    lat, dims, faces, solid = "d3q19", (12, 10, 8), zwalls_3d(), None
+    f0 = O.random_state(lat, dims, 4, np.float64)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.1, spec_of(faces), np.float64)
+    dev.upload_f(f0)
+    dev.step(40)
+    dev.phase("reference_step", 3)
+    dev.step(33)
+    got = dev.download_f()
+    dev.close()
+    ref = f0.copy()
+    oracle_port.single_run(lat, dims, 1.1, faces, ref, None, 40, 0)
+    oracle_port.single_run(lat, dims, 1.1, faces, ref, None, 3, 1)
+    oracle_port.single_run(lat, dims, 1.1, faces, ref, None, 33, 0)
+    assert_bitwise(got, ref, "f after graph/reference/graph")
+
+
+TMA_CASES = [
+    ("d3q19", "periodic", (256, 6, 5), O.periodic()),
+    ("d3q19", "zwalls", (256, 4, 6), zwalls_3d()),
+    ("d3q19", "box", (256, 5, 4), O.closed_box()),
+    ("d3q19", "ylid", (512, 3, 4), [("periodic", (0, 0, 0))] * 2 + [("wall", (0, 0, 0)), ("moving", (0.05, 0.0, 0.01))]
+     + [("periodic", (0, 0, 0))] * 2),
+    ("d3q27", "zwalls", (256, 4, 4), zwalls_3d()),
+    ("d2q9", "lid", (256, 8, 1), O.lid_cavity(0.04)),
+]
+
+
+@pytest.mark.parametrize("variant", ["tma", "vec"])
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("case", TMA_CASES, ids=lambda c: f"{c[0]}-{c[1]}")
+def test_box_kernels_bitwise_wide_rows(gpu, oracle_port, case, dtype, variant, monkeypatch):
+    """The box-geometry stream-collide kernels on rows wide enough for them
+    (TMA tiles need nx % 256 == 0): bit-exact against the oracle, including
+    multi-plane CTAs (TSLB_KZ=3) and the wall/wrap row ends."""
+    lat, name, dims, faces = case
+    monkeypatch.setenv("TSLB_STREAMCOLL", variant)
+    monkeypatch.setenv("TSLB_KZ", "3")
+    f0 = O.random_state(lat, dims, 7, dtype)
+    fo, mo = f0.copy(), np.zeros((O.moments_layout(lat), f0.shape[1]), dtype)
+    oracle_port.single_run(lat, dims, 0.83, faces, fo, mo, 4, 0)
+    fg, mg = _gpu_single(lat, dims, 0.83, faces, f0, 4, None)
+    assert_bitwise(fg, fo, f"{variant} {lat}/{name} f")
+    assert_bitwise(mg, mo, f"{variant} {lat}/{name} moments")

@@ -172,3 +172,21 @@ def test_all_red_tracks_single_fluid(gpu):
     fs, tv = single.view().f, two.view()
     assert np.allclose(tv.fr, fs, rtol=1e-12, atol=0)
     assert np.all(tv.fb == 0.0)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_two_fluid_graph_replay_bitwise(gpu, oracle_port, dtype):
+    """Small domains replay a captured CUDA graph of 32 steps (launch-bound
+    path); 70 steps = 2 replays + 6 direct steps, still bit-exact, and the
+    host-visible u_eq / Pi^neq semantics survive the replay."""
+    lat, dims, faces, solid = CASES[2]
+    st = droplet_state(dims, 5.0, dtype, (0.01, 0.0, 0.0))
+    fr, fb = oracle_port.init_colors(lat, dims, st, solid)
+    fro, fbo = fr.copy(), fb.copy()
+    ref = oracle_port.two_run(lat, dims, 1.3, COLORS["nci"], faces, fro, fbo, 70, False, 0, solid)
+    got = _gpu_two(lat, dims, 1.3, COLORS["nci"], faces, fr, fb, 70, False, solid)
+    fluid = solid == 0
+    assert_bitwise(got["fr"], fro, "fr", fluid)
+    assert_bitwise(got["fb"], fbo, "fb", fluid)
+    D = T.lattice_of(lat).dim
+    assert_bitwise(np.reshape(got["mom"], (D, -1)), ref["mom"], "mom", fluid)
