@@ -249,7 +249,7 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
     using T = decltype(z);
     if (h->variant == 2 && !h->d.has_solid &&
         launch_streamcoll_tma<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
-                                 static_cast<const T*>(h->mo), h->omega, h->kz, h->tmaps, st) == 0)
+                                 static_cast<const T*>(h->mo), h->omega, h->kz, h->vx, h->tmaps, st) == 0)
       return 0;
     if (h->variant >= 1 && !h->d.has_solid &&
         launch_streamcoll_vec<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),

@@ -45,7 +45,7 @@ int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
 struct TmaMaps;
 template <typename T>
 int launch_streamcoll_tma(int lat, int math, const Dom& d, T* f, const T* mo,
-                          double omega, int kz, TmaMaps*& maps, cudaStream_t st);
+                          double omega, int kz, int vx, TmaMaps*& maps, cudaStream_t st);
 void free_tma_maps(TmaMaps* maps);
 template <typename T>
 int launch_collide(int lat, const Dom& d, T* f, const T* mo,

@@ -87,7 +87,8 @@ __device__ __forceinline__ void bulk_wait_read() {
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
-constexpr int NT = 128;  // threads per CTA
+constexpr int NT = 128;   // compute threads per CTA
+constexpr int NTE = NT + 32;  // + one edge/producer warp
 
 // wall bounce with u_wall summed over crossed wall faces in axis order, in T
 // (boundary.hpp:127-137, kernels.hpp:187-192)
@@ -106,12 +107,37 @@ __device__ __forceinline__ T bounce_of(const Dom& d, T out, bool cx, bool cy, bo
   return T(C(out) - bounce_correction<L, A, C>(C(wx), C(wy), C(wz)));
 }
 
+template <class L, typename T, typename C>
+__device__ __forceinline__ NodeMoments<C> node_from(const T* p, int64_t stride) {
+  if constexpr (L::dim == 3)
+    return prepare_node<C>(C(p[0]), C(p[stride]), C(p[2 * stride]), C(p[3 * stride]), C(p[4 * stride]),
+                           C(p[5 * stride]), C(p[6 * stride]), C(p[7 * stride]), C(p[8 * stride]),
+                           C(p[9 * stride]));
+  else
+    return prepare_node<C>(C(p[0]), C(p[stride]), C(p[2 * stride]), C(0), C(p[3 * stride]), C(p[4 * stride]),
+                           C(0), C(p[5 * stride]), C(0), C(0));
+}
+
+template <class L, typename C>
+__device__ __forceinline__ bool needs_exact(const NodeMoments<C>& m) {
+  return (m.rho == C(0) && signbit(m.rho)) || m.pxx == C(0) || m.pyy == C(0) ||
+         (L::dim == 3 && m.pzz == C(0));
+}
+
 }  // namespace
 
+// Tile = TX consecutive x nodes of row (j, k). Slot x of direction a holds
+// the push of node x - c_a, so the shared-memory tile of direction a is
+// written at element e + c_x and stored by TMA at the ALIGNED origin x0 (TMA
+// tensor coordinates must be 16-byte aligned in x): the one element per tile
+// and direction that comes from outside the tile (node x0-1 for c_x = +1,
+// node x0+TX for c_x = -1) is computed by the edge warp ("halo" pushes; with
+// x walls at the row ends the node's own bounce fills it instead). Warps
+// 0-3 collide the tile; warp 4 computes the halo and drives the TMA.
 template <class L, typename T, typename C, int VX>
-__global__ void __launch_bounds__(NT)
+__global__ void __launch_bounds__(NTE)
     k_streamcoll_tma(const __grid_constant__ CUtensorMap fmap, const __grid_constant__ CUtensorMap mmap, Dom d,
-                     T* __restrict__ f, C om1, int kz) {
+                     T* __restrict__ f, const T* __restrict__ mo, C om1, int kz) {
   constexpr int TX = NT * VX;
   constexpr int NM = 1 + L::dim + L::dim * (L::dim + 1) / 2;
   constexpr int Q = L::q;
@@ -121,16 +147,17 @@ __global__ void __launch_bounds__(NT)
   uint64_t* bar = reinterpret_cast<uint64_t*>(out + 2 * Q * TX);
 
   const int tid = int(threadIdx.x);
+  const bool edge_warp = tid >= NT;
+  const int lane = tid & 31;
+  constexpr int PRODUCER = NT;
   const int x0 = int(blockIdx.x) * TX;
   const int j = int(blockIdx.y);
   const int kb = d.k0 + int(blockIdx.z) * kz;
   const int ke = min(kb + kz, d.k0 + d.nzr);
   const int ntile = ke - kb;
-  const bool row_first = x0 == 0;
-  const bool row_last = x0 + TX == d.nx;
   const bool xwall = d.mode[XMin] == kWall;
 
-  if (tid == 0) {
+  if (tid == PRODUCER) {
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
     fence_async_smem();
@@ -140,156 +167,169 @@ __global__ void __launch_bounds__(NT)
     mbar_expect_tx(&bar[s], uint32_t(NM * TX * sizeof(T)));
     tma_load_4d(in + s * NM * TX, &mmap, &bar[s], x0, j, kb + t, 0);
   };
-  if (tid == 0) {
+  if (tid == PRODUCER) {
     issue_load(0, 0);
     if (ntile > 1) issue_load(1, 1);
+  }
+
+  // edge warp: lanes [0,16) left halo node x0-1, lanes [16,32) right halo
+  // node x0+TX; lane % 16 selects the x-shifted direction pair
+  const bool left = lane < 16;
+  const int hp = lane & 15;
+  int hx = left ? x0 - 1 : x0 + TX;
+  bool halo = edge_warp;
+  if (hx < 0 || hx >= d.nx) {
+    if (xwall) halo = false;  // row end at a wall: the node's own bounce fills the slot
+    hx = hx < 0 ? hx + d.nx : hx - d.nx;
   }
 
 #pragma unroll 1
   for (int t = 0; t < ntile; ++t) {
     const int s = t & 1;
     const int k = kb + t;
-    if (tid == 0 && t >= 2) bulk_wait_read<1>();  // out[s] no longer read by tile t-2's stores
+    const bool jlo = j == 0, jhi = j == d.ny - 1, klo = k == 0, khi = k == d.nz - 1;
+    auto bounces = [&](auto A, bool& by, bool& bz) {
+      using dd = Dir<L, decltype(A)::value>;
+      by = (dd::y == 1 && jhi && d.mode[YMax] == kWall) || (dd::y == -1 && jlo && d.mode[YMin] == kWall);
+      bz = (dd::z == 1 && khi && d.mode[ZMax] == kWall) || (dd::z == -1 && klo && d.mode[ZMin] == kWall);
+    };
+    // halo moments straight from global (issued before the barrier wait)
+    NodeMoments<C> hm;
+    if (edge_warp)
+      hm = node_from<L, T, C>(mo + int64_t(hx) + int64_t(d.nx) * (int64_t(j) + int64_t(d.ny) * k), d.mstride);
+    if (tid == PRODUCER && t >= 2) bulk_wait_read<1>();  // tile t-2's stores have read out[s]
     __syncthreads();
     mbar_wait(&bar[s], uint32_t((t >> 1) & 1));
 
-    // moments of this thread's VX nodes from the staged tile
+    T* tout = out + s * Q * TX;
     const T* tin = in + s * NM * TX;
     NodeMoments<C> m[VX];
     bool exact = false;
+    if (!edge_warp) {
 #pragma unroll
-    for (int v = 0; v < VX; ++v) {
-      const int e = tid * VX + v;
-      if constexpr (L::dim == 3)
-        m[v] = prepare_node<C>(C(tin[e]), C(tin[TX + e]), C(tin[2 * TX + e]), C(tin[3 * TX + e]),
-                               C(tin[4 * TX + e]), C(tin[5 * TX + e]), C(tin[6 * TX + e]), C(tin[7 * TX + e]),
-                               C(tin[8 * TX + e]), C(tin[9 * TX + e]));
-      else
-        m[v] = prepare_node<C>(C(tin[e]), C(tin[TX + e]), C(tin[2 * TX + e]), C(0), C(tin[3 * TX + e]),
-                               C(tin[4 * TX + e]), C(0), C(tin[5 * TX + e]), C(0), C(0));
-      exact |= (m[v].rho == C(0) && signbit(m[v].rho)) || m[v].pxx == C(0) || m[v].pyy == C(0) ||
-               (L::dim == 3 && m[v].pzz == C(0));
-    }
-    // per-direction row geometry (block-uniform)
-    const bool jlo = j == 0, jhi = j == d.ny - 1, klo = k == 0, khi = k == d.nz - 1;
-    T* tout = out + s * Q * TX;
-    const int64_t fi = int64_t(d.nx) * (int64_t(j) + int64_t(d.ny) * (int64_t(k) + d.ghost)) + x0 + tid * VX;
-    // hand one direction's VX outputs to the tile (or bounce them off a
-    // y/z wall straight into the node's own opp slot: no TMA store for it)
-    auto emit = [&](auto A, const T (&vals)[VX]) {
-      constexpr int a = decltype(A)::value;
-      using dd = Dir<L, a>;
-      const bool by = (dd::y == 1 && jhi && d.mode[YMax] == kWall) || (dd::y == -1 && jlo && d.mode[YMin] == kWall);
-      const bool bz = (dd::z == 1 && khi && d.mode[ZMax] == kWall) || (dd::z == -1 && klo && d.mode[ZMin] == kWall);
-      if (by || bz) {
-        T b[VX];
-#pragma unroll
-        for (int v = 0; v < VX; ++v) {
-          const int x = x0 + tid * VX + v;
-          const bool cx = xwall && ((dd::x == 1 && x == d.nx - 1) || (dd::x == -1 && x == 0));
-          b[v] = bounce_of<L, a, T, C>(d, vals[v], cx, by, bz);
-        }
-        Vec<T, VX>::st(f + dd::opp * d.fstride + fi, b);
-      } else {
-        Vec<T, VX>::st(tout + a * TX + tid * VX, vals);
+      for (int v = 0; v < VX; ++v) {
+        m[v] = node_from<L, T, C>(tin + tid * VX + v, TX);
+        exact |= needs_exact<L, C>(m[v]);
       }
-    };
-    if (__syncthreads_or(exact)) {
-      unroll<Q>([&](auto A) {
-        constexpr int a = decltype(A)::value;
-        T vals[VX];
-#pragma unroll
-        for (int v = 0; v < VX; ++v) vals[v] = T(post_collision<L, a, C>(m[v], om1));
-        emit(A, vals);
-      });
     } else {
-      unroll<Q>([&](auto A) {
+      exact = halo && needs_exact<L, C>(hm);
+    }
+    const bool ex = __syncthreads_or(exact);
+
+    if (!edge_warp) {
+      const int64_t fi = int64_t(d.nx) * (int64_t(j) + int64_t(d.ny) * (int64_t(k) + d.ghost)) + x0 + tid * VX;
+      // one direction's VX outputs -> the tile (shifted by c_x), or bounced
+      auto emit = [&](auto A, const T (&vals)[VX]) {
         constexpr int a = decltype(A)::value;
-        if constexpr (a == 0) {
-          T vals[VX];
-#pragma unroll
-          for (int v = 0; v < VX; ++v) vals[v] = T(post_rest<L, C>(m[v], om1));
-          emit(A, vals);
-        } else if constexpr (a & 1) {
-          using dd = Dir<L, a>;
-          constexpr C tw = dd::template t<C>();
-          T va[VX], vb[VX];
+        using dd = Dir<L, a>;
+        bool by, bz;
+        bounces(A, by, bz);
+        if (by || bz) {
+          T b[VX];
 #pragma unroll
           for (int v = 0; v < VX; ++v) {
-            const C cu = dot_noseed<dd::x, dd::y, dd::z, C>(m[v].ux, m[v].uy, m[v].uz);
-            const C c3 = C(3) * cu;
-            const C qq = C(4.5) * cu * cu;
-            const C ea = tw * (m[v].rho + c3 + qq - m[v].usq15);
-            const C eb = tw * (m[v].rho - c3 + qq - m[v].usq15);
-            const C r = om1 * regularized_noseed<L, a, C>(m[v]);
-            va[v] = T(ea + r);
-            vb[v] = T(eb + r);
+            const int x = x0 + tid * VX + v;
+            const bool cx = xwall && ((dd::x == 1 && x == d.nx - 1) || (dd::x == -1 && x == 0));
+            b[v] = bounce_of<L, a, T, C>(d, vals[v], cx, by, bz);
           }
-          emit(A, va);
-          emit(std::integral_constant<int, a + 1>{}, vb);
+          Vec<T, VX>::st(f + dd::opp * d.fstride + fi, b);
+        } else if constexpr (dd::x == 0) {
+          Vec<T, VX>::st(tout + a * TX + tid * VX, vals);
+        } else {
+#pragma unroll
+          for (int v = 0; v < VX; ++v) {
+            const int e = tid * VX + v + dd::x;
+            if (e >= 0 && e < TX) {
+              tout[a * TX + e] = vals[v];
+            } else if (xwall) {
+              const int x = x0 + tid * VX + v;
+              if ((dd::x == 1 && x == d.nx - 1) || (dd::x == -1 && x == 0))
+                tout[dd::opp * TX + tid * VX + v] = bounce_of<L, a, T, C>(d, vals[v], true, false, false);
+            }
+          }
+        }
+      };
+      if (ex) {
+        unroll<Q>([&](auto A) {
+          constexpr int a = decltype(A)::value;
+          T vals[VX];
+#pragma unroll
+          for (int v = 0; v < VX; ++v) vals[v] = T(post_collision<L, a, C>(m[v], om1));
+          emit(A, vals);
+        });
+      } else {
+        unroll<Q>([&](auto A) {
+          constexpr int a = decltype(A)::value;
+          if constexpr (a == 0) {
+            T vals[VX];
+#pragma unroll
+            for (int v = 0; v < VX; ++v) vals[v] = T(post_rest<L, C>(m[v], om1));
+            emit(A, vals);
+          } else if constexpr (a & 1) {
+            T va[VX], vb[VX];
+#pragma unroll
+            for (int v = 0; v < VX; ++v) {
+              C ra, rb;
+              post_pair<L, a, C>(m[v], om1, ra, rb);
+              va[v] = T(ra);
+              vb[v] = T(rb);
+            }
+            emit(A, va);
+            emit(std::integral_constant<int, a + 1>{}, vb);
+          }
+        });
+      }
+    } else if (halo) {
+      // halo pushes: pair number hp among the x-shifted pairs
+      int p = 0;
+      unroll<Q>([&](auto A) {
+        constexpr int a = decltype(A)::value;
+        if constexpr ((a & 1) && Dir<L, a>::x != 0) {
+          if (p++ == hp) {
+            // member with c_x = +1 feeds the left halo slot, c_x = -1 the right
+            constexpr int ap = Dir<L, a>::x == 1 ? a : a + 1;
+            constexpr int am = Dir<L, a>::x == 1 ? a + 1 : a;
+            bool by, bz;
+            C ra, rb;
+            if (ex) {
+              ra = post_collision<L, a, C>(hm, om1);
+              rb = post_collision<L, a + 1, C>(hm, om1);
+            } else {
+              post_pair<L, a, C>(hm, om1, ra, rb);
+            }
+            const T vp = T(Dir<L, a>::x == 1 ? ra : rb);
+            const T vm = T(Dir<L, a>::x == 1 ? rb : ra);
+            if (left) {
+              bounces(std::integral_constant<int, ap>{}, by, bz);
+              if (!(by || bz)) tout[ap * TX] = vp;
+            } else {
+              bounces(std::integral_constant<int, am>{}, by, bz);
+              if (!(by || bz)) tout[am * TX + TX - 1] = vm;
+            }
+          }
         }
       });
     }
     fence_async_smem();
     __syncthreads();
-    if (tid == 0) {
+    if (tid == PRODUCER) {
       unroll<Q>([&](auto A) {
         constexpr int a = decltype(A)::value;
         using dd = Dir<L, a>;
+        bool by, bz;
+        bounces(A, by, bz);
+        if (by || bz) return;  // bounced directly above
         int yt = j + dd::y, zt = k + dd::z;
-        bool skip = false;
-        if (yt < 0 || yt >= d.ny) {
-          if (d.mode[yt < 0 ? YMin : YMax] == kWrap) yt = yt < 0 ? yt + d.ny : yt - d.ny;
-          else skip = true;  // wall: bounced above
-        }
-        if (zt < 0 || zt >= d.nz) {
-          const int mz = d.mode[zt < 0 ? ZMin : ZMax];
-          if (mz == kWrap) zt = zt < 0 ? zt + d.nz : zt - d.nz;
-          else if (mz == kWall) skip = true;
-          // kGhost: the ghost plane is inside the tensor
-        }
-        if (!skip) tma_store_4d(&fmap, tout + a * TX, x0 + dd::x, yt, zt + d.ghost, a);
+        if (yt < 0) yt += d.ny;
+        if (yt >= d.ny) yt -= d.ny;
+        if ((zt < 0 || zt >= d.nz) && d.mode[zt < 0 ? ZMin : ZMax] == kWrap) zt = zt < 0 ? zt + d.nz : zt - d.nz;
+        tma_store_4d(&fmap, tout + a * TX, x0, yt, zt + d.ghost, a);
       });
       bulk_commit();
       if (t + 2 < ntile) issue_load(t + 2, s);
     }
-    // row-end elements the shifted boxes clip: x wrap, or x-wall bounce
-    const bool end_lo = row_first && tid == 0, end_hi = row_last && tid == NT - 1;
-    if (end_lo || end_hi) {
-      unroll<Q>([&](auto A) {
-        constexpr int a = decltype(A)::value;
-        using dd = Dir<L, a>;
-        if constexpr (dd::x != 0) {
-          if ((dd::x == -1 && end_lo) || (dd::x == 1 && end_hi)) {
-            const int v = dd::x == -1 ? 0 : VX - 1;
-            const int x = x0 + tid * VX + v;
-            int yt = j + dd::y, zt = k + dd::z;
-            bool by = false, bz = false;
-            if (yt < 0 || yt >= d.ny) {
-              if (d.mode[yt < 0 ? YMin : YMax] == kWrap) yt = yt < 0 ? yt + d.ny : yt - d.ny;
-              else by = true;
-            }
-            if (zt < 0 || zt >= d.nz) {
-              const int mz = d.mode[zt < 0 ? ZMin : ZMax];
-              if (mz == kWrap) zt = zt < 0 ? zt + d.nz : zt - d.nz;
-              else if (mz == kWall) bz = true;
-            }
-            const T val = tout[a * TX + tid * VX + v];
-            if (by || bz) {
-              // already written by the y/z bounce above
-            } else if (xwall) {
-              f[dd::opp * d.fstride + fi + v] = bounce_of<L, a, T, C>(d, val, true, false, false);
-            } else {
-              const int xt = dd::x == -1 ? d.nx - 1 : 0;
-              f[a * d.fstride + int64_t(xt) + int64_t(d.nx) * (int64_t(yt) + int64_t(d.ny) * (zt + d.ghost))] = val;
-            }
-            (void)x;
-          }
-        }
-      });
-    }
   }
-  if (tid == 0) bulk_wait_all();
+  if (tid == PRODUCER) bulk_wait_all();
 }
 
 namespace {
@@ -314,10 +354,9 @@ EncodeFn encoder() {
 
 }  // namespace
 
-template <typename T>
-int launch_streamcoll_tma(int lat, int math, const Dom& d, T* f, const T* mo, double omega, int kz, TmaMaps*& maps,
-                          cudaStream_t st) {
-  constexpr int VX = sizeof(T) == 4 ? 2 : 1;
+template <typename T, int VX>
+int launch_tma_vx(int lat, int math, const Dom& d, T* f, const T* mo, double omega, int kz, TmaMaps*& maps,
+                  cudaStream_t st) {
   constexpr int TX = NT * VX;
   if (kz <= 0) kz = 8;
   if (d.nx % TX != 0 || d.ny > 65535) return 1;
@@ -337,6 +376,7 @@ int launch_streamcoll_tma(int lat, int math, const Dom& d, T* f, const T* mo, do
   const int nm = 1 + dim + dim * (dim + 1) / 2;
   const int64_t key[6] = {d.nx, d.ny, d.nz, d.ghost, d.fstride, d.mstride};
   if (!maps || maps->fbase != f || maps->mbase != mo || maps->lat != lat || maps->esz != int(sizeof(T)) ||
+      maps->tx != TX ||
       std::memcmp(maps->key, key, sizeof key) != 0) {
     if (!maps) maps = new TmaMaps();
     const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
@@ -372,7 +412,7 @@ int launch_streamcoll_tma(int lat, int math, const Dom& d, T* f, const T* mo, do
                       size_t(2) * Lat::q * TX * sizeof(T) + 2 * sizeof(uint64_t);
     auto launch = [&](auto kern, auto om) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
-      kern<<<grid, NT, sm, st>>>(maps->fmap, maps->mmap, d, f, om, kz);
+      kern<<<grid, NTE, sm, st>>>(maps->fmap, maps->mmap, d, f, mo, om, kz);
     };
     if (math == kMathDouble) launch(k_streamcoll_tma<Lat, T, double, VX>, om1d);
     else launch(k_streamcoll_tma<Lat, T, float, VX>, om1f);
@@ -385,9 +425,19 @@ int launch_streamcoll_tma(int lat, int math, const Dom& d, T* f, const T* mo, do
   return 0;
 }
 
-template int launch_streamcoll_tma<float>(int, int, const Dom&, float*, const float*, double, int, TmaMaps*&,
+
+template <typename T>
+int launch_streamcoll_tma(int lat, int math, const Dom& d, T* f, const T* mo, double omega, int kz, int vx,
+                          TmaMaps*& maps, cudaStream_t st) {
+  if (vx <= 0) vx = 1;
+  if (vx > 2 || vx * int(sizeof(T)) > 8) return 1;
+  return vx == 1 ? launch_tma_vx<T, 1>(lat, math, d, f, mo, omega, kz, maps, st)
+                 : launch_tma_vx<T, 2>(lat, math, d, f, mo, omega, kz, maps, st);
+}
+
+template int launch_streamcoll_tma<float>(int, int, const Dom&, float*, const float*, double, int, int, TmaMaps*&,
                                           cudaStream_t);
-template int launch_streamcoll_tma<double>(int, int, const Dom&, double*, const double*, double, int, TmaMaps*&,
+template int launch_streamcoll_tma<double>(int, int, const Dom&, double*, const double*, double, int, int, TmaMaps*&,
                                            cudaStream_t);
 
 }  // namespace tslb_cuda
