@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define TSLB_CUDA_ABI_VERSION 1
+#define TSLB_CUDA_ABI_VERSION 2
 
 typedef struct tslb_cuda_sim* tslb_cuda_handle;
 
@@ -66,6 +66,11 @@ enum tslb_scalar { TSLB_F64 = 0, TSLB_F32 = 1 };
 enum tslb_face { TSLB_FACE_PERIODIC = 0, TSLB_FACE_WALL = 1, TSLB_FACE_MOVING = 2 };
 /* node-local arithmetic: F64 is the reference's (bit-exact); F32 opt-in */
 enum tslb_math { TSLB_MATH_F64 = 0, TSLB_MATH_F32 = 1 };
+/* step schedule of single-fluid box geometries: F1 = moments pass + fused
+ * stream-collide (populations in HBM); M = moment-resident single pass
+ * (populations rebuilt in shared memory, f materialised on demand). Both are
+ * bit-identical to fused_step (kernels.hpp:209-215). */
+enum tslb_schedule { TSLB_SCHED_F1 = 0, TSLB_SCHED_M = 1 };
 enum tslb_status { TSLB_OK = 0, TSLB_EINVAL = 1, TSLB_ECUDA = 2, TSLB_ENOMEM = 3, TSLB_ESTATE = 4 };
 
 /* field ids for upload_field / download_field */
@@ -89,7 +94,7 @@ enum tslb_init { TSLB_INIT_REST = 0, TSLB_INIT_SHEAR = 1, TSLB_INIT_TAYLOR_GREEN
 enum tslb_kclass {
   TSLB_K_MOMENTS = 0, TSLB_K_STREAMCOLL = 1, TSLB_K_CG_MOMENTS = 2,
   TSLB_K_CG_GRADIENT = 3, TSLB_K_CG_STREAMCOLL = 4, TSLB_K_EXCHANGE = 5,
-  TSLB_K_COUNT = 6
+  TSLB_K_MSTEP = 6, TSLB_K_COUNT = 7
 };
 
 int tslb_cuda_abi_version(void);
@@ -120,6 +125,12 @@ int tslb_cuda_create_slab(int lattice, int scalar, int components, int nx,
 
 int tslb_cuda_destroy(tslb_cuda_handle h);
 int tslb_cuda_set_math(tslb_cuda_handle h, int math);
+/* Select the single-fluid step schedule (default: M where supported --
+ * D3Q19/D3Q27, no solid mask, single domain, nx % 32 == 0, ny % 8 == 0 --
+ * else F1). TSLB_EINVAL if M is requested where it is not supported. Same
+ * results either way (fused_step, kernels.hpp:209-215). */
+int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule);
+int tslb_cuda_get_schedule(tslb_cuda_handle h, int* schedule);
 /* dims[0..4] = nx, ny, nz_local, z0, nz_global; info[0..3] = q, dim, np, scalar bytes */
 int tslb_cuda_describe(tslb_cuda_handle h, int* dims, int* info);
 int tslb_cuda_memory_bytes(tslb_cuda_handle h, uint64_t* bytes);

@@ -19,7 +19,8 @@ FACE_PERIODIC, FACE_WALL, FACE_MOVING = 0, 1, 2
 MATH_F64, MATH_F32 = 0, 1
 FIELD = dict(rho=0, mom=1, pineq=2, rho_r=3, rho_b=4, phi=5, gradphi=6, nci_flag=7, solid=8, slow_mask=9)
 INIT = dict(rest=0, shear=1, taylor_green=2, droplet=3)
-KCLASS = ["moments", "streamcoll", "cg_moments", "cg_gradient", "cg_streamcoll", "exchange"]
+KCLASS = ["moments", "streamcoll", "cg_moments", "cg_gradient", "cg_streamcoll", "exchange", "mstep"]
+SCHED_F1, SCHED_M = 0, 1
 
 
 class TslbCudaError(RuntimeError):
@@ -54,6 +55,8 @@ def load(path: str | None = None) -> C.CDLL:
         "tslb_cuda_create_slab": ([i, i, i, i, i, i, i, i, d, vp, vp, vp, vp, vp, i, vp], i),
         "tslb_cuda_destroy": ([H], i),
         "tslb_cuda_set_math": ([H, i], i),
+        "tslb_cuda_set_schedule": ([H, i], i),
+        "tslb_cuda_get_schedule": ([H, vp], i),
         "tslb_cuda_describe": ([H, vp, vp], i),
         "tslb_cuda_memory_bytes": ([H, vp], i),
         "tslb_cuda_upload_f": ([H, i, vp], i),
@@ -92,7 +95,7 @@ def load(path: str | None = None) -> C.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.tslb_cuda_abi_version() != 1:
+    if lib.tslb_cuda_abi_version() != 2:
         raise TslbCudaError("libtslb_cuda.so ABI version mismatch")
     _lib = lib
     return lib

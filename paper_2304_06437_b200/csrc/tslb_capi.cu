@@ -101,11 +101,19 @@ struct tslb_cuda_sim {
   int device = 0;
   int math = kMathDouble;
   // box-geometry stream-collide kernel: 0 scalar, 1 vectorised (pipelined
-  // if kz > 1), 2 TMA-staged (TSLB_STREAMCOLL=scalar|vec|tma overrides)
+  // if kz > 1) (TSLB_STREAMCOLL=scalar|vec overrides)
   int variant = 1;
+  // single-fluid schedule: M (moment-resident single pass, tslb_mstep.cu)
+  // where supported, else F1. In M, `fimplicit` means the populations
+  // f(t+1) = stream_collide(m(t)) are not stored: `mo` holds m(t) (the
+  // reference's lagged moment arrays) and f is materialised on demand.
+  int sched = TSLB_SCHED_F1;
+  bool fimplicit = false;
+  int lz = 0;          // planes per CTA of the M kernel (0 = default; TSLB_LZ)
+  void* mo2 = nullptr; // second moment buffer of the M schedule (ping-pong)
+  void* graph_mo = nullptr;  // moment buffer the captured graph starts from
   int vx = 0;          // nodes per thread in the vectorised kernel (0 = default; TSLB_VX)
   int kz = 0;          // planes per block of the pipelined kernel (<= 1: off; TSLB_KZ)
-  TmaMaps* tmaps = nullptr;  // encoded tensor maps of the TMA stream-collide
   bool staged = false; // slab halos received into staging + masked unpack
   double omega = 1.0;
   int kinds[6] = {0, 0, 0, 0, 0, 0};
@@ -247,10 +255,6 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
   ++h->launches;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
-    if (h->variant == 2 && !h->d.has_solid &&
-        launch_streamcoll_tma<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
-                                 static_cast<const T*>(h->mo), h->omega, h->kz, h->vx, h->tmaps, st) == 0)
-      return 0;
     if (h->variant >= 1 && !h->d.has_solid &&
         launch_streamcoll_vec<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->f[0]),
                                  static_cast<const T*>(h->mo), h->omega, h->vx, h->kz, st) == 0)
@@ -259,6 +263,29 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
                                 static_cast<T*>(h->f[0]), static_cast<const T*>(h->mo),
                                 h->solid, h->slow, h->omega, st);
   });
+}
+
+// M schedule: m(t) in h->mo -> m(t+1) in h->mo2, then swap
+int ph_mstep(tslb_cuda_sim* h, cudaStream_t st) {
+  {
+    Prof p(h, TSLB_K_MSTEP, st);
+    ++h->launches;
+    int rc = by_scalar(h, [&](auto z) {
+      using T = decltype(z);
+      return launch_mstep<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<const T*>(h->mo),
+                             static_cast<T*>(h->mo2), h->omega, h->lz, st);
+    });
+    if (rc) return set_err(TSLB_ESTATE, "M step not supported for this domain");
+  }
+  std::swap(h->mo, h->mo2);
+  return 0;
+}
+
+// store f(t+1) = stream_collide(m(t)) if the M schedule left it implicit
+int materialize(tslb_cuda_sim* h) {
+  if (!h->fimplicit) return 0;
+  h->fimplicit = false;
+  return ph_streamcoll(h, 0, h->nzl, h->s);
 }
 
 int ph_cg_moments(tslb_cuda_sim* h, cudaStream_t st) {
@@ -386,6 +413,18 @@ int enqueue_step(tslb_cuda_sim* h) {
     ++h->steps;
     return 0;
   }
+  if (h->sched == TSLB_SCHED_M) {
+    // first step from stored populations: the moments pass, stream-collide
+    // deferred; afterwards one M pass per step
+    if (!h->fimplicit) {
+      if ((rc = ph_moments(h, h->s))) return rc;
+      h->fimplicit = true;
+    } else if ((rc = ph_mstep(h, h->s))) {
+      return rc;
+    }
+    ++h->steps;
+    return 0;
+  }
   if ((rc = ph_moments(h, h->s))) return rc;
   if (h->xmode != 1) {
     if ((rc = ph_streamcoll(h, 0, h->nzl, h->s))) return rc;
@@ -484,10 +523,11 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   h->device = device;
   h->omega = omega;
   if (const char* e = std::getenv("TSLB_STREAMCOLL"))
-    h->variant = !std::strcmp(e, "scalar") ? 0 : !std::strcmp(e, "tma") ? 2 : 1;
+    h->variant = !std::strcmp(e, "scalar") ? 0 : 1;
   if (const char* e = std::getenv("TSLB_VX")) h->vx = std::atoi(e);
   if (const char* e = std::getenv("TSLB_KZ")) h->kz = std::atoi(e);
   if (const char* e = std::getenv("TSLB_GRAPHS")) h->graphs_ok = std::atoi(e) != 0;
+  if (const char* e = std::getenv("TSLB_LZ")) h->lz = std::atoi(e);
   std::memcpy(h->kinds, kinds, sizeof h->kinds);
   if (color) {
     h->cp.sigma = color[0];
@@ -596,6 +636,14 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
     if ((rc = alloc(h, &h->recv_lo, pb))) return fail(rc);
     if ((rc = alloc(h, &h->recv_hi, pb))) return fail(rc);
   }
+  if (components == 1 && mstep_supported(lattice, d)) {
+    const char* e = std::getenv("TSLB_SCHEDULE");
+    if (!(e && !std::strcmp(e, "f1"))) {
+      if ((rc = alloc(h, &h->mo2, mbytes))) return fail(rc);
+      CK(cudaMemsetAsync(h->mo2, 0, mbytes, h->s));
+      h->sched = TSLB_SCHED_M;
+    }
+  }
   if ((rc = alloc(h, reinterpret_cast<void**>(&h->red),
                   (reduce_partial_count() + 16) * sizeof(double))))
     return fail(rc);
@@ -620,6 +668,7 @@ void drop_graph(tslb_cuda_sim* h) {
 // copy of f, like `auto scratch = b.f` in the reference tests.
 int ensure_scratch(tslb_cuda_sim* h) {
   if (h->scratch) return 0;
+  if (int rc = materialize(h)) return rc;
   const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
   if (int rc = alloc(h, &h->scratch, fbytes)) return rc;
   CK(cudaMemcpyAsync(h->scratch, h->f[0], fbytes, cudaMemcpyDeviceToDevice, h->s));
@@ -677,12 +726,11 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   if (h->s) cudaStreamSynchronize(h->s);
   if (h->cs) cudaStreamSynchronize(h->cs);
   if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
-  void* bufs[] = {h->f[0], h->f[1], h->mo, h->two, h->flag, h->solid, h->slow,
+  void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->two, h->flag, h->solid, h->slow,
                   h->scratch, h->red, h->dig, h->recv_lo, h->recv_hi};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->graph) cudaGraphExecDestroy(h->graph);
-  free_tma_maps(h->tmaps);
   for (auto e : h->pool) cudaEventDestroy(e);
   cudaEvent_t evs[] = {h->ev_b, h->ev_c, h->t0, h->t1};
   for (auto e : evs)
@@ -695,8 +743,38 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
 
 int tslb_cuda_set_math(tslb_cuda_handle h, int math) {
   if (math != kMathDouble && math != kMathFloat) return set_err(TSLB_EINVAL, "bad math mode");
+  CK(cudaSetDevice(h->device));
+  // a pending f(t+1) belongs to the step that was taken with the old mode
+  if (int rc = materialize(h)) return rc;
   h->math = math;
   drop_graph(h);
+  return 0;
+}
+
+int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
+  if (schedule != TSLB_SCHED_F1 && schedule != TSLB_SCHED_M)
+    return set_err(TSLB_EINVAL, "bad schedule %d", schedule);
+  if (schedule == h->sched) return 0;
+  CK(cudaSetDevice(h->device));
+  if (schedule == TSLB_SCHED_M) {
+    if (h->comps != 1 || !mstep_supported(h->lat, h->d))
+      return set_err(TSLB_EINVAL,
+                     "M schedule needs a single-fluid D3Q19/D3Q27 box without solids, "
+                     "one domain, nx %% 32 == 0 and ny %% 8 == 0");
+    if (!h->mo2) {
+      const size_t mbytes = size_t(h->d.mstride) * (1 + h->dim + h->np) * h->esz;
+      if (int rc = alloc(h, &h->mo2, mbytes)) return rc;
+    }
+  } else if (int rc = materialize(h)) {
+    return rc;
+  }
+  h->sched = schedule;
+  drop_graph(h);
+  return sync(h);
+}
+
+int tslb_cuda_get_schedule(tslb_cuda_handle h, int* schedule) {
+  *schedule = h->sched;
   return 0;
 }
 
@@ -726,6 +804,7 @@ int tslb_cuda_upload_f(tslb_cuda_handle h, int species, const void* host) {
   CK(cudaSetDevice(h->device));
   char* base;
   if (int rc = species_base(h, species, &base)) return rc;
+  if (species == 0) h->fimplicit = false;  // every owned slot is overwritten
   const size_t pb = size_t(h->n()) * h->esz;
   const size_t off = size_t(h->d.ghost * h->plane()) * h->esz;
   for (int a = 0; a < h->q; ++a)
@@ -737,6 +816,8 @@ int tslb_cuda_upload_f(tslb_cuda_handle h, int species, const void* host) {
 
 int tslb_cuda_download_f(tslb_cuda_handle h, int species, void* host) {
   CK(cudaSetDevice(h->device));
+  if (species == 0)
+    if (int rc = materialize(h)) return rc;
   char* base;
   if (int rc = species_base(h, species, &base)) return rc;
   const size_t pb = size_t(h->n()) * h->esz;
@@ -782,6 +863,8 @@ int tslb_cuda_upload_field(tslb_cuda_handle h, int field, const void* host) {
   void* base; int cnt, eb; int64_t stride;
   if (int rc = field_desc(h, field, &base, &cnt, &eb, &stride, true)) return rc;
   CK(cudaSetDevice(h->device));
+  // the implicit f(t+1) is a function of the moment arrays being replaced
+  if (int rc = materialize(h)) return rc;
   const size_t pb = size_t(h->n()) * eb;
   for (int c = 0; c < cnt; ++c)
     CK(cudaMemcpyAsync(static_cast<char*>(base) + size_t(c) * stride * eb,
@@ -852,6 +935,7 @@ int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
                                    static_cast<T*>(h->f[1]), h->solid, s, h->s);
     }
     if (h->comps != 1) return set_err(TSLB_EINVAL, "analytic init %d needs one component", kind);
+    h->fimplicit = false;
     return launch_init_analytic<T>(h->lat, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
                                    h->d.has_solid ? h->solid : nullptr, s, h->s);
   });
@@ -867,9 +951,22 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
   long done = 0;
   // small domains are launch bound: replay a captured graph of G steps
   constexpr int64_t kGraphMaxNodes = int64_t(8) << 20;
-  constexpr long kGraphSteps = 32;
+  constexpr long kGraphSteps = 32;  // even: an M graph ends on the buffer it starts from
   if (h->graphs_ok && !h->prof && h->xmode == 0 && h->n() <= kGraphMaxNodes && nsteps >= kGraphSteps) {
-    if (!h->graph) {
+    // an M graph replays M passes only: leave the stored-f state first, and
+    // start from the moment buffer the graph was captured on
+    if (h->sched == TSLB_SCHED_M) {
+      if (!h->fimplicit) {
+        if (int rc = enqueue_step(h)) return rc;
+        ++done;
+      }
+      if (h->graph && h->graph_mo != h->mo) {
+        if (int rc = enqueue_step(h)) return rc;
+        ++done;
+      }
+    }
+    if (!h->graph && nsteps - done >= kGraphSteps) {
+      h->graph_mo = h->mo;
       const long steps0 = h->steps;
       const int64_t l0 = h->launches;
       cudaGraph_t g = nullptr;
@@ -887,7 +984,7 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
       if (ce != cudaSuccess) return set_err(TSLB_ECUDA, "graph instantiate: %s", cudaGetErrorString(ce));
       h->graph_steps = kGraphSteps;
     }
-    for (; done + h->graph_steps <= nsteps; done += h->graph_steps) {
+    for (; h->graph && done + h->graph_steps <= nsteps; done += h->graph_steps) {
       CK(cudaGraphLaunch(h->graph, h->s));
       h->steps += h->graph_steps;
       h->launches += h->graph_launches;
@@ -931,6 +1028,7 @@ int tslb_cuda_time_steps(tslb_cuda_handle h, long nsteps, double* ms) {
 int tslb_cuda_compute_moments(tslb_cuda_handle h) {
   if (h->comps != 1) return set_err(TSLB_EINVAL, "compute_moments is single-fluid");
   CK(cudaSetDevice(h->device));
+  if (int rc = materialize(h)) return rc;
   if (int rc = ph_moments(h, h->s)) return rc;
   return sync(h);
 }
@@ -939,6 +1037,7 @@ int tslb_cuda_stream_collide(tslb_cuda_handle h) {
   if (h->comps != 1) return set_err(TSLB_EINVAL, "stream_collide_fused is single-fluid");
   if (h->decomposed) return set_err(TSLB_ESTATE, "use step() on slab solvers");
   CK(cudaSetDevice(h->device));
+  if (int rc = materialize(h)) return rc;
   if (int rc = ph_streamcoll(h, 0, h->nzl, h->s)) return rc;
   return sync(h);
 }
@@ -947,6 +1046,7 @@ int tslb_cuda_reference_step(tslb_cuda_handle h, long nsteps) {
   if (h->comps != 1 || h->decomposed)
     return set_err(TSLB_EINVAL, "reference_step: single-fluid, single domain only");
   CK(cudaSetDevice(h->device));
+  if (int rc = materialize(h)) return rc;
   if (int rc = ensure_scratch(h)) return rc;
   for (long s = 0; s < nsteps; ++s) {
     if (int rc = ph_moments(h, h->s)) return rc;
@@ -971,6 +1071,7 @@ int tslb_cuda_stream_only(tslb_cuda_handle h) {
   if (h->comps != 1 || h->decomposed)
     return set_err(TSLB_EINVAL, "stream_only: single-fluid, single domain only");
   CK(cudaSetDevice(h->device));
+  if (int rc = materialize(h)) return rc;
   // pushes f into the second buffer (its slots not reached by any push keep
   // their contents, as in the reference), then swaps the two
   if (int rc = ensure_scratch(h)) return rc;
@@ -1018,6 +1119,7 @@ int tslb_cuda_stream_collide_recolor(tslb_cuda_handle h) {
 int tslb_cuda_refresh_moments(tslb_cuda_handle h) {
   CK(cudaSetDevice(h->device));
   if (h->comps == 1) {
+    if (int rc = materialize(h)) return rc;
     if (int rc = ph_moments(h, h->s)) return rc;
   } else {
     if (int rc = ph_cg_moments(h, h->s)) return rc;
@@ -1090,6 +1192,7 @@ int tslb_cuda_color_masses(tslb_cuda_handle h, double* red, double* blue) {
 
 int tslb_cuda_plane_digests(tslb_cuda_handle h, uint64_t* out) {
   CK(cudaSetDevice(h->device));
+  if (int rc = materialize(h)) return rc;
   const int64_t plane_bytes = h->plane() * h->esz;
   const int64_t cpp = (plane_bytes + 16383) / 16384;
   const size_t need = size_t(h->q) * h->nzl * (cpp + 1) * sizeof(uint64_t);

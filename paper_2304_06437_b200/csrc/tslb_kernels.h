@@ -38,15 +38,13 @@ int launch_streamcoll(int lat, int math, const Dom& d, T* f, const T* mo,
 template <typename T>
 int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
                           double omega, int vx, int kz, cudaStream_t st);
-// box geometry, TMA-staged tiles (moments in by TMA loads, populations out
-// by x-shifted TMA tensor stores); `maps` caches the encoded tensor maps
-// (opaque, owned by the caller, freed with free_tma_maps). Returns nonzero
-// (nothing launched) when the shape is not supported.
-struct TmaMaps;
+// moment-resident single-pass step (tslb_mstep.cu): m(t) in `mi` -> m(t+1)
+// in `mo` for box geometries; returns nonzero (nothing launched) when the
+// shape is not supported. lz = planes marched per CTA (0: default).
+bool mstep_supported(int lat, const Dom& d);
 template <typename T>
-int launch_streamcoll_tma(int lat, int math, const Dom& d, T* f, const T* mo,
-                          double omega, int kz, int vx, TmaMaps*& maps, cudaStream_t st);
-void free_tma_maps(TmaMaps* maps);
+int launch_mstep(int lat, int math, const Dom& d, const T* mi, T* mo, double omega,
+                 int lz, cudaStream_t st);
 template <typename T>
 int launch_collide(int lat, const Dom& d, T* f, const T* mo,
                    const uint8_t* solid, double omega, cudaStream_t st);

@@ -4,6 +4,7 @@
 #pragma once
 
 #include "tslb_collision.cuh"
+#include "tslb_domain.cuh"
 
 namespace tslb_cuda {
 
@@ -124,6 +125,24 @@ __device__ __forceinline__ void row_outputs(const NodeMoments<C> (&m)[VX], C om1
       }
     }
   });
+}
+
+// Bounce of direction A at node fi: f[opp][fi] = T(C(out) - 6 t (c.u_wall))
+// with u_wall summed in T over the crossed wall faces in axis order.
+template <class L, int A, typename T, typename C>
+__device__ __forceinline__ T bounce_value(const Dom& d, T out, bool cross_x,
+                                          bool cross_y, bool cross_z) {
+  using dd = Dir<L, A>;
+  T wx = T(0), wy = T(0), wz = T(0);
+  auto add = [&](int face) {
+    wx += T(d.uw[face][0]);
+    wy += T(d.uw[face][1]);
+    wz += T(d.uw[face][2]);
+  };
+  if (cross_x) add(dd::x > 0 ? XMax : XMin);
+  if (cross_y) add(dd::y > 0 ? YMax : YMin);
+  if (cross_z) add(dd::z > 0 ? ZMax : ZMin);
+  return T(C(out) - bounce_correction<L, A, C>(C(wx), C(wy), C(wz)));
 }
 
 }  // namespace tslb_cuda

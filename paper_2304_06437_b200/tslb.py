@@ -419,6 +419,17 @@ class DeviceSolver:
     def set_math(self, mode: int):
         self._call("tslb_cuda_set_math", mode)
 
+    def set_schedule(self, schedule: str):
+        """"f1" (moments pass + fused stream-collide) or "m" (moment-resident
+        single pass); same results bit for bit."""
+        self._call("tslb_cuda_set_schedule", {"f1": _lib.SCHED_F1, "m": _lib.SCHED_M}[schedule])
+
+    @property
+    def schedule(self) -> str:
+        v = C.c_int()
+        self._call("tslb_cuda_get_schedule", C.byref(v))
+        return "m" if v.value == _lib.SCHED_M else "f1"
+
     def init_analytic(self, kind: str, amplitude=0.0, radius=0.0):
         self._call("tslb_cuda_init_analytic", _lib.INIT[kind], float(amplitude), float(radius))
 

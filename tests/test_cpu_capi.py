@@ -14,7 +14,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 40
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
-    assert _lib.load().tslb_cuda_abi_version() == 1
+    assert _lib.load().tslb_cuda_abi_version() == 2
 
 
 def test_library_is_sm100a_native():
@@ -22,7 +22,7 @@ def test_library_is_sm100a_native():
     out = subprocess.run(["cuobjdump", "--list-elf", path], capture_output=True, text=True).stdout
     assert "sm_100a" in out
     sass = subprocess.run(["cuobjdump", "-sass", path], capture_output=True, text=True).stdout
-    assert "k_streamcoll" in sass and "k_moments" in sass and "STG" in sass
+    assert "k_streamcoll" in sass and "k_moments" in sass and "k_mstep" in sass and "STG" in sass
 
 
 def test_no_cpu_fallback_without_device():

@@ -1,0 +1,223 @@
+"""GPU parity of the moment-resident single-pass schedule (M, tslb_mstep.cu)
+against the CPU oracle: f(N) (materialised from m(N-1)) and the moment
+arrays m(N-1) must be bit-identical to fused_step run N times (kernels.hpp:
+209-215), for double and float storage, every face combination of a box,
+multiple z chunks per column (TSLB_LZ), graph replay, and every host-mirror
+transition (download, upload, refresh, phase calls, math-mode switch)."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2304_06437_b200 import _lib
+from paper_2304_06437_b200 import tslb as T
+
+from helpers import assert_bitwise, corner_box_3d, spec_of, zwalls_3d
+
+pytestmark = pytest.mark.gpu
+
+DT = [np.float64, np.float32]
+
+
+def xwalls_3d():
+    f = O.periodic()
+    f[0] = ("moving", (0.0, 0.02, -0.01))
+    f[1] = ("wall", (0, 0, 0))
+    return f
+
+
+def ylid_3d():
+    f = O.periodic()
+    f[2] = ("wall", (0, 0, 0))
+    f[3] = ("moving", (0.05, 0.0, 0.01))
+    return f
+
+
+CASES = [
+    ("periodic", (32, 8, 5), O.periodic()),
+    ("periodic-nz1", (32, 8, 1), O.periodic()),
+    ("periodic-wide", (64, 16, 11), O.periodic()),
+    ("zwalls", (32, 16, 9), zwalls_3d()),
+    ("zwalls-nz2", (32, 8, 2), zwalls_3d()),
+    ("xwalls", (64, 8, 4), xwalls_3d()),
+    ("ylid", (32, 16, 5), ylid_3d()),
+    ("closed-box", (64, 8, 4), O.closed_box()),
+    ("box-corners", (32, 16, 7), corner_box_3d()),
+]
+
+
+def _moments(dev, lat):
+    L = T.lattice_of(lat)
+    return np.concatenate([dev.download_field("rho")[None], dev.download_field("mom").reshape(L.dim, -1),
+                           dev.download_field("pineq").reshape(L.npineq, -1)])
+
+
+def _oracle(oracle_port, lat, dims, omega, faces, f0, steps):
+    f = f0.copy()
+    mo = np.zeros((O.moments_layout(lat), f.shape[1]), f.dtype)
+    oracle_port.single_run(lat, dims, omega, faces, f, mo, steps, 0)
+    return f, mo
+
+
+@pytest.mark.parametrize("lz", ["", "3"])
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("lat", ["d3q19", "d3q27"])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: c[0])
+def test_mstep_bitwise(gpu, oracle_port, case, lat, dtype, lz, monkeypatch):
+    name, dims, faces = case
+    if lz:
+        monkeypatch.setenv("TSLB_LZ", lz)
+    f0 = O.random_state(lat, dims, 11, dtype)
+    steps = 5
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 0.87, spec_of(faces), dtype)
+    try:
+        assert dev.schedule == "m", "M schedule should be the default for this box"
+        dev.upload_f(f0)
+        dev.step(steps)
+        mg = _moments(dev, lat)
+        fg = dev.download_f()
+    finally:
+        dev.close()
+    fo, mo = _oracle(oracle_port, lat, dims, 0.87, faces, f0, steps)
+    assert_bitwise(mg, mo, f"M {lat}/{name} moments m(N-1)")
+    assert_bitwise(fg, fo, f"M {lat}/{name} f(N)")
+
+
+@pytest.mark.parametrize("lat", ["d3q19", "d3q27"])
+@pytest.mark.parametrize("case", [CASES[2], CASES[8]], ids=lambda c: c[0])
+def test_mstep_f32_math_equals_f1(gpu, case, lat):
+    """fp32 node arithmetic (opt-in): no oracle bits, but the two schedules
+    perform the same float operations, so they must agree bit for bit."""
+    name, dims, faces = case
+    f0 = O.random_state(lat, dims, 5, np.float32)
+    out = {}
+    for sched in ("f1", "m"):
+        dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.3, spec_of(faces), np.float32)
+        try:
+            dev.set_schedule(sched)
+            dev.set_math(_lib.MATH_F32)
+            dev.upload_f(f0)
+            dev.step(6)
+            out[sched] = (dev.download_f(), _moments(dev, lat))
+        finally:
+            dev.close()
+    assert_bitwise(out["m"][0], out["f1"][0], f"f32 math {lat}/{name} f")
+    assert_bitwise(out["m"][1], out["f1"][1], f"f32 math {lat}/{name} moments")
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_mstep_graph_replay_parity(gpu, oracle_port, dtype):
+    """Small domains replay a captured graph of 32 M passes; odd step counts
+    leave the ping-pong buffers swapped, which the next call must honour."""
+    lat, dims, faces = "d3q19", (32, 16, 12), zwalls_3d()
+    f0 = O.random_state(lat, dims, 3, dtype)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.15, spec_of(faces), dtype)
+    try:
+        dev.upload_f(f0)
+        for n in (40, 33, 35, 64):
+            dev.step(n)
+        mg = _moments(dev, lat)
+        fg = dev.download_f()
+    finally:
+        dev.close()
+    fo, mo = _oracle(oracle_port, lat, dims, 1.15, faces, f0, 172)
+    assert_bitwise(mg, mo, "graph M moments")
+    assert_bitwise(fg, fo, "graph M f")
+
+
+def test_mstep_host_mirror_transitions(gpu, oracle_port):
+    """Every API that reads or replaces state while f is implicit."""
+    lat, dims, faces, om = "d3q19", (32, 8, 6), corner_box_3d(), 1.4
+    dt = np.float64
+    f0 = O.random_state(lat, dims, 21, dt)
+    ref = f0.copy()
+    rmo = np.zeros((O.moments_layout(lat), ref.shape[1]), dt)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), om, spec_of(faces), dt)
+    try:
+        dev.upload_f(f0)
+        # step, read f mid-run (materialise), keep stepping
+        dev.step(3)
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, 3, 0)
+        assert_bitwise(dev.download_f(), ref, "f after 3")
+        dev.step(4)
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, 4, 0)
+        assert_bitwise(_moments(dev, lat), rmo, "lagged moments after 7")
+        # refresh_moments: moments of the current f
+        dev.phase("refresh_moments")
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, 1, 2)
+        assert_bitwise(_moments(dev, lat), rmo, "refreshed moments")
+        assert_bitwise(dev.download_f(), ref, "f after refresh")
+        # step again from the stored-f state
+        dev.step(2)
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, 2, 0)
+        # overwrite moments while f is implicit: the step that follows
+        # recomputes them from f, as fused_step does
+        junk = np.full_like(rmo[0], 7.0)
+        dev.upload_field("rho", junk)
+        dev.step(2)
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, 2, 0)
+        assert_bitwise(dev.download_f(), ref, "f after moment upload + steps")
+        # phase calls on an implicit f
+        dev.step(1)
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, 1, 0)
+        dev.phase("compute_moments")
+        dev.phase("stream_collide")
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, 1, 0)
+        assert_bitwise(dev.download_f(), ref, "f after phase calls")
+        # digest of an implicit f equals the digest of the stored one
+        dev.step(2)
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, 2, 0)
+        d_implicit = dev.plane_digests()
+        assert_bitwise(dev.download_f(), ref, "f after digest")
+        assert np.array_equal(d_implicit, dev.plane_digests())
+        # upload f while implicit: the next step starts from the upload
+        f1 = O.random_state(lat, dims, 22, dt)
+        dev.step(1)
+        dev.upload_f(f1)
+        dev.step(3)
+        ref = f1.copy()
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, 3, 0)
+        assert_bitwise(dev.download_f(), ref, "f after re-upload")
+        # switching schedules mid-run
+        dev.step(2)
+        dev.set_schedule("f1")
+        dev.step(2)
+        dev.set_schedule("m")
+        dev.step(3)
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, 7, 0)
+        assert_bitwise(dev.download_f(), ref, "f across schedule switches")
+        assert_bitwise(_moments(dev, lat), rmo, "moments across schedule switches")
+    finally:
+        dev.close()
+
+
+def test_mstep_diagnostics_use_lagged_moments(gpu, oracle_port):
+    lat, dims, faces = "d3q19", (32, 8, 4), O.periodic()
+    f0 = O.random_state(lat, dims, 9, np.float64)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.2, spec_of(faces), np.float64)
+    try:
+        dev.upload_f(f0)
+        dev.step(4)
+        mass, mom = dev.totals()
+        mg = _moments(dev, lat)
+    finally:
+        dev.close()
+    fo, mo = _oracle(oracle_port, lat, dims, 1.2, faces, f0, 4)
+    assert_bitwise(mg, mo, "moments")
+    assert abs(mass - mo[0].sum()) <= 1e-12 * mo[0].size
+    assert np.allclose(mom, mo[1:4].sum(1), rtol=0, atol=1e-12 * mo[0].size)
+
+
+def test_schedule_rules(gpu):
+    spec = spec_of(O.periodic())
+    dev = T.DeviceSolver("d3q19", T.GridDims(30, 8, 4), 1.0, spec, np.float32)
+    try:
+        assert dev.schedule == "f1"
+        with pytest.raises(RuntimeError):
+            dev.set_schedule("m")
+    finally:
+        dev.close()
+    dev = T.DeviceSolver("d2q9", T.GridDims(64, 64, 1), 1.0, spec, np.float32)
+    try:
+        assert dev.schedule == "f1"
+    finally:
+        dev.close()
