@@ -182,13 +182,17 @@ def kernel_bytes(lat, comps, es):
     npi = D * (D + 1) // 2
     nm = 1 + D + npi
     if comps == 1:
-        return {"moments": (q + nm) * es, "streamcoll": (nm + q) * es}
+        # F1: moments pass + stream-collide; M: one moment-resident pass
+        return {"moments": (q + nm) * es, "streamcoll": (nm + q) * es, "mstep": 2 * nm * es}
     return {"cg_moments": (2 * q + 3 + nm) * es, "cg_gradient": (1 + D) * es,
             "cg_streamcoll": (3 + D + npi + D + 2 * q) * es}
 
 
-def step_bytes(lat, comps, es):
-    return sum(kernel_bytes(lat, comps, es).values())
+def step_bytes(lat, comps, es, schedule="f1"):
+    kb = kernel_bytes(lat, comps, es)
+    if comps == 1:
+        return kb["mstep"] if schedule == "m" else kb["moments"] + kb["streamcoll"]
+    return sum(kb.values())
 
 
 def main():
@@ -200,6 +204,7 @@ def main():
     ap.add_argument("--workload", default="tgv-d3q19", choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=0, help="override the per-GPU cube edge (3D)")
     ap.add_argument("--math", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--schedule", default="auto", choices=["auto", "m", "f1"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sample-nz", type=int, default=16)
@@ -259,6 +264,8 @@ def main():
     sim = T.DeviceSolver(lat, g, W["omega"], spec, dtype, W["comps"], None, color, dev_id, slab=slab)
     if args.math == "f32":
         sim.set_math(_lib.MATH_F32)
+    if args.schedule != "auto" and W["comps"] == 1:
+        sim.set_schedule(args.schedule)
     if world > 1:
         import ctypes as C
         uid = (C.c_char * 128)()
@@ -310,7 +317,8 @@ def main():
     local_nodes = nx * ny * nzp
     achieved = per_node[dom] * local_nodes / (k_ms / k_n / 1e3) / 1e9
     hbm, peak_kind, _ = peaks()
-    sb = step_bytes(lat, W["comps"], es)
+    sched = sim.schedule if W["comps"] == 1 else "f1"
+    sb = step_bytes(lat, W["comps"], es, sched)
     step_bw = glups * sb / world  # per-GPU GB/s of the whole step
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": None, "kernel": f"k_{dom}",
@@ -343,8 +351,10 @@ def main():
                           + (f" (global {nx}x{ny}x{nz_g}, z slabs)" if world > 1 else ""),
                           "lattice": lat.name, "nodes": nodes, "storage": W["storage"],
                           "node_math": (args.math if W["comps"] == 1 else W["storage"] + " (as the reference)"),
-                          "schedule": "F1: moments + fused stream-collide" if W["comps"] == 1
-                          else "colour moments + gradient + fused prepare/stream-collide-recolour",
+                          "schedule": ({"m": "M: moment-resident single pass (populations rebuilt in shared "
+                                             "memory; f materialised on read)",
+                                        "f1": "F1: moments + fused stream-collide"}[sched] if W["comps"] == 1
+                                       else "colour moments + gradient + fused prepare/stream-collide-recolour"),
                           "l2": "state >> 126 MB L2, no flush needed" if nodes > 10 ** 7
                           else "L2-resident (correctness config)",
                           "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},

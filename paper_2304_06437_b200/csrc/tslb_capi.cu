@@ -112,6 +112,7 @@ struct tslb_cuda_sim {
   int lz = 0;          // planes per CTA of the M kernel (0 = default; TSLB_LZ)
   void* mo2 = nullptr; // second moment buffer of the M schedule (ping-pong)
   void* graph_mo = nullptr;  // moment buffer the captured graph starts from
+  MstepMaps* mmaps = nullptr;  // TMA tensor maps of the M kernel's inputs
   int vx = 0;          // nodes per thread in the vectorised kernel (0 = default; TSLB_VX)
   int kz = 0;          // planes per block of the pipelined kernel (<= 1: off; TSLB_KZ)
   bool staged = false; // slab halos received into staging + masked unpack
@@ -273,7 +274,7 @@ int ph_mstep(tslb_cuda_sim* h, cudaStream_t st) {
     int rc = by_scalar(h, [&](auto z) {
       using T = decltype(z);
       return launch_mstep<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<const T*>(h->mo),
-                             static_cast<T*>(h->mo2), h->omega, h->lz, st);
+                             static_cast<T*>(h->mo2), h->omega, h->lz, h->mmaps, st);
     });
     if (rc) return set_err(TSLB_ESTATE, "M step not supported for this domain");
   }
@@ -731,6 +732,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->graph) cudaGraphExecDestroy(h->graph);
+  free_mstep_maps(h->mmaps);
   for (auto e : h->pool) cudaEventDestroy(e);
   cudaEvent_t evs[] = {h->ev_b, h->ev_c, h->t0, h->t1};
   for (auto e : evs)

@@ -40,11 +40,15 @@ int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
                           double omega, int vx, int kz, cudaStream_t st);
 // moment-resident single-pass step (tslb_mstep.cu): m(t) in `mi` -> m(t+1)
 // in `mo` for box geometries; returns nonzero (nothing launched) when the
-// shape is not supported. lz = planes marched per CTA (0: default).
+// shape is not supported. lz = planes marched per CTA (0: default); `maps`
+// caches the TMA tensor maps of the input buffers (opaque, owned by the
+// caller, freed with free_mstep_maps).
+struct MstepMaps;
+void free_mstep_maps(MstepMaps* maps);
 bool mstep_supported(int lat, const Dom& d);
 template <typename T>
 int launch_mstep(int lat, int math, const Dom& d, const T* mi, T* mo, double omega,
-                 int lz, cudaStream_t st);
+                 int lz, MstepMaps*& maps, cudaStream_t st);
 template <typename T>
 int launch_collide(int lat, const Dom& d, T* f, const T* mo,
                    const uint8_t* solid, double omega, cudaStream_t st);

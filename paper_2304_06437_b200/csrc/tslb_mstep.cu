@@ -25,12 +25,15 @@
 // 68-69), so every API reads the same bits as after F1.
 //
 // Shape: a CTA owns a 32 x 8 column tile and marches through LZ planes
-// (2.5-D blocking). Moments of plane z+1 are staged with cp.async while
-// plane z is collided; slots live in per-direction plane rings sized by the
-// direction's c_z (a slot of destination plane d is written while the march
-// is at plane d - c_z, or at d for a bounce, and read at plane d + 1), so a
-// single __syncthreads per plane orders every write before its read. Pure-z
-// and rest directions never leave the thread: they ride a register ring.
+// (2.5-D blocking). The moments of plane z+1 -- all 1+D+np arrays of the
+// tile plus the rows just below and above it -- arrive by ONE TMA tensor
+// load (cp.async.bulk.tensor, 4-D box, mbarrier completion) while plane z
+// is collided; the x-halo columns and wrapped rows come in by cp.async.
+// Slots live in per-direction plane rings sized by the direction's c_z (a
+// slot of destination plane d is written while the march is at plane
+// d - c_z, or at d for a bounce, and read after the march passed d), two
+// barriers per plane. Pure-z and rest directions never leave the thread:
+// they ride a register ring.
 // Ring nodes outside the tile (one-node x/y halo, the planes just below and
 // above the march) only rebuild the directions that land inside the tile;
 // they never bounce (a push that lands in the tile cannot cross a wall).
@@ -42,7 +45,9 @@
 // reference order only for rho == -0.0; the moments this kernel reads are
 // always produced by a +0-seeded sum (k_moments or this kernel), which
 // cannot return -0.0, so the rewrite is exact here.
+#include <cuda.h>
 #include <cuda_pipeline.h>
+#include <cuda_runtime.h>
 
 #include <cstdint>
 
@@ -52,22 +57,35 @@
 #include "tslb_pair.cuh"
 
 namespace tslb_cuda {
+
+// encoded tensor maps of the moment buffers used as M-step inputs
+struct MstepMaps {
+  struct Entry {
+    CUtensorMap map;
+    const void* base = nullptr;
+    int64_t key[5] = {0, 0, 0, 0, 0};
+  } e[2];
+  int next = 0;
+};
+void free_mstep_maps(MstepMaps* m) { delete m; }
+
 namespace mstep {
 
 constexpr int TX = 32;                     // tile width (one warp per row)
 constexpr int TY = 8;                      // tile rows (warps per CTA)
 constexpr int NT = TX * TY;                // threads = tile columns
 constexpr int NH = 2 * TX + 2 * TY + 4;    // halo ring nodes
-constexpr int NS = NT + NH;                // staged nodes per plane
+constexpr int TR = TY + 2;                 // staged tile rows (with y halo)
+constexpr int TC = TR * TX;                // staged elements per moment array
 
 template <class L>
 __host__ __device__ constexpr bool is_reg(int a) {
   return L::c[a][0] == 0 && L::c[a][1] == 0;
 }
-// plane-ring depth of slot direction a (see header): 4 for c_z = +1, else 3
+// plane-ring depth of slot direction a (see header): 3 for c_z = +1, else 2
 template <class L>
 __host__ __device__ constexpr int ring_depth(int a) {
-  return L::c[a][2] == 1 ? 4 : 3;
+  return L::c[a][2] == 1 ? 3 : 2;
 }
 template <class L>
 __host__ __device__ constexpr int slot_base(int a) {
@@ -84,9 +102,47 @@ template <class L>
 __host__ __device__ constexpr int n_moments() {
   return 1 + L::dim + L::dim * (L::dim + 1) / 2;
 }
+__host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) / 128 * 128; }
+
+// dynamic shared memory: [tile buf 0 | tile buf 1 | wstg 0 | wstg 1 | slots | mbarriers]
 template <class L, typename T>
-constexpr size_t smem_bytes() {
-  return (size_t(slot_planes<L>()) * NT + size_t(2) * n_moments<L>() * NS) * sizeof(T);
+struct Smem {
+  static constexpr size_t tile = align128(size_t(n_moments<L>()) * TC * sizeof(T));
+  static constexpr size_t wstg = align128(size_t(n_moments<L>()) * NH * sizeof(T));
+  static constexpr size_t slots = size_t(slot_planes<L>()) * NT * sizeof(T);
+  static constexpr size_t off_wstg = 2 * tile;
+  static constexpr size_t off_slots = off_wstg + 2 * wstg;
+  static constexpr size_t off_bar = align128(off_slots + slots);
+  static constexpr size_t total = off_bar + 2 * sizeof(uint64_t);
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void tma_load_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
 }
 
 // coordinate after crossing a face: wrapped (periodic) or -1 (wall: absent)
@@ -97,21 +153,20 @@ __device__ __forceinline__ int wrap_coord(int g, int n, int lo, int hi) {
 }
 
 // ring offsets (in elements) of destination planes z-1, z, z+1 relative to
-// the plane being pushed, for 3- and 4-deep rings
+// the plane being pushed, for 2- and 3-deep rings
 struct Ring {
-  int o3[3], o4[3];
-  int p3, p4;
+  int o2[2], o3[3];
+  int p2, p3;
   __device__ __forceinline__ void set() {
+    o2[0] = (p2 ^ 1) * NT;
+    o2[1] = p2 * NT;
     o3[0] = (p3 == 0 ? 2 : p3 - 1) * NT;
     o3[1] = p3 * NT;
     o3[2] = (p3 == 2 ? 0 : p3 + 1) * NT;
-    o4[0] = ((p4 + 3) & 3) * NT;
-    o4[1] = p4 * NT;
-    o4[2] = ((p4 + 1) & 3) * NT;
   }
   __device__ __forceinline__ void advance() {
+    p2 ^= 1;
     p3 = p3 == 2 ? 0 : p3 + 1;
-    p4 = (p4 + 1) & 3;
     set();
   }
 };
@@ -119,22 +174,20 @@ struct Ring {
 template <class L, int A, int DZ, typename T>
 __device__ __forceinline__ T* slot(T* sl, const Ring& rg, int lx, int ly) {
   constexpr int base = slot_base<L>(A) * NT;
-  const int ro = ring_depth<L>(A) == 4 ? rg.o4[DZ + 1] : rg.o3[DZ + 1];
+  int ro;
+  if constexpr (ring_depth<L>(A) == 3) ro = rg.o3[DZ + 1];
+  else ro = rg.o2[DZ + 1];  // DZ is -1 or 0 for 2-deep rings
   return sl + base + ro + ly * TX + lx;
 }
 
 template <class L, typename T, typename C>
-__device__ __forceinline__ NodeMoments<C> staged_node(const T* s, int node) {
+__device__ __forceinline__ NodeMoments<C> node_at(const T* s, int stride) {
   constexpr int NM = n_moments<L>();
   T v[NM];
 #pragma unroll
-  for (int c = 0; c < NM; ++c) v[c] = s[c * NS + node];
-  if constexpr (L::dim == 3)
-    return prepare_node<C>(C(v[0]), C(v[1]), C(v[2]), C(v[3]), C(v[4]), C(v[5]),
-                           C(v[6]), C(v[7]), C(v[8]), C(v[9]));
-  else
-    return prepare_node<C>(C(v[0]), C(v[1]), C(v[2]), C(0), C(v[3]), C(v[4]), C(0),
-                           C(v[5]), C(0), C(0));
+  for (int c = 0; c < NM; ++c) v[c] = s[c * stride];
+  return prepare_node<C>(C(v[0]), C(v[1]), C(v[2]), C(v[3]), C(v[4]), C(v[5]), C(v[6]), C(v[7]), C(v[8]),
+                         C(v[9]));
 }
 
 // per-thread wall contact of the tile node (only for WALLS kernels)
@@ -189,16 +242,16 @@ __device__ __forceinline__ void push_tile(const Dom& d, T* sl, const Ring& rg, T
         emit<L, a, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(ra));
         emit<L, a + 1, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(rb));
       } else if constexpr (ua) {
-        emit<L, a, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(post_collision<L, a, C>(m, om1)));
+        emit<L, a, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(post_single<L, a, C>(m, om1)));
       } else if constexpr (ub) {
-        emit<L, a + 1, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(post_collision<L, a + 1, C>(m, om1)));
+        emit<L, a + 1, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(post_single<L, a + 1, C>(m, om1)));
       }
     }
   });
 }
 
 // A halo node at tile-local (hx, hy) on side (SX, SY): only the directions
-// pointing into the tile, reference order (no pair partner is needed).
+// pointing into the tile.
 template <class L, typename T, typename C, int SX, int SY, int ZC>
 __device__ __forceinline__ void push_halo(T* sl, const Ring& rg, int hx, int hy,
                                           const NodeMoments<C>& m, C om1) {
@@ -212,7 +265,7 @@ __device__ __forceinline__ void push_halo(T* sl, const Ring& rg, int hx, int hy,
       bool in = true;
       if constexpr (SX == 0 && dd::x != 0) in = unsigned(tx) < unsigned(TX);
       if constexpr (SY == 0 && dd::y != 0) in = in && unsigned(ty) < unsigned(TY);
-      if (in) *slot<L, a, dd::z>(sl, rg, tx, ty) = T(post_collision<L, a, C>(m, om1));
+      if (in) *slot<L, a, dd::z>(sl, rg, tx, ty) = T(post_single<L, a, C>(m, om1));
     }
   });
 }
@@ -276,14 +329,19 @@ __device__ __forceinline__ void finalize(const Dom& d, T* sl, const Ring& rg, co
   mo[9 * ms + idx] = T(pyz - jy * jz);
 }
 
-template <class L, typename T, typename C, bool WALLS>
-__global__ void __launch_bounds__(NT, 2)
-    k_mstep(Dom d, const T* __restrict__ mi, T* __restrict__ mo, C om1, int lz) {
+template <class L, typename T, typename C, bool WALLS, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
+    k_mstep(const __grid_constant__ CUtensorMap tmap, Dom d, const T* __restrict__ mi, T* __restrict__ mo,
+            C om1, int lz) {
   static_assert(L::dim == 3, "the M step is 3-D");
+  using SM = Smem<L, T>;
   constexpr int NM = n_moments<L>();
-  extern __shared__ __align__(16) unsigned char smraw[];
-  T* sl = reinterpret_cast<T*>(smraw);
-  T* stg = sl + slot_planes<L>() * NT;  // [2][NM][NS] staged moments
+  extern __shared__ __align__(128) unsigned char smraw[];
+  T* tile = reinterpret_cast<T*>(smraw);                  // [2][NM][TR][TX]
+  T* wstg = reinterpret_cast<T*>(smraw + SM::off_wstg);   // [2][NM][NH]
+  T* sl = reinterpret_cast<T*>(smraw + SM::off_slots);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + SM::off_bar);
+  constexpr int TILE_B = int(SM::tile / sizeof(T)), WSTG_B = int(SM::wstg / sizeof(T));
 
   const int tid = threadIdx.x, lx = tid & (TX - 1), ly = tid >> 5;
   const int x0 = int(blockIdx.x) * TX, y0 = int(blockIdx.y) * TY;
@@ -292,7 +350,9 @@ __global__ void __launch_bounds__(NT, 2)
   const int64_t col = gx + int64_t(d.nx) * gy;
 
   // halo role of this thread: warp 0 the row below the tile, warp 1 the row
-  // above, warps 2/3 the columns left/right, warp 4 the four corners
+  // above, warps 2/3 the columns left/right, warp 4 the four corners. Rows
+  // inside the domain come with the TMA tile; the x columns, the corners and
+  // wrapped rows are fetched by the lane itself (cp.async into wstg).
   int hnode = -1, role = 0, hx = 0, hy = 0;
   if (ly == 0) { hnode = lx; role = 0; hx = lx; hy = -1; }
   else if (ly == 1) { hnode = TX + lx; role = 1; hx = lx; hy = TY; }
@@ -305,11 +365,23 @@ __global__ void __launch_bounds__(NT, 2)
     hy = (lx & 2) ? TY : -1;
   }
   int64_t hcol = 0;
+  bool hfetch = false;  // this lane loads its halo node itself
+  int hoff = 0, hstride = TC;  // where the halo node's moments are staged
   if (hnode >= 0) {
     const int hgx = wrap_coord(x0 + hx, d.nx, d.mode[XMin], d.mode[XMax]);
     const int hgy = wrap_coord(y0 + hy, d.ny, d.mode[YMin], d.mode[YMax]);
-    if (hgx < 0 || hgy < 0) hnode = -1;
-    else hcol = hgx + int64_t(d.nx) * hgy;
+    if (hgx < 0 || hgy < 0) {
+      hnode = -1;
+    } else {
+      hcol = hgx + int64_t(d.nx) * hgy;
+      hfetch = role >= 2 || hgy != y0 + hy;
+      if (hfetch) {
+        hoff = hnode;
+        hstride = NH;
+      } else {
+        hoff = (hy + 1) * TX + hx;
+      }
+    }
   }
   Contact ct{};
   if constexpr (WALLS) {
@@ -318,19 +390,27 @@ __global__ void __launch_bounds__(NT, 2)
     ct.ylo = gy == 0 && d.mode[YMin] == kWall;
     ct.yhi = gy == d.ny - 1 && d.mode[YMax] == kWall;
   }
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
 
-  auto issue = [&](int z, int buf) {
+  constexpr uint32_t kTileBytes = uint32_t(NM * TC * sizeof(T));
+  auto issue = [&](int z, int b) {
     const int zz = wrap_coord(z, d.nz, d.mode[ZMin], d.mode[ZMax]);
     if (zz < 0) return;
-    T* s = stg + buf * NM * NS;
-    const int64_t pl = int64_t(zz) * d.plane;
+    if (tid == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(&bar[b], kTileBytes);
+      tma_load_4d(tile + b * TILE_B, &tmap, &bar[b], x0, y0 - 1, zz, 0);
+    }
+    if (hfetch) {
+      T* w = wstg + b * WSTG_B + hnode;
+      const T* g = mi + int64_t(zz) * d.plane + hcol;
 #pragma unroll
-    for (int c = 0; c < NM; ++c)
-      __pipeline_memcpy_async(s + c * NS + tid, mi + c * d.mstride + pl + col, sizeof(T));
-    if (hnode >= 0) {
-#pragma unroll
-      for (int c = 0; c < NM; ++c)
-        __pipeline_memcpy_async(s + c * NS + NT + hnode, mi + c * d.mstride + pl + hcol, sizeof(T));
+      for (int c = 0; c < NM; ++c) __pipeline_memcpy_async(w + c * NH, g + c * d.mstride, sizeof(T));
     }
   };
 
@@ -338,32 +418,36 @@ __global__ void __launch_bounds__(NT, 2)
 #pragma unroll
   for (int a = 0; a < L::q; ++a) R[a][0] = R[a][1] = R[a][2] = T(0);
   Ring rg;
+  rg.p2 = 0;
   rg.p3 = 0;
-  rg.p4 = 0;
   rg.set();
   int buf = 0;
+  uint32_t phase = 0;  // bit b: parity of the next completion of bar[b]
 
   auto plane = [&](auto ZCc, int z) {
     constexpr int ZC = decltype(ZCc)::value;
     if (ZC != -1) issue(z + 1, buf ^ 1);
     __pipeline_commit();
-    __pipeline_wait_prior(1);
     if (wrap_coord(z, d.nz, d.mode[ZMin], d.mode[ZMax]) >= 0) {
-      const T* s = stg + buf * NM * NS;
+      mbar_wait(&bar[buf], (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+      __pipeline_wait_prior(1);
+      const T* tb = tile + buf * TILE_B;
       if constexpr (WALLS) {
         ct.zlo = z == 0 && d.mode[ZMin] == kWall;
         ct.zhi = z == d.nz - 1 && d.mode[ZMax] == kWall;
       }
-      const NodeMoments<C> m = staged_node<L, T, C>(s, tid);
+      const NodeMoments<C> m = node_at<L, T, C>(tb + (ly + 1) * TX + lx, TC);
       push_tile<L, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, m, om1);
       if (hnode >= 0) {
-        const NodeMoments<C> hm = staged_node<L, T, C>(s, NT + hnode);
+        const T* hb = (hfetch ? wstg + buf * WSTG_B : tb) + hoff;
+        const NodeMoments<C> hm = node_at<L, T, C>(hb, hstride);
         push_ring<L, T, C, ZC>(sl, rg, role, hx, hy, hm, om1);
       }
     }
     __syncthreads();
-    if (z - 1 >= za)
-      finalize<L, T, C>(d, sl, rg, R, lx, ly, mo, col + int64_t(z - 1) * d.plane);
+    if (z - 1 >= za) finalize<L, T, C>(d, sl, rg, R, lx, ly, mo, col + int64_t(z - 1) * d.plane);
+    __syncthreads();
 #pragma unroll
     for (int a = 0; a < L::q; ++a) {
       R[a][0] = R[a][1];
@@ -381,47 +465,97 @@ __global__ void __launch_bounds__(NT, 2)
   plane(std::integral_constant<int, -1>{}, zb);
 }
 
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encoder() {
+  static EncodeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  }
+  return fn;
+}
+
+// 4-D map (x, y, z, moment array) with a {TX, TY + 2, 1, NM} box
+template <typename T>
+const CUtensorMap* tensor_map(MstepMaps*& maps, const Dom& d, int nm, const T* base) {
+  if (!maps) maps = new MstepMaps();
+  const int64_t key[5] = {d.nx, d.ny, d.nz, d.mstride, int64_t(sizeof(T)) * 16 + nm};
+  for (auto& e : maps->e) {
+    bool same = e.base == base;
+    for (int i = 0; i < 5 && same; ++i) same = e.key[i] == key[i];
+    if (same) return &e.map;
+  }
+  EncodeFn enc = encoder();
+  if (!enc) return nullptr;
+  auto& e = maps->e[maps->next];
+  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const cuuint64_t es = sizeof(T);
+  const cuuint32_t estr[4] = {1, 1, 1, 1};
+  const cuuint64_t dim[4] = {cuuint64_t(d.nx), cuuint64_t(d.ny), cuuint64_t(d.nz), cuuint64_t(nm)};
+  const cuuint64_t str[3] = {cuuint64_t(d.nx) * es, cuuint64_t(d.plane) * es, cuuint64_t(d.mstride) * es};
+  const cuuint32_t box[4] = {cuuint32_t(TX), cuuint32_t(TR), 1, cuuint32_t(nm)};
+  if (enc(&e.map, dt, 4, const_cast<T*>(base), dim, str, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return nullptr;
+  e.base = base;
+  for (int i = 0; i < 5; ++i) e.key[i] = key[i];
+  maps->next ^= 1;
+  return &e.map;
+}
+
 }  // namespace mstep
 
 bool mstep_supported(int lat, const Dom& d) {
   return (lat == kD3Q19 || lat == kD3Q27) && !d.has_solid && d.ghost == 0 &&
-         d.nx % mstep::TX == 0 && d.ny % mstep::TY == 0;
+         d.nx % mstep::TX == 0 && d.ny % mstep::TY == 0 && mstep::encoder() != nullptr;
 }
 
 template <typename T>
 int launch_mstep(int lat, int math, const Dom& d, const T* mi, T* mo, double omega,
-                 int lz, cudaStream_t st) {
+                 int lz, MstepMaps*& maps, cudaStream_t st) {
   using namespace mstep;
   if (!mstep_supported(lat, d)) return 1;
-  if (lz <= 0) lz = 32;
+  if (lz <= 0) lz = 64;
   bool walls = false;
   for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
   const dim3 grid(unsigned(d.nx / TX), unsigned(d.ny / TY), unsigned((d.nz + lz - 1) / lz));
   if (grid.y > 65535 || grid.z > 65535) return 1;
   const double om1d = 1.0 - double(T(omega));
   const float om1f = 1.0f - float(omega);
-  auto go = [&](auto L, auto kern, auto om1) {
-    using Lat = decltype(L);
-    constexpr size_t smem = smem_bytes<Lat, T>();
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    kern<<<grid, NT, smem, st>>>(d, mi, mo, om1, lz);
-  };
   auto by_lat = [&](auto L) {
     using Lat = decltype(L);
+    const CUtensorMap* tm = tensor_map<T>(maps, d, n_moments<Lat>(), mi);
+    if (!tm) return 1;
+    constexpr size_t smem = Smem<Lat, T>::total;
+    auto go = [&](auto kern, auto om1) {
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      kern<<<grid, NT, smem, st>>>(*tm, d, mi, mo, om1, lz);
+    };
+    // fp32 node math fits three CTAs per SM (registers and shared memory)
     if (math == kMathDouble) {
-      if (walls) go(L, k_mstep<Lat, T, double, true>, om1d);
-      else go(L, k_mstep<Lat, T, double, false>, om1d);
+      if (walls) go(k_mstep<Lat, T, double, true, 2>, om1d);
+      else go(k_mstep<Lat, T, double, false, 2>, om1d);
     } else {
-      if (walls) go(L, k_mstep<Lat, T, float, true>, om1f);
-      else go(L, k_mstep<Lat, T, float, false>, om1f);
+      if (walls) go(k_mstep<Lat, T, float, true, 3>, om1f);
+      else go(k_mstep<Lat, T, float, false, 3>, om1f);
     }
+    return 0;
   };
-  if (lat == kD3Q19) by_lat(D3Q19{});
-  else by_lat(D3Q27{});
-  return 0;
+  return lat == kD3Q19 ? by_lat(D3Q19{}) : by_lat(D3Q27{});
 }
 
-template int launch_mstep<float>(int, int, const Dom&, const float*, float*, double, int, cudaStream_t);
-template int launch_mstep<double>(int, int, const Dom&, const double*, double*, double, int, cudaStream_t);
+template int launch_mstep<float>(int, int, const Dom&, const float*, float*, double, int, MstepMaps*&,
+                                 cudaStream_t);
+template int launch_mstep<double>(int, int, const Dom&, const double*, double*, double, int, MstepMaps*&,
+                                  cudaStream_t);
 
 }  // namespace tslb_cuda

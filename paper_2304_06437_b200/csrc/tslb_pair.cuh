@@ -50,22 +50,6 @@ __device__ __forceinline__ C dot_noseed(C x, C y, C z) {
   return s;
 }
 
-// Post-collision values of the pair (A, A+1 = opp(A)), A odd.
-template <class L, int A, typename C>
-__device__ __forceinline__ void post_pair(const NodeMoments<C>& m, C om1,
-                                          C& out_a, C& out_b) {
-  using d = Dir<L, A>;
-  constexpr C t = d::template t<C>();
-  const C cu = dot_noseed<d::x, d::y, d::z, C>(m.ux, m.uy, m.uz);
-  const C c3 = C(3) * cu;
-  const C q = C(4.5) * cu * cu;
-  const C ea = t * (m.rho + c3 + q - m.usq15);
-  const C eb = t * (m.rho - c3 + q - m.usq15);
-  const C r = om1 * regularized<L, A, C>(m);  // reference order, shared
-  out_a = ea + r;
-  out_b = eb + r;
-}
-
 template <class L, typename C>
 __device__ __forceinline__ C post_rest(const NodeMoments<C>& m, C om1) {
   constexpr C t = Dir<L, 0>::template t<C>();
@@ -74,8 +58,15 @@ __device__ __forceinline__ C post_rest(const NodeMoments<C>& m, C om1) {
   return e + om1 * regularized<L, 0, C>(m);
 }
 
-// regularized_dir without the +0 seed: identical whenever the first picked
-// stress component is nonzero (checked by the caller, see header).
+// regularized_dir and c . u without the +0 seeds of the reference's loops.
+// Exactness: a seed only ever changes the SIGN OF A ZERO intermediate, and
+// sign-of-zero differences survive +, -, * only as sign-of-zero differences.
+// The regularised term r is finally added to the equilibrium part
+// ea = t ((rho + 3cu + 4.5cu^2) - usq15), which is never -0.0 unless
+// rho == -0.0 (x + y == -0 needs both operands -0 under round-to-nearest);
+// so ea + r is bit-identical whether r is +0 or -0, and likewise
+// rho + 3cu for cu = +-0. Callers guarantee rho != -0.0 (moments from a
+// +0-seeded sum), see tslb_streamcoll_vec.cu / tslb_mstep.cu.
 template <class L, int A, typename S>
 __device__ __forceinline__ S regularized_noseed(const NodeMoments<S>& m) {
   using d = Dir<L, A>;
@@ -99,6 +90,33 @@ __device__ __forceinline__ S regularized_noseed(const NodeMoments<S>& m) {
   add(d::y * d::z != 0, d::y * d::z, m.pyz2);
   if (first) s = S(0);
   return t45 * (s - m.trcs2);
+}
+
+// Post-collision values of the pair (A, A+1 = opp(A)), A odd: Q_a : Pi^neq
+// is shared by a and opp(a), and c_opp . u = -(c_a . u) exactly.
+template <class L, int A, typename C>
+__device__ __forceinline__ void post_pair(const NodeMoments<C>& m, C om1,
+                                          C& out_a, C& out_b) {
+  using d = Dir<L, A>;
+  constexpr C t = d::template t<C>();
+  const C cu = dot_noseed<d::x, d::y, d::z, C>(m.ux, m.uy, m.uz);
+  const C c3 = C(3) * cu;
+  const C q = C(4.5) * cu * cu;
+  const C ea = t * (m.rho + c3 + q - m.usq15);
+  const C eb = t * (m.rho - c3 + q - m.usq15);
+  const C r = om1 * regularized_noseed<L, A, C>(m);
+  out_a = ea + r;
+  out_b = eb + r;
+}
+
+// One direction, seed-free (same exactness argument)
+template <class L, int A, typename C>
+__device__ __forceinline__ C post_single(const NodeMoments<C>& m, C om1) {
+  using d = Dir<L, A>;
+  constexpr C t = d::template t<C>();
+  const C cu = dot_noseed<d::x, d::y, d::z, C>(m.ux, m.uy, m.uz);
+  const C e = t * (m.rho + C(3) * cu + C(4.5) * cu * cu - m.usq15);
+  return e + om1 * regularized_noseed<L, A, C>(m);
 }
 
 template <class L, typename T, typename C, int VX, bool EXACT>
