@@ -74,7 +74,7 @@ namespace mstep {
 constexpr int TX = 32;                     // tile width (one warp per row)
 constexpr int TY = 8;                      // tile rows (warps per CTA)
 constexpr int NT = TX * TY;                // threads = tile columns
-constexpr int NH = 2 * TX + 2 * TY + 4;    // halo ring nodes
+constexpr int NH = 2 * TX + 2 * (TY + 2);  // halo ring nodes (x columns include the corners)
 constexpr int TR = TY + 2;                 // staged tile rows (with y halo)
 constexpr int TC = TR * TX;                // staged elements per moment array
 
@@ -108,7 +108,8 @@ __host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) / 128
 template <class L, typename T>
 struct Smem {
   static constexpr size_t tile = align128(size_t(n_moments<L>()) * TC * sizeof(T));
-  static constexpr size_t wstg = align128(size_t(n_moments<L>()) * NH * sizeof(T));
+  // one copy of the ring per halo task half (see push_ring)
+  static constexpr size_t wstg = align128(size_t(n_moments<L>()) * 2 * NH * sizeof(T));
   static constexpr size_t slots = size_t(slot_planes<L>()) * NT * sizeof(T);
   static constexpr size_t off_wstg = 2 * tile;
   static constexpr size_t off_slots = off_wstg + 2 * wstg;
@@ -152,17 +153,68 @@ __device__ __forceinline__ int wrap_coord(int g, int n, int lo, int hi) {
   return g;
 }
 
-// ring offsets (in elements) of destination planes z-1, z, z+1 relative to
-// the plane being pushed, for 2- and 3-deep rings
+// Shared-memory slot accesses as single instructions: 32-bit shared
+// address + compile-time byte offset; the guarded store is one predicated
+// st.shared (the compiler otherwise wraps each guarded store in a
+// reconvergence region).
+template <typename T>
+struct Shm;
+template <>
+struct Shm<float> {
+  template <int OFF>
+  __device__ static __forceinline__ void st(uint32_t a, float v) {
+    asm volatile("st.shared.f32 [%0+%2], %1;" ::"r"(a), "f"(v), "n"(OFF) : "memory");
+  }
+  template <int OFF>
+  __device__ static __forceinline__ void st_if(uint32_t a, float v, bool p) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.shared.f32 [%0+%3], %1;\n}" ::"r"(a), "f"(v),
+                 "r"(int(p)), "n"(OFF)
+                 : "memory");
+  }
+  template <int OFF>
+  __device__ static __forceinline__ float ld(uint32_t a) {
+    float v;
+    asm volatile("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(a), "n"(OFF) : "memory");
+    return v;
+  }
+};
+template <>
+struct Shm<double> {
+  template <int OFF>
+  __device__ static __forceinline__ void st(uint32_t a, double v) {
+    asm volatile("st.shared.f64 [%0+%2], %1;" ::"r"(a), "d"(v), "n"(OFF) : "memory");
+  }
+  template <int OFF>
+  __device__ static __forceinline__ void st_if(uint32_t a, double v, bool p) {
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q st.shared.f64 [%0+%3], %1;\n}" ::"r"(a), "d"(v),
+                 "r"(int(p)), "n"(OFF)
+                 : "memory");
+  }
+  template <int OFF>
+  __device__ static __forceinline__ double ld(uint32_t a) {
+    double v;
+    asm volatile("ld.shared.f64 %0, [%1+%2];" : "=d"(v) : "r"(a), "n"(OFF) : "memory");
+    return v;
+  }
+};
+
+// Slot addressing. Each thread keeps the shared addresses of its own
+// column's slot in the ring planes of destination planes z-1, z, z+1
+// relative to the plane being pushed (2-deep rings: z-1, z; 3-deep: z-1, z,
+// z+1); a push by (dx, dy) is then that address plus a compile-time offset.
+template <typename T>
 struct Ring {
-  int o2[2], o3[3];
+  uint32_t own;            // shared address of sl[ly * TX + lx]
+  uint32_t q2[2];
+  uint32_t q3[3];
   int p2, p3;
   __device__ __forceinline__ void set() {
-    o2[0] = (p2 ^ 1) * NT;
-    o2[1] = p2 * NT;
-    o3[0] = (p3 == 0 ? 2 : p3 - 1) * NT;
-    o3[1] = p3 * NT;
-    o3[2] = (p3 == 2 ? 0 : p3 + 1) * NT;
+    constexpr uint32_t P = NT * sizeof(T);
+    q2[0] = own + (p2 ^ 1) * P;
+    q2[1] = own + p2 * P;
+    q3[0] = own + (p3 == 0 ? 2 : p3 - 1) * P;
+    q3[1] = own + p3 * P;
+    q3[2] = own + (p3 == 2 ? 0 : p3 + 1) * P;
   }
   __device__ __forceinline__ void advance() {
     p2 ^= 1;
@@ -171,13 +223,15 @@ struct Ring {
   }
 };
 
+// byte offset of direction A's slot shifted by (DX, DY) from the own column
+template <class L, int A, int DX, int DY, typename T>
+__host__ __device__ constexpr int slot_off() {
+  return int((slot_base<L>(A) * NT + DY * TX + DX) * int(sizeof(T)));
+}
 template <class L, int A, int DZ, typename T>
-__device__ __forceinline__ T* slot(T* sl, const Ring& rg, int lx, int ly) {
-  constexpr int base = slot_base<L>(A) * NT;
-  int ro;
-  if constexpr (ring_depth<L>(A) == 3) ro = rg.o3[DZ + 1];
-  else ro = rg.o2[DZ + 1];  // DZ is -1 or 0 for 2-deep rings
-  return sl + base + ro + ly * TX + lx;
+__device__ __forceinline__ uint32_t ring_addr(const Ring<T>& rg) {
+  if constexpr (ring_depth<L>(A) == 3) return rg.q3[DZ + 1];
+  else return rg.q2[DZ + 1];  // DZ is -1 or 0 for 2-deep rings
 }
 
 template <class L, typename T, typename C>
@@ -198,7 +252,7 @@ struct Contact {
 // Output of direction A from a tile node: bounce into its own opposite slot
 // or push into the slot of the destination (dropped if outside the tile).
 template <class L, int A, typename T, typename C, bool WALLS, int ZC>
-__device__ __forceinline__ void emit(const Dom& d, T* sl, const Ring& rg, T (&R)[L::q][3],
+__device__ __forceinline__ void emit(const Dom& d, const Ring<T>& rg, T (&R)[L::q][3],
                                      int lx, int ly, const Contact& ct, T o) {
   using dd = Dir<L, A>;
   if constexpr (WALLS && ZC == 0) {
@@ -208,7 +262,7 @@ __device__ __forceinline__ void emit(const Dom& d, T* sl, const Ring& rg, T (&R)
     if (cx || cy || cz) {
       const T b = bounce_value<L, A, T, C>(d, o, cx, cy, cz);
       if constexpr (is_reg<L>(dd::opp)) R[dd::opp][1] = b;
-      else *slot<L, dd::opp, 0>(sl, rg, lx, ly) = b;
+      else Shm<T>::template st<slot_off<L, dd::opp, 0, 0, T>()>(ring_addr<L, dd::opp, 0>(rg), b);
       return;
     }
   }
@@ -219,84 +273,105 @@ __device__ __forceinline__ void emit(const Dom& d, T* sl, const Ring& rg, T (&R)
     bool in = true;
     if constexpr (dd::x != 0) in = unsigned(tx) < unsigned(TX);
     if constexpr (dd::y != 0) in = in && unsigned(ty) < unsigned(TY);
-    if (in) *slot<L, A, dd::z>(sl, rg, tx, ty) = o;
+    if constexpr (dd::x == 0 && dd::y == 0) {
+      Shm<T>::template st<slot_off<L, A, 0, 0, T>()>(ring_addr<L, A, dd::z>(rg), o);
+    } else {
+      Shm<T>::template st_if<slot_off<L, A, dd::x, dd::y, T>()>(ring_addr<L, A, dd::z>(rg), o, in);
+    }
   }
 }
 
 // All directions of a tile node; ZC != 0 (a plane just outside the march)
 // keeps only the directions with c_z == ZC.
 template <class L, typename T, typename C, bool WALLS, int ZC>
-__device__ __forceinline__ void push_tile(const Dom& d, T* sl, const Ring& rg, T (&R)[L::q][3],
+__device__ __forceinline__ void push_tile(const Dom& d, const Ring<T>& rg, T (&R)[L::q][3],
                                           int lx, int ly, const Contact& ct,
                                           const NodeMoments<C>& m, C om1) {
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
     if constexpr (a == 0) {
-      if constexpr (ZC == 0) emit<L, 0, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(post_rest<L, C>(m, om1)));
+      if constexpr (ZC == 0) emit<L, 0, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, T(post_rest<L, C>(m, om1)));
     } else if constexpr (a & 1) {
       constexpr bool ua = ZC == 0 || Dir<L, a>::z == ZC;
       constexpr bool ub = ZC == 0 || Dir<L, a + 1>::z == ZC;
       if constexpr (ua && ub) {
         C ra, rb;
         post_pair<L, a, C>(m, om1, ra, rb);
-        emit<L, a, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(ra));
-        emit<L, a + 1, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(rb));
+        emit<L, a, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, T(ra));
+        emit<L, a + 1, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, T(rb));
       } else if constexpr (ua) {
-        emit<L, a, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(post_single<L, a, C>(m, om1)));
+        emit<L, a, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, T(post_single<L, a, C>(m, om1)));
       } else if constexpr (ub) {
-        emit<L, a + 1, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, T(post_single<L, a + 1, C>(m, om1)));
+        emit<L, a + 1, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, T(post_single<L, a + 1, C>(m, om1)));
       }
     }
   });
 }
 
-// A halo node at tile-local (hx, hy) on side (SX, SY): only the directions
-// pointing into the tile.
-template <class L, typename T, typename C, int SX, int SY, int ZC>
-__device__ __forceinline__ void push_halo(T* sl, const Ring& rg, int hx, int hy,
+// Halo pushes. A halo node at tile-local (hx, hy) on side (SX, SY) only
+// rebuilds the directions that land inside the tile. The four sides (x
+// columns including the corners) are split into eight tasks of about equal
+// cost -- side = warp / 2, and each of the two warps of a side takes every
+// other of the side's directions -- so every warp reaches the barrier with
+// the same work.
+template <class L, int SX, int SY, int ZC>
+__host__ __device__ constexpr bool halo_dir(int a) {
+  return !is_reg<L>(a) && (SX == 0 || L::c[a][0] == -SX) && (SY == 0 || L::c[a][1] == -SY) &&
+         (ZC == 0 || L::c[a][2] == ZC);
+}
+template <class L, int SX, int SY, int ZC>
+__host__ __device__ constexpr int halo_rank(int a) {
+  int r = 0;
+  for (int b = 0; b < a; ++b)
+    if (halo_dir<L, SX, SY, ZC>(b)) ++r;
+  return r;
+}
+
+template <class L, typename T, typename C, int SX, int SY, int ZC, int PART>
+__device__ __forceinline__ void push_halo(const Ring<T>& rg, int hdelta, int hx, int hy,
                                           const NodeMoments<C>& m, C om1) {
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
     using dd = Dir<L, a>;
-    constexpr bool use = !is_reg<L>(a) && (SX == 0 || dd::x == -SX) &&
-                         (SY == 0 || dd::y == -SY) && (ZC == 0 || dd::z == ZC);
+    constexpr bool use = halo_dir<L, SX, SY, ZC>(a) && (halo_rank<L, SX, SY, ZC>(a) & 1) == PART;
     if constexpr (use) {
       const int tx = hx + dd::x, ty = hy + dd::y;
       bool in = true;
       if constexpr (SX == 0 && dd::x != 0) in = unsigned(tx) < unsigned(TX);
-      if constexpr (SY == 0 && dd::y != 0) in = in && unsigned(ty) < unsigned(TY);
-      if (in) *slot<L, a, dd::z>(sl, rg, tx, ty) = T(post_single<L, a, C>(m, om1));
+      if constexpr (SY == 0) in = in && unsigned(ty) < unsigned(TY);  // x columns carry the corners
+      Shm<T>::template st_if<slot_off<L, a, dd::x, dd::y, T>()>(ring_addr<L, a, dd::z>(rg) + hdelta, 
+                                                                 T(post_single<L, a, C>(m, om1)), in);
     }
   });
 }
 
 template <class L, typename T, typename C, int ZC>
-__device__ __forceinline__ void push_ring(T* sl, const Ring& rg, int role, int hx, int hy,
+__device__ __forceinline__ void push_ring(const Ring<T>& rg, int hdelta, int task, int hx, int hy,
                                           const NodeMoments<C>& m, C om1) {
-  switch (role) {
-    case 0: push_halo<L, T, C, 0, -1, ZC>(sl, rg, hx, hy, m, om1); break;
-    case 1: push_halo<L, T, C, 0, 1, ZC>(sl, rg, hx, hy, m, om1); break;
-    case 2: push_halo<L, T, C, -1, 0, ZC>(sl, rg, hx, hy, m, om1); break;
-    case 3: push_halo<L, T, C, 1, 0, ZC>(sl, rg, hx, hy, m, om1); break;
-    case 4: push_halo<L, T, C, -1, -1, ZC>(sl, rg, hx, hy, m, om1); break;
-    case 5: push_halo<L, T, C, 1, -1, ZC>(sl, rg, hx, hy, m, om1); break;
-    case 6: push_halo<L, T, C, -1, 1, ZC>(sl, rg, hx, hy, m, om1); break;
-    default: push_halo<L, T, C, 1, 1, ZC>(sl, rg, hx, hy, m, om1); break;
+  switch (task) {
+    case 0: push_halo<L, T, C, 0, -1, ZC, 0>(rg, hdelta, hx, hy, m, om1); break;
+    case 1: push_halo<L, T, C, 0, -1, ZC, 1>(rg, hdelta, hx, hy, m, om1); break;
+    case 2: push_halo<L, T, C, 0, 1, ZC, 0>(rg, hdelta, hx, hy, m, om1); break;
+    case 3: push_halo<L, T, C, 0, 1, ZC, 1>(rg, hdelta, hx, hy, m, om1); break;
+    case 4: push_halo<L, T, C, -1, 0, ZC, 0>(rg, hdelta, hx, hy, m, om1); break;
+    case 5: push_halo<L, T, C, -1, 0, ZC, 1>(rg, hdelta, hx, hy, m, om1); break;
+    case 6: push_halo<L, T, C, 1, 0, ZC, 0>(rg, hdelta, hx, hy, m, om1); break;
+    default: push_halo<L, T, C, 1, 0, ZC, 1>(rg, hdelta, hx, hy, m, om1); break;
   }
 }
 
 // compute_moments of one node from its gathered slots (kernels.hpp:74-107;
 // same accumulation order and formulae as k_moments)
 template <class L, typename T, typename C>
-__device__ __forceinline__ void finalize(const Dom& d, T* sl, const Ring& rg, const T (&R)[L::q][3],
-                                         int lx, int ly, T* __restrict__ mo, int64_t idx) {
+__device__ __forceinline__ void finalize(const Dom& d, const Ring<T>& rg, const T (&R)[L::q][3],
+                                         T* __restrict__ mo, int64_t idx) {
   C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pzz = 0, pxy = 0, pxz = 0, pyz = 0;
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
     using dd = Dir<L, a>;
     T v;
     if constexpr (is_reg<L>(a)) v = R[a][0];
-    else v = *slot<L, a, -1>(sl, rg, lx, ly);
+    else v = Shm<T>::template ld<slot_off<L, a, 0, 0, T>()>(ring_addr<L, a, -1>(rg));
     const C fa = C(v);
     r += fa;
     if constexpr (dd::x == 1) jx += fa;
@@ -338,7 +413,7 @@ __global__ void __launch_bounds__(NT, MINB)
   constexpr int NM = n_moments<L>();
   extern __shared__ __align__(128) unsigned char smraw[];
   T* tile = reinterpret_cast<T*>(smraw);                  // [2][NM][TR][TX]
-  T* wstg = reinterpret_cast<T*>(smraw + SM::off_wstg);   // [2][NM][NH]
+  T* wstg = reinterpret_cast<T*>(smraw + SM::off_wstg);   // [2][NM][2 NH]
   T* sl = reinterpret_cast<T*>(smraw + SM::off_slots);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + SM::off_bar);
   constexpr int TILE_B = int(SM::tile / sizeof(T)), WSTG_B = int(SM::wstg / sizeof(T));
@@ -349,20 +424,22 @@ __global__ void __launch_bounds__(NT, MINB)
   const int gx = x0 + lx, gy = y0 + ly;
   const int64_t col = gx + int64_t(d.nx) * gy;
 
-  // halo role of this thread: warp 0 the row below the tile, warp 1 the row
-  // above, warps 2/3 the columns left/right, warp 4 the four corners. Rows
-  // inside the domain come with the TMA tile; the x columns, the corners and
-  // wrapped rows are fetched by the lane itself (cp.async into wstg).
-  int hnode = -1, role = 0, hx = 0, hy = 0;
-  if (ly == 0) { hnode = lx; role = 0; hx = lx; hy = -1; }
-  else if (ly == 1) { hnode = TX + lx; role = 1; hx = lx; hy = TY; }
-  else if (ly == 2 && lx < TY) { hnode = 2 * TX + lx; role = 2; hx = -1; hy = lx; }
-  else if (ly == 3 && lx < TY) { hnode = 2 * TX + TY + lx; role = 3; hx = TX; hy = lx; }
-  else if (ly == 4 && lx < 4) {
-    hnode = 2 * TX + 2 * TY + lx;
-    role = 4 + lx;
-    hx = (lx & 1) ? TX : -1;
-    hy = (lx & 2) ? TY : -1;
+  // halo task of this warp (see push_ring): side = warp / 2 (row below, row
+  // above, column left, column right; the columns run from y0-1 to y0+TY and
+  // so include the corners), half = warp % 2. Rows inside the domain come
+  // with the TMA tile; the columns and wrapped rows are fetched by the lane
+  // itself (cp.async into its half's copy of the ring in wstg).
+  constexpr int WH = 2 * NH;  // wstg elements per moment array
+  const int side = ly >> 1, half = ly & 1;
+  int hnode = -1, hx = 0, hy = 0;
+  if (side < 2) {
+    hnode = side * TX + lx;
+    hx = lx;
+    hy = side == 0 ? -1 : TY;
+  } else if (lx < TY + 2) {
+    hnode = 2 * TX + (side - 2) * (TY + 2) + lx;
+    hx = side == 2 ? -1 : TX;
+    hy = lx - 1;
   }
   int64_t hcol = 0;
   bool hfetch = false;  // this lane loads its halo node itself
@@ -374,15 +451,17 @@ __global__ void __launch_bounds__(NT, MINB)
       hnode = -1;
     } else {
       hcol = hgx + int64_t(d.nx) * hgy;
-      hfetch = role >= 2 || hgy != y0 + hy;
+      hfetch = side >= 2 || hgy != y0 + hy;
       if (hfetch) {
-        hoff = hnode;
-        hstride = NH;
+        hoff = half * NH + hnode;
+        hstride = WH;
       } else {
         hoff = (hy + 1) * TX + hx;
       }
     }
   }
+  // halo node's column relative to the thread's own, in bytes
+  const int hdelta = ((hy - ly) * TX + (hx - lx)) * int(sizeof(T));
   Contact ct{};
   if constexpr (WALLS) {
     ct.xlo = gx == 0 && d.mode[XMin] == kWall;
@@ -407,17 +486,18 @@ __global__ void __launch_bounds__(NT, MINB)
       tma_load_4d(tile + b * TILE_B, &tmap, &bar[b], x0, y0 - 1, zz, 0);
     }
     if (hfetch) {
-      T* w = wstg + b * WSTG_B + hnode;
+      T* w = wstg + b * WSTG_B + hoff;
       const T* g = mi + int64_t(zz) * d.plane + hcol;
 #pragma unroll
-      for (int c = 0; c < NM; ++c) __pipeline_memcpy_async(w + c * NH, g + c * d.mstride, sizeof(T));
+      for (int c = 0; c < NM; ++c) __pipeline_memcpy_async(w + c * WH, g + c * d.mstride, sizeof(T));
     }
   };
 
   T R[L::q][3];
 #pragma unroll
   for (int a = 0; a < L::q; ++a) R[a][0] = R[a][1] = R[a][2] = T(0);
-  Ring rg;
+  Ring<T> rg;
+  rg.own = smem_u32(sl + ly * TX + lx);
   rg.p2 = 0;
   rg.p3 = 0;
   rg.set();
@@ -438,15 +518,15 @@ __global__ void __launch_bounds__(NT, MINB)
         ct.zhi = z == d.nz - 1 && d.mode[ZMax] == kWall;
       }
       const NodeMoments<C> m = node_at<L, T, C>(tb + (ly + 1) * TX + lx, TC);
-      push_tile<L, T, C, WALLS, ZC>(d, sl, rg, R, lx, ly, ct, m, om1);
+      push_tile<L, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, m, om1);
       if (hnode >= 0) {
         const T* hb = (hfetch ? wstg + buf * WSTG_B : tb) + hoff;
         const NodeMoments<C> hm = node_at<L, T, C>(hb, hstride);
-        push_ring<L, T, C, ZC>(sl, rg, role, hx, hy, hm, om1);
+        push_ring<L, T, C, ZC>(rg, hdelta, ly, hx, hy, hm, om1);
       }
     }
     __syncthreads();
-    if (z - 1 >= za) finalize<L, T, C>(d, sl, rg, R, lx, ly, mo, col + int64_t(z - 1) * d.plane);
+    if (z - 1 >= za) finalize<L, T, C>(d, rg, R, mo, col + int64_t(z - 1) * d.plane);
     __syncthreads();
 #pragma unroll
     for (int a = 0; a < L::q; ++a) {
@@ -540,13 +620,17 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, T* mo, double ome
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       kern<<<grid, NT, smem, st>>>(*tm, d, mi, mo, om1, lz);
     };
-    // fp32 node math fits three CTAs per SM (registers and shared memory)
+    // fp32 storage + fp32 math: three CTAs per SM (~76 KB shared memory, <= 80
+    // registers); fp64 math keeps two (capping it at 80 registers costs more
+    // ILP than the third CTA buys); fp64 storage holds one CTA per SM
+    constexpr int MB = sizeof(T) == 4 ? 3 : 1;
+    constexpr int MBD = sizeof(T) == 4 ? 2 : 1;
     if (math == kMathDouble) {
-      if (walls) go(k_mstep<Lat, T, double, true, 2>, om1d);
-      else go(k_mstep<Lat, T, double, false, 2>, om1d);
+      if (walls) go(k_mstep<Lat, T, double, true, MBD>, om1d);
+      else go(k_mstep<Lat, T, double, false, MBD>, om1d);
     } else {
-      if (walls) go(k_mstep<Lat, T, float, true, 3>, om1f);
-      else go(k_mstep<Lat, T, float, false, 3>, om1f);
+      if (walls) go(k_mstep<Lat, T, float, true, MB>, om1f);
+      else go(k_mstep<Lat, T, float, false, MB>, om1f);
     }
     return 0;
   };
