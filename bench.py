@@ -320,12 +320,28 @@ def main():
     sched = sim.schedule if W["comps"] == 1 else "f1"
     sb = step_bytes(lat, W["comps"], es, sched)
     step_bw = glups * sb / world  # per-GPU GB/s of the whole step
+    traffic, tsrc = None, None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh).get(f"{lat.name}/{W['storage']}/{dom}")
+        if tr:
+            traffic, tsrc = round(tr["bytes_per_node"] * local_nodes / 1e9, 3), tr["source"]
+    except (OSError, ValueError):
+        pass
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-            "frac": round(achieved / hbm, 4), "traffic": None, "kernel": f"k_{dom}",
+            "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_unit": "GB per launch",
+            "traffic_source": tsrc, "kernel": f"k_{dom}",
             "kernel_bytes_per_node": per_node[dom], "peak_kind": peak_kind,
             "per_kernel_ms": {k: round(v[0] / v[1], 4) for k, v in prof.items()},
             "step_bytes_per_lu": sb, "step_frac": round(step_bw / hbm, 4),
             "step_frac_of_8TBs": round(step_bw / 8000.0, 4)}
+    if W["comps"] == 1:
+        # the F1 schedule's ceiling: every population through HBM twice
+        # (census bytes, bench.hpp:62-63); M beats it by moving fewer bytes
+        f1b = kernel_bytes(lat, 1, es)["moments"] + kernel_bytes(lat, 1, es)["streamcoll"]
+        roof["f1_bytes_per_lu"] = f1b
+        roof["f1_roofline_glups"] = round(hbm / f1b, 3)
+        roof["vs_f1_roofline"] = round(glups / world / (hbm / f1b), 4)
 
     e2e = None
     if default and not args.no_e2e and world == 1:

@@ -111,6 +111,7 @@ struct tslb_cuda_sim {
   bool fimplicit = false;
   int lz = 0;          // planes per CTA of the M kernel (0 = default; TSLB_LZ)
   void* mo2 = nullptr; // second moment buffer of the M schedule (ping-pong)
+  void* gm = nullptr;  // M on z slabs: neighbours' boundary-plane moments [NM][2][plane]
   void* graph_mo = nullptr;  // moment buffer the captured graph starts from
   MstepMaps* mmaps = nullptr;  // TMA tensor maps of the M kernel's inputs
   int vx = 0;          // nodes per thread in the vectorised kernel (0 = default; TSLB_VX)
@@ -266,27 +267,91 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
   });
 }
 
-// M schedule: m(t) in h->mo -> m(t+1) in h->mo2, then swap
-int ph_mstep(tslb_cuda_sim* h, cudaStream_t st) {
-  {
-    Prof p(h, TSLB_K_MSTEP, st);
-    ++h->launches;
-    int rc = by_scalar(h, [&](auto z) {
-      using T = decltype(z);
-      return launch_mstep<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<const T*>(h->mo),
-                             static_cast<T*>(h->mo2), h->omega, h->lz, h->mmaps, st);
-    });
-    if (rc) return set_err(TSLB_ESTATE, "M step not supported for this domain");
-  }
-  std::swap(h->mo, h->mo2);
+// M schedule: m(t) in h->mo -> m(t+1) in h->mo2 for z chunks [c0, c0+n)
+// (n <= 0: all); the caller swaps the buffers once every chunk is done
+int ph_mstep(tslb_cuda_sim* h, cudaStream_t st, int c0 = 0, int n = 0) {
+  Prof p(h, TSLB_K_MSTEP, st);
+  ++h->launches;
+  int rc = by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_mstep<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<const T*>(h->mo),
+                           static_cast<const T*>(h->gm), static_cast<T*>(h->mo2), h->omega, h->lz, c0, n,
+                           h->mmaps, st);
+  });
+  if (rc) return set_err(TSLB_ESTATE, "M step not supported for this domain");
   return 0;
 }
 
-// store f(t+1) = stream_collide(m(t)) if the M schedule left it implicit
+// M on slabs: ship the boundary planes of the moment buffer `buf` into the
+// neighbours' ghost planes (their `gm`), all 1+D+np arrays. Same grouping
+// as the F1 exchange: +z direction first, then -z, so every peer pair
+// matches its sends and receives in order (also when up == down).
+int exchange_moments_nccl(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
+  NcclApi& N = nccl();
+  const ncclDataType_t ty = h->scalar == TSLB_F64 ? ncclFloat64 : ncclFloat32;
+  const size_t cnt = size_t(h->plane());
+  const int nm = 1 + h->dim + h->np;
+  auto arr = [&](int c, int k) {
+    return static_cast<const char*>(buf) + (size_t(c) * h->d.mstride + size_t(k) * h->plane()) * h->esz;
+  };
+  auto ghost = [&](int c, int side) {
+    return static_cast<char*>(h->gm) + (size_t(2 * c + side) * h->plane()) * h->esz;
+  };
+  Prof p(h, TSLB_K_EXCHANGE, st);
+  N.GroupStart();
+  if (h->up >= 0)
+    for (int c = 0; c < nm; ++c) N.Send(arr(c, h->nzl - 1), cnt, ty, h->up, h->comm, st);
+  if (h->down >= 0)
+    for (int c = 0; c < nm; ++c) N.Recv(ghost(c, 0), cnt, ty, h->down, h->comm, st);
+  if (h->down >= 0)
+    for (int c = 0; c < nm; ++c) N.Send(arr(c, 0), cnt, ty, h->down, h->comm, st);
+  if (h->up >= 0)
+    for (int c = 0; c < nm; ++c) N.Recv(ghost(c, 1), cnt, ty, h->up, h->comm, st);
+  ncclResult_t r = N.GroupEnd();
+  if (r != ncclSuccess)
+    return set_err(TSLB_ECUDA, "NCCL moment halo exchange: %s", N.ErrStr ? N.ErrStr(r) : "error");
+  return 0;
+}
+
+// local transport of the same (single-device verification)
+int exchange_moments_local(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
+  const size_t bytes = size_t(h->plane()) * h->esz;
+  const int nm = 1 + h->dim + h->np;
+  auto arr = [&](int c, int k) {
+    return static_cast<const char*>(buf) + (size_t(c) * h->d.mstride + size_t(k) * h->plane()) * h->esz;
+  };
+  auto ghost = [&](tslb_cuda_sim* p, int c, int side) {
+    return static_cast<char*>(p->gm) + (size_t(2 * c + side) * p->plane()) * p->esz;
+  };
+  Prof p(h, TSLB_K_EXCHANGE, st);
+  for (int c = 0; c < nm; ++c) {
+    if (h->up_peer)
+      CK(cudaMemcpyAsync(ghost(h->up_peer, c, 0), arr(c, h->nzl - 1), bytes, cudaMemcpyDeviceToDevice, st));
+    if (h->down_peer)
+      CK(cudaMemcpyAsync(ghost(h->down_peer, c, 1), arr(c, 0), bytes, cudaMemcpyDeviceToDevice, st));
+  }
+  return 0;
+}
+
+// store f(t+1) = stream_collide(m(t)) if the M schedule left it implicit;
+// on slabs the pushes entering through the slab faces are rebuilt from the
+// ghost moments instead of exchanged
 int materialize(tslb_cuda_sim* h) {
   if (!h->fimplicit) return 0;
   h->fimplicit = false;
-  return ph_streamcoll(h, 0, h->nzl, h->s);
+  if (int rc = ph_streamcoll(h, 0, h->nzl, h->s)) return rc;
+  if (!h->decomposed) return 0;
+  return by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    for (int side = 0; side < 2; ++side) {
+      if (h->d.mode[side ? ZMax : ZMin] != kGhost) continue;
+      ++h->launches;
+      if (launch_ghost_push<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
+                               static_cast<const T*>(h->gm), h->omega, side, h->s))
+        return set_err(TSLB_ESTATE, "ghost push: bad lattice");
+    }
+    return 0;
+  });
 }
 
 int ph_cg_moments(tslb_cuda_sim* h, cudaStream_t st) {
@@ -415,13 +480,33 @@ int enqueue_step(tslb_cuda_sim* h) {
     return 0;
   }
   if (h->sched == TSLB_SCHED_M) {
-    // first step from stored populations: the moments pass, stream-collide
-    // deferred; afterwards one M pass per step
     if (!h->fimplicit) {
+      // first step from stored populations: the moments pass (and, on
+      // slabs, the ghost planes of m(t)); the stream-collide is deferred
       if ((rc = ph_moments(h, h->s))) return rc;
+      if (h->xmode == 1 && (rc = exchange_moments_nccl(h, h->mo, h->s))) return rc;
       h->fimplicit = true;
-    } else if ((rc = ph_mstep(h, h->s))) {
-      return rc;
+    } else if (h->xmode == 1) {
+      // slab: the two boundary chunks first, their new boundary planes go to
+      // the neighbours on the comm stream while the interior chunks run
+      const int nzc = mstep_chunks(h->range(0, h->nzl), h->lz);
+      if (nzc <= 2) {
+        if ((rc = ph_mstep(h, h->s))) return rc;
+        if ((rc = exchange_moments_nccl(h, h->mo2, h->s))) return rc;
+      } else {
+        if ((rc = ph_mstep(h, h->s, 0, 1))) return rc;
+        if ((rc = ph_mstep(h, h->s, nzc - 1, 1))) return rc;
+        CK(cudaEventRecord(h->ev_b, h->s));
+        CK(cudaStreamWaitEvent(h->cs, h->ev_b, 0));
+        if ((rc = exchange_moments_nccl(h, h->mo2, h->cs))) return rc;
+        CK(cudaEventRecord(h->ev_c, h->cs));
+        if ((rc = ph_mstep(h, h->s, 1, nzc - 2))) return rc;
+        CK(cudaStreamWaitEvent(h->s, h->ev_c, 0));
+      }
+      std::swap(h->mo, h->mo2);
+    } else {
+      if ((rc = ph_mstep(h, h->s))) return rc;
+      std::swap(h->mo, h->mo2);
     }
     ++h->steps;
     return 0;
@@ -642,6 +727,11 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
     if (!(e && !std::strcmp(e, "f1"))) {
       if ((rc = alloc(h, &h->mo2, mbytes))) return fail(rc);
       CK(cudaMemsetAsync(h->mo2, 0, mbytes, h->s));
+      if (decomposed) {
+        const size_t gb = size_t(d.plane) * 2 * (1 + h->dim + h->np) * h->esz;
+        if ((rc = alloc(h, &h->gm, gb))) return fail(rc);
+        CK(cudaMemsetAsync(h->gm, 0, gb, h->s));
+      }
       h->sched = TSLB_SCHED_M;
     }
   }
@@ -727,7 +817,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   if (h->s) cudaStreamSynchronize(h->s);
   if (h->cs) cudaStreamSynchronize(h->cs);
   if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
-  void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->two, h->flag, h->solid, h->slow,
+  void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->two, h->flag, h->solid, h->slow,
                   h->scratch, h->red, h->dig, h->recv_lo, h->recv_hi};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -762,10 +852,15 @@ int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
     if (h->comps != 1 || !mstep_supported(h->lat, h->d))
       return set_err(TSLB_EINVAL,
                      "M schedule needs a single-fluid D3Q19/D3Q27 box without solids, "
-                     "one domain, nx %% 32 == 0 and ny %% 8 == 0");
+                     "nx %% 32 == 0 and ny %% 8 == 0");
     if (!h->mo2) {
       const size_t mbytes = size_t(h->d.mstride) * (1 + h->dim + h->np) * h->esz;
       if (int rc = alloc(h, &h->mo2, mbytes)) return rc;
+    }
+    if (h->decomposed && !h->gm) {
+      const size_t gb = size_t(h->plane()) * 2 * (1 + h->dim + h->np) * h->esz;
+      if (int rc = alloc(h, &h->gm, gb)) return rc;
+      CK(cudaMemsetAsync(h->gm, 0, gb, h->s));
     }
   } else if (int rc = materialize(h)) {
     return rc;
@@ -1293,7 +1388,41 @@ int tslb_cuda_group_step(tslb_cuda_handle* slabs, int count, long nsteps) {
   // (single-device verification transport).
   cudaStream_t st = slabs[0]->s;
   CK(cudaSetDevice(slabs[0]->device));
+  bool all_m = true, any_m = false;
+  for (int r = 0; r < count; ++r) {
+    all_m = all_m && slabs[r]->sched == TSLB_SCHED_M;
+    any_m = any_m || slabs[r]->sched == TSLB_SCHED_M;
+  }
+  if (any_m && !all_m) return set_err(TSLB_ESTATE, "linked slabs must share one step schedule");
   for (long s = 0; s < nsteps; ++s) {
+    if (all_m) {
+      // the NCCL path's order: boundary chunks, exchange of the new boundary
+      // planes, interior chunks, swap (first step: moments + exchange)
+      const bool first = !slabs[0]->fimplicit;
+      for (int r = 0; r < count; ++r) {
+        tslb_cuda_sim* h = slabs[r];
+        const int nzc = mstep_chunks(h->range(0, h->nzl), h->lz);
+        int rc = 0;
+        if (first) rc = ph_moments(h, st);
+        else if (nzc <= 2) rc = ph_mstep(h, st);
+        else if (!(rc = ph_mstep(h, st, 0, 1))) rc = ph_mstep(h, st, nzc - 1, 1);
+        if (rc) return rc;
+      }
+      for (int r = 0; r < count; ++r)
+        if (int rc = exchange_moments_local(slabs[r], first ? slabs[r]->mo : slabs[r]->mo2, st)) return rc;
+      for (int r = 0; r < count; ++r) {
+        tslb_cuda_sim* h = slabs[r];
+        if (!first) {
+          const int nzc = mstep_chunks(h->range(0, h->nzl), h->lz);
+          if (nzc > 2)
+            if (int rc = ph_mstep(h, st, 1, nzc - 2)) return rc;
+          std::swap(h->mo, h->mo2);
+        }
+        h->fimplicit = true;
+        ++h->steps;
+      }
+      continue;
+    }
     for (int r = 0; r < count; ++r)
       if (int rc = ph_moments(slabs[r], st)) return rc;
     for (int r = 0; r < count; ++r)

@@ -39,16 +39,24 @@ template <typename T>
 int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
                           double omega, int vx, int kz, cudaStream_t st);
 // moment-resident single-pass step (tslb_mstep.cu): m(t) in `mi` -> m(t+1)
-// in `mo` for box geometries; returns nonzero (nothing launched) when the
-// shape is not supported. lz = planes marched per CTA (0: default); `maps`
-// caches the TMA tensor maps of the input buffers (opaque, owned by the
-// caller, freed with free_mstep_maps).
+// in `mo` for box geometries, z chunks [chunk0, chunk0 + nchunks) of lz
+// planes (nchunks <= 0: to the end); `gm` holds the slab ghost planes
+// ([NM][2][plane], below/above) when a z face is a slab interface. Returns
+// nonzero (nothing launched) when the shape is not supported. `maps` caches
+// the TMA tensor maps (opaque, owned by the caller, freed with
+// free_mstep_maps).
 struct MstepMaps;
 void free_mstep_maps(MstepMaps* maps);
 bool mstep_supported(int lat, const Dom& d);
+int mstep_chunks(const Dom& d, int lz);
 template <typename T>
-int launch_mstep(int lat, int math, const Dom& d, const T* mi, T* mo, double omega,
-                 int lz, MstepMaps*& maps, cudaStream_t st);
+int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
+                 int lz, int chunk0, int nchunks, MstepMaps*& maps, cudaStream_t st);
+// slab f materialisation: pushes entering boundary plane `side` (0 below,
+// 1 above) rebuilt from the ghost moments
+template <typename T>
+int launch_ghost_push(int lat, int math, const Dom& d, T* f, const T* gm, double omega, int side,
+                      cudaStream_t st);
 template <typename T>
 int launch_collide(int lat, const Dom& d, T* f, const T* mo,
                    const uint8_t* solid, double omega, cudaStream_t st);

@@ -64,7 +64,7 @@ struct MstepMaps {
     CUtensorMap map;
     const void* base = nullptr;
     int64_t key[5] = {0, 0, 0, 0, 0};
-  } e[2];
+  } e[3];  // the two moment buffers (ping-pong) and the slab ghost planes
   int next = 0;
 };
 void free_mstep_maps(MstepMaps* m) { delete m; }
@@ -77,6 +77,7 @@ constexpr int NT = TX * TY;                // threads = tile columns
 constexpr int NH = 2 * TX + 2 * (TY + 2);  // halo ring nodes (x columns include the corners)
 constexpr int TR = TY + 2;                 // staged tile rows (with y halo)
 constexpr int TC = TR * TX;                // staged elements per moment array
+constexpr int kDefaultLz = 64;             // planes marched per CTA
 
 template <class L>
 __host__ __device__ constexpr bool is_reg(int a) {
@@ -151,6 +152,26 @@ __device__ __forceinline__ int wrap_coord(int g, int n, int lo, int hi) {
   if (g < 0) return lo == kWrap ? g + n : -1;
   if (g >= n) return hi == kWrap ? g - n : -1;
   return g;
+}
+
+// Where the moments of plane z (possibly outside [0, nz)) come from:
+// 0 nowhere (beyond a wall), 1 an owned plane zz (wrapped if periodic),
+// 2 the slab ghost plane zz (0 below, 1 above) received from a neighbour.
+__device__ __forceinline__ int plane_src(const Dom& d, int z, int& zz) {
+  if (z >= 0 && z < d.nz) {
+    zz = z;
+    return 1;
+  }
+  const int face = z < 0 ? ZMin : ZMax;
+  if (d.mode[face] == kWrap) {
+    zz = z < 0 ? z + d.nz : z - d.nz;
+    return 1;
+  }
+  if (d.mode[face] == kGhost) {
+    zz = z < 0 ? 0 : 1;
+    return 2;
+  }
+  return 0;
 }
 
 // Shared-memory slot accesses as single instructions: 32-bit shared
@@ -406,8 +427,8 @@ __device__ __forceinline__ void finalize(const Dom& d, const Ring<T>& rg, const 
 
 template <class L, typename T, typename C, bool WALLS, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
-    k_mstep(const __grid_constant__ CUtensorMap tmap, Dom d, const T* __restrict__ mi, T* __restrict__ mo,
-            C om1, int lz) {
+    k_mstep(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap, Dom d,
+            const T* __restrict__ mi, const T* __restrict__ gm, T* __restrict__ mo, C om1, int lz, int zc0) {
   static_assert(L::dim == 3, "the M step is 3-D");
   using SM = Smem<L, T>;
   constexpr int NM = n_moments<L>();
@@ -420,7 +441,7 @@ __global__ void __launch_bounds__(NT, MINB)
 
   const int tid = threadIdx.x, lx = tid & (TX - 1), ly = tid >> 5;
   const int x0 = int(blockIdx.x) * TX, y0 = int(blockIdx.y) * TY;
-  const int za = int(blockIdx.z) * lz, zb = min(za + lz, d.nz);
+  const int za = (int(blockIdx.z) + zc0) * lz, zb = min(za + lz, d.nz);
   const int gx = x0 + lx, gy = y0 + ly;
   const int64_t col = gx + int64_t(d.nx) * gy;
 
@@ -478,18 +499,20 @@ __global__ void __launch_bounds__(NT, MINB)
 
   constexpr uint32_t kTileBytes = uint32_t(NM * TC * sizeof(T));
   auto issue = [&](int z, int b) {
-    const int zz = wrap_coord(z, d.nz, d.mode[ZMin], d.mode[ZMax]);
-    if (zz < 0) return;
+    int zz = 0;
+    const int src = plane_src(d, z, zz);
+    if (src == 0) return;
     if (tid == 0) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_expect_tx(&bar[b], kTileBytes);
-      tma_load_4d(tile + b * TILE_B, &tmap, &bar[b], x0, y0 - 1, zz, 0);
+      tma_load_4d(tile + b * TILE_B, src == 1 ? &tmap : &gmap, &bar[b], x0, y0 - 1, zz, 0);
     }
     if (hfetch) {
       T* w = wstg + b * WSTG_B + hoff;
-      const T* g = mi + int64_t(zz) * d.plane + hcol;
+      const T* g = (src == 1 ? mi : gm) + int64_t(zz) * d.plane + hcol;
+      const int64_t cs = src == 1 ? d.mstride : 2 * d.plane;
 #pragma unroll
-      for (int c = 0; c < NM; ++c) __pipeline_memcpy_async(w + c * WH, g + c * d.mstride, sizeof(T));
+      for (int c = 0; c < NM; ++c) __pipeline_memcpy_async(w + c * WH, g + c * cs, sizeof(T));
     }
   };
 
@@ -508,7 +531,8 @@ __global__ void __launch_bounds__(NT, MINB)
     constexpr int ZC = decltype(ZCc)::value;
     if (ZC != -1) issue(z + 1, buf ^ 1);
     __pipeline_commit();
-    if (wrap_coord(z, d.nz, d.mode[ZMin], d.mode[ZMax]) >= 0) {
+    int zz_unused = 0;
+    if (plane_src(d, z, zz_unused) != 0) {
       mbar_wait(&bar[buf], (phase >> buf) & 1u);
       phase ^= 1u << buf;
       __pipeline_wait_prior(1);
@@ -563,24 +587,33 @@ EncodeFn encoder() {
   return fn;
 }
 
-// 4-D map (x, y, z, moment array) with a {TX, TY + 2, 1, NM} box
+// 4-D map (x, y, z, moment array) with a {TX, TY + 2, 1, NM} box over the
+// moment buffer `base` (ghost = false), or over the slab ghost planes
+// (ghost = true: layout [NM][2][plane], the "z" coordinate picks the side)
 template <typename T>
-const CUtensorMap* tensor_map(MstepMaps*& maps, const Dom& d, int nm, const T* base) {
+const CUtensorMap* tensor_map(MstepMaps*& maps, const Dom& d, int nm, const T* base, bool ghost) {
   if (!maps) maps = new MstepMaps();
-  const int64_t key[5] = {d.nx, d.ny, d.nz, d.mstride, int64_t(sizeof(T)) * 16 + nm};
-  for (auto& e : maps->e) {
-    bool same = e.base == base;
-    for (int i = 0; i < 5 && same; ++i) same = e.key[i] == key[i];
-    if (same) return &e.map;
+  const int64_t key[5] = {d.nx, d.ny, ghost ? -1 : d.nz, d.mstride, int64_t(sizeof(T)) * 16 + nm};
+  auto same = [&](const MstepMaps::Entry& e) {
+    bool eq = e.base == base;
+    for (int i = 0; i < 5 && eq; ++i) eq = e.key[i] == key[i];
+    return eq;
+  };
+  if (ghost) {
+    if (same(maps->e[2])) return &maps->e[2].map;
+  } else {
+    for (int i = 0; i < 2; ++i)
+      if (same(maps->e[i])) return &maps->e[i].map;
   }
   EncodeFn enc = encoder();
   if (!enc) return nullptr;
-  auto& e = maps->e[maps->next];
+  auto& e = ghost ? maps->e[2] : maps->e[maps->next];
   const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
   const cuuint64_t es = sizeof(T);
   const cuuint32_t estr[4] = {1, 1, 1, 1};
-  const cuuint64_t dim[4] = {cuuint64_t(d.nx), cuuint64_t(d.ny), cuuint64_t(d.nz), cuuint64_t(nm)};
-  const cuuint64_t str[3] = {cuuint64_t(d.nx) * es, cuuint64_t(d.plane) * es, cuuint64_t(d.mstride) * es};
+  const cuuint64_t dim[4] = {cuuint64_t(d.nx), cuuint64_t(d.ny), cuuint64_t(ghost ? 2 : d.nz), cuuint64_t(nm)};
+  const cuuint64_t str[3] = {cuuint64_t(d.nx) * es, cuuint64_t(d.plane) * es,
+                             ghost ? cuuint64_t(2 * d.plane) * es : cuuint64_t(d.mstride) * es};
   const cuuint32_t box[4] = {cuuint32_t(TX), cuuint32_t(TR), 1, cuuint32_t(nm)};
   if (enc(&e.map, dt, 4, const_cast<T*>(base), dim, str, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -588,37 +621,98 @@ const CUtensorMap* tensor_map(MstepMaps*& maps, const Dom& d, int nm, const T* b
     return nullptr;
   e.base = base;
   for (int i = 0; i < 5; ++i) e.key[i] = key[i];
-  maps->next ^= 1;
+  if (!ghost) maps->next ^= 1;
   return &e.map;
+}
+
+// Incoming pushes of a slab boundary plane from the neighbour's nodes, built
+// from the ghost moments (f materialisation of the M schedule on slabs):
+// f_a(x, y, k) = T(post_collision_a(m(x - c_a))) for the directions entering
+// through the slab face, exactly the values the F1 exchange would deliver;
+// sources beyond an x/y wall do not exist (that slot holds the bounce).
+template <class L, typename T, typename C>
+__global__ void __launch_bounds__(128) k_ghost_push(Dom d, T* __restrict__ f, const T* __restrict__ gm,
+                                                    C om1, int side) {
+  const int i = int(blockIdx.x) * 128 + int(threadIdx.x), j = int(blockIdx.y);
+  if (i >= d.nx) return;
+  const int k = side ? d.nz - 1 : 0;
+  const int cz_in = side ? -1 : 1;
+  const T* g = gm + int64_t(side) * d.plane;
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    using dd = Dir<L, a>;
+    if constexpr (dd::z != 0) {
+      if (dd::z != cz_in) return;
+      const int sx = wrap_coord(i - dd::x, d.nx, d.mode[XMin], d.mode[XMax]);
+      const int sy = wrap_coord(j - dd::y, d.ny, d.mode[YMin], d.mode[YMax]);
+      if (sx < 0 || sy < 0) return;
+      const T* p = g + sx + int64_t(d.nx) * sy;
+      const int64_t cs = 2 * d.plane;
+      const NodeMoments<C> m = prepare_node<C>(C(p[0]), C(p[cs]), C(p[2 * cs]), C(p[3 * cs]), C(p[4 * cs]),
+                                               C(p[5 * cs]), C(p[6 * cs]), C(p[7 * cs]), C(p[8 * cs]),
+                                               C(p[9 * cs]));
+      f[a * d.fstride + fidx(d, i, j, k)] = T(post_collision<L, a, C>(m, om1));
+    }
+  });
 }
 
 }  // namespace mstep
 
 bool mstep_supported(int lat, const Dom& d) {
-  return (lat == kD3Q19 || lat == kD3Q27) && !d.has_solid && d.ghost == 0 &&
-         d.nx % mstep::TX == 0 && d.ny % mstep::TY == 0 && mstep::encoder() != nullptr;
+  return (lat == kD3Q19 || lat == kD3Q27) && !d.has_solid && d.nx % mstep::TX == 0 &&
+         d.ny % mstep::TY == 0 && mstep::encoder() != nullptr;
+}
+
+int mstep_chunks(const Dom& d, int lz) {
+  if (lz <= 0) lz = mstep::kDefaultLz;
+  return (d.nz + lz - 1) / lz;
 }
 
 template <typename T>
-int launch_mstep(int lat, int math, const Dom& d, const T* mi, T* mo, double omega,
-                 int lz, MstepMaps*& maps, cudaStream_t st) {
+int launch_ghost_push(int lat, int math, const Dom& d, T* f, const T* gm, double omega, int side,
+                      cudaStream_t st) {
+  using namespace mstep;
+  const dim3 grid(unsigned((d.nx + 127) / 128), unsigned(d.ny));
+  auto go = [&](auto L) {
+    using Lat = decltype(L);
+    if (math == kMathDouble)
+      k_ghost_push<Lat, T, double><<<grid, 128, 0, st>>>(d, f, gm, 1.0 - double(T(omega)), side);
+    else
+      k_ghost_push<Lat, T, float><<<grid, 128, 0, st>>>(d, f, gm, 1.0f - float(omega), side);
+    return 0;
+  };
+  if (lat == kD3Q19) return go(D3Q19{});
+  if (lat == kD3Q27) return go(D3Q27{});
+  return 1;
+}
+
+template <typename T>
+int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
+                 int lz, int chunk0, int nchunks, MstepMaps*& maps, cudaStream_t st) {
   using namespace mstep;
   if (!mstep_supported(lat, d)) return 1;
-  if (lz <= 0) lz = 64;
+  if ((d.mode[ZMin] == kGhost || d.mode[ZMax] == kGhost) && !gm) return 1;
+  if (lz <= 0) lz = kDefaultLz;
+  const int nzc = (d.nz + lz - 1) / lz;
+  if (nchunks <= 0) nchunks = nzc - chunk0;
+  if (chunk0 < 0 || chunk0 + nchunks > nzc) return 1;
+  if (nchunks == 0) return 0;
   bool walls = false;
   for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
-  const dim3 grid(unsigned(d.nx / TX), unsigned(d.ny / TY), unsigned((d.nz + lz - 1) / lz));
+  const dim3 grid(unsigned(d.nx / TX), unsigned(d.ny / TY), unsigned(nchunks));
   if (grid.y > 65535 || grid.z > 65535) return 1;
   const double om1d = 1.0 - double(T(omega));
   const float om1f = 1.0f - float(omega);
   auto by_lat = [&](auto L) {
     using Lat = decltype(L);
-    const CUtensorMap* tm = tensor_map<T>(maps, d, n_moments<Lat>(), mi);
+    const CUtensorMap* tm = tensor_map<T>(maps, d, n_moments<Lat>(), mi, false);
     if (!tm) return 1;
+    const CUtensorMap* gmp = gm ? tensor_map<T>(maps, d, n_moments<Lat>(), gm, true) : tm;
+    if (!gmp) return 1;
     constexpr size_t smem = Smem<Lat, T>::total;
     auto go = [&](auto kern, auto om1) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      kern<<<grid, NT, smem, st>>>(*tm, d, mi, mo, om1, lz);
+      kern<<<grid, NT, smem, st>>>(*tm, *gmp, d, mi, gm, mo, om1, lz, chunk0);
     };
     // fp32 storage + fp32 math: three CTAs per SM (~76 KB shared memory, <= 80
     // registers); fp64 math keeps two (capping it at 80 registers costs more
@@ -637,9 +731,11 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, T* mo, double ome
   return lat == kD3Q19 ? by_lat(D3Q19{}) : by_lat(D3Q27{});
 }
 
-template int launch_mstep<float>(int, int, const Dom&, const float*, float*, double, int, MstepMaps*&,
-                                 cudaStream_t);
-template int launch_mstep<double>(int, int, const Dom&, const double*, double*, double, int, MstepMaps*&,
-                                  cudaStream_t);
+template int launch_mstep<float>(int, int, const Dom&, const float*, const float*, float*, double, int, int,
+                                 int, MstepMaps*&, cudaStream_t);
+template int launch_mstep<double>(int, int, const Dom&, const double*, const double*, double*, double, int, int,
+                                  int, MstepMaps*&, cudaStream_t);
+template int launch_ghost_push<float>(int, int, const Dom&, float*, const float*, double, int, cudaStream_t);
+template int launch_ghost_push<double>(int, int, const Dom&, double*, const double*, double, int, cudaStream_t);
 
 }  // namespace tslb_cuda
