@@ -50,6 +50,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "tslb_collision.cuh"
 #include "tslb_domain.cuh"
@@ -83,10 +84,18 @@ template <class L>
 __host__ __device__ constexpr bool is_reg(int a) {
   return L::c[a][0] == 0 && L::c[a][1] == 0;
 }
-// plane-ring depth of slot direction a (see header): 3 for c_z = +1, else 2
+// Lattice L with the slot-ring variant RD: 0 = two barriers per plane
+// (rings 2 / 3 deep, least shared memory), 1 = one barrier per plane (rings
+// 3 / 4 deep: a slot of plane d may then be rewritten only after every warp
+// has passed the NEXT plane's barrier).
+template <class B, int RD>
+struct SL : B {
+  static constexpr int rd = RD;
+};
+// plane-ring depth of slot direction a: (3 for c_z = +1, else 2) + rd
 template <class L>
 __host__ __device__ constexpr int ring_depth(int a) {
-  return L::c[a][2] == 1 ? 3 : 2;
+  return (L::c[a][2] == 1 ? 3 : 2) + L::rd;
 }
 template <class L>
 __host__ __device__ constexpr int slot_base(int a) {
@@ -221,26 +230,30 @@ struct Shm<double> {
 
 // Slot addressing. Each thread keeps the shared addresses of its own
 // column's slot in the ring planes of destination planes z-1, z, z+1
-// relative to the plane being pushed (2-deep rings: z-1, z; 3-deep: z-1, z,
-// z+1); a push by (dx, dy) is then that address plus a compile-time offset.
-template <typename T>
+// relative to the plane being pushed, for the shallow (DA) and deep (DA+1)
+// rings; a push by (dx, dy) is then that address plus a compile-time offset.
+template <class L, typename T>
 struct Ring {
-  uint32_t own;            // shared address of sl[ly * TX + lx]
-  uint32_t q2[2];
-  uint32_t q3[3];
-  int p2, p3;
-  __device__ __forceinline__ void set() {
-    constexpr uint32_t P = NT * sizeof(T);
-    q2[0] = own + (p2 ^ 1) * P;
-    q2[1] = own + p2 * P;
-    q3[0] = own + (p3 == 0 ? 2 : p3 - 1) * P;
-    q3[1] = own + p3 * P;
-    q3[2] = own + (p3 == 2 ? 0 : p3 + 1) * P;
+  static constexpr int DA = 2 + L::rd, DB = DA + 1;
+  static constexpr uint32_t P = NT * sizeof(T);
+  // qa[k] = address of ring plane (p + k - 1) mod DA: qa[0] holds destination
+  // plane z-1, qa[1] plane z, qa[2 mod DA] plane z+1; advancing the march
+  // rotates the array (register renames, no index arithmetic)
+  uint32_t qa[DA], qb[DB];
+  __device__ __forceinline__ void init(uint32_t own) {
+#pragma unroll
+    for (int k = 0; k < DA; ++k) qa[k] = own + uint32_t((k - 1 + DA) % DA) * P;
+#pragma unroll
+    for (int k = 0; k < DB; ++k) qb[k] = own + uint32_t((k - 1 + DB) % DB) * P;
   }
   __device__ __forceinline__ void advance() {
-    p2 ^= 1;
-    p3 = p3 == 2 ? 0 : p3 + 1;
-    set();
+    const uint32_t ta = qa[0], tb = qb[0];
+#pragma unroll
+    for (int k = 0; k + 1 < DA; ++k) qa[k] = qa[k + 1];
+    qa[DA - 1] = ta;
+#pragma unroll
+    for (int k = 0; k + 1 < DB; ++k) qb[k] = qb[k + 1];
+    qb[DB - 1] = tb;
   }
 };
 
@@ -250,9 +263,9 @@ __host__ __device__ constexpr int slot_off() {
   return int((slot_base<L>(A) * NT + DY * TX + DX) * int(sizeof(T)));
 }
 template <class L, int A, int DZ, typename T>
-__device__ __forceinline__ uint32_t ring_addr(const Ring<T>& rg) {
-  if constexpr (ring_depth<L>(A) == 3) return rg.q3[DZ + 1];
-  else return rg.q2[DZ + 1];  // DZ is -1 or 0 for 2-deep rings
+__device__ __forceinline__ uint32_t ring_addr(const Ring<L, T>& rg) {
+  if constexpr (ring_depth<L>(A) == Ring<L, T>::DB) return rg.qb[(DZ + 1) % Ring<L, T>::DB];
+  else return rg.qa[(DZ + 1) % Ring<L, T>::DA];
 }
 
 template <class L, typename T, typename C>
@@ -273,7 +286,7 @@ struct Contact {
 // Output of direction A from a tile node: bounce into its own opposite slot
 // or push into the slot of the destination (dropped if outside the tile).
 template <class L, int A, typename T, typename C, bool WALLS, int ZC>
-__device__ __forceinline__ void emit(const Dom& d, const Ring<T>& rg, T (&R)[L::q][3],
+__device__ __forceinline__ void emit(const Dom& d, const Ring<L, T>& rg, T (&R)[L::q][3],
                                      int lx, int ly, const Contact& ct, T o) {
   using dd = Dir<L, A>;
   if constexpr (WALLS && ZC == 0) {
@@ -305,7 +318,7 @@ __device__ __forceinline__ void emit(const Dom& d, const Ring<T>& rg, T (&R)[L::
 // All directions of a tile node; ZC != 0 (a plane just outside the march)
 // keeps only the directions with c_z == ZC.
 template <class L, typename T, typename C, bool WALLS, int ZC>
-__device__ __forceinline__ void push_tile(const Dom& d, const Ring<T>& rg, T (&R)[L::q][3],
+__device__ __forceinline__ void push_tile(const Dom& d, const Ring<L, T>& rg, T (&R)[L::q][3],
                                           int lx, int ly, const Contact& ct,
                                           const NodeMoments<C>& m, C om1) {
   unroll<L::q>([&](auto A) {
@@ -349,7 +362,7 @@ __host__ __device__ constexpr int halo_rank(int a) {
 }
 
 template <class L, typename T, typename C, int SX, int SY, int ZC, int PART>
-__device__ __forceinline__ void push_halo(const Ring<T>& rg, int hdelta, int hx, int hy,
+__device__ __forceinline__ void push_halo(const Ring<L, T>& rg, int hdelta, int hx, int hy,
                                           const NodeMoments<C>& m, C om1) {
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
@@ -367,7 +380,7 @@ __device__ __forceinline__ void push_halo(const Ring<T>& rg, int hdelta, int hx,
 }
 
 template <class L, typename T, typename C, int ZC>
-__device__ __forceinline__ void push_ring(const Ring<T>& rg, int hdelta, int task, int hx, int hy,
+__device__ __forceinline__ void push_ring(const Ring<L, T>& rg, int hdelta, int task, int hx, int hy,
                                           const NodeMoments<C>& m, C om1) {
   switch (task) {
     case 0: push_halo<L, T, C, 0, -1, ZC, 0>(rg, hdelta, hx, hy, m, om1); break;
@@ -384,7 +397,7 @@ __device__ __forceinline__ void push_ring(const Ring<T>& rg, int hdelta, int tas
 // compute_moments of one node from its gathered slots (kernels.hpp:74-107;
 // same accumulation order and formulae as k_moments)
 template <class L, typename T, typename C>
-__device__ __forceinline__ void finalize(const Dom& d, const Ring<T>& rg, const T (&R)[L::q][3],
+__device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, const T (&R)[L::q][3],
                                          T* __restrict__ mo, int64_t idx) {
   C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pzz = 0, pxy = 0, pxz = 0, pyz = 0;
   unroll<L::q>([&](auto A) {
@@ -519,11 +532,8 @@ __global__ void __launch_bounds__(NT, MINB)
   T R[L::q][3];
 #pragma unroll
   for (int a = 0; a < L::q; ++a) R[a][0] = R[a][1] = R[a][2] = T(0);
-  Ring<T> rg;
-  rg.own = smem_u32(sl + ly * TX + lx);
-  rg.p2 = 0;
-  rg.p3 = 0;
-  rg.set();
+  Ring<L, T> rg;
+  rg.init(smem_u32(sl + ly * TX + lx));
   int buf = 0;
   uint32_t phase = 0;  // bit b: parity of the next completion of bar[b]
 
@@ -551,7 +561,7 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     __syncthreads();
     if (z - 1 >= za) finalize<L, T, C>(d, rg, R, mo, col + int64_t(z - 1) * d.plane);
-    __syncthreads();
+    if constexpr (L::rd == 0) __syncthreads();
 #pragma unroll
     for (int a = 0; a < L::q; ++a) {
       R[a][0] = R[a][1];
@@ -703,6 +713,16 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
   if (grid.y > 65535 || grid.z > 65535) return 1;
   const double om1d = 1.0 - double(T(omega));
   const float om1f = 1.0f - float(omega);
+  // slot-ring variant: one barrier per plane (deeper rings, two CTAs per SM)
+  // for D3Q19 with fp32 storage -- measured faster than two barriers at three
+  // CTAs per SM for fp32 node math (43.5 vs 36.7 GLUPS) and equal for fp64
+  // (r01 s9); D3Q27 and fp64 storage would lose a CTA, so they keep two
+  // barriers. TSLB_MSTEP_RD=0/1 overrides (measurements).
+  static const int rd_env = [] {
+    const char* e = std::getenv("TSLB_MSTEP_RD");
+    return e ? std::atoi(e) : -1;
+  }();
+  const bool deep = rd_env >= 0 ? rd_env == 1 : (lat == kD3Q19 && sizeof(T) == 4);
   auto by_lat = [&](auto L) {
     using Lat = decltype(L);
     const CUtensorMap* tm = tensor_map<T>(maps, d, n_moments<Lat>(), mi, false);
@@ -710,6 +730,7 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
     const CUtensorMap* gmp = gm ? tensor_map<T>(maps, d, n_moments<Lat>(), gm, true) : tm;
     if (!gmp) return 1;
     constexpr size_t smem = Smem<Lat, T>::total;
+    if (smem > 227 * 1024) return 1;
     auto go = [&](auto kern, auto om1) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       kern<<<grid, NT, smem, st>>>(*tm, *gmp, d, mi, gm, mo, om1, lz, chunk0);
@@ -717,7 +738,7 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
     // fp32 storage + fp32 math: three CTAs per SM (~76 KB shared memory, <= 80
     // registers); fp64 math keeps two (capping it at 80 registers costs more
     // ILP than the third CTA buys); fp64 storage holds one CTA per SM
-    constexpr int MB = sizeof(T) == 4 ? 3 : 1;
+    constexpr int MB = sizeof(T) == 4 && Lat::rd == 0 ? 3 : sizeof(T) == 4 ? 2 : 1;
     constexpr int MBD = sizeof(T) == 4 ? 2 : 1;
     if (math == kMathDouble) {
       if (walls) go(k_mstep<Lat, T, double, true, MBD>, om1d);
@@ -728,7 +749,11 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
     }
     return 0;
   };
-  return lat == kD3Q19 ? by_lat(D3Q19{}) : by_lat(D3Q27{});
+  auto by_rd = [&](auto B) {
+    using Base = decltype(B);
+    return deep ? by_lat(SL<Base, 1>{}) : by_lat(SL<Base, 0>{});
+  };
+  return lat == kD3Q19 ? by_rd(D3Q19{}) : by_rd(D3Q27{});
 }
 
 template int launch_mstep<float>(int, int, const Dom&, const float*, const float*, float*, double, int, int,
