@@ -724,15 +724,21 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   }
   if (components == 1 && mstep_supported(lattice, d)) {
     const char* e = std::getenv("TSLB_SCHEDULE");
+    // M needs a second moment buffer (and ghost planes on slabs); where HBM
+    // cannot hold it (e.g. D3Q27 1024^3 fp32) the solver stays on F1
     if (!(e && !std::strcmp(e, "f1"))) {
-      if ((rc = alloc(h, &h->mo2, mbytes))) return fail(rc);
-      CK(cudaMemsetAsync(h->mo2, 0, mbytes, h->s));
-      if (decomposed) {
-        const size_t gb = size_t(d.plane) * 2 * (1 + h->dim + h->np) * h->esz;
-        if ((rc = alloc(h, &h->gm, gb))) return fail(rc);
-        CK(cudaMemsetAsync(h->gm, 0, gb, h->s));
+      const size_t gb = decomposed ? size_t(d.plane) * 2 * (1 + h->dim + h->np) * h->esz : 0;
+      if (cudaMalloc(&h->mo2, mbytes) == cudaSuccess &&
+          (!gb || cudaMalloc(&h->gm, gb) == cudaSuccess)) {
+        h->bytes += mbytes + gb;
+        CK(cudaMemsetAsync(h->mo2, 0, mbytes, h->s));
+        if (gb) CK(cudaMemsetAsync(h->gm, 0, gb, h->s));
+        h->sched = TSLB_SCHED_M;
+      } else {
+        cudaGetLastError();  // clear the allocation failure
+        if (h->mo2) cudaFree(h->mo2);
+        h->mo2 = nullptr;
       }
-      h->sched = TSLB_SCHED_M;
     }
   }
   if ((rc = alloc(h, reinterpret_cast<void**>(&h->red),
