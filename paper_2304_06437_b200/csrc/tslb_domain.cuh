@@ -76,4 +76,69 @@ __device__ __forceinline__ int64_t fidx(const Dom& d, int i, int j, int k) {
          int64_t(d.nx) * (int64_t(j) + int64_t(d.ny) * (int64_t(k) + d.ghost));
 }
 
+// Per-thread face geometry: linear deltas for a +/- step on each axis
+// (already wrapped for periodic faces, ghost-shifted for slab faces) and
+// whether the step bounces off a wall.
+struct Steps {
+  int64_t dp[3], dm[3];
+  bool bp[3], bm[3];
+};
+
+__device__ __forceinline__ Steps face_steps(const Dom& d, int i, int j, int k) {
+  Steps s;
+  const int c[3] = {i, j, k};
+  const int nd[3] = {d.nx, d.ny, d.nz};
+  const int64_t unit[3] = {1, int64_t(d.nx), d.plane};
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    s.dp[ax] = unit[ax];
+    s.dm[ax] = -unit[ax];
+    s.bp[ax] = false;
+    s.bm[ax] = false;
+    if (c[ax] == nd[ax] - 1) {
+      const int m = d.mode[2 * ax + 1];
+      if (m == kWrap) s.dp[ax] = -int64_t(nd[ax] - 1) * unit[ax];
+      if (m == kWall) s.bp[ax] = true;
+    }
+    if (c[ax] == 0) {
+      const int m = d.mode[2 * ax];
+      if (m == kWrap) s.dm[ax] = int64_t(nd[ax] - 1) * unit[ax];
+      if (m == kWall) s.bm[ax] = true;
+    }
+  }
+  return s;
+}
+
+// The same with 32-bit deltas (a plane holds < 2^31 nodes): cheaper address
+// arithmetic for stencil kernels that index relative to a node pointer.
+struct Steps32 {
+  int dp[3], dm[3];
+  bool bp[3], bm[3];
+};
+
+__device__ __forceinline__ Steps32 face_steps32(const Dom& d, int i, int j, int k) {
+  Steps32 s;
+  const int c[3] = {i, j, k};
+  const int nd[3] = {d.nx, d.ny, d.nz};
+  const int unit[3] = {1, d.nx, int(d.plane)};
+#pragma unroll
+  for (int ax = 0; ax < 3; ++ax) {
+    s.dp[ax] = unit[ax];
+    s.dm[ax] = -unit[ax];
+    s.bp[ax] = false;
+    s.bm[ax] = false;
+    if (c[ax] == nd[ax] - 1) {
+      const int m = d.mode[2 * ax + 1];
+      if (m == kWrap) s.dp[ax] = -(nd[ax] - 1) * unit[ax];
+      if (m == kWall) s.bp[ax] = true;
+    }
+    if (c[ax] == 0) {
+      const int m = d.mode[2 * ax];
+      if (m == kWrap) s.dm[ax] = (nd[ax] - 1) * unit[ax];
+      if (m == kWall) s.bm[ax] = true;
+    }
+  }
+  return s;
+}
+
 }  // namespace tslb_cuda

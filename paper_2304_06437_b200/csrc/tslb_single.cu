@@ -102,39 +102,6 @@ __device__ __forceinline__ NodeMoments<C> load_node(const Dom& d,
   }
 }
 
-// Per-thread face geometry: linear deltas for a +/- step on each axis
-// (already wrapped for periodic faces, ghost-shifted for slab faces) and
-// whether the step bounces off a wall.
-struct Steps {
-  int64_t dp[3], dm[3];
-  bool bp[3], bm[3];
-};
-
-__device__ __forceinline__ Steps face_steps(const Dom& d, int i, int j, int k) {
-  Steps s;
-  const int c[3] = {i, j, k};
-  const int nd[3] = {d.nx, d.ny, d.nz};
-  const int64_t unit[3] = {1, int64_t(d.nx), d.plane};
-#pragma unroll
-  for (int ax = 0; ax < 3; ++ax) {
-    s.dp[ax] = unit[ax];
-    s.dm[ax] = -unit[ax];
-    s.bp[ax] = false;
-    s.bm[ax] = false;
-    if (c[ax] == nd[ax] - 1) {
-      const int m = d.mode[2 * ax + 1];
-      if (m == kWrap) s.dp[ax] = -int64_t(nd[ax] - 1) * unit[ax];
-      if (m == kWall) s.bp[ax] = true;
-    }
-    if (c[ax] == 0) {
-      const int m = d.mode[2 * ax];
-      if (m == kWrap) s.dm[ax] = int64_t(nd[ax] - 1) * unit[ax];
-      if (m == kWall) s.bm[ax] = true;
-    }
-  }
-  return s;
-}
-
 // Generic (slow-bit) resolution with solids: resolve_push, boundary.hpp:118-144.
 // Returns true on bounce; u_wall summed in T over crossed wall faces.
 template <typename T>

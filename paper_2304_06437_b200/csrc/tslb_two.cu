@@ -17,6 +17,7 @@
 #include "tslb_collision.cuh"
 #include "tslb_domain.cuh"
 #include "tslb_kernels.h"
+#include "tslb_pair.cuh"
 
 namespace tslb_cuda {
 
@@ -387,6 +388,158 @@ __global__ void __launch_bounds__(BX2)
 }
 
 // ---------------------------------------------------------------------------
+// Box geometries (no solid mask): neighbours and push targets come from the
+// node coordinates (face_steps) instead of the classify_nodes slow mask, and
+// the regularised collision of opposite directions is shared (post_pair,
+// exact for rho != -0: rho here is a +0-seeded sum over g, see
+// tslb_pair.cuh). The interface terms keep the reference order per
+// direction. Same results, bit for bit, as k_cg_gradient / k_cg_streamcoll.
+template <class L, typename T, bool WALLS>
+__global__ void __launch_bounds__(BX2) k_cg_gradient_box(Dom d, TF<T> s) {
+  int i, j, k;
+  if (!node_coords<BX2>(d, i, j, k)) return;
+  const int64_t mi = midx(d, i, j, k);
+  const Steps32 st = face_steps32(d, i, j, k);
+  const T* __restrict__ ph = s.phi + mi;
+  const T phi0 = ph[0];
+  T gx = 0, gy = 0, gz = 0;
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    using dd = Dir<L, a>;
+    if constexpr (a > 0) {
+      int delta = 0;
+      bool wall = false;
+      if constexpr (dd::x == 1) { delta += st.dp[0]; wall |= st.bp[0]; }
+      if constexpr (dd::x == -1) { delta += st.dm[0]; wall |= st.bm[0]; }
+      if constexpr (dd::y == 1) { delta += st.dp[1]; wall |= st.bp[1]; }
+      if constexpr (dd::y == -1) { delta += st.dm[1]; wall |= st.bm[1]; }
+      if constexpr (dd::z == 1) { delta += st.dp[2]; wall |= st.bp[2]; }
+      if constexpr (dd::z == -1) { delta += st.dm[2]; wall |= st.bm[2]; }
+      const T pn = (WALLS && wall) ? phi0 : __ldg(ph + delta);
+      constexpr T w = dd::template t<T>();
+      const T tp = w * pn;
+      if constexpr (dd::x == 1) gx += tp;
+      if constexpr (dd::x == -1) gx -= tp;
+      if constexpr (dd::y == 1) gy += tp;
+      if constexpr (dd::y == -1) gy -= tp;
+      if constexpr (dd::z == 1) gz += tp;
+      if constexpr (dd::z == -1) gz -= tp;
+    }
+  });
+  const int64_t ms = d.mstride;
+  s.grad[mi] = T(3) * gx;
+  s.grad[ms + mi] = T(3) * gy;
+  if constexpr (L::dim == 3) s.grad[2 * ms + mi] = T(3) * gz;
+}
+
+template <class L, typename T, bool FOLD, bool WALLS>
+__global__ void __launch_bounds__(BX2)
+    k_cg_streamcoll_box(Dom d, T* __restrict__ fr, T* __restrict__ fb, TF<T> s, T omega, T tau,
+                        ColorParamsDev cp) {
+  int i, j, k;
+  if (!node_coords<BX2>(d, i, j, k)) return;
+  const int64_t fi = fidx(d, i, j, k);
+  const int64_t mi = midx(d, i, j, k);
+  const int64_t ms = d.mstride;
+  T ux, uy, uz, p[6];
+  if constexpr (FOLD) {
+    prepare_node_stress<L, T>(d, s, mi, tau, cp, ux, uy, uz, p);
+  } else {
+    ux = s.mom[mi];
+    uy = s.mom[ms + mi];
+    uz = L::dim == 3 ? s.mom[2 * ms + mi] : T(0);
+    constexpr int np = L::dim * (L::dim + 1) / 2;
+#pragma unroll
+    for (int c = 0; c < np; ++c) p[c] = s.pin[c * ms + mi];
+  }
+  const T r = s.rho[mi];
+  NodeMoments<T> m;
+  if constexpr (L::dim == 3)
+    m = prepare_node<T>(r, ux, uy, uz, p[0], p[1], p[2], p[3], p[4], p[5]);
+  else
+    m = prepare_node<T>(r, ux, uy, T(0), p[0], p[1], T(0), p[2], T(0), T(0));
+  const T om1 = T(1) - omega;
+  const T pert_coef = T(2.25) * T(cp.sigma) * omega;
+  const T rr = s.rho_r[mi];
+  const T rb = s.rho_b[mi];
+  const T red_frac = rr / r;
+  const T rec_amp = T(cp.beta) * (rr * rb / r);
+  const T gx = s.grad[mi];
+  const T gy = s.grad[ms + mi];
+  const T gz = L::dim == 3 ? s.grad[2 * ms + mi] : T(0);
+  const T gn = sqrt(gx * gx + gy * gy + gz * gz);
+  const bool interface = gn > T(cp.grad_threshold);
+  const T pert_amp = interface ? pert_coef * gn : T(0);
+  const T inv_gn = interface ? T(1) / gn : T(0);
+  const T nhx = gx * inv_gn, nhy = gy * inv_gn, nhz = gz * inv_gn;
+  const bool linear = cp.linear != 0;
+  const Steps32 st = face_steps32(d, i, j, k);
+  T* __restrict__ frn = fr + fi;
+  T* __restrict__ fbn = fb + fi;
+
+  // one direction: perturbation + recolouring (reference order), then push
+  // or bounce (multicomponent.hpp:340-398)
+  auto out = [&](auto A, T g_out) {
+    constexpr int a = decltype(A)::value;
+    using dd = Dir<L, a>;
+    constexpr T t = dd::template t<T>();
+    constexpr T b = dd::template b<T>();
+    T fr_out;
+    if (interface) {
+      const T cn = dot_c<dd::x, dd::y, dd::z>(nhx, nhy, nhz);
+      const T shape = !linear ? t * cn * cn - b : t * cn - b;
+      g_out += pert_amp * shape;
+      fr_out = red_frac * g_out + rec_amp * t * cn * inv_cnorm<T, dd::norm2>();
+    } else {
+      fr_out = red_frac * g_out;
+    }
+    const T fb_out = g_out - fr_out;
+    int delta = 0;
+    bool bounce = false;
+    if constexpr (dd::x == 1) { delta += st.dp[0]; bounce |= st.bp[0]; }
+    if constexpr (dd::x == -1) { delta += st.dm[0]; bounce |= st.bm[0]; }
+    if constexpr (dd::y == 1) { delta += st.dp[1]; bounce |= st.bp[1]; }
+    if constexpr (dd::y == -1) { delta += st.dm[1]; bounce |= st.bm[1]; }
+    if constexpr (dd::z == 1) { delta += st.dp[2]; bounce |= st.bp[2]; }
+    if constexpr (dd::z == -1) { delta += st.dm[2]; bounce |= st.bm[2]; }
+    if (WALLS && bounce) {
+      T wx = T(0), wy = T(0), wz = T(0);
+      auto add = [&](bool crossed, int face) {
+        if (crossed) {
+          wx += T(d.uw[face][0]);
+          wy += T(d.uw[face][1]);
+          wz += T(d.uw[face][2]);
+        }
+      };
+      if constexpr (dd::x == 1) add(st.bp[0], XMax);
+      if constexpr (dd::x == -1) add(st.bm[0], XMin);
+      if constexpr (dd::y == 1) add(st.bp[1], YMax);
+      if constexpr (dd::y == -1) add(st.bm[1], YMin);
+      if constexpr (dd::z == 1) add(st.bp[2], ZMax);
+      if constexpr (dd::z == -1) add(st.bm[2], ZMin);
+      const T corr = bounce_correction<L, a, T>(wx, wy, wz);
+      const T corr_r = red_frac * corr;
+      frn[dd::opp * d.fstride] = fr_out - corr_r;
+      fbn[dd::opp * d.fstride] = fb_out - (corr - corr_r);
+    } else {
+      frn[a * d.fstride + delta] = fr_out;
+      fbn[a * d.fstride + delta] = fb_out;
+    }
+  };
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    if constexpr (a == 0) {
+      out(A, post_rest<L, T>(m, om1));
+    } else if constexpr (a & 1) {
+      T ga, gb;
+      post_pair<L, a, T>(m, om1, ga, gb);
+      out(A, ga);
+      out(std::integral_constant<int, a + 1>{}, gb);
+    }
+  });
+}
+
+// ---------------------------------------------------------------------------
 // device droplet initialiser (initialize_colors, multicomponent.hpp:427-449,
 // with the tslb_main droplet profile 0.5 (1 + tanh(R - r)))
 template <class L, typename T>
@@ -445,7 +598,14 @@ int launch_cg_gradient(int lat, const Dom& d, const TwoFields& s,
                        const uint8_t* solid, const uint32_t* slow,
                        const ColorParamsDev& cp, cudaStream_t st) {
   return with_lat2(lat, [&](auto L) {
-    k_cg_gradient<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s), solid, slow, cp);
+    bool walls = false;
+    for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
+    if (!d.has_solid && cp.nci_strength == 0.0 && walls)
+      k_cg_gradient_box<decltype(L), T, true><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s));
+    else if (!d.has_solid && cp.nci_strength == 0.0)
+      k_cg_gradient_box<decltype(L), T, false><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s));
+    else
+      k_cg_gradient<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s), solid, slow, cp);
   });
 }
 
@@ -468,6 +628,18 @@ int launch_cg_streamcoll(int lat, const Dom& d, T* fr, T* fb,
   const T om = T(omega);
   const T tau = T(1) / om;
   return with_lat2(lat, [&](auto L) {
+    // the fused step (fold_prepare) reads rho from k_cg_moments, a +0-seeded
+    // sum, so the pair rewrite is exact; the standalone phase may see
+    // user-written moments and keeps the reference order
+    if (!d.has_solid && fold_prepare) {
+      bool walls = false;
+      for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
+      if (walls)
+        k_cg_streamcoll_box<decltype(L), T, true, true><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
+      else
+        k_cg_streamcoll_box<decltype(L), T, true, false><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
+      return;
+    }
     if (fold_prepare)
       k_cg_streamcoll<decltype(L), T, true>
           <<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), solid, slow, om, tau, cp);
