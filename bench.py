@@ -312,13 +312,18 @@ def main():
     # roofline of the dominant kernel: algorithmic bytes per launch / mean
     # launch duration (CUDA events on the solver stream, timed region)
     per_node = kernel_bytes(lat, W["comps"], es)
+    if W["comps"] == 2 and "cg_gradient" not in prof:
+        # gradient folded into the recolouring stream-collide: it reads phi
+        # (its stencil from cache) instead of the stored gradient
+        npi = lat.dim * (lat.dim + 1) // 2
+        per_node = {"cg_moments": per_node["cg_moments"], "cg_streamcoll": (3 + lat.dim + npi + 1 + 2 * lat.q) * es}
     dom = max((k for k in per_node if k in prof), key=lambda k: prof[k][0])
     k_ms, k_n = prof[dom]
     local_nodes = nx * ny * nzp
     achieved = per_node[dom] * local_nodes / (k_ms / k_n / 1e3) / 1e9
     hbm, peak_kind, _ = peaks()
     sched = sim.schedule if W["comps"] == 1 else "f1"
-    sb = step_bytes(lat, W["comps"], es, sched)
+    sb = step_bytes(lat, W["comps"], es, sched) if W["comps"] == 1 else sum(per_node.values())
     step_bw = glups * sb / world  # per-GPU GB/s of the whole step
     traffic, tsrc = None, None
     try:
@@ -370,6 +375,8 @@ def main():
                           "schedule": ({"m": "M: moment-resident single pass (populations rebuilt in shared "
                                              "memory; f materialised on read)",
                                         "f1": "F1: moments + fused stream-collide"}[sched] if W["comps"] == 1
+                                       else "colour moments + fused gradient/prepare/stream-collide-recolour"
+                                       if "cg_gradient" not in prof
                                        else "colour moments + gradient + fused prepare/stream-collide-recolour"),
                           "l2": "state >> 126 MB L2, no flush needed" if nodes > 10 ** 7
                           else "L2-resident (correctness config)",

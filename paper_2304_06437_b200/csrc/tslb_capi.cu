@@ -143,6 +143,10 @@ struct tslb_cuda_sim {
   int64_t graph_launches = 0;
   bool graphs_ok = true;
   bool stress_pending = false;
+  // two-fluid: the fused step folded the gradient phase into the recolouring
+  // kernel; the gradient arrays are filled when something reads them
+  bool grad_pending = false;
+  bool grad_pending_after_graph = false;
   long steps = 0;
   // profiling
   bool prof = false;
@@ -369,6 +373,7 @@ int ph_cg_moments(tslb_cuda_sim* h, cudaStream_t st) {
 int ph_cg_gradient(tslb_cuda_sim* h, cudaStream_t st) {
   Prof p(h, TSLB_K_CG_GRADIENT, st);
   ++h->launches;
+  h->grad_pending = false;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
     return launch_cg_gradient<T>(h->lat, h->range(0, h->nzl), h->tf(), h->solid,
@@ -384,6 +389,12 @@ int ph_cg_prepare(tslb_cuda_sim* h, cudaStream_t st) {
     return launch_cg_prepare_stress<T>(h->lat, h->range(0, h->nzl), h->tf(),
                                        h->solid, h->omega, h->cp, st);
   });
+}
+
+// the gradient arrays of the last fused two-fluid step, if still owed
+int finish_gradient(tslb_cuda_sim* h) {
+  if (!h->grad_pending) return 0;
+  return ph_cg_gradient(h, h->s);
 }
 
 int ph_cg_streamcoll(tslb_cuda_sim* h, int fold, cudaStream_t st) {
@@ -473,8 +484,23 @@ int enqueue_step(tslb_cuda_sim* h) {
   int rc;
   if (h->comps == 2) {
     if ((rc = ph_cg_moments(h, h->s))) return rc;
-    if ((rc = ph_cg_gradient(h, h->s))) return rc;
-    if ((rc = ph_cg_streamcoll(h, 1, h->s))) return rc;
+    // box geometry without NCI: gradient folded into the stream-collide
+    int folded = 1;
+    {
+      Prof p(h, TSLB_K_CG_STREAMCOLL, h->s);
+      folded = by_scalar(h, [&](auto z) {
+        using T = decltype(z);
+        return launch_cg_streamcoll_grad<T>(h->lat, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
+                                            static_cast<T*>(h->f[1]), h->tf(), h->omega, h->cp, h->s);
+      });
+    }
+    if (folded == 0) {
+      ++h->launches;
+      h->grad_pending = true;
+    } else {
+      if ((rc = ph_cg_gradient(h, h->s))) return rc;
+      if ((rc = ph_cg_streamcoll(h, 1, h->s))) return rc;
+    }
     h->stress_pending = true;
     ++h->steps;
     return 0;
@@ -966,6 +992,7 @@ int tslb_cuda_upload_field(tslb_cuda_handle h, int field, const void* host) {
   void* base; int cnt, eb; int64_t stride;
   if (int rc = field_desc(h, field, &base, &cnt, &eb, &stride, true)) return rc;
   CK(cudaSetDevice(h->device));
+  if (int rc = finish_gradient(h)) return rc;
   // the implicit f(t+1) is a function of the moment arrays being replaced
   if (int rc = materialize(h)) return rc;
   const size_t pb = size_t(h->n()) * eb;
@@ -979,6 +1006,7 @@ int tslb_cuda_upload_field(tslb_cuda_handle h, int field, const void* host) {
 
 int tslb_cuda_download_field(tslb_cuda_handle h, int field, void* host) {
   CK(cudaSetDevice(h->device));
+  if (int rc = finish_gradient(h)) return rc;
   // two-fluid: after a step the host-visible mom/pineq are u_eq / Pi^neq
   // (prepare_stress output, multicomponent.hpp:271-309); the fused step keeps
   // the raw values on the device, so finish the phase lazily here.
@@ -1078,6 +1106,7 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
       for (long k = 0; k < kGraphSteps && !rc; ++k) rc = enqueue_step(h);
       cudaError_t ce = cudaStreamEndCapture(h->s, &g);
       h->steps = steps0;
+      h->grad_pending_after_graph = h->grad_pending;
       h->graph_launches = h->launches - l0;
       h->launches = l0;
       if (rc) return rc;
@@ -1091,7 +1120,10 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
       CK(cudaGraphLaunch(h->graph, h->s));
       h->steps += h->graph_steps;
       h->launches += h->graph_launches;
-      if (h->comps == 2) h->stress_pending = true;
+      if (h->comps == 2) {
+        h->stress_pending = true;
+        h->grad_pending = h->grad_pending_after_graph;
+      }
     }
   }
   for (long k = done; k < nsteps; ++k)
@@ -1194,6 +1226,7 @@ int tslb_cuda_stream_only(tslb_cuda_handle h) {
 int tslb_cuda_color_moments(tslb_cuda_handle h) {
   if (h->comps != 2) return set_err(TSLB_EINVAL, "color_moments is two-fluid");
   CK(cudaSetDevice(h->device));
+  if (int rc = finish_gradient(h)) return rc;
   if (int rc = ph_cg_moments(h, h->s)) return rc;
   return sync(h);
 }
@@ -1208,6 +1241,7 @@ int tslb_cuda_gradient_and_nci(tslb_cuda_handle h) {
 int tslb_cuda_prepare_stress(tslb_cuda_handle h) {
   if (h->comps != 2) return set_err(TSLB_EINVAL, "prepare_stress is two-fluid");
   CK(cudaSetDevice(h->device));
+  if (int rc = finish_gradient(h)) return rc;
   if (int rc = ph_cg_prepare(h, h->s)) return rc;
   return sync(h);
 }
@@ -1215,6 +1249,7 @@ int tslb_cuda_prepare_stress(tslb_cuda_handle h) {
 int tslb_cuda_stream_collide_recolor(tslb_cuda_handle h) {
   if (h->comps != 2) return set_err(TSLB_EINVAL, "stream_collide_recolor is two-fluid");
   CK(cudaSetDevice(h->device));
+  if (int rc = finish_gradient(h)) return rc;
   if (int rc = ph_cg_streamcoll(h, 0, h->s)) return rc;
   return sync(h);
 }
@@ -1252,6 +1287,7 @@ int tslb_cuda_totals(tslb_cuda_handle h, double* mass, double* momentum3) {
 int tslb_cuda_stability(tslb_cuda_handle h, int* finite, double* max_speed,
                         double* min_rho, double* max_rho, int64_t* first_bad) {
   CK(cudaSetDevice(h->device));
+  if (int rc = finish_gradient(h)) return rc;
   if (h->comps == 2 && h->stress_pending)
     if (int rc = ph_cg_prepare(h, h->s)) return rc;
   double* part = h->red;

@@ -94,6 +94,11 @@ int launch_cg_streamcoll(int lat, const Dom& d, T* fr, T* fb,
                          const uint32_t* slow, double omega,
                          const ColorParamsDev& cp, int fold_prepare,
                          cudaStream_t st);
+// gradient folded into the recolouring stream-collide (box, NCI off);
+// nonzero when not applicable
+template <typename T>
+int launch_cg_streamcoll_grad(int lat, const Dom& d, T* fr, T* fb, const TwoFields& s,
+                              double omega, const ColorParamsDev& cp, cudaStream_t st);
 template <typename T>
 int launch_init_colors(int lat, const Dom& d, T* fr, T* fb,
                        const uint8_t* solid, const InitSpec& s,

@@ -394,15 +394,16 @@ __global__ void __launch_bounds__(BX2)
 // exact for rho != -0: rho here is a +0-seeded sum over g, see
 // tslb_pair.cuh). The interface terms keep the reference order per
 // direction. Same results, bit for bit, as k_cg_gradient / k_cg_streamcoll.
+// grad phi at one node from its neighbours (gradient_and_nci,
+// multicomponent.hpp:178-200: wall neighbours take phi(x)); accumulation in
+// the reference's direction order
 template <class L, typename T, bool WALLS>
-__global__ void __launch_bounds__(BX2) k_cg_gradient_box(Dom d, TF<T> s) {
-  int i, j, k;
-  if (!node_coords<BX2>(d, i, j, k)) return;
-  const int64_t mi = midx(d, i, j, k);
-  const Steps32 st = face_steps32(d, i, j, k);
-  const T* __restrict__ ph = s.phi + mi;
+__device__ __forceinline__ void gradient_at(const T* __restrict__ ph, const Steps32& st, T& gx, T& gy,
+                                            T& gz) {
   const T phi0 = ph[0];
-  T gx = 0, gy = 0, gz = 0;
+  gx = 0;
+  gy = 0;
+  gz = 0;
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
     using dd = Dir<L, a>;
@@ -426,13 +427,28 @@ __global__ void __launch_bounds__(BX2) k_cg_gradient_box(Dom d, TF<T> s) {
       if constexpr (dd::z == -1) gz -= tp;
     }
   });
-  const int64_t ms = d.mstride;
-  s.grad[mi] = T(3) * gx;
-  s.grad[ms + mi] = T(3) * gy;
-  if constexpr (L::dim == 3) s.grad[2 * ms + mi] = T(3) * gz;
+  gx = T(3) * gx;
+  gy = T(3) * gy;
+  gz = T(3) * gz;
 }
 
-template <class L, typename T, bool FOLD, bool WALLS>
+template <class L, typename T, bool WALLS>
+__global__ void __launch_bounds__(BX2) k_cg_gradient_box(Dom d, TF<T> s) {
+  int i, j, k;
+  if (!node_coords<BX2>(d, i, j, k)) return;
+  const int64_t mi = midx(d, i, j, k);
+  T gx, gy, gz;
+  gradient_at<L, T, WALLS>(s.phi + mi, face_steps32(d, i, j, k), gx, gy, gz);
+  const int64_t ms = d.mstride;
+  s.grad[mi] = gx;
+  s.grad[ms + mi] = gy;
+  if constexpr (L::dim == 3) s.grad[2 * ms + mi] = gz;
+}
+
+// GRAD: compute grad phi in place from the phi stencil instead of reading
+// the gradient arrays (the step's gradient phase folded in; the host
+// mirror computes the arrays lazily when they are read)
+template <class L, typename T, bool FOLD, bool WALLS, bool GRAD>
 __global__ void __launch_bounds__(BX2)
     k_cg_streamcoll_box(Dom d, T* __restrict__ fr, T* __restrict__ fb, TF<T> s, T omega, T tau,
                         ColorParamsDev cp) {
@@ -464,16 +480,22 @@ __global__ void __launch_bounds__(BX2)
   const T rb = s.rho_b[mi];
   const T red_frac = rr / r;
   const T rec_amp = T(cp.beta) * (rr * rb / r);
-  const T gx = s.grad[mi];
-  const T gy = s.grad[ms + mi];
-  const T gz = L::dim == 3 ? s.grad[2 * ms + mi] : T(0);
+  const Steps32 st = face_steps32(d, i, j, k);
+  T gx, gy, gz;
+  if constexpr (GRAD) {
+    gradient_at<L, T, WALLS>(s.phi + mi, st, gx, gy, gz);
+    if constexpr (L::dim == 2) gz = T(0);
+  } else {
+    gx = s.grad[mi];
+    gy = s.grad[ms + mi];
+    gz = L::dim == 3 ? s.grad[2 * ms + mi] : T(0);
+  }
   const T gn = sqrt(gx * gx + gy * gy + gz * gz);
   const bool interface = gn > T(cp.grad_threshold);
   const T pert_amp = interface ? pert_coef * gn : T(0);
   const T inv_gn = interface ? T(1) / gn : T(0);
   const T nhx = gx * inv_gn, nhy = gy * inv_gn, nhz = gz * inv_gn;
   const bool linear = cp.linear != 0;
-  const Steps32 st = face_steps32(d, i, j, k);
   T* __restrict__ frn = fr + fi;
   T* __restrict__ fbn = fb + fi;
 
@@ -635,9 +657,9 @@ int launch_cg_streamcoll(int lat, const Dom& d, T* fr, T* fb,
       bool walls = false;
       for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
       if (walls)
-        k_cg_streamcoll_box<decltype(L), T, true, true><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
+        k_cg_streamcoll_box<decltype(L), T, true, true, false><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
       else
-        k_cg_streamcoll_box<decltype(L), T, true, false><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
+        k_cg_streamcoll_box<decltype(L), T, true, false, false><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
       return;
     }
     if (fold_prepare)
@@ -646,6 +668,24 @@ int launch_cg_streamcoll(int lat, const Dom& d, T* fr, T* fb,
     else
       k_cg_streamcoll<decltype(L), T, false>
           <<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), solid, slow, om, tau, cp);
+  });
+}
+
+// The step's gradient + prepare_stress + stream_collide_recolor in one
+// kernel (box geometries, NCI off). Returns nonzero when not applicable.
+template <typename T>
+int launch_cg_streamcoll_grad(int lat, const Dom& d, T* fr, T* fb, const TwoFields& s, double omega,
+                              const ColorParamsDev& cp, cudaStream_t st) {
+  if (d.has_solid || cp.nci_strength != 0.0) return 1;
+  const T om = T(omega);
+  const T tau = T(1) / om;
+  bool walls = false;
+  for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
+  return with_lat2(lat, [&](auto L) {
+    if (walls)
+      k_cg_streamcoll_box<decltype(L), T, true, true, true><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
+    else
+      k_cg_streamcoll_box<decltype(L), T, true, false, true><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
   });
 }
 
@@ -674,6 +714,10 @@ int launch_init_colors(int lat, const Dom& d, T* fr, T* fb,
                                        const uint32_t*, double,               \
                                        const ColorParamsDev&, int,            \
                                        cudaStream_t);                         \
+  template int launch_cg_streamcoll_grad<T>(int, const Dom&, T*, T*,         \
+                                            const TwoFields&, double,         \
+                                            const ColorParamsDev&,            \
+                                            cudaStream_t);                    \
   template int launch_init_colors<T>(int, const Dom&, T*, T*,                 \
                                      const uint8_t*, const InitSpec&,         \
                                      cudaStream_t);
