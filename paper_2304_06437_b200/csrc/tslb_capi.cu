@@ -109,6 +109,12 @@ struct tslb_cuda_sim {
   // reference's lagged moment arrays) and f is materialised on demand.
   int sched = TSLB_SCHED_F1;
   bool fimplicit = false;
+  // lazy f under M: `f0_pending` = the current f is the analytic f(0) of
+  // `f0_spec` and the buffer does not hold it (yet); `m0_ready` = mo2 holds
+  // the moments of the current f (the first step's moments pass, done by the
+  // initialiser)
+  bool f0_pending = false, m0_ready = false;
+  InitSpec f0_spec{};
   int lz = 0;          // planes per CTA of the M kernel (0 = default; TSLB_LZ)
   void* mo2 = nullptr; // second moment buffer of the M schedule (ping-pong)
   void* gm = nullptr;  // M on z slabs: neighbours' boundary-plane moments [NM][2][plane]
@@ -244,7 +250,29 @@ int by_scalar(const tslb_cuda_sim* h, F&& f) {
 }
 
 // -- phases -------------------------------------------------------------------
+// the single-fluid population buffer, allocated on first use under M and
+// filled with the pending analytic f(0) if there is one
+int ensure_f(tslb_cuda_sim* h) {
+  if (!h->f[0]) {
+    const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
+    if (int rc = alloc(h, &h->f[0], fbytes)) return rc;
+    CK(cudaMemsetAsync(h->f[0], 0, fbytes, h->s));
+  }
+  if (h->f0_pending) {
+    h->f0_pending = false;
+    ++h->launches;
+    return by_scalar(h, [&](auto z) {
+      using T = decltype(z);
+      return launch_init_analytic<T>(h->lat, h->range(0, h->nzl), static_cast<T*>(h->f[0]), nullptr,
+                                     h->f0_spec, h->s);
+    });
+  }
+  return 0;
+}
+
 int ph_moments(tslb_cuda_sim* h, cudaStream_t st) {
+  if (h->comps == 1)
+    if (int rc = ensure_f(h)) return rc;
   Prof p(h, TSLB_K_MOMENTS, st);
   ++h->launches;
   return by_scalar(h, [&](auto z) {
@@ -257,6 +285,7 @@ int ph_moments(tslb_cuda_sim* h, cudaStream_t st) {
 
 int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
   if (k1 <= k0) return 0;
+  if (int rc = ensure_f(h)) return rc;
   Prof p(h, TSLB_K_STREAMCOLL, st);
   ++h->launches;
   return by_scalar(h, [&](auto z) {
@@ -335,6 +364,19 @@ int exchange_moments_local(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
       CK(cudaMemcpyAsync(ghost(h->down_peer, c, 1), arr(c, 0), bytes, cudaMemcpyDeviceToDevice, st));
   }
   return 0;
+}
+
+// the first step's moments pass: precomputed by the M initialiser, or from f
+int first_moments(tslb_cuda_sim* h, cudaStream_t st) {
+  if (h->m0_ready) {
+    std::swap(h->mo, h->mo2);
+    h->m0_ready = false;
+    // the current f is now f(1) = stream_collide(m(0)), which overwrites every
+    // slot of the buffer when it is materialised: f(0) is no longer owed
+    h->f0_pending = false;
+    return 0;
+  }
+  return ph_moments(h, st);
 }
 
 // store f(t+1) = stream_collide(m(t)) if the M schedule left it implicit;
@@ -509,7 +551,7 @@ int enqueue_step(tslb_cuda_sim* h) {
     if (!h->fimplicit) {
       // first step from stored populations: the moments pass (and, on
       // slabs, the ghost planes of m(t)); the stream-collide is deferred
-      if ((rc = ph_moments(h, h->s))) return rc;
+      if ((rc = first_moments(h, h->s))) return rc;
       if (h->xmode == 1 && (rc = exchange_moments_nccl(h, h->mo, h->s))) return rc;
       h->fimplicit = true;
     } else if (h->xmode == 1) {
@@ -698,11 +740,6 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   CK(cudaEventCreate(&h->t0));
   CK(cudaEventCreate(&h->t1));
 
-  const size_t fbytes = size_t(d.fstride) * h->q * h->esz;
-  for (int sp = 0; sp < components; ++sp) {
-    if ((rc = alloc(h, &h->f[sp], fbytes))) return fail(rc);
-    CK(cudaMemsetAsync(h->f[sp], 0, fbytes, h->s));
-  }
   const size_t mbytes = size_t(d.mstride) * (1 + h->dim + h->np) * h->esz;
   if ((rc = alloc(h, &h->mo, mbytes))) return fail(rc);
   CK(cudaMemsetAsync(h->mo, 0, mbytes, h->s));
@@ -767,6 +804,15 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
       }
     }
   }
+  // populations: always for two-fluid and F1; under M the single-fluid f is
+  // only allocated when something needs it (ensure_f)
+  if (components == 2 || h->sched != TSLB_SCHED_M) {
+    const size_t fbytes = size_t(d.fstride) * h->q * h->esz;
+    for (int sp = 0; sp < components; ++sp) {
+      if ((rc = alloc(h, &h->f[sp], fbytes))) return fail(rc);
+      CK(cudaMemsetAsync(h->f[sp], 0, fbytes, h->s));
+    }
+  }
   if ((rc = alloc(h, reinterpret_cast<void**>(&h->red),
                   (reduce_partial_count() + 16) * sizeof(double))))
     return fail(rc);
@@ -792,6 +838,7 @@ void drop_graph(tslb_cuda_sim* h) {
 int ensure_scratch(tslb_cuda_sim* h) {
   if (h->scratch) return 0;
   if (int rc = materialize(h)) return rc;
+  if (int rc = ensure_f(h)) return rc;
   const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
   if (int rc = alloc(h, &h->scratch, fbytes)) return rc;
   CK(cudaMemcpyAsync(h->scratch, h->f[0], fbytes, cudaMemcpyDeviceToDevice, h->s));
@@ -799,7 +846,15 @@ int ensure_scratch(tslb_cuda_sim* h) {
 }
 
 // base of population species 0/1 (f / fr, fb) or 2 (scratch buffer)
-int species_base(tslb_cuda_sim* h, int species, char** base) {
+int species_base(tslb_cuda_sim* h, int species, char** base, bool overwrite = false) {
+  if (species == 0 && h->comps == 1) {
+    if (overwrite) {
+      // every owned slot is about to be replaced: no pending f(0) to fill
+      h->f0_pending = false;
+      h->m0_ready = false;
+    }
+    if (int rc = ensure_f(h)) return rc;
+  }
   if (species == 2 && h->comps == 1 && !h->decomposed) {
     if (int rc = ensure_scratch(h)) return rc;
     *base = static_cast<char*>(h->scratch);
@@ -870,6 +925,7 @@ int tslb_cuda_set_math(tslb_cuda_handle h, int math) {
   CK(cudaSetDevice(h->device));
   // a pending f(t+1) belongs to the step that was taken with the old mode
   if (int rc = materialize(h)) return rc;
+  h->m0_ready = false;  // the initialiser's moments used the old arithmetic
   h->math = math;
   drop_graph(h);
   return 0;
@@ -894,8 +950,9 @@ int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
       if (int rc = alloc(h, &h->gm, gb)) return rc;
       CK(cudaMemsetAsync(h->gm, 0, gb, h->s));
     }
-  } else if (int rc = materialize(h)) {
-    return rc;
+  } else {
+    if (int rc = materialize(h)) return rc;
+    h->m0_ready = false;
   }
   h->sched = schedule;
   drop_graph(h);
@@ -932,8 +989,8 @@ int tslb_cuda_memory_bytes(tslb_cuda_handle h, uint64_t* bytes) {
 int tslb_cuda_upload_f(tslb_cuda_handle h, int species, const void* host) {
   CK(cudaSetDevice(h->device));
   char* base;
-  if (int rc = species_base(h, species, &base)) return rc;
   if (species == 0) h->fimplicit = false;  // every owned slot is overwritten
+  if (int rc = species_base(h, species, &base, true)) return rc;
   const size_t pb = size_t(h->n()) * h->esz;
   const size_t off = size_t(h->d.ghost * h->plane()) * h->esz;
   for (int a = 0; a < h->q; ++a)
@@ -1067,6 +1124,16 @@ int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
     }
     if (h->comps != 1) return set_err(TSLB_EINVAL, "analytic init %d needs one component", kind);
     h->fimplicit = false;
+    if (h->sched == TSLB_SCHED_M && !h->d.has_solid) {
+      // M: f(0) is not stored; the first step's moments pass is done here
+      h->f0_spec = s;
+      h->f0_pending = true;
+      h->m0_ready = true;
+      return launch_init_moments<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<T*>(h->mo2), s, h->s);
+    }
+    h->f0_pending = false;
+    h->m0_ready = false;
+    if (int rc = ensure_f(h)) return rc;
     return launch_init_analytic<T>(h->lat, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
                                    h->d.has_solid ? h->solid : nullptr, s, h->s);
   });
@@ -1173,6 +1240,7 @@ int tslb_cuda_stream_collide(tslb_cuda_handle h) {
   if (h->decomposed) return set_err(TSLB_ESTATE, "use step() on slab solvers");
   CK(cudaSetDevice(h->device));
   if (int rc = materialize(h)) return rc;
+  h->m0_ready = false;
   if (int rc = ph_streamcoll(h, 0, h->nzl, h->s)) return rc;
   return sync(h);
 }
@@ -1182,6 +1250,7 @@ int tslb_cuda_reference_step(tslb_cuda_handle h, long nsteps) {
     return set_err(TSLB_EINVAL, "reference_step: single-fluid, single domain only");
   CK(cudaSetDevice(h->device));
   if (int rc = materialize(h)) return rc;
+  h->m0_ready = false;
   if (int rc = ensure_scratch(h)) return rc;
   for (long s = 0; s < nsteps; ++s) {
     if (int rc = ph_moments(h, h->s)) return rc;
@@ -1207,6 +1276,7 @@ int tslb_cuda_stream_only(tslb_cuda_handle h) {
     return set_err(TSLB_EINVAL, "stream_only: single-fluid, single domain only");
   CK(cudaSetDevice(h->device));
   if (int rc = materialize(h)) return rc;
+  h->m0_ready = false;
   // pushes f into the second buffer (its slots not reached by any push keep
   // their contents, as in the reference), then swaps the two
   if (int rc = ensure_scratch(h)) return rc;
@@ -1332,6 +1402,8 @@ int tslb_cuda_color_masses(tslb_cuda_handle h, double* red, double* blue) {
 int tslb_cuda_plane_digests(tslb_cuda_handle h, uint64_t* out) {
   CK(cudaSetDevice(h->device));
   if (int rc = materialize(h)) return rc;
+  if (h->comps == 1)
+    if (int rc = ensure_f(h)) return rc;
   const int64_t plane_bytes = h->plane() * h->esz;
   const int64_t cpp = (plane_bytes + 16383) / 16384;
   const size_t need = size_t(h->q) * h->nzl * (cpp + 1) * sizeof(uint64_t);
@@ -1445,7 +1517,7 @@ int tslb_cuda_group_step(tslb_cuda_handle* slabs, int count, long nsteps) {
         tslb_cuda_sim* h = slabs[r];
         const int nzc = mstep_chunks(h->range(0, h->nzl), h->lz);
         int rc = 0;
-        if (first) rc = ph_moments(h, st);
+        if (first) rc = first_moments(h, st);
         else if (nzc <= 2) rc = ph_mstep(h, st);
         else if (!(rc = ph_mstep(h, st, 0, 1))) rc = ph_mstep(h, st, nzc - 1, 1);
         if (rc) return rc;

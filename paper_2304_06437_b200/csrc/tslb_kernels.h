@@ -70,6 +70,10 @@ int launch_classify(int lat, const Dom& d, const uint8_t* solid,
 template <typename T>
 int launch_init_analytic(int lat, const Dom& d, T* f, const uint8_t* solid,
                          const InitSpec& s, cudaStream_t st);
+// moments of the analytic f(0) without storing f(0) (M schedule)
+template <typename T>
+int launch_init_moments(int lat, int math, const Dom& d, T* mo, const InitSpec& s,
+                        cudaStream_t st);
 
 // ---- two fluid (tslb_two.cu)
 struct TwoFields {

@@ -314,14 +314,9 @@ __global__ void __launch_bounds__(BX)
 // device analytic initialisers (initialize_regularized pattern,
 // kernels.hpp:295-311, with the node state computed on the device)
 // ---------------------------------------------------------------------------
+// node state of the analytic initialisers (rest, shear, Taylor-Green)
 template <class L, typename T>
-__global__ void __launch_bounds__(BX)
-    k_init_analytic(Dom d, T* __restrict__ f, const uint8_t* __restrict__ solid,
-                    InitSpec s) {
-  int i, j, k;
-  if (!node_coords<BX>(d, i, j, k)) return;
-  const int64_t fi = fidx(d, i, j, k);
-  if (solid && solid[fi]) return;
+__device__ __forceinline__ NodeMoments<T> init_state(const InitSpec& s, int i, int j, int k) {
   const double two_pi = 6.283185307179586476925286766559;
   double rho = 1.0, ux = 0.0, uy = 0.0, uz = 0.0;
   const int kg = k + s.z0;
@@ -343,12 +338,82 @@ __global__ void __launch_bounds__(BX)
       rho = 1.0 + 3.0 * (U0 * U0 / 4.0) * (cos(2 * X) + cos(2 * Y));
     }
   }
-  const NodeMoments<T> m = prepare_node<T>(T(rho), T(ux), T(uy), T(uz), T(0),
-                                           T(0), T(0), T(0), T(0), T(0));
+  return prepare_node<T>(T(rho), T(ux), T(uy), T(uz), T(0), T(0), T(0), T(0), T(0), T(0));
+}
+
+// f(0) = f_eq + f_neq of the node state, in T (initialize_regularized,
+// kernels.hpp:295-311)
+template <class L, int A, typename T>
+__device__ __forceinline__ T init_population(const NodeMoments<T>& m) {
+  return equilibrium<L, A, T>(m) + regularized<L, A, T>(m);
+}
+
+template <class L, typename T>
+__global__ void __launch_bounds__(BX)
+    k_init_analytic(Dom d, T* __restrict__ f, const uint8_t* __restrict__ solid,
+                    InitSpec s) {
+  int i, j, k;
+  if (!node_coords<BX>(d, i, j, k)) return;
+  const int64_t fi = fidx(d, i, j, k);
+  if (solid && solid[fi]) return;
+  const NodeMoments<T> m = init_state<L, T>(s, i, j, k);
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
-    f[a * d.fstride + fi] = equilibrium<L, a, T>(m) + regularized<L, a, T>(m);
+    f[a * d.fstride + fi] = init_population<L, a, T>(m);
   });
+}
+
+// The moments pass of the first step applied to the analytic f(0), without
+// storing f(0) (M schedule, box geometries): the populations are formed in
+// registers exactly as k_init_analytic stores them and reduced exactly as
+// k_moments does (compute_moments, kernels.hpp:74-107).
+template <class L, typename T, typename C>
+__global__ void __launch_bounds__(BX)
+    k_init_moments(Dom d, T* __restrict__ mo, InitSpec s) {
+  int i, j, k;
+  if (!node_coords<BX>(d, i, j, k)) return;
+  const int64_t mi = midx(d, i, j, k);
+  const NodeMoments<T> m = init_state<L, T>(s, i, j, k);
+  C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pzz = 0, pxy = 0, pxz = 0, pyz = 0;
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    using dd = Dir<L, a>;
+    const C fa = C(init_population<L, a, T>(m));
+    r += fa;
+    if constexpr (dd::x == 1) jx += fa;
+    if constexpr (dd::x == -1) jx -= fa;
+    if constexpr (dd::y == 1) jy += fa;
+    if constexpr (dd::y == -1) jy -= fa;
+    if constexpr (dd::z == 1) jz += fa;
+    if constexpr (dd::z == -1) jz -= fa;
+    if constexpr (dd::x != 0) pxx += fa;
+    if constexpr (dd::y != 0) pyy += fa;
+    if constexpr (dd::z != 0) pzz += fa;
+    if constexpr (dd::x * dd::y == 1) pxy += fa;
+    if constexpr (dd::x * dd::y == -1) pxy -= fa;
+    if constexpr (dd::x * dd::z == 1) pxz += fa;
+    if constexpr (dd::x * dd::z == -1) pxz -= fa;
+    if constexpr (dd::y * dd::z == 1) pyz += fa;
+    if constexpr (dd::y * dd::z == -1) pyz -= fa;
+  });
+  const C c3 = cs2<C>();
+  const int64_t ms = d.mstride;
+  mo[mi] = T(r);
+  mo[ms + mi] = T(jx);
+  mo[2 * ms + mi] = T(jy);
+  if constexpr (L::dim == 3) {
+    mo[3 * ms + mi] = T(jz);
+    mo[4 * ms + mi] = T(pxx - c3 * r - jx * jx);
+    mo[5 * ms + mi] = T(pyy - c3 * r - jy * jy);
+    mo[6 * ms + mi] = T(pzz - c3 * r - jz * jz);
+    mo[7 * ms + mi] = T(pxy - jx * jy);
+    mo[8 * ms + mi] = T(pxz - jx * jz);
+    mo[9 * ms + mi] = T(pyz - jy * jz);
+  } else {
+    mo[3 * ms + mi] = T(pxx - c3 * r - jx * jx);
+    mo[4 * ms + mi] = T(pyy - c3 * r - jy * jy);
+    mo[5 * ms + mi] = T(pxy - jx * jy);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -462,7 +527,20 @@ int launch_init_analytic(int lat, const Dom& d, T* f, const uint8_t* solid,
   });
 }
 
+template <typename T>
+int launch_init_moments(int lat, int math, const Dom& d, T* mo, const InitSpec& s, cudaStream_t st) {
+  return with_lat(lat, [&](auto L) {
+    using Lat = decltype(L);
+    if (math == kMathDouble)
+      k_init_moments<Lat, T, double><<<grid_of(d), BX, 0, st>>>(d, mo, s);
+    else
+      k_init_moments<Lat, T, float><<<grid_of(d), BX, 0, st>>>(d, mo, s);
+  });
+}
+
 #define TSLB_INST(T)                                                          \
+  template int launch_init_moments<T>(int, int, const Dom&, T*, const InitSpec&, \
+                                      cudaStream_t);                          \
   template int launch_moments<T>(int, int, const Dom&, const T*, T*,          \
                                  const uint8_t*, cudaStream_t);               \
   template int launch_streamcoll<T>(int, int, const Dom&, T*, const T*,       \

@@ -221,3 +221,48 @@ def test_schedule_rules(gpu):
         assert dev.schedule == "f1"
     finally:
         dev.close()
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("init", ["taylor_green", "shear", "rest"])
+def test_mstep_device_init_without_f(gpu, init, dtype):
+    """Under M the analytic initialiser stores m(0) instead of f(0) (the f
+    buffer is allocated only when read): every observable equals the F1
+    solver's, bit for bit -- f(0) on download before any step, the lagged
+    moments, f(N) and m(N-1) after steps."""
+    lat, dims, faces = "d3q19", (32, 16, 8), zwalls_3d()
+    out = {}
+    for sched in ("m", "f1"):
+        dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.1, spec_of(faces), dtype)
+        try:
+            if sched == "f1":
+                dev.set_schedule("f1")
+            dev.init_analytic(init, 0.04)
+            if sched == "m":  # two moment sets (20 arrays), no population buffer (19)
+                assert dev.memory_bytes() < 30 * dims[0] * dims[1] * dims[2] * np.dtype(dtype).itemsize
+            out[sched] = [dev.download_f(), _moments(dev, lat)]
+            dev.step(4)
+            out[sched] += [_moments(dev, lat), dev.download_f()]
+            dev.init_analytic(init, 0.02)   # re-init after stepping
+            dev.step(3)
+            out[sched] += [dev.download_f()]
+        finally:
+            dev.close()
+    for a, b, what in zip(out["m"], out["f1"], ["f(0)", "moments after init", "m(3)", "f(4)", "f(3) after re-init"]):
+        assert_bitwise(a, b, f"M vs F1 {init}: {what}")
+
+
+def test_mstep_lazy_f_memory(gpu):
+    """A device-initialised M solver holds moments only until f is read."""
+    dims = (64, 32, 16)
+    dev = T.DeviceSolver("d3q19", T.GridDims(*dims), 1.2, spec_of(O.periodic()), np.float32)
+    try:
+        dev.init_analytic("taylor_green", 0.03)
+        dev.step(5)
+        before = dev.memory_bytes()
+        f = dev.download_f()
+        after = dev.memory_bytes()
+        assert after - before >= 19 * dims[0] * dims[1] * dims[2] * 4
+        assert np.isfinite(f).all()
+    finally:
+        dev.close()
