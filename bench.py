@@ -325,17 +325,18 @@ def main():
     sched = sim.schedule if W["comps"] == 1 else "f1"
     sb = step_bytes(lat, W["comps"], es, sched) if W["comps"] == 1 else sum(per_node.values())
     step_bw = glups * sb / world  # per-GPU GB/s of the whole step
-    traffic, tsrc = None, None
+    traffic, tsrc, limiter = None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh).get(f"{lat.name}/{W['storage']}/{dom}")
         if tr:
             traffic, tsrc = round(tr["bytes_per_node"] * local_nodes / 1e9, 3), tr["source"]
+            limiter = tr.get("limiter")
     except (OSError, ValueError):
         pass
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
             "frac": round(achieved / hbm, 4), "traffic": traffic, "traffic_unit": "GB per launch",
-            "traffic_source": tsrc, "kernel": f"k_{dom}",
+            "traffic_source": tsrc, "limiter": limiter, "kernel": f"k_{dom}",
             "kernel_bytes_per_node": per_node[dom], "peak_kind": peak_kind,
             "per_kernel_ms": {k: round(v[0] / v[1], 4) for k, v in prof.items()},
             "step_bytes_per_lu": sb, "step_frac": round(step_bw / hbm, 4),
