@@ -44,10 +44,10 @@ WORKLOADS = {
     "tgv-d3q19": dict(lat="d3q19", dims=(1024, 1024, 1024), faces="periodic", comps=1, init="taylor_green",
                       amp=0.03, omega=1.6, storage="f32",
                       desc="D3Q19 periodic Taylor-Green {n}"),
-    "channel-d3q27": dict(lat="d3q27", dims=(1024, 1024, 1024), faces="couette", comps=1, init="rest", amp=0.0,
-                          omega=1.0, storage="f32",
-                          desc="D3Q27 channel {n}: walls at y, y-max moving (0.05,0,0) (Couette; the reference "
-                               "has no body force), rest init"),
+    "channel-d3q27": dict(lat="d3q27", dims=(1024, 1024, 1024), faces="channel", comps=1, init="rest", amp=0.0,
+                          omega=1.0, storage="f32", umax=0.05,
+                          desc="D3Q27 Poiseuille channel {n}: no-slip walls at y, body force along x for "
+                               "u_max 0.05 (single-fluid forcing extension), rest init"),
     "droplet-d3q19": dict(lat="d3q19", dims=(512, 512, 512), faces="periodic", comps=2, init="droplet",
                           radius=512 / 6.0, omega=1 / 0.75, storage="f32", sigma=0.03, beta=0.7,
                           desc="D3Q19 two-component colour-gradient droplet {n}, R = 85.33, sigma 0.03, beta 0.7"),
@@ -170,9 +170,9 @@ def spec_of(T, kind):
         return T.BoundarySpec.all_periodic()
     if kind == "lid":
         return T.BoundarySpec.lid_cavity(0.025)
-    s = T.BoundarySpec.all_periodic()  # couette
+    s = T.BoundarySpec.all_periodic()  # channel: no-slip walls at y
     s.faces[T.YMin] = T.Face(T.FaceKind.NoSlipWall)
-    s.faces[T.YMax] = T.Face(T.FaceKind.MovingWall, (0.05, 0.0, 0.0))
+    s.faces[T.YMax] = T.Face(T.FaceKind.NoSlipWall)
     return s
 
 
@@ -266,6 +266,10 @@ def main():
         sim.set_math(_lib.MATH_F32)
     if args.schedule != "auto" and W["comps"] == 1:
         sim.set_schedule(args.schedule)
+    if "umax" in W:
+        # Poiseuille: u_max = F H^2 / (8 nu), H = ny (halfway bounce-back)
+        nu = (1.0 / W["omega"] - 0.5) / 3.0
+        sim.set_body_force(8.0 * nu * W["umax"] / float(ny) ** 2, 0.0, 0.0)
     if world > 1:
         import ctypes as C
         uid = (C.c_char * 128)()

@@ -678,6 +678,10 @@ template <typename T>
 struct CollisionParams {
   T omega = T(1);
   T rho0 = T(1);
+  // EXTENSION (not in the reference): single-fluid body force, applied as the
+  // velocity shift u_eq = j + tau F of the moments pass (tslb_cuda.h,
+  // tslb_cuda_set_body_force). Zero leaves every result unchanged.
+  std::array<T, 3> force{};
   T tau() const { return T(1) / omega; }
   T nu() const { return cs2_v<T> * (tau() - T(0.5)); }
 };
@@ -1152,6 +1156,10 @@ class SimCore {
           const int* color_i)
       : dims_(g), prm_(prm), spec_(spec), pool_(pool) {
     dev_ = detail::Device::make<Lat, T>(g, double(prm.omega), spec, solid, components, color, color_i);
+    if (components == 1 && (prm.force[0] != T(0) || prm.force[1] != T(0) || prm.force[2] != T(0))) {
+      const double f3[3] = {double(prm.force[0]), double(prm.force[1]), double(prm.force[2])};
+      detail::check(tslb_cuda_set_body_force(dev_.get(), f3));
+    }
     geo_ = detail::geometry_of(dev_.get(), g);
   }
 

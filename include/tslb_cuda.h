@@ -131,6 +131,13 @@ int tslb_cuda_set_math(tslb_cuda_handle h, int math);
  * results either way (fused_step, kernels.hpp:209-215). */
 int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule);
 int tslb_cuda_get_schedule(tslb_cuda_handle h, int* schedule);
+/* Single-fluid body force F (EXTENSION: the reference has no single-fluid
+ * forcing; used for the Poiseuille channel of BASELINE config 3). Velocity
+ * shift of the reference's two-fluid prepare_stress (multicomponent.hpp:
+ * 286-304) applied in compute_moments: the stored velocity is
+ * u_eq = j + tau F, Pi^neq = (sum f cc - cs2 rho) - u_eq u_eq. F = 0 (the
+ * default) leaves every result bit-identical to the reference. */
+int tslb_cuda_set_body_force(tslb_cuda_handle h, const double* force3);
 /* dims[0..4] = nx, ny, nz_local, z0, nz_global; info[0..3] = q, dim, np, scalar bytes */
 int tslb_cuda_describe(tslb_cuda_handle h, int* dims, int* info);
 int tslb_cuda_memory_bytes(tslb_cuda_handle h, uint64_t* bytes);

@@ -123,6 +123,12 @@ class Oracle:
         self._check(self._fn("classify")(LATTICES[lat], nx, ny, nz, _ptr(kinds), _ptr(uw), _ptr(sol), _ptr(so), _ptr(sl), C.byref(nf)))
         return so, sl, int(nf.value)
 
+    def set_body_force(self, fx=0.0, fy=0.0, fz=0.0):
+        """Body-force extension of the port (not in the reference)."""
+        if self.kind != "port":
+            raise ValueError("the reference has no single-fluid body force")
+        self.lib.tslbo_set_body_force(C.c_double(fx), C.c_double(fy), C.c_double(fz))
+
     # -- single fluid -----------------------------------------------------
     def single_run(self, lat, dims, omega, faces, f, moments=None, steps=1, mode=0, solid=None, workers=1):
         """Advance f (q, n) in place; returns (f, moments)."""

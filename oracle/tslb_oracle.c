@@ -18,6 +18,15 @@ static _Thread_local char g_err[256];
 
 const char* tslbo_last_error(void) { return g_err; }
 
+/* Body force of the single-fluid forcing extension (not in the reference;
+ * see tslb_oracle.h). Process-wide, test infrastructure. */
+static double g_force[3] = {0.0, 0.0, 0.0};
+void tslbo_set_body_force(double fx, double fy, double fz) {
+  g_force[0] = fx;
+  g_force[1] = fy;
+  g_force[2] = fz;
+}
+
 static int fail(const char* msg) {
   snprintf(g_err, sizeof g_err, "%s", msg);
   return 1;

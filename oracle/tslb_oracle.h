@@ -72,6 +72,14 @@ int tslbo_stability(int scalar, int dim, uint64_t n, const uint8_t* solid,
                     const void* rho, const void* mom, int* finite,
                     double* max_speed, double* min_rho, double* max_rho);
 
+/* Single-fluid body force F (EXTENSION: the reference has no single-fluid
+ * forcing; parity for F != 0 is unpinned). Velocity-shift convention of the
+ * reference's two-fluid prepare_stress (multicomponent.hpp:286-304), in the
+ * single-fluid arithmetic: compute_moments stores u_eq = j + tau F and
+ * Pi^neq = (sum f cc - cs2 rho) - u_eq u_eq, tau = 1 / double(T(omega)),
+ * F rounded to T. F = 0 leaves every result unchanged. */
+void tslbo_set_body_force(double fx, double fy, double fz);
+
 uint64_t tslbo_fnv1a(const void* data, size_t n, uint64_t h);
 
 /* count_kernel_cost (bench.hpp:30-66) generalised to D3Q27 */

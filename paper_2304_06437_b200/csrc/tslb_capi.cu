@@ -959,6 +959,27 @@ int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
   return sync(h);
 }
 
+int tslb_cuda_set_body_force(tslb_cuda_handle h, const double* force) {
+  if (!force) return set_err(TSLB_EINVAL, "null force");
+  if (h->comps != 1) return set_err(TSLB_EINVAL, "the body force is a single-fluid extension");
+  CK(cudaSetDevice(h->device));
+  // a pending f(t+1) = stream_collide(m(t)) does not depend on F; the
+  // initialiser's precomputed moments do
+  h->m0_ready = false;
+  Dom& d = h->d;
+  d.forced = force[0] != 0.0 || force[1] != 0.0 || force[2] != 0.0;
+  // tau = 1 / omega with omega stored as T; F rounded to T (the
+  // CollisionParams<T> convention); products in double as on the host
+  const double omega_t = h->scalar == TSLB_F32 ? double(float(h->omega)) : h->omega;
+  const double tau = 1.0 / omega_t;
+  for (int c = 0; c < 3; ++c) {
+    const double fc = h->scalar == TSLB_F32 ? double(float(force[c])) : force[c];
+    d.tf[c] = (c < h->dim) ? tau * fc : 0.0;
+  }
+  drop_graph(h);
+  return 0;
+}
+
 int tslb_cuda_get_schedule(tslb_cuda_handle h, int* schedule) {
   *schedule = h->sched;
   return 0;

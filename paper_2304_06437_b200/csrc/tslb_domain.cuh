@@ -32,7 +32,22 @@ struct Dom {
   int has_solid;         // solid mask / slow mask present
   int xblocks;           // blocks per x row in the row-tiled launch
   int k0, nzr;           // launch range: planes [k0, k0 + nzr)
+  // single-fluid body force (extension, tslb_cuda_set_body_force): the
+  // moments pass stores u_eq = j + tf (tf = tau F) when `forced`
+  int forced;
+  double tf[3];
 };
+
+/// the forcing shift of the moments pass (identity when not forced, so the
+/// unforced results keep every bit, including signed zeros)
+template <typename C>
+__device__ __forceinline__ void force_shift(const Dom& d, C& jx, C& jy, C& jz) {
+  if (d.forced) {
+    jx = jx + C(d.tf[0]);
+    jy = jy + C(d.tf[1]);
+    jz = jz + C(d.tf[2]);
+  }
+}
 
 /// Row-tiled launch grid: blocks (x block, row j, plane k) as a 3-D grid
 /// when ny and the plane range fit the grid limits (no index divisions in

@@ -424,6 +424,8 @@ __device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, con
     if constexpr (dd::y * dd::z == 1) pyz += fa;
     if constexpr (dd::y * dd::z == -1) pyz -= fa;
   });
+  if constexpr (L::dim == 3) force_shift<C>(d, jx, jy, jz);
+  else { C z0 = 0; force_shift<C>(d, jx, jy, z0); }
   const C c3 = cs2<C>();
   const int64_t ms = d.mstride;
   mo[idx] = T(r);

@@ -63,6 +63,8 @@ __global__ void __launch_bounds__(BX) k_moments(Dom d, const T* __restrict__ f,
     if constexpr (dd::y * dd::z == 1) pyz += fa;
     if constexpr (dd::y * dd::z == -1) pyz -= fa;
   });
+  if constexpr (L::dim == 3) force_shift<C>(d, jx, jy, jz);
+  else { C z0 = 0; force_shift<C>(d, jx, jy, z0); }
   const C c3 = cs2<C>();
   const int64_t ms = d.mstride;
   mo[mi] = T(r);
@@ -396,6 +398,8 @@ __global__ void __launch_bounds__(BX)
     if constexpr (dd::y * dd::z == 1) pyz += fa;
     if constexpr (dd::y * dd::z == -1) pyz -= fa;
   });
+  if constexpr (L::dim == 3) force_shift<C>(d, jx, jy, jz);
+  else { C z0 = 0; force_shift<C>(d, jx, jy, z0); }
   const C c3 = cs2<C>();
   const int64_t ms = d.mstride;
   mo[mi] = T(r);

@@ -175,6 +175,8 @@ class BoundarySpec:
 class CollisionParams:
     omega: float = 1.0
     rho0: float = 1.0
+    # single-fluid body force: an extension (the reference has none)
+    force: tuple = (0.0, 0.0, 0.0)
 
     def tau(self) -> float:
         return 1.0 / self.omega
@@ -424,6 +426,11 @@ class DeviceSolver:
         single pass); same results bit for bit."""
         self._call("tslb_cuda_set_schedule", {"f1": _lib.SCHED_F1, "m": _lib.SCHED_M}[schedule])
 
+    def set_body_force(self, fx=0.0, fy=0.0, fz=0.0):
+        """Single-fluid body force (extension)."""
+        f = np.array([fx, fy, fz], np.float64)
+        self._call("tslb_cuda_set_body_force", _ptr(f))
+
     @property
     def schedule(self) -> str:
         v = C.c_int()
@@ -586,6 +593,8 @@ class _SimBase:
         self._cp = cp
         self.dtype = np.dtype(dtype)
         self.dev = DeviceSolver(self.lattice, g, prm.omega, spec, dtype, components, solid, cp, device)
+        if components == 1 and any(float(v) != 0.0 for v in getattr(prm, "force", (0.0, 0.0, 0.0))):
+            self.dev.set_body_force(*prm.force)
         self._geo = None
         self._steps = 0
         self._host_dirty = False

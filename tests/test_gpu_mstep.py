@@ -266,3 +266,69 @@ def test_mstep_lazy_f_memory(gpu):
         assert np.isfinite(f).all()
     finally:
         dev.close()
+
+
+# --- body-force extension (not in the reference; parity with the C port) ---
+def _ywalls():
+    f = O.periodic()
+    f[2] = ("wall", (0, 0, 0))
+    f[3] = ("moving", (0.01, 0.0, 0.0))
+    return f
+
+
+@pytest.mark.parametrize("sched", ["m", "f1"])
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("lat,dims,faces", [("d3q19", (32, 16, 6), _ywalls()), ("d3q27", (32, 8, 5), O.periodic()),
+                                            ("d2q9", (24, 20, 1), _ywalls())], ids=["d3q19", "d3q27", "d2q9"])
+def test_body_force_bitwise(gpu, oracle_port, lat, dims, faces, dtype, sched):
+    if lat == "d2q9" and sched == "m":
+        pytest.skip("the M schedule is 3-D")
+    F = (3e-5, -1e-5, 2e-5 if dims[2] > 1 else 0.0)
+    f0 = O.random_state(lat, dims, 31, dtype)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.05, spec_of(faces), dtype)
+    try:
+        if sched == "f1":
+            dev.set_schedule("f1")
+        dev.set_body_force(*F)
+        dev.upload_f(f0)
+        dev.step(6)
+        mg = _moments(dev, lat)
+        fg = dev.download_f()
+    finally:
+        dev.close()
+    try:
+        oracle_port.set_body_force(*F)
+        fo, mo = _oracle(oracle_port, lat, dims, 1.05, faces, f0, 6)
+    finally:
+        oracle_port.set_body_force(0.0, 0.0, 0.0)
+    assert_bitwise(mg, mo, f"forced {lat} {sched} moments")
+    assert_bitwise(fg, fo, f"forced {lat} {sched} f")
+
+
+@pytest.mark.parametrize("lat", ["d3q19", "d3q27"])
+def test_poiseuille_profile(gpu, lat):
+    """Body-force driven channel between no-slip walls (BASELINE config 3's
+    flow): the steady profile is the analytic parabola u = F y'(H - y')/(2 nu)
+    with the walls half a node outside the fluid (halfway bounce-back)."""
+    H = 24
+    dims = (32, H, 8)
+    nu, om = 1.0 / 6.0, 1.0
+    F = 8 * nu * 0.02 / H ** 2
+    faces = O.periodic()
+    faces[2] = ("wall", (0, 0, 0))
+    faces[3] = ("wall", (0, 0, 0))
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), om, spec_of(faces), np.float64)
+    try:
+        assert dev.schedule == "m"
+        dev.set_body_force(F, 0.0, 0.0)
+        dev.init_analytic("rest")
+        dev.step(12000)
+        dev.phase("refresh_moments")
+        u = dev.download_field("mom").reshape(3, dims[2], dims[1], dims[0])[0]
+    finally:
+        dev.close()
+    tau = 1.0 / om
+    prof = (u - tau * F + F / 2).mean(axis=(0, 2))   # stored u_eq = j + tau F; fluid velocity j + F/2
+    y = np.arange(H) + 0.5
+    ua = F / (2 * nu) * y * (H - y)
+    assert np.abs(prof - ua).max() <= 5e-3 * ua.max()
