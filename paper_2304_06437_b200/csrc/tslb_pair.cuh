@@ -119,32 +119,6 @@ __device__ __forceinline__ C post_single(const NodeMoments<C>& m, C om1) {
   return e + om1 * regularized_noseed<L, A, C>(m);
 }
 
-template <class L, typename T, typename C, int VX, bool EXACT>
-__device__ __forceinline__ void row_outputs(const NodeMoments<C> (&m)[VX], C om1, T (&o)[L::q][VX]) {
-  unroll<L::q>([&](auto A) {
-    constexpr int a = decltype(A)::value;
-#pragma unroll
-    for (int x = 0; x < VX; ++x) {
-      if constexpr (EXACT) {
-        o[a][x] = T(post_collision<L, a, C>(m[x], om1));
-      } else if constexpr (a == 0) {
-        o[0][x] = T(post_rest<L, C>(m[x], om1));
-      } else if constexpr (a & 1) {
-        using dd = Dir<L, a>;
-        constexpr C t = dd::template t<C>();
-        const C cu = dot_noseed<dd::x, dd::y, dd::z, C>(m[x].ux, m[x].uy, m[x].uz);
-        const C c3 = C(3) * cu;
-        const C qq = C(4.5) * cu * cu;
-        const C ea = t * (m[x].rho + c3 + qq - m[x].usq15);
-        const C eb = t * (m[x].rho - c3 + qq - m[x].usq15);
-        const C r = om1 * regularized_noseed<L, a, C>(m[x]);
-        o[a][x] = T(ea + r);
-        o[a + 1][x] = T(eb + r);
-      }
-    }
-  });
-}
-
 // Bounce of direction A at node fi: f[opp][fi] = T(C(out) - 6 t (c.u_wall))
 // with u_wall summed in T over the crossed wall faces in axis order.
 template <class L, int A, typename T, typename C>
