@@ -203,6 +203,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="tgv-d3q19", choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=0, help="override the per-GPU cube edge (3D)")
+    ap.add_argument("--dims", default="", help="override the per-GPU extent nx,ny,nz (3D)")
     ap.add_argument("--math", default="f64", choices=["f64", "f32"])
     ap.add_argument("--schedule", default="auto", choices=["auto", "m", "f1"])
     ap.add_argument("--no-e2e", action="store_true")
@@ -217,6 +218,8 @@ def main():
     dims = W["dims"]
     if args.n and dims[2] > 1:
         dims = (args.n, args.n, args.n)
+    if args.dims and dims[2] > 1:
+        dims = tuple(int(v) for v in args.dims.split(","))
     default = args.workload == "tgv-d3q19"
     metric = METRIC if default else f"GLUPS ({args.workload})"
 

@@ -332,3 +332,32 @@ def test_poiseuille_profile(gpu, lat):
     y = np.arange(H) + 0.5
     ua = F / (2 * nu) * y * (H - y)
     assert np.abs(prof - ua).max() <= 5e-3 * ua.max()
+
+
+# --- full-size, size-independent checks (BASELINE.json shapes) ------------
+@pytest.mark.parametrize("lat,n", [("d3q19", 1024), ("d3q27", 512)])
+def test_full_size_m_equals_f1_digests(gpu, lat, n):
+    """At the benchmark sizes the oracle is too slow, so the two device
+    schedules check each other: M and F1 from the same device-initialised
+    Taylor-Green state agree on the FNV digest of every population plane
+    after 6 steps (a checksum of checksums; each schedule is bit-exact
+    against the oracle at small sizes), and mass is conserved."""
+    dims = (n, n, n)
+    dig, mass = {}, {}
+    for sched in ("m", "f1"):
+        dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.6, T.BoundarySpec.all_periodic(), np.float32)
+        try:
+            if sched == "f1":
+                dev.set_schedule("f1")
+            dev.init_analytic("taylor_green", 0.03)
+            dev.step(1)
+            m0, _ = dev.totals()
+            dev.step(5)
+            m1, _ = dev.totals()
+            dig[sched] = dev.plane_digests()
+            mass[sched] = (m0, m1)
+        finally:
+            dev.close()
+    assert np.array_equal(dig["m"], dig["f1"])
+    for m0, m1 in mass.values():
+        assert abs(m1 - m0) <= 1e-6 * m0
