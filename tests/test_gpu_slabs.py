@@ -108,3 +108,36 @@ def test_mstep_slabs_equal_oracle(gpu, oracle_port, name, faces, lat, parts, dty
     oracle_port.single_run(lat, dims, 1.25, faces, ref, rmo, 5, 0)
     assert_bitwise(mo, rmo, f"M slabs x{parts} moments")
     assert_bitwise(f, ref, f"M slabs x{parts} f")
+
+
+# --- the NCCL transport itself, on one device: a single-rank communicator ---
+@pytest.mark.parametrize("sched", ["m", "f1"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_nccl_self_exchange_equals_periodic_box(gpu, sched, dtype, monkeypatch):
+    """One slab [0, nzl) of a 2*nzl box attached to a ONE-rank NCCL
+    communicator: its up and down neighbour is itself, so every step ships
+    its boundary planes (moment planes under M, pushed populations under F1)
+    through ncclSend/ncclRecv to itself -- exactly a periodic box of height
+    nzl. This exercises the multi-GPU step (boundary chunks, exchange on the
+    comm stream, interior chunks, join) on real NCCL with one GPU."""
+    monkeypatch.setenv("TSLB_LZ", "2")  # several z chunks: boundary / interior split
+    lat, nx, ny, nzl = "d3q19", 32, 16, 8
+    f0 = O.random_state(lat, (nx, ny, nzl), 5, dtype)
+    spec = spec_of(O.periodic())
+    ref = T.DeviceSolver(lat, T.GridDims(nx, ny, nzl), 1.2, spec, dtype)
+    slab = T.DeviceSolver(lat, T.GridDims(nx, ny, 2 * nzl), 1.2, spec, dtype, 1, None, slab=(0, nzl))
+    try:
+        for d in (ref, slab):
+            d.set_schedule(sched)
+        uid = (C.c_char * 128)()
+        _lib.call("tslb_cuda_nccl_unique_id", uid)
+        _lib.call("tslb_cuda_attach_nccl", slab.h, uid, 1, 0)
+        for d in (ref, slab):
+            d.upload_f(f0)
+            d.step(7)
+        assert_bitwise(slab.download_f(), ref.download_f(), f"NCCL self-exchange ({sched}) f")
+        for fld in ("rho", "mom", "pineq"):
+            assert_bitwise(slab.download_field(fld), ref.download_field(fld), f"NCCL self-exchange ({sched}) {fld}")
+    finally:
+        slab.close()
+        ref.close()
