@@ -256,8 +256,8 @@ def main():
     lat = T.lattice_of(W["lat"])
     dtype = np.float32 if W["storage"] == "f32" else np.float64
     es = np.dtype(dtype).itemsize
-    if world > 1 and (lat.dim != 3 or W["comps"] != 1):
-        raise SystemExit("multi-GPU slabs: 3-D single-fluid workloads only")
+    if world > 1 and lat.dim != 3:
+        raise SystemExit("multi-GPU slabs: 3-D workloads only")
     nx, ny, nzp = dims
     nz_g = nzp * world
     g = T.GridDims(nx, ny, nz_g)

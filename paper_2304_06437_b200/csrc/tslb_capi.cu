@@ -166,8 +166,9 @@ struct tslb_cuda_sim {
   int rank = 0, nranks = 1, up = -1, down = -1;
   tslb_cuda_sim* up_peer = nullptr;
   tslb_cuda_sim* down_peer = nullptr;
-  void* recv_lo = nullptr;  // staging (masked geometries)
+  void* recv_lo = nullptr;  // staging (masked geometries), per species
   void* recv_hi = nullptr;
+  void* phig = nullptr;     // two-fluid slabs: phi with a ghost plane below and above
   int zp[9], zm[9], nzp = 0, nzm = 0;  // directions with c_z = +1 / -1
   int zpx[9], zpy[9], zmx[9], zmy[9];
 
@@ -189,7 +190,7 @@ struct tslb_cuda_sim {
     t.pin = m_arr(1 + dim);
     t.rho_r = t_arr(0);
     t.rho_b = t_arr(1);
-    t.phi = t_arr(2);
+    t.phi = phig ? static_cast<char*>(phig) + size_t(plane()) * esz : t_arr(2);
     t.grad = t_arr(3);
     t.flag = flag;
     return t;
@@ -452,33 +453,36 @@ int ph_cg_streamcoll(tslb_cuda_sim* h, int fold, cudaStream_t st) {
 
 // -- slab exchange ------------------------------------------------------------
 // plane k (-1 .. nzl) of population array a, species 0
-void* plane_ptr(const tslb_cuda_sim* h, int a, int k) {
-  return static_cast<char*>(h->fa(0, a)) +
+void* plane_ptr(const tslb_cuda_sim* h, int a, int k, int sp = 0) {
+  return static_cast<char*>(h->fa(sp, a)) +
          size_t((int64_t(k) + h->d.ghost) * h->plane()) * h->esz;
 }
 
 // destination for a received plane: in place, or the staging buffer
-void* recv_ptr(const tslb_cuda_sim* h, bool from_below, int e, int a) {
+void* recv_ptr(const tslb_cuda_sim* h, bool from_below, int e, int a, int sp = 0) {
   if (h->staged) {
     void* base = from_below ? h->recv_lo : h->recv_hi;
-    return static_cast<char*>(base) + size_t(e) * h->plane() * h->esz;
+    return static_cast<char*>(base) + size_t(9 * sp + e) * h->plane() * h->esz;
   }
-  return plane_ptr(h, a, from_below ? 0 : h->nzl - 1);
+  return plane_ptr(h, a, from_below ? 0 : h->nzl - 1, sp);
 }
 
 int unpack(tslb_cuda_sim* h, cudaStream_t st) {
   if (!h->staged) return 0;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
-    if (h->d.mode[ZMin] == kGhost) {
-      ++h->launches;
-      launch_unpack<T>(h->d, static_cast<T*>(h->f[0]), static_cast<const T*>(h->recv_lo),
-                       h->solid, h->nzp, h->zp, h->zpx, h->zpy, 0, -1, st);
-    }
-    if (h->d.mode[ZMax] == kGhost) {
-      ++h->launches;
-      launch_unpack<T>(h->d, static_cast<T*>(h->f[0]), static_cast<const T*>(h->recv_hi),
-                       h->solid, h->nzm, h->zm, h->zmx, h->zmy, h->nzl - 1, h->nzl, st);
+    const size_t sp_off = size_t(9) * h->plane();
+    for (int sp = 0; sp < h->comps; ++sp) {
+      if (h->d.mode[ZMin] == kGhost) {
+        ++h->launches;
+        launch_unpack<T>(h->d, static_cast<T*>(h->f[sp]), static_cast<const T*>(h->recv_lo) + sp * sp_off,
+                         h->solid, h->nzp, h->zp, h->zpx, h->zpy, 0, -1, st);
+      }
+      if (h->d.mode[ZMax] == kGhost) {
+        ++h->launches;
+        launch_unpack<T>(h->d, static_cast<T*>(h->f[sp]), static_cast<const T*>(h->recv_hi) + sp * sp_off,
+                         h->solid, h->nzm, h->zm, h->zmx, h->zmy, h->nzl - 1, h->nzl, st);
+      }
     }
     return 0;
   });
@@ -490,14 +494,18 @@ int exchange_nccl(tslb_cuda_sim* h, cudaStream_t st) {
   const size_t cnt = size_t(h->plane());
   Prof p(h, TSLB_K_EXCHANGE, st);
   N.GroupStart();
-  if (h->up >= 0)
-    for (int e = 0; e < h->nzp; ++e) N.Send(plane_ptr(h, h->zp[e], h->nzl), cnt, ty, h->up, h->comm, st);
-  if (h->down >= 0)
-    for (int e = 0; e < h->nzp; ++e) N.Recv(recv_ptr(h, true, e, h->zp[e]), cnt, ty, h->down, h->comm, st);
-  if (h->down >= 0)
-    for (int e = 0; e < h->nzm; ++e) N.Send(plane_ptr(h, h->zm[e], -1), cnt, ty, h->down, h->comm, st);
-  if (h->up >= 0)
-    for (int e = 0; e < h->nzm; ++e) N.Recv(recv_ptr(h, false, e, h->zm[e]), cnt, ty, h->up, h->comm, st);
+  for (int sp = 0; sp < h->comps; ++sp) {
+    if (h->up >= 0)
+      for (int e = 0; e < h->nzp; ++e) N.Send(plane_ptr(h, h->zp[e], h->nzl, sp), cnt, ty, h->up, h->comm, st);
+    if (h->down >= 0)
+      for (int e = 0; e < h->nzp; ++e)
+        N.Recv(recv_ptr(h, true, e, h->zp[e], sp), cnt, ty, h->down, h->comm, st);
+    if (h->down >= 0)
+      for (int e = 0; e < h->nzm; ++e) N.Send(plane_ptr(h, h->zm[e], -1, sp), cnt, ty, h->down, h->comm, st);
+    if (h->up >= 0)
+      for (int e = 0; e < h->nzm; ++e)
+        N.Recv(recv_ptr(h, false, e, h->zm[e], sp), cnt, ty, h->up, h->comm, st);
+  }
   ncclResult_t r = N.GroupEnd();
   if (r != ncclSuccess)
     return set_err(TSLB_ECUDA, "NCCL halo exchange: %s", N.ErrStr ? N.ErrStr(r) : "error");
@@ -508,22 +516,78 @@ int exchange_nccl(tslb_cuda_sim* h, cudaStream_t st) {
 int exchange_local(tslb_cuda_sim* h, cudaStream_t st) {
   const size_t bytes = size_t(h->plane()) * h->esz;
   Prof p(h, TSLB_K_EXCHANGE, st);
-  if (h->up_peer)
-    for (int e = 0; e < h->nzp; ++e)
-      CK(cudaMemcpyAsync(recv_ptr(h->up_peer, true, e, h->zp[e]),
-                         plane_ptr(h, h->zp[e], h->nzl), bytes,
-                         cudaMemcpyDeviceToDevice, st));
+  for (int sp = 0; sp < h->comps; ++sp) {
+    if (h->up_peer)
+      for (int e = 0; e < h->nzp; ++e)
+        CK(cudaMemcpyAsync(recv_ptr(h->up_peer, true, e, h->zp[e], sp),
+                           plane_ptr(h, h->zp[e], h->nzl, sp), bytes,
+                           cudaMemcpyDeviceToDevice, st));
+    if (h->down_peer)
+      for (int e = 0; e < h->nzm; ++e)
+        CK(cudaMemcpyAsync(recv_ptr(h->down_peer, false, e, h->zm[e], sp),
+                           plane_ptr(h, h->zm[e], -1, sp), bytes,
+                           cudaMemcpyDeviceToDevice, st));
+  }
+  return 0;
+}
+
+// two-fluid slabs: phi boundary planes -> the neighbours' phi ghost planes
+// (the gradient stencil of the boundary planes), same grouping as above
+int exchange_phi_nccl(tslb_cuda_sim* h, cudaStream_t st) {
+  NcclApi& N = nccl();
+  const ncclDataType_t ty = h->scalar == TSLB_F64 ? ncclFloat64 : ncclFloat32;
+  const size_t cnt = size_t(h->plane());
+  char* phi = static_cast<char*>(h->tf().phi);
+  auto pl = [&](int k) { return phi + (int64_t(k) * h->plane()) * h->esz; };
+  Prof p(h, TSLB_K_EXCHANGE, st);
+  N.GroupStart();
+  if (h->up >= 0) N.Send(pl(h->nzl - 1), cnt, ty, h->up, h->comm, st);
+  if (h->down >= 0) N.Recv(pl(-1), cnt, ty, h->down, h->comm, st);
+  if (h->down >= 0) N.Send(pl(0), cnt, ty, h->down, h->comm, st);
+  if (h->up >= 0) N.Recv(pl(h->nzl), cnt, ty, h->up, h->comm, st);
+  ncclResult_t r = N.GroupEnd();
+  if (r != ncclSuccess)
+    return set_err(TSLB_ECUDA, "NCCL phi halo exchange: %s", N.ErrStr ? N.ErrStr(r) : "error");
+  return 0;
+}
+
+int exchange_phi_local(tslb_cuda_sim* h, cudaStream_t st) {
+  const size_t bytes = size_t(h->plane()) * h->esz;
+  auto pl = [&](const tslb_cuda_sim* x, int k) {
+    return static_cast<char*>(x->tf().phi) + (int64_t(k) * x->plane()) * x->esz;
+  };
+  Prof p(h, TSLB_K_EXCHANGE, st);
+  if (h->up_peer) CK(cudaMemcpyAsync(pl(h->up_peer, -1), pl(h, h->nzl - 1), bytes, cudaMemcpyDeviceToDevice, st));
   if (h->down_peer)
-    for (int e = 0; e < h->nzm; ++e)
-      CK(cudaMemcpyAsync(recv_ptr(h->down_peer, false, e, h->zm[e]),
-                         plane_ptr(h, h->zm[e], -1), bytes,
-                         cudaMemcpyDeviceToDevice, st));
+    CK(cudaMemcpyAsync(pl(h->down_peer, h->down_peer->nzl), pl(h, 0), bytes, cudaMemcpyDeviceToDevice, st));
   return 0;
 }
 
 // One fused step (fused_step / two_fluid_step) enqueued on h->s.
 int enqueue_step(tslb_cuda_sim* h) {
   int rc;
+  if (h->comps == 2 && h->xmode == 1) {
+    // two-fluid slab: colour moments, phi ghost planes, folded recolouring
+    // stream-collide, population halos of both species
+    if ((rc = ph_cg_moments(h, h->s))) return rc;
+    if ((rc = exchange_phi_nccl(h, h->s))) return rc;
+    {
+      Prof p(h, TSLB_K_CG_STREAMCOLL, h->s);
+      ++h->launches;
+      rc = by_scalar(h, [&](auto z) {
+        using T = decltype(z);
+        return launch_cg_streamcoll_grad<T>(h->lat, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
+                                            static_cast<T*>(h->f[1]), h->tf(), h->omega, h->cp, h->s);
+      });
+      if (rc) return set_err(TSLB_ESTATE, "two-fluid slab step needs a box geometry without NCI");
+    }
+    if ((rc = exchange_nccl(h, h->s))) return rc;
+    if ((rc = unpack(h, h->s))) return rc;
+    h->grad_pending = true;
+    h->stress_pending = true;
+    ++h->steps;
+    return 0;
+  }
   if (h->comps == 2) {
     if ((rc = ph_cg_moments(h, h->s))) return rc;
     // box geometry without NCI: gradient folded into the stream-collide
@@ -641,8 +705,8 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   if (!kinds || !uw) return set_err(TSLB_EINVAL, "face arrays are required");
   if (int rc = check_axes(kinds)) return rc;
   const bool decomposed = nzl != nz;
-  if (decomposed && components == 2)
-    return set_err(TSLB_EINVAL, "two-fluid slab decomposition is not supported");
+  if (decomposed && components == 2 && color && color[2] != 0.0)
+    return set_err(TSLB_EINVAL, "two-fluid slabs: the near-contact force (NCI) is not decomposed");
   CK(cudaSetDevice(device));
 
   auto* h = new tslb_cuda_sim();
@@ -724,6 +788,10 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
         d.has_solid = 1;
         break;
       }
+  if (decomposed && components == 2 && d.has_solid) {
+    delete h;
+    return set_err(TSLB_EINVAL, "two-fluid slabs: box geometries only (no solid mask)");
+  }
   d.xblocks = (nx + 127) / 128;
   d.k0 = 0;
   d.nzr = nzl;
@@ -747,6 +815,11 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
     const size_t tb = size_t(d.mstride) * (3 + h->dim) * h->esz;
     if ((rc = alloc(h, &h->two, tb))) return fail(rc);
     CK(cudaMemsetAsync(h->two, 0, tb, h->s));
+    if (decomposed) {
+      const size_t pg = size_t(d.plane) * (nzl + 2) * h->esz;
+      if ((rc = alloc(h, &h->phig, pg))) return fail(rc);
+      CK(cudaMemsetAsync(h->phig, 0, pg, h->s));
+    }
     if ((rc = alloc(h, reinterpret_cast<void**>(&h->flag), size_t(d.mstride)))) return fail(rc);
     CK(cudaMemsetAsync(h->flag, 0, size_t(d.mstride), h->s));
   }
@@ -781,7 +854,7 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   // the received planes are staged and unpacked under that mask.
   h->staged = decomposed && (d.has_solid || d.mode[XMin] == kWall || d.mode[YMin] == kWall);
   if (h->staged) {
-    const size_t pb = size_t(d.plane) * 9 * h->esz;
+    const size_t pb = size_t(d.plane) * 9 * components * h->esz;
     if ((rc = alloc(h, &h->recv_lo, pb))) return fail(rc);
     if ((rc = alloc(h, &h->recv_hi, pb))) return fail(rc);
   }
@@ -904,7 +977,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   if (h->s) cudaStreamSynchronize(h->s);
   if (h->cs) cudaStreamSynchronize(h->cs);
   if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
-  void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->two, h->flag, h->solid, h->slow,
+  void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->phig, h->two, h->flag, h->solid, h->slow,
                   h->scratch, h->red, h->dig, h->recv_lo, h->recv_hi};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1049,7 +1122,7 @@ int field_desc(tslb_cuda_sim* h, int field, void** base, int* count, int* eb,
     case TSLB_FIELD_PINEQ: *base = h->m_arr(1 + h->dim); *count = h->np; return 0;
     case TSLB_FIELD_RHO_R: if (!two) break; *base = h->t_arr(0); *count = 1; return 0;
     case TSLB_FIELD_RHO_B: if (!two) break; *base = h->t_arr(1); *count = 1; return 0;
-    case TSLB_FIELD_PHI: if (!two) break; *base = h->t_arr(2); *count = 1; return 0;
+    case TSLB_FIELD_PHI: if (!two) break; *base = h->tf().phi; *count = 1; return 0;
     case TSLB_FIELD_GRADPHI: if (!two) break; *base = h->t_arr(3); *count = h->dim; return 0;
     case TSLB_FIELD_NCI_FLAG: if (!two) break; *base = h->flag; *count = 1; *eb = 1; return 0;
     case TSLB_FIELD_SOLID:
@@ -1529,6 +1602,35 @@ int tslb_cuda_group_step(tslb_cuda_handle* slabs, int count, long nsteps) {
     any_m = any_m || slabs[r]->sched == TSLB_SCHED_M;
   }
   if (any_m && !all_m) return set_err(TSLB_ESTATE, "linked slabs must share one step schedule");
+  if (slabs[0]->comps == 2) {
+    for (long s = 0; s < nsteps; ++s) {
+      for (int r = 0; r < count; ++r)
+        if (int rc = ph_cg_moments(slabs[r], st)) return rc;
+      for (int r = 0; r < count; ++r)
+        if (int rc = exchange_phi_local(slabs[r], st)) return rc;
+      for (int r = 0; r < count; ++r) {
+        tslb_cuda_sim* h = slabs[r];
+        ++h->launches;
+        const int rc = by_scalar(h, [&](auto z) {
+          using T = decltype(z);
+          return launch_cg_streamcoll_grad<T>(h->lat, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
+                                              static_cast<T*>(h->f[1]), h->tf(), h->omega, h->cp, st);
+        });
+        if (rc) return set_err(TSLB_ESTATE, "two-fluid slab step needs a box geometry without NCI");
+      }
+      for (int r = 0; r < count; ++r)
+        if (int rc = exchange_local(slabs[r], st)) return rc;
+      for (int r = 0; r < count; ++r) {
+        if (int rc = unpack(slabs[r], st)) return rc;
+        slabs[r]->grad_pending = true;
+        slabs[r]->stress_pending = true;
+        ++slabs[r]->steps;
+      }
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    return 0;
+  }
   for (long s = 0; s < nsteps; ++s) {
     if (all_m) {
       // the NCCL path's order: boundary chunks, exchange of the new boundary

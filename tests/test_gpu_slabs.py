@@ -141,3 +141,85 @@ def test_nccl_self_exchange_equals_periodic_box(gpu, sched, dtype, monkeypatch):
     finally:
         slab.close()
         ref.close()
+
+
+# --- two-fluid z slabs: phi ghost planes + both species' population halos ---
+def _two_cp():
+    return T.ColorParams(sigma=0.02, beta=0.7)
+
+
+def _droplet(dims, dtype):
+    from helpers import droplet_state
+    st = droplet_state(dims, min(dims[:2]) / 3.5, dtype, (0.01, -0.005, 0.004))
+    return Oracle_port().init_colors("d3q19", dims, st, None)
+
+
+def Oracle_port():
+    return O.Oracle("port")
+
+
+TWO_FACES = [
+    ("periodic", O.periodic()),
+    ("zwalls", zwalls_3d()),
+    ("ywalls-staged", [("periodic", (0, 0, 0))] * 2 + [("wall", (0, 0, 0)), ("moving", (0.02, 0.0, 0.0))]
+     + [("periodic", (0, 0, 0))] * 2),
+]
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("parts", [2, 3])
+@pytest.mark.parametrize("name,faces", TWO_FACES, ids=[t[0] for t in TWO_FACES])
+def test_two_fluid_slabs_equal_single_domain(gpu, name, faces, parts, dtype):
+    dims = (20, 14, 12)
+    fr, fb = _droplet(dims, dtype)
+    plane = dims[0] * dims[1]
+    one = T.DeviceSolver("d3q19", T.GridDims(*dims), 1.25, spec_of(faces), dtype, 2, None, _two_cp())
+    one.upload_f(fr, 0)
+    one.upload_f(fb, 1)
+    one.step(5)
+    ref = [one.download_f(0), one.download_f(1)] + [one.download_field(k) for k in ("phi", "gradphi", "rho")]
+    one.close()
+    slabs = [T.DeviceSolver("d3q19", T.GridDims(*dims), 1.25, spec_of(faces), dtype, 2, None, _two_cp(), slab=s)
+             for s in split(dims[2], parts)]
+    try:
+        for sv, (z0, nzl) in zip(slabs, split(dims[2], parts)):
+            sv.upload_f(np.ascontiguousarray(fr[:, z0 * plane:(z0 + nzl) * plane]), 0)
+            sv.upload_f(np.ascontiguousarray(fb[:, z0 * plane:(z0 + nzl) * plane]), 1)
+        arr = (C.c_void_p * parts)(*[s.h.value for s in slabs])
+        _lib.call("tslb_cuda_link_local", arr, parts)
+        _lib.call("tslb_cuda_group_step", arr, parts, 5)
+        got = [np.concatenate([s.download_f(sp) for s in slabs], axis=1) for sp in (0, 1)]
+        got.append(np.concatenate([s.download_field("phi") for s in slabs]))
+        got.append(np.concatenate([s.download_field("gradphi").reshape(3, -1) for s in slabs], axis=1))
+        got.append(np.concatenate([s.download_field("rho") for s in slabs]))
+    finally:
+        for s in slabs:
+            s.close()
+    for g, r, what in zip(got, ref, ["fr", "fb", "phi", "gradphi", "rho"]):
+        assert_bitwise(np.reshape(g, np.shape(r)) if what != "gradphi" else g, np.reshape(r, np.shape(g)),
+                       f"two-fluid {parts} slabs {what}")
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_two_fluid_nccl_self_exchange(gpu, dtype):
+    """Two-fluid slab on a one-rank NCCL communicator == periodic box."""
+    dims = (20, 14, 6)
+    fr, fb = _droplet(dims, dtype)
+    spec = spec_of(O.periodic())
+    ref = T.DeviceSolver("d3q19", T.GridDims(*dims), 1.25, spec, dtype, 2, None, _two_cp())
+    slab = T.DeviceSolver("d3q19", T.GridDims(dims[0], dims[1], 2 * dims[2]), 1.25, spec, dtype, 2, None, _two_cp(),
+                          slab=(0, dims[2]))
+    try:
+        uid = (C.c_char * 128)()
+        _lib.call("tslb_cuda_nccl_unique_id", uid)
+        _lib.call("tslb_cuda_attach_nccl", slab.h, uid, 1, 0)
+        for d in (ref, slab):
+            d.upload_f(fr, 0)
+            d.upload_f(fb, 1)
+            d.step(6)
+        for sp in (0, 1):
+            assert_bitwise(slab.download_f(sp), ref.download_f(sp), f"two-fluid NCCL self-exchange species {sp}")
+        assert_bitwise(slab.download_field("gradphi"), ref.download_field("gradphi"), "gradphi")
+    finally:
+        slab.close()
+        ref.close()
