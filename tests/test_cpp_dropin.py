@@ -35,7 +35,8 @@ def test_dropin_demo_compiles(tmp_path):
 def test_reference_suites_compile_against_dropin():
     from paper_2304_06437_b200 import build
     build.build()
-    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "dropin-tests", "ref-tests"],
+    r = subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "oracle"), "dropin-tests", "ref-tests",
+                        "dropin-acceptance"],
                        capture_output=True, text=True)
     assert r.returncode == 0, r.stderr[-3000:]
 
@@ -70,3 +71,16 @@ def test_reference_unit_suite_passes_against_dropin(gpu, suite):
     r = subprocess.run([exe], capture_output=True, text=True, timeout=900)
     print(r.stdout[-3000:])
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
+
+
+@pytest.mark.gpu
+def test_reference_acceptance_gate_passes_against_dropin(gpu):
+    """The reference's acceptance gate (proj/tests/acceptance.cpp, every check
+    prints PASS/FAIL, exit status = failures), compiled unchanged against the
+    B200 drop-in, passes on the device."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_acceptance")
+    if not os.path.exists(exe):
+        pytest.skip("built where /root/reference exists (make -C oracle dropin-acceptance)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=1500)
+    print(r.stdout[-5000:])
+    assert r.returncode == 0, (r.stdout[-5000:], r.stderr[-3000:])
