@@ -163,6 +163,18 @@ inline int run_all() {
     }                                                                                \
     ::doctest::detail::report(thrown_, "throws " #type ": " #expr, __FILE__, __LINE__, false); \
   } while (0)
+// doctest: passes when expr throws `type` whose what() equals the message
+#define CHECK_THROWS_WITH_AS(expr, message, type)                                   \
+  do {                                                                               \
+    bool ok_ = false;                                                                \
+    try {                                                                            \
+      (void)(expr);                                                                  \
+    } catch (const type& e_) {                                                       \
+      ok_ = std::string(e_.what()) == std::string(message);                          \
+    } catch (...) {                                                                  \
+    }                                                                                \
+    ::doctest::detail::report(ok_, "throws " #type " with " #message ": " #expr, __FILE__, __LINE__, false); \
+  } while (0)
 #define CHECK_NOTHROW(...)                                                           \
   do {                                                                               \
     bool ok_ = true;                                                                 \

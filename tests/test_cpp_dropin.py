@@ -61,7 +61,7 @@ def test_dropin_demo_runs_on_gpu(tmp_path, gpu):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("suite", ["unit_lattice_fields", "unit_collision_stream", "unit_boundary",
-                                   "unit_multicomponent"])
+                                   "unit_multicomponent", "unit_analysis_bench", "unit_config_io"])
 def test_reference_unit_suite_passes_against_dropin(gpu, suite):
     """The reference's own unit suite, compiled unchanged against the B200
     drop-in, passes on the device."""
