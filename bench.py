@@ -51,6 +51,8 @@ WORKLOADS = {
     "droplet-d3q19": dict(lat="d3q19", dims=(512, 512, 512), faces="periodic", comps=2, init="droplet",
                           radius=512 / 6.0, omega=1 / 0.75, storage="f32", sigma=0.03, beta=0.7,
                           desc="D3Q19 two-component colour-gradient droplet {n}, R = 85.33, sigma 0.03, beta 0.7"),
+    "tgv-d2q9": dict(lat="d2q9", dims=(4096, 4096, 1), faces="periodic", comps=1, init="taylor_green", amp=0.03,
+                     omega=1.6, storage="f32", desc="D2Q9 periodic Taylor-Green {n} (the paper's 2-D size)"),
     "cavity-d2q9": dict(lat="d2q9", dims=(256, 256, 1), faces="lid", comps=1, init="rest", amp=0.0,
                         omega=1 / (0.064 * 3 + 0.5), storage="f64",
                         desc="D2Q9 lid-driven cavity {n}, Re 100, fp64"),
