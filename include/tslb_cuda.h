@@ -148,6 +148,12 @@ int tslb_cuda_upload_f(tslb_cuda_handle h, int species, const void* host);
 int tslb_cuda_download_f(tslb_cuda_handle h, int species, void* host);
 int tslb_cuda_upload_field(tslb_cuda_handle h, int field, const void* host);
 int tslb_cuda_download_field(tslb_cuda_handle h, int field, void* host);
+/* Device-side sampler for the output writers (io.hpp; tslb_main.cpp:137-188):
+ * one 2-D slice of a field -- the plane perpendicular to `axis` (0 x, 1 y,
+ * 2 z) at local `index` -- without moving the whole field. Output per array
+ * of the field: axis 2 -> nx*ny (x fastest), axis 1 -> nx*nz (x fastest),
+ * axis 0 -> ny*nz (y fastest). Same host-visible values as download_field. */
+int tslb_cuda_download_slice(tslb_cuda_handle h, int field, int axis, int index, void* host);
 int tslb_cuda_download_geometry(tslb_cuda_handle h, uint8_t* solid,
                                 uint32_t* slow_mask, uint64_t* n_fluid);
 int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,

@@ -58,6 +58,7 @@ def load(path: str | None = None) -> C.CDLL:
         "tslb_cuda_set_schedule": ([H, i], i),
         "tslb_cuda_get_schedule": ([H, vp], i),
         "tslb_cuda_set_body_force": ([H, vp], i),
+        "tslb_cuda_download_slice": ([H, i, i, i, vp], i),
         "tslb_cuda_describe": ([H, vp, vp], i),
         "tslb_cuda_memory_bytes": ([H, vp], i),
         "tslb_cuda_upload_f": ([H, i, vp], i),

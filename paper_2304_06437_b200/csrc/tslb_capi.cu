@@ -1183,6 +1183,36 @@ int tslb_cuda_download_field(tslb_cuda_handle h, int field, void* host) {
   return sync(h);
 }
 
+int tslb_cuda_download_slice(tslb_cuda_handle h, int field, int axis, int index, void* host) {
+  if (axis < 0 || axis > 2) return set_err(TSLB_EINVAL, "slice axis must be 0, 1 or 2");
+  const int ext[3] = {h->nx, h->ny, h->nzl};
+  if (index < 0 || index >= ext[axis]) return set_err(TSLB_EINVAL, "slice index %d outside [0, %d)", index, ext[axis]);
+  if (field == TSLB_FIELD_SLOW_MASK) return set_err(TSLB_EINVAL, "slices of the slow mask are not provided");
+  CK(cudaSetDevice(h->device));
+  if (int rc = finish_gradient(h)) return rc;
+  if (h->comps == 2 && h->stress_pending && (field == TSLB_FIELD_MOM || field == TSLB_FIELD_PINEQ))
+    if (int rc = ph_cg_prepare(h, h->s)) return rc;
+  void* base; int cnt, eb; int64_t stride;
+  if (int rc = field_desc(h, field, &base, &cnt, &eb, &stride, false)) return rc;
+  // one strided 2-D copy per array: rows of `width` bytes, `rows` of them,
+  // `spitch` apart in device memory, packed on the host
+  const size_t nx = size_t(h->nx), ny = size_t(h->ny), nz = size_t(h->nzl);
+  size_t off, width, spitch, rows;
+  if (axis == 2) {         // x-y plane: contiguous
+    off = size_t(index) * nx * ny; width = nx * ny * eb; spitch = width; rows = 1;
+  } else if (axis == 1) {  // x-z plane: nz rows of nx, one plane apart
+    off = size_t(index) * nx; width = nx * eb; spitch = nx * ny * eb; rows = nz;
+  } else {                 // y-z plane: ny * nz single elements, one row apart
+    off = size_t(index); width = eb; spitch = nx * eb; rows = ny * nz;
+  }
+  const size_t plane_bytes = width * rows;
+  for (int c = 0; c < cnt; ++c)
+    CK(cudaMemcpy2DAsync(static_cast<char*>(host) + c * plane_bytes, width,
+                         static_cast<const char*>(base) + (size_t(c) * stride + off) * eb, spitch, width, rows,
+                         cudaMemcpyDeviceToHost, h->s));
+  return sync(h);
+}
+
 int tslb_cuda_download_geometry(tslb_cuda_handle h, uint8_t* solid,
                                 uint32_t* slow_mask, uint64_t* n_fluid) {
   if (solid)

@@ -388,6 +388,16 @@ class DeviceSolver:
         self._call("tslb_cuda_download_field", _lib.FIELD[name], _ptr(out))
         return out[0] if cnt == 1 else out
 
+    def download_slice(self, name, axis: int, index: int) -> np.ndarray:
+        """One 2-D slice of a field (device-side sampler, tslb_cuda.h):
+        returns (arrays, rows, cols) with the fastest axis last."""
+        cnt, dt = self._fshape(name)
+        ext = [self.dims.nx, self.dims.ny, self.nzl]
+        rows_cols = {2: (ext[1], ext[0]), 1: (ext[2], ext[0]), 0: (ext[2], ext[1])}[axis]
+        out = np.empty((cnt, *rows_cols), dt)
+        self._call("tslb_cuda_download_slice", _lib.FIELD[name], int(axis), int(index), _ptr(out))
+        return out
+
     def upload_field(self, name, arr):
         cnt, dt = self._fshape(name)
         a = np.ascontiguousarray(np.asarray(arr, dt).reshape(cnt, self.n))

@@ -338,3 +338,24 @@ def test_box_kernels_bitwise_wide_rows(gpu, oracle_port, case, dtype, variant, m
     fg, mg = _gpu_single(lat, dims, 0.83, faces, f0, 4, None)
     assert_bitwise(fg, fo, f"{variant} {lat}/{name} f")
     assert_bitwise(mg, mo, f"{variant} {lat}/{name} moments")
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+@pytest.mark.parametrize("sched", ["m", "f1"])
+def test_slice_sampler_matches_full_download(gpu, axis, sched):
+    """download_slice (device-side sampler for the output writers) returns
+    exactly the corresponding plane of download_field, for every axis."""
+    dims = (32, 16, 6)
+    dev = T.DeviceSolver("d3q19", T.GridDims(*dims), 1.3, spec_of(zwalls_3d()), np.float32)
+    try:
+        dev.set_schedule(sched)
+        dev.init_analytic("taylor_green", 0.03)
+        dev.step(3)
+        for name in ("rho", "mom", "pineq"):
+            full = dev.download_field(name).reshape(-1, dims[2], dims[1], dims[0])
+            idx = dims[axis] // 2
+            sl = dev.download_slice(name, axis, idx)
+            want = {2: full[:, idx], 1: full[:, :, idx], 0: full[:, :, :, idx]}[axis]
+            assert_bitwise(sl, want, f"slice {name} axis {axis}")
+    finally:
+        dev.close()
