@@ -355,7 +355,7 @@ def test_slice_sampler_matches_full_download(gpu, axis, sched):
             full = dev.download_field(name).reshape(-1, dims[2], dims[1], dims[0])
             idx = dims[axis] // 2
             sl = dev.download_slice(name, axis, idx)
-            want = {2: full[:, idx], 1: full[:, :, idx], 0: full[:, :, :, idx]}[axis]
+            want = full[:, idx] if axis == 2 else full[:, :, idx] if axis == 1 else full[:, :, :, idx]
             assert_bitwise(sl, want, f"slice {name} axis {axis}")
     finally:
         dev.close()
