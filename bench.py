@@ -334,13 +334,14 @@ def main():
     sched = sim.schedule if W["comps"] == 1 else "f1"
     sb = step_bytes(lat, W["comps"], es, sched) if W["comps"] == 1 else sum(per_node.values())
     step_bw = glups * sb / world  # per-GPU GB/s of the whole step
-    traffic, tsrc, limiter = None, None, None
+    traffic, tsrc, limiter, fp64_ops = None, None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh).get(f"{lat.name}/{W['storage']}/{dom}")
         if tr:
             traffic, tsrc = round(tr["bytes_per_node"] * local_nodes / 1e9, 3), tr["source"]
             limiter = tr.get("limiter")
+            fp64_ops = tr.get("fp64_ops_per_lu") if args.math == "f64" else None
     except (OSError, ValueError):
         pass
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
@@ -350,6 +351,15 @@ def main():
             "per_kernel_ms": {k: round(v[0] / v[1], 4) for k, v in prof.items()},
             "step_bytes_per_lu": sb, "step_frac": round(step_bw / hbm, 4),
             "step_frac_of_8TBs": round(step_bw / 8000.0, 4)}
+    if fp64_ops:
+        # the pipe that binds the fp64-arithmetic M kernel: executed DADD+DMUL
+        # per LU (ncu SASS mix) against 64 fp64 lanes/clk/SM at the sampled clock
+        mhz = (clk or {}).get("sm_mhz") or 1965.0
+        peak_t = 148 * 64 * mhz * 1e6 / 1e12
+        ach_t = fp64_ops * glups / world * 1e9 / 1e12
+        roof["fp64_pipe"] = {"ops_per_lu": fp64_ops, "achieved_tops": round(ach_t, 2),
+                             "peak_tops": round(peak_t, 2), "frac": round(ach_t / peak_t, 4),
+                             "source": "profiles/traffic.json"}
     if W["comps"] == 1:
         # the F1 schedule's ceiling: every population through HBM twice
         # (census bytes, bench.hpp:62-63); M beats it by moving fewer bytes
