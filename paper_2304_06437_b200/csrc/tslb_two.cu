@@ -397,10 +397,13 @@ __global__ void __launch_bounds__(BX2)
 // grad phi at one node from its neighbours (gradient_and_nci,
 // multicomponent.hpp:178-200: wall neighbours take phi(x)); accumulation in
 // the reference's direction order
+// (phi is indexed as base + 32-bit node index: a node index of a domain that
+// fits in HBM is < 2^32, and the uniform base keeps the address arithmetic
+// to one instruction per load)
 template <class L, typename T, bool WALLS>
-__device__ __forceinline__ void gradient_at(const T* __restrict__ ph, const Steps32& st, T& gx, T& gy,
-                                            T& gz) {
-  const T phi0 = ph[0];
+__device__ __forceinline__ void gradient_at(const T* __restrict__ phi, uint32_t mi, const Steps32& st,
+                                            T& gx, T& gy, T& gz) {
+  const T phi0 = phi[mi];
   gx = 0;
   gy = 0;
   gz = 0;
@@ -416,7 +419,7 @@ __device__ __forceinline__ void gradient_at(const T* __restrict__ ph, const Step
       if constexpr (dd::y == -1) { delta += st.dm[1]; wall |= st.bm[1]; }
       if constexpr (dd::z == 1) { delta += st.dp[2]; wall |= st.bp[2]; }
       if constexpr (dd::z == -1) { delta += st.dm[2]; wall |= st.bm[2]; }
-      const T pn = (WALLS && wall) ? phi0 : __ldg(ph + delta);
+      const T pn = (WALLS && wall) ? phi0 : __ldg(phi + (mi + uint32_t(delta)));
       constexpr T w = dd::template t<T>();
       const T tp = w * pn;
       if constexpr (dd::x == 1) gx += tp;
@@ -438,7 +441,7 @@ __global__ void __launch_bounds__(BX2) k_cg_gradient_box(Dom d, TF<T> s) {
   if (!node_coords<BX2>(d, i, j, k)) return;
   const int64_t mi = midx(d, i, j, k);
   T gx, gy, gz;
-  gradient_at<L, T, WALLS>(s.phi + mi, face_steps32(d, i, j, k), gx, gy, gz);
+  gradient_at<L, T, WALLS>(s.phi, uint32_t(mi), face_steps32(d, i, j, k), gx, gy, gz);
   const int64_t ms = d.mstride;
   s.grad[mi] = gx;
   s.grad[ms + mi] = gy;
@@ -483,7 +486,7 @@ __global__ void __launch_bounds__(BX2)
   const Steps32 st = face_steps32(d, i, j, k);
   T gx, gy, gz;
   if constexpr (GRAD) {
-    gradient_at<L, T, WALLS>(s.phi + mi, st, gx, gy, gz);
+    gradient_at<L, T, WALLS>(s.phi, uint32_t(mi), st, gx, gy, gz);
     if constexpr (L::dim == 2) gz = T(0);
   } else {
     gx = s.grad[mi];
@@ -496,18 +499,19 @@ __global__ void __launch_bounds__(BX2)
   const T inv_gn = interface ? T(1) / gn : T(0);
   const T nhx = gx * inv_gn, nhy = gy * inv_gn, nhz = gz * inv_gn;
   const bool linear = cp.linear != 0;
-  T* __restrict__ frn = fr + fi;
-  T* __restrict__ fbn = fb + fi;
+  const uint32_t fi32 = uint32_t(fi);
 
   // one direction: perturbation + recolouring (reference order), then push
-  // or bounce (multicomponent.hpp:340-398)
-  auto out = [&](auto A, T g_out) {
+  // or bounce (multicomponent.hpp:340-398). IFACE is the node's interface
+  // test, hoisted out of the direction loop (one branch per node).
+  auto out = [&](auto A, auto IF, T g_out) {
     constexpr int a = decltype(A)::value;
+    constexpr bool IFACE = decltype(IF)::value;
     using dd = Dir<L, a>;
     constexpr T t = dd::template t<T>();
     constexpr T b = dd::template b<T>();
     T fr_out;
-    if (interface) {
+    if constexpr (IFACE) {
       const T cn = dot_c<dd::x, dd::y, dd::z>(nhx, nhy, nhz);
       const T shape = !linear ? t * cn * cn - b : t * cn - b;
       g_out += pert_amp * shape;
@@ -541,24 +545,28 @@ __global__ void __launch_bounds__(BX2)
       if constexpr (dd::z == -1) add(st.bm[2], ZMin);
       const T corr = bounce_correction<L, a, T>(wx, wy, wz);
       const T corr_r = red_frac * corr;
-      frn[dd::opp * d.fstride] = fr_out - corr_r;
-      fbn[dd::opp * d.fstride] = fb_out - (corr - corr_r);
+      (fr + dd::opp * d.fstride)[fi32] = fr_out - corr_r;
+      (fb + dd::opp * d.fstride)[fi32] = fb_out - (corr - corr_r);
     } else {
-      frn[a * d.fstride + delta] = fr_out;
-      fbn[a * d.fstride + delta] = fb_out;
+      (fr + a * d.fstride)[fi32 + uint32_t(delta)] = fr_out;
+      (fb + a * d.fstride)[fi32 + uint32_t(delta)] = fb_out;
     }
   };
-  unroll<L::q>([&](auto A) {
-    constexpr int a = decltype(A)::value;
-    if constexpr (a == 0) {
-      out(A, post_rest<L, T>(m, om1));
-    } else if constexpr (a & 1) {
-      T ga, gb;
-      post_pair<L, a, T>(m, om1, ga, gb);
-      out(A, ga);
-      out(std::integral_constant<int, a + 1>{}, gb);
-    }
-  });
+  auto all_dirs = [&](auto IF) {
+    unroll<L::q>([&](auto A) {
+      constexpr int a = decltype(A)::value;
+      if constexpr (a == 0) {
+        out(A, IF, post_rest<L, T>(m, om1));
+      } else if constexpr (a & 1) {
+        T ga, gb;
+        post_pair<L, a, T>(m, om1, ga, gb);
+        out(A, IF, ga);
+        out(std::integral_constant<int, a + 1>{}, IF, gb);
+      }
+    });
+  };
+  if (interface) all_dirs(std::true_type{});
+  else all_dirs(std::false_type{});
 }
 
 // ---------------------------------------------------------------------------
