@@ -499,7 +499,12 @@ __global__ void __launch_bounds__(BX2)
   const T inv_gn = interface ? T(1) / gn : T(0);
   const T nhx = gx * inv_gn, nhy = gy * inv_gn, nhz = gz * inv_gn;
   const bool linear = cp.linear != 0;
-  const uint32_t fi32 = uint32_t(fi);
+  // per-thread slot pointers of the direction being written, advanced by one
+  // array stride per direction (directions are visited in order): one 64-bit
+  // add per direction and species instead of a fresh a * fstride product
+  T* pr = fr + fi;
+  T* pb = fb + fi;
+  const int64_t fs = d.fstride;
 
   // one direction: perturbation + recolouring (reference order), then push
   // or bounce (multicomponent.hpp:340-398). IFACE is the node's interface
@@ -545,12 +550,15 @@ __global__ void __launch_bounds__(BX2)
       if constexpr (dd::z == -1) add(st.bm[2], ZMin);
       const T corr = bounce_correction<L, a, T>(wx, wy, wz);
       const T corr_r = red_frac * corr;
-      (fr + dd::opp * d.fstride)[fi32] = fr_out - corr_r;
-      (fb + dd::opp * d.fstride)[fi32] = fb_out - (corr - corr_r);
+      constexpr int so = dd::opp - a;  // the opposite array is the neighbouring one
+      pr[so * fs] = fr_out - corr_r;
+      pb[so * fs] = fb_out - (corr - corr_r);
     } else {
-      (fr + a * d.fstride)[fi32 + uint32_t(delta)] = fr_out;
-      (fb + a * d.fstride)[fi32 + uint32_t(delta)] = fb_out;
+      pr[delta] = fr_out;
+      pb[delta] = fb_out;
     }
+    pr += fs;
+    pb += fs;
   };
   auto all_dirs = [&](auto IF) {
     unroll<L::q>([&](auto A) {
