@@ -52,6 +52,9 @@ int mstep_chunks(const Dom& d, int lz);
 template <typename T>
 int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
                  int lz, int chunk0, int nchunks, MstepMaps*& maps, cudaStream_t st);
+// D2Q9 form of the M step (tslb_mstep2d.cu; launched through launch_mstep)
+template <typename T>
+int launch_mstep2d(int math, const Dom& d, const T* mi, T* mo, double omega, cudaStream_t st);
 // slab f materialisation: pushes entering boundary plane `side` (0 below,
 // 1 above) rebuilt from the ghost moments
 template <typename T>

@@ -671,6 +671,7 @@ __global__ void __launch_bounds__(128) k_ghost_push(Dom d, T* __restrict__ f, co
 }  // namespace mstep
 
 bool mstep_supported(int lat, const Dom& d) {
+  if (lat == kD2Q9) return !d.has_solid && d.nz == 1 && d.ghost == 0;  // tslb_mstep2d.cu
   return (lat == kD3Q19 || lat == kD3Q27) && !d.has_solid && d.nx % mstep::TX == 0 &&
          d.ny % mstep::TY == 0 && mstep::encoder() != nullptr;
 }
@@ -703,6 +704,7 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
                  int lz, int chunk0, int nchunks, MstepMaps*& maps, cudaStream_t st) {
   using namespace mstep;
   if (!mstep_supported(lat, d)) return 1;
+  if (lat == kD2Q9) return chunk0 == 0 ? launch_mstep2d<T>(math, d, mi, mo, omega, st) : 1;
   if ((d.mode[ZMin] == kGhost || d.mode[ZMax] == kGhost) && !gm) return 1;
   if (lz <= 0) lz = kDefaultLz;
   const int nzc = (d.nz + lz - 1) / lz;

@@ -1,0 +1,214 @@
+// Moment-resident single pass for D2Q9 (the M schedule in 2-D): m(t) -> m(t+1)
+// in one kernel, bit-identical to compute_moments(stream_collide_fused(m(t)))
+// (kernels.hpp:74-107, 154-204), like k_mstep for 3-D (tslb_mstep.cu) but
+// with no shared memory and no barriers:
+//
+//   * a warp owns 30 consecutive columns (lanes 1..30) and marches up a strip
+//     of rows; lanes 0 and 31 recompute the columns just left and right of
+//     the strip (the halo) from the same instruction stream;
+//   * each lane rebuilds the 9 post-collision populations of its node
+//     (regularised collision, reference operand order, opposite pairs share
+//     Q:Pi^neq) and rounds them to T; pushes along c_x = +-1 move one lane
+//     with a warp shuffle, pushes along c_y land in a per-lane register ring
+//     of destination rows y-1, y, y+1; wall bounces write the node's own
+//     opposite slot (kernels.hpp:178-199), and a slot whose source lies
+//     beyond a wall is never taken from the shuffle;
+//   * once the march has passed row y, each owned lane reduces its 9 slots in
+//     direction order to m(t+1) exactly as compute_moments (same sums, same
+//     order) and stores them.
+//
+// HBM traffic: 2 x 6 scalars per lattice update (48 B fp32) instead of F1's
+// 120 B; the row strips overlap by one halo row at each end (the rows just
+// outside the strip push only their c_y-inward directions).
+#include <cstdint>
+
+#include "tslb_collision.cuh"
+#include "tslb_domain.cuh"
+#include "tslb_kernels.h"
+#include "tslb_pair.cuh"
+
+namespace tslb_cuda {
+namespace mstep2d {
+
+constexpr int OWN = 30;  // owned columns per warp (lanes 1..30)
+constexpr int WPB = 4;   // warps per block
+constexpr unsigned FULL = 0xffffffffu;
+
+__device__ __forceinline__ int wrap_coord(int g, int n, int lo, int hi) {
+  if (g < 0) return lo == kWrap ? g + n : -1;
+  if (g >= n) return hi == kWrap ? g - n : -1;
+  return g;
+}
+
+template <typename T, typename C>
+__device__ __forceinline__ NodeMoments<C> prep(const T (&v)[6]) {
+  return prepare_node<C>(C(v[0]), C(v[1]), C(v[2]), C(0), C(v[3]), C(v[4]), C(0), C(v[5]), C(0), C(0));
+}
+
+template <class L, typename T, typename C, bool WALLS>
+__global__ void __launch_bounds__(32 * WPB)
+    k_mstep2d(Dom d, const T* __restrict__ mi, T* __restrict__ mo, C om1, int rows) {
+  using Lat = L;
+  const int lane = threadIdx.x & 31;
+  const int strip = int(blockIdx.x) * WPB + int(threadIdx.x >> 5);
+  const int xg = strip * OWN - 1 + lane;  // this lane's column (may lie outside [0, nx))
+  const int xs = xg > d.nx ? -1 : wrap_coord(xg, d.nx, d.mode[XMin], d.mode[XMax]);
+  const bool owned = lane >= 1 && lane <= OWN && xg < d.nx;
+  const int ya = int(blockIdx.y) * rows, yb = min(ya + rows, d.ny);
+  // is the lane that pushes into this one along c_x = +1 / -1 a real node?
+  const bool src = xs >= 0;
+  const bool from_left = __shfl_up_sync(FULL, src, 1);
+  const bool from_right = __shfl_down_sync(FULL, src, 1);
+  const int64_t ms = d.mstride;
+  bool cxlo = false, cxhi = false;
+  if constexpr (WALLS) {
+    cxlo = xg == 0 && d.mode[XMin] == kWall;
+    cxhi = xg == d.nx - 1 && d.mode[XMax] == kWall;
+  }
+
+  auto load = [&](int y, T (&v)[6]) {
+    const int yy = wrap_coord(y, d.ny, d.mode[YMin], d.mode[YMax]);
+    if (yy < 0 || !src) {
+      v[0] = T(1);
+#pragma unroll
+      for (int c = 1; c < 6; ++c) v[c] = T(0);
+      return;
+    }
+    const int64_t idx = xs + int64_t(d.nx) * yy;
+#pragma unroll
+    for (int c = 0; c < 6; ++c) v[c] = __ldg(mi + c * ms + idx);
+  };
+
+  T R[9][3];  // slot of direction a for destination rows y-1, y, y+1
+#pragma unroll
+  for (int a = 0; a < 9; ++a) R[a][0] = R[a][1] = R[a][2] = T(0);
+  T cur[6], nxt[6];
+  load(ya - 1, cur);
+
+  auto row = [&](auto ZCc, int y) {
+    constexpr int ZC = decltype(ZCc)::value;
+    if (ZC != -1) load(y + 1, nxt);
+    if (wrap_coord(y, d.ny, d.mode[YMin], d.mode[YMax]) >= 0) {  // uniform: the row exists
+      const NodeMoments<C> m = prep<T, C>(cur);
+      bool cylo = false, cyhi = false;
+      if constexpr (WALLS) {
+        cylo = y == 0 && d.mode[YMin] == kWall;
+        cyhi = y == d.ny - 1 && d.mode[YMax] == kWall;
+      }
+      // push of direction A (value o) into the slot of x + c_A, row y + c_y
+      auto push = [&](auto A, T o) {
+        constexpr int a = decltype(A)::value;
+        using dd = Dir<Lat, a>;
+        if constexpr (ZC == 0 || dd::y == ZC) {
+          T r = o;
+          bool ok = src;
+          if constexpr (dd::x == 1) {
+            r = __shfl_up_sync(FULL, o, 1);
+            ok = from_left;
+          }
+          if constexpr (dd::x == -1) {
+            r = __shfl_down_sync(FULL, o, 1);
+            ok = from_right;
+          }
+          if (ok) R[a][1 + dd::y] = r;
+          if constexpr (WALLS && ZC == 0) {
+            const bool bx = (dd::x == 1 && cxhi) || (dd::x == -1 && cxlo);
+            const bool by = (dd::y == 1 && cyhi) || (dd::y == -1 && cylo);
+            if (bx || by) R[dd::opp][1] = bounce_value<Lat, a, T, C>(d, o, bx, by, false);
+          }
+        }
+      };
+      unroll<9>([&](auto A) {
+        constexpr int a = decltype(A)::value;
+        if constexpr (a == 0) {
+          if constexpr (ZC == 0) push(A, T(post_rest<Lat, C>(m, om1)));
+        } else if constexpr (a & 1) {
+          constexpr bool ua = ZC == 0 || Dir<Lat, a>::y == ZC;
+          constexpr bool ub = ZC == 0 || Dir<Lat, a + 1>::y == ZC;
+          if constexpr (ua && ub) {
+            C ra, rb;
+            post_pair<Lat, a, C>(m, om1, ra, rb);
+            push(A, T(ra));
+            push(std::integral_constant<int, a + 1>{}, T(rb));
+          } else if constexpr (ua) {
+            push(A, T(post_single<Lat, a, C>(m, om1)));
+          } else if constexpr (ub) {
+            push(std::integral_constant<int, a + 1>{}, T(post_single<Lat, a + 1, C>(m, om1)));
+          }
+        }
+      });
+    }
+    // the march has passed row y - 1: reduce it (compute_moments order)
+    if (y - 1 >= ya && owned) {
+      C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pxy = 0;
+      unroll<9>([&](auto A) {
+        constexpr int a = decltype(A)::value;
+        using dd = Dir<Lat, a>;
+        const C fa = C(R[a][0]);
+        r += fa;
+        if constexpr (dd::x == 1) jx += fa;
+        if constexpr (dd::x == -1) jx -= fa;
+        if constexpr (dd::y == 1) jy += fa;
+        if constexpr (dd::y == -1) jy -= fa;
+        if constexpr (dd::x != 0) pxx += fa;
+        if constexpr (dd::y != 0) pyy += fa;
+        if constexpr (dd::x * dd::y == 1) pxy += fa;
+        if constexpr (dd::x * dd::y == -1) pxy -= fa;
+      });
+      force_shift<C>(d, jx, jy, jz);
+      const C c3 = cs2<C>();
+      const int64_t idx = xg + int64_t(d.nx) * (y - 1);
+      mo[idx] = T(r);
+      mo[ms + idx] = T(jx);
+      mo[2 * ms + idx] = T(jy);
+      mo[3 * ms + idx] = T(pxx - c3 * r - jx * jx);
+      mo[4 * ms + idx] = T(pyy - c3 * r - jy * jy);
+      mo[5 * ms + idx] = T(pxy - jx * jy);
+    }
+#pragma unroll
+    for (int a = 0; a < 9; ++a) {
+      R[a][0] = R[a][1];
+      R[a][1] = R[a][2];
+    }
+#pragma unroll
+    for (int c = 0; c < 6; ++c) cur[c] = nxt[c];
+  };
+
+  row(std::integral_constant<int, 1>{}, ya - 1);
+#pragma unroll 1
+  for (int y = ya; y < yb; ++y) row(std::integral_constant<int, 0>{}, y);
+  row(std::integral_constant<int, -1>{}, yb);
+}
+
+}  // namespace mstep2d
+
+template <typename T>
+int launch_mstep2d(int math, const Dom& d, const T* mi, T* mo, double omega, cudaStream_t st) {
+  using namespace mstep2d;
+  if (d.has_solid || d.nz != 1 || d.ghost) return 1;
+  const int strips = (d.nx + OWN - 1) / OWN;
+  const unsigned bx = unsigned((strips + WPB - 1) / WPB);
+  // rows per warp: long strips amortise the two halo rows; small domains
+  // (launch-bound, e.g. the 256^2 cavity) trade that for parallelism
+  int rows = 64;
+  while (rows > 4 && int64_t(strips) * ((d.ny + rows - 1) / rows) < 148 * 32) rows /= 2;
+  const dim3 grid(bx, unsigned((d.ny + rows - 1) / rows));
+  if (grid.y > 65535) return 1;
+  bool walls = false;
+  for (int fc = 0; fc < 4; ++fc) walls |= d.mode[fc] == kWall;
+  if (math == kMathDouble) {
+    const double om1 = 1.0 - double(T(omega));
+    if (walls) k_mstep2d<D2Q9, T, double, true><<<grid, 32 * WPB, 0, st>>>(d, mi, mo, om1, rows);
+    else k_mstep2d<D2Q9, T, double, false><<<grid, 32 * WPB, 0, st>>>(d, mi, mo, om1, rows);
+  } else {
+    const float om1 = 1.0f - float(omega);
+    if (walls) k_mstep2d<D2Q9, T, float, true><<<grid, 32 * WPB, 0, st>>>(d, mi, mo, om1, rows);
+    else k_mstep2d<D2Q9, T, float, false><<<grid, 32 * WPB, 0, st>>>(d, mi, mo, om1, rows);
+  }
+  return 0;
+}
+
+template int launch_mstep2d<float>(int, const Dom&, const float*, float*, double, cudaStream_t);
+template int launch_mstep2d<double>(int, const Dom&, const double*, double*, double, cudaStream_t);
+
+}  // namespace tslb_cuda

@@ -1,3 +1,4 @@
 #!/bin/bash
+# quick GPU iteration: the -m gpu tests selected by -k "$1"
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_single.py -m gpu -q -p no:cacheprovider -k "${1:-slice}" > gpurun_out/slice_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/slice_pytest.log
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider -k "${1:-slice}" > gpurun_out/quick_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/quick_pytest.log

@@ -218,7 +218,7 @@ def test_schedule_rules(gpu):
         dev.close()
     dev = T.DeviceSolver("d2q9", T.GridDims(64, 64, 1), 1.0, spec, np.float32)
     try:
-        assert dev.schedule == "f1"
+        assert dev.schedule == "m"  # the 2-D M kernel (tslb_mstep2d.cu)
     finally:
         dev.close()
 
@@ -281,8 +281,6 @@ def _ywalls():
 @pytest.mark.parametrize("lat,dims,faces", [("d3q19", (32, 16, 6), _ywalls()), ("d3q27", (32, 8, 5), O.periodic()),
                                             ("d2q9", (24, 20, 1), _ywalls())], ids=["d3q19", "d3q27", "d2q9"])
 def test_body_force_bitwise(gpu, oracle_port, lat, dims, faces, dtype, sched):
-    if lat == "d2q9" and sched == "m":
-        pytest.skip("the M schedule is 3-D")
     F = (3e-5, -1e-5, 2e-5 if dims[2] > 1 else 0.0)
     f0 = O.random_state(lat, dims, 31, dtype)
     dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.05, spec_of(faces), dtype)
@@ -361,3 +359,74 @@ def test_full_size_m_equals_f1_digests(gpu, lat, n):
     assert np.array_equal(dig["m"], dig["f1"])
     for m0, m1 in mass.values():
         assert abs(m1 - m0) <= 1e-6 * m0
+
+
+# --- the 2-D M kernel (warp strips, shuffles, register rings) --------------
+def _mixed2d():
+    f = O.periodic()
+    f[2] = ("wall", (0, 0, 0))
+    f[3] = ("moving", (0.04, 0.0, 0.0))
+    return f
+
+
+def _xwalls2d():
+    f = O.periodic()
+    f[0] = ("moving", (0.0, 0.03, 0.0))
+    f[1] = ("wall", (0, 0, 0))
+    return f
+
+
+CASES_2D = [
+    ("periodic", (64, 20, 1), O.periodic()),
+    ("periodic-narrow", (12, 9, 1), O.periodic()),
+    ("periodic-odd", (97, 31, 1), O.periodic()),
+    ("lid", (61, 33, 1), O.lid_cavity(0.05)),
+    ("box", (30, 30, 1), O.closed_box()),
+    ("mixed", (45, 17, 1), _mixed2d()),
+    ("xwalls", (31, 40, 1), _xwalls2d()),
+    ("rows-1", (40, 1, 1), O.periodic()),
+]
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("case", CASES_2D, ids=lambda c: c[0])
+def test_mstep2d_bitwise(gpu, oracle_port, case, dtype):
+    name, dims, faces = case
+    f0 = O.random_state("d2q9", dims, 13, dtype)
+    dev = T.DeviceSolver("d2q9", T.GridDims(*dims), 1.37, spec_of(faces), dtype)
+    try:
+        assert dev.schedule == "m"
+        dev.upload_f(f0)
+        dev.step(7)
+        mg = _moments(dev, "d2q9")
+        fg = dev.download_f()
+        dev.step(40)  # graph replay on small domains
+        mg2 = _moments(dev, "d2q9")
+        fg2 = dev.download_f()
+    finally:
+        dev.close()
+    fo, mo = _oracle(oracle_port, "d2q9", dims, 1.37, faces, f0, 7)
+    assert_bitwise(mg, mo, f"M2D {name} moments")
+    assert_bitwise(fg, fo, f"M2D {name} f")
+    mo2 = mo.copy()
+    oracle_port.single_run("d2q9", dims, 1.37, faces, fo, mo2, 40, 0)
+    assert_bitwise(mg2, mo2, f"M2D {name} moments after 47")
+    assert_bitwise(fg2, fo, f"M2D {name} f after 47")
+
+
+def test_mstep2d_f32_math_equals_f1(gpu):
+    dims, faces = (97, 31, 1), O.lid_cavity(0.05)
+    f0 = O.random_state("d2q9", dims, 5, np.float32)
+    out = {}
+    for sched in ("f1", "m"):
+        dev = T.DeviceSolver("d2q9", T.GridDims(*dims), 1.3, spec_of(faces), np.float32)
+        try:
+            dev.set_schedule(sched)
+            dev.set_math(_lib.MATH_F32)
+            dev.upload_f(f0)
+            dev.step(6)
+            out[sched] = (dev.download_f(), _moments(dev, "d2q9"))
+        finally:
+            dev.close()
+    assert_bitwise(out["m"][0], out["f1"][0], "2-D f32 math f")
+    assert_bitwise(out["m"][1], out["f1"][1], "2-D f32 math moments")
