@@ -21,6 +21,7 @@
 // 120 B; the row strips overlap by one halo row at each end (the rows just
 // outside the strip push only their c_y-inward directions).
 #include <cstdint>
+#include <cstdlib>
 
 #include "tslb_collision.cuh"
 #include "tslb_domain.cuh"
@@ -188,10 +189,16 @@ int launch_mstep2d(int math, const Dom& d, const T* mi, T* mo, double omega, cud
   if (d.has_solid || d.nz != 1 || d.ghost) return 1;
   const int strips = (d.nx + OWN - 1) / OWN;
   const unsigned bx = unsigned((strips + WPB - 1) / WPB);
-  // rows per warp: long strips amortise the two halo rows; small domains
-  // (launch-bound, e.g. the 256^2 cavity) trade that for parallelism
-  int rows = 64;
+  // rows per warp: 16 measured best at 4096^2 (72.8 GLUPS vs 67.5 at 64 and
+  // 71.2 at 8: the two halo rows vs wave quantisation); small domains
+  // (launch-bound, e.g. the 256^2 cavity) shorten strips for parallelism
+  int rows = 16;
   while (rows > 4 && int64_t(strips) * ((d.ny + rows - 1) / rows) < 148 * 32) rows /= 2;
+  static const int rows_env = [] {
+    const char* e = std::getenv("TSLB_ROWS2D");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (rows_env > 0) rows = rows_env;
   const dim3 grid(bx, unsigned((d.ny + rows - 1) / rows));
   if (grid.y > 65535) return 1;
   bool walls = false;

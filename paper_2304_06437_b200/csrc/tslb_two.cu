@@ -397,13 +397,13 @@ __global__ void __launch_bounds__(BX2)
 // grad phi at one node from its neighbours (gradient_and_nci,
 // multicomponent.hpp:178-200: wall neighbours take phi(x)); accumulation in
 // the reference's direction order
-// (phi is indexed as base + 32-bit node index: a node index of a domain that
-// fits in HBM is < 2^32, and the uniform base keeps the address arithmetic
-// to one instruction per load)
+// (neighbours as the node's pointer + a signed 32-bit offset: on z slabs the
+// plane below node k = 0 is phi's ghost plane, at a negative offset)
 template <class L, typename T, bool WALLS>
-__device__ __forceinline__ void gradient_at(const T* __restrict__ phi, uint32_t mi, const Steps32& st,
+__device__ __forceinline__ void gradient_at(const T* __restrict__ phi, int64_t mi, const Steps32& st,
                                             T& gx, T& gy, T& gz) {
-  const T phi0 = phi[mi];
+  const T* __restrict__ ph = phi + mi;
+  const T phi0 = ph[0];
   gx = 0;
   gy = 0;
   gz = 0;
@@ -419,7 +419,7 @@ __device__ __forceinline__ void gradient_at(const T* __restrict__ phi, uint32_t 
       if constexpr (dd::y == -1) { delta += st.dm[1]; wall |= st.bm[1]; }
       if constexpr (dd::z == 1) { delta += st.dp[2]; wall |= st.bp[2]; }
       if constexpr (dd::z == -1) { delta += st.dm[2]; wall |= st.bm[2]; }
-      const T pn = (WALLS && wall) ? phi0 : __ldg(phi + (mi + uint32_t(delta)));
+      const T pn = (WALLS && wall) ? phi0 : __ldg(ph + delta);
       constexpr T w = dd::template t<T>();
       const T tp = w * pn;
       if constexpr (dd::x == 1) gx += tp;
@@ -441,7 +441,7 @@ __global__ void __launch_bounds__(BX2) k_cg_gradient_box(Dom d, TF<T> s) {
   if (!node_coords<BX2>(d, i, j, k)) return;
   const int64_t mi = midx(d, i, j, k);
   T gx, gy, gz;
-  gradient_at<L, T, WALLS>(s.phi, uint32_t(mi), face_steps32(d, i, j, k), gx, gy, gz);
+  gradient_at<L, T, WALLS>(s.phi, mi, face_steps32(d, i, j, k), gx, gy, gz);
   const int64_t ms = d.mstride;
   s.grad[mi] = gx;
   s.grad[ms + mi] = gy;
@@ -486,7 +486,7 @@ __global__ void __launch_bounds__(BX2)
   const Steps32 st = face_steps32(d, i, j, k);
   T gx, gy, gz;
   if constexpr (GRAD) {
-    gradient_at<L, T, WALLS>(s.phi, uint32_t(mi), st, gx, gy, gz);
+    gradient_at<L, T, WALLS>(s.phi, mi, st, gx, gy, gz);
     if constexpr (L::dim == 2) gz = T(0);
   } else {
     gx = s.grad[mi];
