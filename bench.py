@@ -53,6 +53,10 @@ WORKLOADS = {
                           desc="D3Q19 two-component colour-gradient droplet {n}, R = 85.33, sigma 0.03, beta 0.7"),
     "tgv-d2q9": dict(lat="d2q9", dims=(4096, 4096, 1), faces="periodic", comps=1, init="taylor_green", amp=0.03,
                      omega=1.6, storage="f32", desc="D2Q9 periodic Taylor-Green {n} (the paper's 2-D size)"),
+    "porous-d3q19": dict(lat="d3q19", dims=(512, 512, 512), faces="periodic", comps=1, init="rest", amp=0.0,
+                         omega=1.0, storage="f32", force=(1e-6, 0.0, 0.0), spheres=(12.0, 0.25, 5),
+                         desc="D3Q19 periodic porous medium {n}: random overlapping spheres (r 12, ~25 % solid, "
+                              "bounce-back), body force along x, rest init"),
     "cavity-d2q9": dict(lat="d2q9", dims=(256, 256, 1), faces="lid", comps=1, init="rest", amp=0.0,
                         omega=1 / (0.064 * 3 + 0.5), storage="f64",
                         desc="D2Q9 lid-driven cavity {n}, Re 100, fp64"),
@@ -178,20 +182,41 @@ def spec_of(T, kind):
     return s
 
 
-def kernel_bytes(lat, comps, es):
-    """Algorithmic bytes per node of each kernel class."""
+def sphere_pack(dims, radius, frac, seed):
+    """Solid mask of random overlapping periodic spheres, about `frac` of the
+    nodes solid (x fastest, the solver's node order)."""
+    nx, ny, nz = dims
+    rng = np.random.default_rng(seed)
+    vol = 4.0 / 3.0 * np.pi * radius ** 3
+    count = int(round(-np.log(1.0 - frac) * nx * ny * nz / vol))
+    s = np.zeros((nz, ny, nx), np.uint8)
+    r = int(np.ceil(radius))
+    off = np.arange(-r, r + 1)
+    d2 = off[:, None, None] ** 2 + off[None, :, None] ** 2 + off[None, None, :] ** 2
+    ball = (d2 <= radius * radius).astype(np.uint8)
+    for c in rng.random((count, 3)) * np.array([nz, ny, nx]):
+        iz, iy, ix = (np.floor(c).astype(int)[:, None] + off[None, :]) % np.array([[nz], [ny], [nx]])
+        s[np.ix_(iz, iy, ix)] |= ball
+    return s.ravel()
+
+
+def kernel_bytes(lat, comps, es, solid=False):
+    """Algorithmic bytes per node of each kernel class (SURVEY.md §8(d));
+    masked geometries add the solid mask (1 B), the per-node direction masks
+    of the F1 stream-collide (4 B) and the M step's solid bits (4 B)."""
     q, D = lat.q, lat.dim
     npi = D * (D + 1) // 2
     nm = 1 + D + npi
     if comps == 1:
         # F1: moments pass + stream-collide; M: one moment-resident pass
-        return {"moments": (q + nm) * es, "streamcoll": (nm + q) * es, "mstep": 2 * nm * es}
+        sb = 1 if solid else 0
+        return {"moments": (q + nm) * es + sb, "streamcoll": (nm + q) * es + 5 * sb, "mstep": 2 * nm * es + 4 * sb}
     return {"cg_moments": (2 * q + 3 + nm) * es, "cg_gradient": (1 + D) * es,
             "cg_streamcoll": (3 + D + npi + D + 2 * q) * es}
 
 
-def step_bytes(lat, comps, es, schedule="f1"):
-    kb = kernel_bytes(lat, comps, es)
+def step_bytes(lat, comps, es, schedule="f1", solid=False):
+    kb = kernel_bytes(lat, comps, es, solid)
     if comps == 1:
         return kb["mstep"] if schedule == "m" else kb["moments"] + kb["streamcoll"]
     return sum(kb.values())
@@ -266,7 +291,12 @@ def main():
     spec = spec_of(T, W["faces"])
     color = T.ColorParams(sigma=W.get("sigma", 0.01), beta=W.get("beta", 0.7)) if W["comps"] == 2 else None
     slab = (rank * nzp, nzp) if world > 1 else None
-    sim = T.DeviceSolver(lat, g, W["omega"], spec, dtype, W["comps"], None, color, dev_id, slab=slab)
+    solid = None
+    if "spheres" in W:
+        if world > 1:
+            raise SystemExit("masked geometries run on whole domains (one GPU)")
+        solid = sphere_pack(dims, *W["spheres"])
+    sim = T.DeviceSolver(lat, g, W["omega"], spec, dtype, W["comps"], solid, color, dev_id, slab=slab)
     if args.math == "f32":
         sim.set_math(_lib.MATH_F32)
     if args.schedule != "auto" and W["comps"] == 1:
@@ -275,6 +305,8 @@ def main():
         # Poiseuille: u_max = F H^2 / (8 nu), H = ny (halfway bounce-back)
         nu = (1.0 / W["omega"] - 0.5) / 3.0
         sim.set_body_force(8.0 * nu * W["umax"] / float(ny) ** 2, 0.0, 0.0)
+    if "force" in W:
+        sim.set_body_force(*W["force"])
     if world > 1:
         import ctypes as C
         uid = (C.c_char * 128)()
@@ -320,7 +352,8 @@ def main():
 
     # roofline of the dominant kernel: algorithmic bytes per launch / mean
     # launch duration (CUDA events on the solver stream, timed region)
-    per_node = kernel_bytes(lat, W["comps"], es)
+    masked = solid is not None
+    per_node = kernel_bytes(lat, W["comps"], es, masked)
     if W["comps"] == 2 and "cg_gradient" not in prof:
         # gradient folded into the recolouring stream-collide: it reads phi
         # (its stencil from cache) instead of the stored gradient
@@ -332,12 +365,12 @@ def main():
     achieved = per_node[dom] * local_nodes / (k_ms / k_n / 1e3) / 1e9
     hbm, peak_kind, _ = peaks()
     sched = sim.schedule if W["comps"] == 1 else "f1"
-    sb = step_bytes(lat, W["comps"], es, sched) if W["comps"] == 1 else sum(per_node.values())
+    sb = step_bytes(lat, W["comps"], es, sched, masked) if W["comps"] == 1 else sum(per_node.values())
     step_bw = glups * sb / world  # per-GPU GB/s of the whole step
     traffic, tsrc, limiter, fp64_ops = None, None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            tr = json.load(fh).get(f"{lat.name}/{W['storage']}/{dom}")
+            tr = None if masked else json.load(fh).get(f"{lat.name}/{W['storage']}/{dom}")
         if tr:
             traffic, tsrc = round(tr["bytes_per_node"] * local_nodes / 1e9, 3), tr["source"]
             limiter = tr.get("limiter")
@@ -363,7 +396,7 @@ def main():
     if W["comps"] == 1:
         # the F1 schedule's ceiling: every population through HBM twice
         # (census bytes, bench.hpp:62-63); M beats it by moving fewer bytes
-        f1b = kernel_bytes(lat, 1, es)["moments"] + kernel_bytes(lat, 1, es)["streamcoll"]
+        f1b = kernel_bytes(lat, 1, es, masked)["moments"] + kernel_bytes(lat, 1, es, masked)["streamcoll"]
         roof["f1_bytes_per_lu"] = f1b
         roof["f1_roofline_glups"] = round(hbm / f1b, 3)
         roof["vs_f1_roofline"] = round(glups / world / (hbm / f1b), 4)
@@ -391,6 +424,7 @@ def main():
                "config": {"workload": W["desc"].format(n=n_desc) + (" per GPU" if lat.dim == 3 else "")
                           + (f" (global {nx}x{ny}x{nz_g}, z slabs)" if world > 1 else ""),
                           "lattice": lat.name, "nodes": nodes, "storage": W["storage"],
+                          **({"solid_fraction": round(float(solid.mean()), 4)} if masked else {}),
                           "node_math": (args.math if W["comps"] == 1 else W["storage"] + " (as the reference)"),
                           "schedule": ({"m": "M: moment-resident single pass (populations rebuilt in shared "
                                              "memory; f materialised on read)",

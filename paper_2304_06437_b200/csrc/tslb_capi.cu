@@ -134,6 +134,7 @@ struct tslb_cuda_sim {
   uint8_t* flag = nullptr;
   uint8_t* solid = nullptr;
   uint32_t* slow = nullptr;
+  uint32_t* sbits = nullptr;  // M on a masked geometry: per-node solid bits
   void* scratch = nullptr;
   double* red = nullptr;  // partials + outputs
   uint64_t* dig = nullptr;
@@ -310,7 +311,7 @@ int ph_mstep(tslb_cuda_sim* h, cudaStream_t st, int c0 = 0, int n = 0) {
     using T = decltype(z);
     return launch_mstep<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<const T*>(h->mo),
                            static_cast<const T*>(h->gm), static_cast<T*>(h->mo2), h->omega, h->lz, c0, n,
-                           h->mmaps, st);
+                           h->mmaps, h->sbits, st);
   });
   if (rc) return set_err(TSLB_ESTATE, "M step not supported for this domain");
   return 0;
@@ -864,16 +865,24 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
     // cannot hold it (e.g. D3Q27 1024^3 fp32) the solver stays on F1
     if (!(e && !std::strcmp(e, "f1"))) {
       const size_t gb = decomposed ? size_t(d.plane) * 2 * (1 + h->dim + h->np) * h->esz : 0;
+      // masked geometries: 4 B of solid bits per node (mstep_supported keeps
+      // them off slabs)
+      const size_t sb = d.has_solid ? size_t(d.mstride) * 4 : 0;
       if (cudaMalloc(&h->mo2, mbytes) == cudaSuccess &&
-          (!gb || cudaMalloc(&h->gm, gb) == cudaSuccess)) {
-        h->bytes += mbytes + gb;
+          (!gb || cudaMalloc(&h->gm, gb) == cudaSuccess) &&
+          (!sb || cudaMalloc(reinterpret_cast<void**>(&h->sbits), sb) == cudaSuccess)) {
+        h->bytes += mbytes + gb + sb;
         CK(cudaMemsetAsync(h->mo2, 0, mbytes, h->s));
         if (gb) CK(cudaMemsetAsync(h->gm, 0, gb, h->s));
+        if (sb && launch_solid_bits(lattice, d, h->solid, h->sbits, h->s))
+          return fail(set_err(TSLB_ECUDA, "solid bits: launch failed"));
         h->sched = TSLB_SCHED_M;
       } else {
         cudaGetLastError();  // clear the allocation failure
         if (h->mo2) cudaFree(h->mo2);
+        if (h->gm) cudaFree(h->gm);
         h->mo2 = nullptr;
+        h->gm = nullptr;
       }
     }
   }
@@ -978,7 +987,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   if (h->cs) cudaStreamSynchronize(h->cs);
   if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
   void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->phig, h->two, h->flag, h->solid, h->slow,
-                  h->scratch, h->red, h->dig, h->recv_lo, h->recv_hi};
+                  h->sbits, h->scratch, h->red, h->dig, h->recv_lo, h->recv_hi};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -1012,8 +1021,8 @@ int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
   if (schedule == TSLB_SCHED_M) {
     if (h->comps != 1 || !mstep_supported(h->lat, h->d))
       return set_err(TSLB_EINVAL,
-                     "M schedule needs a single-fluid D3Q19/D3Q27 box without solids, "
-                     "nx %% 32 == 0 and ny %% 8 == 0");
+                     "M schedule needs a single-fluid D3Q19/D3Q27 domain with nx %% 32 == 0 "
+                     "and ny %% 8 == 0 (or D2Q9 without solids); solid masks only on whole domains");
     if (!h->mo2) {
       const size_t mbytes = size_t(h->d.mstride) * (1 + h->dim + h->np) * h->esz;
       if (int rc = alloc(h, &h->mo2, mbytes)) return rc;
@@ -1022,6 +1031,11 @@ int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
       const size_t gb = size_t(h->plane()) * 2 * (1 + h->dim + h->np) * h->esz;
       if (int rc = alloc(h, &h->gm, gb)) return rc;
       CK(cudaMemsetAsync(h->gm, 0, gb, h->s));
+    }
+    if (h->d.has_solid && !h->sbits) {
+      if (int rc = alloc(h, reinterpret_cast<void**>(&h->sbits), size_t(h->d.mstride) * 4)) return rc;
+      if (launch_solid_bits(h->lat, h->d, h->solid, h->sbits, h->s))
+        return set_err(TSLB_ECUDA, "solid bits: launch failed");
     }
   } else {
     if (int rc = materialize(h)) return rc;

@@ -51,7 +51,9 @@ bool mstep_supported(int lat, const Dom& d);
 int mstep_chunks(const Dom& d, int lz);
 template <typename T>
 int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
-                 int lz, int chunk0, int nchunks, MstepMaps*& maps, cudaStream_t st);
+                 int lz, int chunk0, int nchunks, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st);
+// per-node solid bits of a masked geometry for the 3-D M step (tslb_mstep.cu)
+int launch_solid_bits(int lat, const Dom& d, const uint8_t* solid, uint32_t* bits, cudaStream_t st);
 // D2Q9 form of the M step (tslb_mstep2d.cu; launched through launch_mstep)
 template <typename T>
 int launch_mstep2d(int math, const Dom& d, const T* mi, T* mo, double omega, cudaStream_t st);

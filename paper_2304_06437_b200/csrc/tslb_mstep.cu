@@ -115,15 +115,19 @@ __host__ __device__ constexpr int n_moments() {
 __host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) / 128 * 128; }
 
 // dynamic shared memory: [tile buf 0 | tile buf 1 | wstg 0 | wstg 1 | slots | mbarriers]
-template <class L, typename T>
+template <class L, typename T, bool SOLID = false>
 struct Smem {
   static constexpr size_t tile = align128(size_t(n_moments<L>()) * TC * sizeof(T));
   // one copy of the ring per halo task half (see push_ring)
   static constexpr size_t wstg = align128(size_t(n_moments<L>()) * 2 * NH * sizeof(T));
   static constexpr size_t slots = size_t(slot_planes<L>()) * NT * sizeof(T);
+  // solid geometries: the per-node solid bits of the tile and of the halo
+  // ring (cp.async, double buffered) -- [2][NT + 2 NH] u32
+  static constexpr size_t bits = SOLID ? align128(size_t(2) * (NT + 2 * NH) * 4) : 0;
   static constexpr size_t off_wstg = 2 * tile;
   static constexpr size_t off_slots = off_wstg + 2 * wstg;
-  static constexpr size_t off_bar = align128(off_slots + slots);
+  static constexpr size_t off_bits = align128(off_slots + slots);
+  static constexpr size_t off_bar = align128(off_bits + bits);
   static constexpr size_t total = off_bar + 2 * sizeof(uint64_t);
 };
 
@@ -278,26 +282,42 @@ __device__ __forceinline__ NodeMoments<C> node_at(const T* s, int stride) {
                          C(v[9]));
 }
 
-// per-thread wall contact of the tile node (only for WALLS kernels)
+// per-thread wall contact of the tile node (only for WALLS kernels) and,
+// for solid geometries, its solid bits (bit a: the push target of
+// direction a is solid; bit 31: the node itself is solid)
 struct Contact {
   bool xlo, xhi, ylo, yhi, zlo, zhi;
+  uint32_t sb;
 };
+constexpr uint32_t kSelfSolid = 1u << 31;
 
 // Output of direction A from a tile node: bounce into its own opposite slot
 // or push into the slot of the destination (dropped if outside the tile).
-template <class L, int A, typename T, typename C, bool WALLS, int ZC>
+template <class L, int A, typename T, typename C, bool WALLS, bool SOLID, int ZC>
 __device__ __forceinline__ void emit(const Dom& d, const Ring<L, T>& rg, T (&R)[L::q][3],
                                      int lx, int ly, const Contact& ct, T o) {
   using dd = Dir<L, A>;
-  if constexpr (WALLS && ZC == 0) {
-    const bool cx = (dd::x == 1 && ct.xhi) || (dd::x == -1 && ct.xlo);
-    const bool cy = (dd::y == 1 && ct.yhi) || (dd::y == -1 && ct.ylo);
-    const bool cz = (dd::z == 1 && ct.zhi) || (dd::z == -1 && ct.zlo);
-    if (cx || cy || cz) {
+  if constexpr ((WALLS || SOLID) && ZC == 0) {
+    // wall faces crossed (resolve_push, boundary.hpp:118-144), else a solid
+    // target: both bounce into the node's own opposite slot
+    const bool cx = WALLS && ((dd::x == 1 && ct.xhi) || (dd::x == -1 && ct.xlo));
+    const bool cy = WALLS && ((dd::y == 1 && ct.yhi) || (dd::y == -1 && ct.ylo));
+    const bool cz = WALLS && ((dd::z == 1 && ct.zhi) || (dd::z == -1 && ct.zlo));
+    if (cx || cy || cz) {  // (spatially coherent: a branch)
       const T b = bounce_value<L, A, T, C>(d, o, cx, cy, cz);
       if constexpr (is_reg<L>(dd::opp)) R[dd::opp][1] = b;
       else Shm<T>::template st<slot_off<L, dd::opp, 0, 0, T>()>(ring_addr<L, dd::opp, 0>(rg), b);
       return;
+    }
+    if constexpr (SOLID) {
+      // solid target, no wall crossed: the bounce is o itself (the wall
+      // correction of u_w = 0 is +0 and o - (+0) == o for every o). The
+      // scattered pattern is handled without branches: a predicated store
+      // into the own opposite slot, and the regular push below also runs
+      // (it lands in the solid target's slot, which is never reduced)
+      const bool cs = (ct.sb >> A) & 1u;
+      if constexpr (is_reg<L>(dd::opp)) R[dd::opp][1] = cs ? o : R[dd::opp][1];
+      else Shm<T>::template st_if<slot_off<L, dd::opp, 0, 0, T>()>(ring_addr<L, dd::opp, 0>(rg), o, cs);
     }
   }
   if constexpr (is_reg<L>(A)) {
@@ -317,26 +337,26 @@ __device__ __forceinline__ void emit(const Dom& d, const Ring<L, T>& rg, T (&R)[
 
 // All directions of a tile node; ZC != 0 (a plane just outside the march)
 // keeps only the directions with c_z == ZC.
-template <class L, typename T, typename C, bool WALLS, int ZC>
+template <class L, typename T, typename C, bool WALLS, bool SOLID, int ZC>
 __device__ __forceinline__ void push_tile(const Dom& d, const Ring<L, T>& rg, T (&R)[L::q][3],
                                           int lx, int ly, const Contact& ct,
                                           const NodeMoments<C>& m, C om1) {
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
     if constexpr (a == 0) {
-      if constexpr (ZC == 0) emit<L, 0, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, T(post_rest<L, C>(m, om1)));
+      if constexpr (ZC == 0) emit<L, 0, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(post_rest<L, C>(m, om1)));
     } else if constexpr (a & 1) {
       constexpr bool ua = ZC == 0 || Dir<L, a>::z == ZC;
       constexpr bool ub = ZC == 0 || Dir<L, a + 1>::z == ZC;
       if constexpr (ua && ub) {
         C ra, rb;
         post_pair<L, a, C>(m, om1, ra, rb);
-        emit<L, a, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, T(ra));
-        emit<L, a + 1, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, T(rb));
+        emit<L, a, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(ra));
+        emit<L, a + 1, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(rb));
       } else if constexpr (ua) {
-        emit<L, a, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, T(post_single<L, a, C>(m, om1)));
+        emit<L, a, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(post_single<L, a, C>(m, om1)));
       } else if constexpr (ub) {
-        emit<L, a + 1, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, T(post_single<L, a + 1, C>(m, om1)));
+        emit<L, a + 1, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(post_single<L, a + 1, C>(m, om1)));
       }
     }
   });
@@ -440,18 +460,21 @@ __device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, con
   mo[9 * ms + idx] = T(pyz - jy * jz);
 }
 
-template <class L, typename T, typename C, bool WALLS, int MINB>
+template <class L, typename T, typename C, bool WALLS, bool SOLID, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
     k_mstep(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap, Dom d,
-            const T* __restrict__ mi, const T* __restrict__ gm, T* __restrict__ mo, C om1, int lz, int zc0) {
+            const T* __restrict__ mi, const T* __restrict__ gm, T* __restrict__ mo, C om1, int lz, int zc0,
+            const uint32_t* __restrict__ sbits) {
   static_assert(L::dim == 3, "the M step is 3-D");
-  using SM = Smem<L, T>;
+  using SM = Smem<L, T, SOLID>;
   constexpr int NM = n_moments<L>();
   extern __shared__ __align__(128) unsigned char smraw[];
   T* tile = reinterpret_cast<T*>(smraw);                  // [2][NM][TR][TX]
   T* wstg = reinterpret_cast<T*>(smraw + SM::off_wstg);   // [2][NM][2 NH]
   T* sl = reinterpret_cast<T*>(smraw + SM::off_slots);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + SM::off_bar);
+  uint32_t* bstg = reinterpret_cast<uint32_t*>(smraw + SM::off_bits);  // [2][NT + 2 NH]
+  constexpr int BITS_B = NT + 2 * NH;
   constexpr int TILE_B = int(SM::tile / sizeof(T)), WSTG_B = int(SM::wstg / sizeof(T));
 
   const int tid = threadIdx.x, lx = tid & (TX - 1), ly = tid >> 5;
@@ -529,6 +552,11 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
       for (int c = 0; c < NM; ++c) __pipeline_memcpy_async(w + c * WH, g + c * cs, sizeof(T));
     }
+    if constexpr (SOLID) {  // (solid geometries never run on slabs: src == 1)
+      const uint32_t* gb = sbits + int64_t(zz) * d.plane;
+      __pipeline_memcpy_async(bstg + b * BITS_B + tid, gb + col, 4);
+      if (hnode >= 0) __pipeline_memcpy_async(bstg + b * BITS_B + NT + half * NH + hnode, gb + hcol, 4);
+    }
   };
 
   T R[L::q][3];
@@ -538,6 +566,7 @@ __global__ void __launch_bounds__(NT, MINB)
   rg.init(smem_u32(sl + ly * TX + lx));
   int buf = 0;
   uint32_t phase = 0;  // bit b: parity of the next completion of bar[b]
+  bool solid_prev = false;  // the tile node of the plane being reduced is solid
 
   auto plane = [&](auto ZCc, int z) {
     constexpr int ZC = decltype(ZCc)::value;
@@ -553,16 +582,35 @@ __global__ void __launch_bounds__(NT, MINB)
         ct.zlo = z == 0 && d.mode[ZMin] == kWall;
         ct.zhi = z == d.nz - 1 && d.mode[ZMax] == kWall;
       }
-      const NodeMoments<C> m = node_at<L, T, C>(tb + (ly + 1) * TX + lx, TC);
-      push_tile<L, T, C, WALLS, ZC>(d, rg, R, lx, ly, ct, m, om1);
-      if (hnode >= 0) {
+      bool solid = false, hsolid = false;
+      if constexpr (SOLID) {
+        ct.sb = bstg[buf * BITS_B + tid];
+        solid = (ct.sb & kSelfSolid) != 0;
+        hsolid = hnode >= 0 && (bstg[buf * BITS_B + NT + half * NH + hnode] & kSelfSolid);
+        // solid nodes push nothing (stream_collide skips them); their moment
+        // arrays keep their values (compute_moments skips them too), carried
+        // into the output buffer of the ping-pong pair here
+        if (ZC == 0 && solid) {
+#pragma unroll
+          for (int c = 0; c < NM; ++c)
+            mo[c * d.mstride + col + int64_t(z) * d.plane] = tb[c * TC + (ly + 1) * TX + lx];
+        }
+      }
+      if (!solid) {
+        const NodeMoments<C> m = node_at<L, T, C>(tb + (ly + 1) * TX + lx, TC);
+        push_tile<L, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, m, om1);
+      }
+      if (hnode >= 0 && !hsolid) {
         const T* hb = (hfetch ? wstg + buf * WSTG_B : tb) + hoff;
         const NodeMoments<C> hm = node_at<L, T, C>(hb, hstride);
         push_ring<L, T, C, ZC>(rg, hdelta, ly, hx, hy, hm, om1);
       }
     }
     __syncthreads();
-    if (z - 1 >= za) finalize<L, T, C>(d, rg, R, mo, col + int64_t(z - 1) * d.plane);
+    // compute_moments skips solid nodes (their moment arrays keep their values)
+    if (z - 1 >= za && !(SOLID && solid_prev))
+      finalize<L, T, C>(d, rg, R, mo, col + int64_t(z - 1) * d.plane);
+    if constexpr (SOLID) solid_prev = (ct.sb & kSelfSolid) != 0;  // (ct.sb: plane z)
     if constexpr (L::rd == 0) __syncthreads();
 #pragma unroll
     for (int a = 0; a < L::q; ++a) {
@@ -668,12 +716,53 @@ __global__ void __launch_bounds__(128) k_ghost_push(Dom d, T* __restrict__ f, co
   });
 }
 
+// Solid bits of every node for the M step on a masked geometry: bit a set
+// when the push of direction a crosses no wall face and its (wrapped) target
+// is solid -- the bounce case resolve_push adds for solids
+// (boundary.hpp:118-144); bit 31 when the node itself is solid.
+template <class L>
+__global__ void __launch_bounds__(128)
+    k_solid_bits(Dom d, const uint8_t* __restrict__ solid, uint32_t* __restrict__ bits) {
+  const int i = int(blockIdx.x) * 128 + int(threadIdx.x), j = int(blockIdx.y), k = int(blockIdx.z);
+  if (i >= d.nx) return;
+  const int nd[3] = {d.nx, d.ny, d.nz};
+  uint32_t b = solid[fidx(d, i, j, k)] ? kSelfSolid : 0u;
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    if constexpr (a > 0) {
+      using dd = Dir<L, a>;
+      int tc[3] = {i + dd::x, j + dd::y, k + dd::z};
+      bool wall = false;
+#pragma unroll
+      for (int ax = 0; ax < 3; ++ax) {
+        if (tc[ax] < 0 || tc[ax] >= nd[ax]) {
+          const int m = d.mode[2 * ax + (tc[ax] < 0 ? 0 : 1)];
+          if (m == kWrap) tc[ax] += tc[ax] < 0 ? nd[ax] : -nd[ax];
+          else wall = true;
+        }
+      }
+      if (!wall && solid[fidx(d, tc[0], tc[1], tc[2])]) b |= 1u << a;
+    }
+  });
+  bits[midx(d, i, j, k)] = b;
+}
+
 }  // namespace mstep
 
 bool mstep_supported(int lat, const Dom& d) {
   if (lat == kD2Q9) return !d.has_solid && d.nz == 1 && d.ghost == 0;  // tslb_mstep2d.cu
-  return (lat == kD3Q19 || lat == kD3Q27) && !d.has_solid && d.nx % mstep::TX == 0 &&
+  return (lat == kD3Q19 || lat == kD3Q27) && (!d.has_solid || d.ghost == 0) && d.nx % mstep::TX == 0 &&
          d.ny % mstep::TY == 0 && mstep::encoder() != nullptr;
+}
+
+int launch_solid_bits(int lat, const Dom& d, const uint8_t* solid, uint32_t* bits, cudaStream_t st) {
+  using namespace mstep;
+  if (d.nz > 65535 || d.ny > 65535) return 1;
+  const dim3 grid(unsigned((d.nx + 127) / 128), unsigned(d.ny), unsigned(d.nz));
+  if (lat == kD3Q19) k_solid_bits<D3Q19><<<grid, 128, 0, st>>>(d, solid, bits);
+  else if (lat == kD3Q27) k_solid_bits<D3Q27><<<grid, 128, 0, st>>>(d, solid, bits);
+  else return 1;
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 int mstep_chunks(const Dom& d, int lz) {
@@ -701,9 +790,10 @@ int launch_ghost_push(int lat, int math, const Dom& d, T* f, const T* gm, double
 
 template <typename T>
 int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
-                 int lz, int chunk0, int nchunks, MstepMaps*& maps, cudaStream_t st) {
+                 int lz, int chunk0, int nchunks, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st) {
   using namespace mstep;
   if (!mstep_supported(lat, d)) return 1;
+  if (d.has_solid && !sbits) return 1;
   if (lat == kD2Q9) return chunk0 == 0 ? launch_mstep2d<T>(math, d, mi, mo, omega, st) : 1;
   if ((d.mode[ZMin] == kGhost || d.mode[ZMax] == kGhost) && !gm) return 1;
   if (lz <= 0) lz = kDefaultLz;
@@ -733,23 +823,27 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
     if (!tm) return 1;
     const CUtensorMap* gmp = gm ? tensor_map<T>(maps, d, n_moments<Lat>(), gm, true) : tm;
     if (!gmp) return 1;
-    constexpr size_t smem = Smem<Lat, T>::total;
-    if (smem > 227 * 1024) return 1;
-    auto go = [&](auto kern, auto om1) {
+    auto go = [&](auto kern, auto om1, size_t smem) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      kern<<<grid, NT, smem, st>>>(*tm, *gmp, d, mi, gm, mo, om1, lz, chunk0);
+      kern<<<grid, NT, smem, st>>>(*tm, *gmp, d, mi, gm, mo, om1, lz, chunk0, sbits);
     };
+    constexpr size_t sm0 = Smem<Lat, T, false>::total, sm1 = Smem<Lat, T, true>::total;
+    if ((d.has_solid ? sm1 : sm0) > 227 * 1024) return 1;
     // fp32 storage + fp32 math: three CTAs per SM (~76 KB shared memory, <= 80
     // registers); fp64 math keeps two (capping it at 80 registers costs more
     // ILP than the third CTA buys); fp64 storage holds one CTA per SM
     constexpr int MB = sizeof(T) == 4 && Lat::rd == 0 ? 3 : sizeof(T) == 4 ? 2 : 1;
     constexpr int MBD = sizeof(T) == 4 ? 2 : 1;
     if (math == kMathDouble) {
-      if (walls) go(k_mstep<Lat, T, double, true, MBD>, om1d);
-      else go(k_mstep<Lat, T, double, false, MBD>, om1d);
+      if (d.has_solid && walls) go(k_mstep<Lat, T, double, true, true, MBD>, om1d, sm1);
+      else if (d.has_solid) go(k_mstep<Lat, T, double, false, true, MBD>, om1d, sm1);
+      else if (walls) go(k_mstep<Lat, T, double, true, false, MBD>, om1d, sm0);
+      else go(k_mstep<Lat, T, double, false, false, MBD>, om1d, sm0);
     } else {
-      if (walls) go(k_mstep<Lat, T, float, true, MB>, om1f);
-      else go(k_mstep<Lat, T, float, false, MB>, om1f);
+      if (d.has_solid && walls) go(k_mstep<Lat, T, float, true, true, MB>, om1f, sm1);
+      else if (d.has_solid) go(k_mstep<Lat, T, float, false, true, MB>, om1f, sm1);
+      else if (walls) go(k_mstep<Lat, T, float, true, false, MB>, om1f, sm0);
+      else go(k_mstep<Lat, T, float, false, false, MB>, om1f, sm0);
     }
     return 0;
   };
@@ -761,9 +855,9 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
 }
 
 template int launch_mstep<float>(int, int, const Dom&, const float*, const float*, float*, double, int, int,
-                                 int, MstepMaps*&, cudaStream_t);
+                                 int, MstepMaps*&, const uint32_t*, cudaStream_t);
 template int launch_mstep<double>(int, int, const Dom&, const double*, const double*, double*, double, int, int,
-                                  int, MstepMaps*&, cudaStream_t);
+                                  int, MstepMaps*&, const uint32_t*, cudaStream_t);
 template int launch_ghost_push<float>(int, int, const Dom&, float*, const float*, double, int, cudaStream_t);
 template int launch_ghost_push<double>(int, int, const Dom&, double*, const double*, double, int, cudaStream_t);
 

@@ -11,7 +11,7 @@ from oracle import oracle as O
 from paper_2304_06437_b200 import _lib
 from paper_2304_06437_b200 import tslb as T
 
-from helpers import assert_bitwise, corner_box_3d, spec_of, zwalls_3d
+from helpers import assert_bitwise, block_solid, corner_box_3d, random_solid, spec_of, zwalls_3d
 
 pytestmark = pytest.mark.gpu
 
@@ -430,3 +430,76 @@ def test_mstep2d_f32_math_equals_f1(gpu):
             dev.close()
     assert_bitwise(out["m"][0], out["f1"][0], "2-D f32 math f")
     assert_bitwise(out["m"][1], out["f1"][1], "2-D f32 math moments")
+
+
+# -- masked geometries (solid bits, tslb_mstep.cu k_solid_bits) --------------
+SOLID_CASES = [
+    ("periodic+random", (32, 8, 6), O.periodic(), lambda d: random_solid(d, 0.12, 3)),
+    ("box+random", (32, 16, 7), O.closed_box(), lambda d: random_solid(d, 0.08, 9)),
+    ("corners+block", (64, 8, 5), corner_box_3d(), lambda d: block_solid(d, (5, 2, 1), (40, 6, 4))),
+    ("zwalls+dense", (32, 8, 9), zwalls_3d(), lambda d: random_solid(d, 0.45, 21)),
+]
+
+
+@pytest.mark.parametrize("lz", ["", "2"])
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("lat", ["d3q19", "d3q27"])
+@pytest.mark.parametrize("case", SOLID_CASES, ids=lambda c: c[0])
+def test_mstep_solid_bitwise(gpu, oracle_port, case, lat, dtype, lz, monkeypatch):
+    """M on a solid mask: fluid nodes bit-identical to the oracle; every node
+    (solid ones included: moments carried through, f untouched) identical to
+    the F1 schedule."""
+    name, dims, faces, mk = case
+    if lz:
+        monkeypatch.setenv("TSLB_LZ", lz)
+    solid = mk(dims)
+    f0 = O.random_state(lat, dims, 17, dtype, solid)
+    steps = 5
+    out = {}
+    for sched in ("m", "f1"):
+        dev = T.DeviceSolver(lat, T.GridDims(*dims), 0.93, spec_of(faces), dtype, 1, solid)
+        try:
+            if sched == "m":
+                assert dev.schedule == "m", "M should be the default on a masked whole domain"
+            dev.set_schedule(sched)
+            dev.upload_f(f0)
+            dev.step(steps)
+            out[sched] = (dev.download_f(), _moments(dev, lat))
+        finally:
+            dev.close()
+    fo, mo = f0.copy(), np.zeros((O.moments_layout(lat), f0.shape[1]), dtype)
+    oracle_port.single_run(lat, dims, 0.93, faces, fo, mo, steps, 0, solid)
+    fluid = solid == 0
+    assert_bitwise(out["m"][0], fo, f"M {lat}/{name} f", fluid)
+    assert_bitwise(out["m"][1], mo, f"M {lat}/{name} moments", fluid)
+    assert_bitwise(out["m"][0], out["f1"][0], f"M vs F1 {lat}/{name} f (all nodes)")
+    assert_bitwise(out["m"][1], out["f1"][1], f"M vs F1 {lat}/{name} moments (all nodes)")
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_mstep_solid_graph_and_switch(gpu, oracle_port, dtype):
+    """Graph replay (odd step counts) and F1 <-> M switches on a masked
+    domain, with the solid bits built on the switch."""
+    lat, dims, faces = "d3q19", (32, 16, 10), O.closed_box()
+    solid = random_solid(dims, 0.15, 77)
+    f0 = O.random_state(lat, dims, 8, dtype, solid)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.2, spec_of(faces), dtype, 1, solid)
+    try:
+        dev.set_schedule("f1")
+        dev.upload_f(f0)
+        dev.step(3)
+        dev.set_schedule("m")
+        dev.step(37)
+        dev.set_schedule("f1")
+        dev.step(2)
+        dev.set_schedule("m")
+        dev.step(33)
+        mg = _moments(dev, lat)
+        fg = dev.download_f()
+    finally:
+        dev.close()
+    fo, mo = f0.copy(), np.zeros((O.moments_layout(lat), f0.shape[1]), dtype)
+    oracle_port.single_run(lat, dims, 1.2, faces, fo, mo, 75, 0, solid)
+    fluid = solid == 0
+    assert_bitwise(fg, fo, "switch/graph M f", fluid)
+    assert_bitwise(mg, mo, "switch/graph M moments", fluid)
