@@ -134,7 +134,7 @@ struct tslb_cuda_sim {
   uint8_t* flag = nullptr;
   uint8_t* solid = nullptr;
   uint32_t* slow = nullptr;
-  uint32_t* sbits = nullptr;  // M on a masked geometry: per-node solid bits
+  uint32_t* sbits = nullptr;  // M on a masked geometry: per-node solid bits (with ghost planes)
   void* scratch = nullptr;
   double* red = nullptr;  // partials + outputs
   uint64_t* dig = nullptr;
@@ -311,7 +311,7 @@ int ph_mstep(tslb_cuda_sim* h, cudaStream_t st, int c0 = 0, int n = 0) {
     using T = decltype(z);
     return launch_mstep<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<const T*>(h->mo),
                            static_cast<const T*>(h->gm), static_cast<T*>(h->mo2), h->omega, h->lz, c0, n,
-                           h->mmaps, h->sbits, st);
+                           h->mmaps, h->sbits ? h->sbits + size_t(h->d.ghost) * h->plane() : nullptr, st);
   });
   if (rc) return set_err(TSLB_ESTATE, "M step not supported for this domain");
   return 0;
@@ -395,7 +395,8 @@ int materialize(tslb_cuda_sim* h) {
       if (h->d.mode[side ? ZMax : ZMin] != kGhost) continue;
       ++h->launches;
       if (launch_ghost_push<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
-                               static_cast<const T*>(h->gm), h->omega, side, h->s))
+                               static_cast<const T*>(h->gm), h->omega, side,
+                               h->d.has_solid ? h->solid : nullptr, h->s))
         return set_err(TSLB_ESTATE, "ghost push: bad lattice");
     }
     return 0;
@@ -865,9 +866,8 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
     // cannot hold it (e.g. D3Q27 1024^3 fp32) the solver stays on F1
     if (!(e && !std::strcmp(e, "f1"))) {
       const size_t gb = decomposed ? size_t(d.plane) * 2 * (1 + h->dim + h->np) * h->esz : 0;
-      // masked geometries: 4 B of solid bits per node (mstep_supported keeps
-      // them off slabs)
-      const size_t sb = d.has_solid ? size_t(d.mstride) * 4 : 0;
+      // masked geometries: 4 B of solid bits per node (+ the ghost planes)
+      const size_t sb = d.has_solid ? size_t(d.plane) * (nzl + 2 * d.ghost) * 4 : 0;
       if (cudaMalloc(&h->mo2, mbytes) == cudaSuccess &&
           (!gb || cudaMalloc(&h->gm, gb) == cudaSuccess) &&
           (!sb || cudaMalloc(reinterpret_cast<void**>(&h->sbits), sb) == cudaSuccess)) {
@@ -1033,7 +1033,9 @@ int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
       CK(cudaMemsetAsync(h->gm, 0, gb, h->s));
     }
     if (h->d.has_solid && !h->sbits) {
-      if (int rc = alloc(h, reinterpret_cast<void**>(&h->sbits), size_t(h->d.mstride) * 4)) return rc;
+      if (int rc = alloc(h, reinterpret_cast<void**>(&h->sbits),
+                         size_t(h->plane()) * (h->nzl + 2 * h->d.ghost) * 4))
+        return rc;
       if (launch_solid_bits(h->lat, h->d, h->solid, h->sbits, h->s))
         return set_err(TSLB_ECUDA, "solid bits: launch failed");
     }

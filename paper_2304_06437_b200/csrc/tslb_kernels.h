@@ -61,7 +61,7 @@ int launch_mstep2d(int math, const Dom& d, const T* mi, T* mo, double omega, cud
 // 1 above) rebuilt from the ghost moments
 template <typename T>
 int launch_ghost_push(int lat, int math, const Dom& d, T* f, const T* gm, double omega, int side,
-                      cudaStream_t st);
+                      const uint8_t* solid, cudaStream_t st);
 template <typename T>
 int launch_collide(int lat, const Dom& d, T* f, const T* mo,
                    const uint8_t* solid, double omega, cudaStream_t st);

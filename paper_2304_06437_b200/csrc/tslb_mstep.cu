@@ -552,8 +552,8 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll
       for (int c = 0; c < NM; ++c) __pipeline_memcpy_async(w + c * WH, g + c * cs, sizeof(T));
     }
-    if constexpr (SOLID) {  // (solid geometries never run on slabs: src == 1)
-      const uint32_t* gb = sbits + int64_t(zz) * d.plane;
+    if constexpr (SOLID) {  // sbits points at plane 0; slab ghost planes at z = -1, nz
+      const uint32_t* gb = sbits + int64_t(src == 1 ? zz : z) * d.plane;
       __pipeline_memcpy_async(bstg + b * BITS_B + tid, gb + col, 4);
       if (hnode >= 0) __pipeline_memcpy_async(bstg + b * BITS_B + NT + half * NH + hnode, gb + hcol, 4);
     }
@@ -692,12 +692,15 @@ const CUtensorMap* tensor_map(MstepMaps*& maps, const Dom& d, int nm, const T* b
 // sources beyond an x/y wall do not exist (that slot holds the bounce).
 template <class L, typename T, typename C>
 __global__ void __launch_bounds__(128) k_ghost_push(Dom d, T* __restrict__ f, const T* __restrict__ gm,
-                                                    C om1, int side) {
+                                                    C om1, int side, const uint8_t* __restrict__ solid) {
   const int i = int(blockIdx.x) * 128 + int(threadIdx.x), j = int(blockIdx.y);
   if (i >= d.nx) return;
   const int k = side ? d.nz - 1 : 0;
   const int cz_in = side ? -1 : 1;
   const T* g = gm + int64_t(side) * d.plane;
+  // masked geometries: a solid node keeps its populations, a solid source
+  // pushes nothing (that slot holds the node's own bounce)
+  if (solid && solid[fidx(d, i, j, k)]) return;
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
     using dd = Dir<L, a>;
@@ -706,6 +709,7 @@ __global__ void __launch_bounds__(128) k_ghost_push(Dom d, T* __restrict__ f, co
       const int sx = wrap_coord(i - dd::x, d.nx, d.mode[XMin], d.mode[XMax]);
       const int sy = wrap_coord(j - dd::y, d.ny, d.mode[YMin], d.mode[YMax]);
       if (sx < 0 || sy < 0) return;
+      if (solid && solid[fidx(d, sx, sy, k - dd::z)]) return;
       const T* p = g + sx + int64_t(d.nx) * sy;
       const int64_t cs = 2 * d.plane;
       const NodeMoments<C> m = prepare_node<C>(C(p[0]), C(p[cs]), C(p[2 * cs]), C(p[3 * cs]), C(p[4 * cs]),
@@ -719,15 +723,19 @@ __global__ void __launch_bounds__(128) k_ghost_push(Dom d, T* __restrict__ f, co
 // Solid bits of every node for the M step on a masked geometry: bit a set
 // when the push of direction a crosses no wall face and its (wrapped) target
 // is solid -- the bounce case resolve_push adds for solids
-// (boundary.hpp:118-144); bit 31 when the node itself is solid.
+// (boundary.hpp:118-144); bit 31 when the node itself is solid. On z slabs
+// `bits` has the ghost planes too (index (k + ghost) plane + ...): their
+// nodes are halo sources of the M step, only their own bit is used; a push
+// across a slab face targets the ghost plane of the mask.
 template <class L>
 __global__ void __launch_bounds__(128)
     k_solid_bits(Dom d, const uint8_t* __restrict__ solid, uint32_t* __restrict__ bits) {
-  const int i = int(blockIdx.x) * 128 + int(threadIdx.x), j = int(blockIdx.y), k = int(blockIdx.z);
+  const int i = int(blockIdx.x) * 128 + int(threadIdx.x), j = int(blockIdx.y);
+  const int k = int(blockIdx.z) - d.ghost;
   if (i >= d.nx) return;
   const int nd[3] = {d.nx, d.ny, d.nz};
   uint32_t b = solid[fidx(d, i, j, k)] ? kSelfSolid : 0u;
-  unroll<L::q>([&](auto A) {
+  if (k >= 0 && k < d.nz) unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
     if constexpr (a > 0) {
       using dd = Dir<L, a>;
@@ -738,27 +746,27 @@ __global__ void __launch_bounds__(128)
         if (tc[ax] < 0 || tc[ax] >= nd[ax]) {
           const int m = d.mode[2 * ax + (tc[ax] < 0 ? 0 : 1)];
           if (m == kWrap) tc[ax] += tc[ax] < 0 ? nd[ax] : -nd[ax];
-          else wall = true;
+          else if (m == kWall) wall = true;  // (kGhost: the ghost plane)
         }
       }
       if (!wall && solid[fidx(d, tc[0], tc[1], tc[2])]) b |= 1u << a;
     }
   });
-  bits[midx(d, i, j, k)] = b;
+  bits[int64_t(d.nx) * (int64_t(j) + int64_t(d.ny) * (k + d.ghost)) + i] = b;
 }
 
 }  // namespace mstep
 
 bool mstep_supported(int lat, const Dom& d) {
   if (lat == kD2Q9) return !d.has_solid && d.nz == 1 && d.ghost == 0;  // tslb_mstep2d.cu
-  return (lat == kD3Q19 || lat == kD3Q27) && (!d.has_solid || d.ghost == 0) && d.nx % mstep::TX == 0 &&
+  return (lat == kD3Q19 || lat == kD3Q27) && d.nx % mstep::TX == 0 &&
          d.ny % mstep::TY == 0 && mstep::encoder() != nullptr;
 }
 
 int launch_solid_bits(int lat, const Dom& d, const uint8_t* solid, uint32_t* bits, cudaStream_t st) {
   using namespace mstep;
-  if (d.nz > 65535 || d.ny > 65535) return 1;
-  const dim3 grid(unsigned((d.nx + 127) / 128), unsigned(d.ny), unsigned(d.nz));
+  if (d.nz + 2 * d.ghost > 65535 || d.ny > 65535) return 1;
+  const dim3 grid(unsigned((d.nx + 127) / 128), unsigned(d.ny), unsigned(d.nz + 2 * d.ghost));
   if (lat == kD3Q19) k_solid_bits<D3Q19><<<grid, 128, 0, st>>>(d, solid, bits);
   else if (lat == kD3Q27) k_solid_bits<D3Q27><<<grid, 128, 0, st>>>(d, solid, bits);
   else return 1;
@@ -772,15 +780,15 @@ int mstep_chunks(const Dom& d, int lz) {
 
 template <typename T>
 int launch_ghost_push(int lat, int math, const Dom& d, T* f, const T* gm, double omega, int side,
-                      cudaStream_t st) {
+                      const uint8_t* solid, cudaStream_t st) {
   using namespace mstep;
   const dim3 grid(unsigned((d.nx + 127) / 128), unsigned(d.ny));
   auto go = [&](auto L) {
     using Lat = decltype(L);
     if (math == kMathDouble)
-      k_ghost_push<Lat, T, double><<<grid, 128, 0, st>>>(d, f, gm, 1.0 - double(T(omega)), side);
+      k_ghost_push<Lat, T, double><<<grid, 128, 0, st>>>(d, f, gm, 1.0 - double(T(omega)), side, solid);
     else
-      k_ghost_push<Lat, T, float><<<grid, 128, 0, st>>>(d, f, gm, 1.0f - float(omega), side);
+      k_ghost_push<Lat, T, float><<<grid, 128, 0, st>>>(d, f, gm, 1.0f - float(omega), side, solid);
     return 0;
   };
   if (lat == kD3Q19) return go(D3Q19{});
@@ -858,7 +866,9 @@ template int launch_mstep<float>(int, int, const Dom&, const float*, const float
                                  int, MstepMaps*&, const uint32_t*, cudaStream_t);
 template int launch_mstep<double>(int, int, const Dom&, const double*, const double*, double*, double, int, int,
                                   int, MstepMaps*&, const uint32_t*, cudaStream_t);
-template int launch_ghost_push<float>(int, int, const Dom&, float*, const float*, double, int, cudaStream_t);
-template int launch_ghost_push<double>(int, int, const Dom&, double*, const double*, double, int, cudaStream_t);
+template int launch_ghost_push<float>(int, int, const Dom&, float*, const float*, double, int, const uint8_t*,
+                                      cudaStream_t);
+template int launch_ghost_push<double>(int, int, const Dom&, double*, const double*, double, int,
+                                       const uint8_t*, cudaStream_t);
 
 }  // namespace tslb_cuda

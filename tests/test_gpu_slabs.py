@@ -223,3 +223,85 @@ def test_two_fluid_nccl_self_exchange(gpu, dtype):
     finally:
         slab.close()
         ref.close()
+
+
+# --- M on masked slabs: solid bits with ghost planes, solid-aware ghost push ---
+@pytest.mark.parametrize("lz", ["", "2"])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("parts", [2, 3, 4])
+@pytest.mark.parametrize("lat,faces,frac", [
+    ("d3q19", O.periodic(), 0.12),
+    ("d3q19", zwalls_3d(), 0.3),
+    ("d3q27", O.closed_box(), 0.1),
+])
+def test_mstep_masked_slabs(gpu, oracle_port, lat, faces, frac, parts, dtype, lz, monkeypatch):
+    """Masked slabs run the M step too: every node (solid ones included)
+    equals the undivided domain under F1, fluid nodes equal the oracle."""
+    if lz:
+        monkeypatch.setenv("TSLB_LZ", lz)
+    dims = (32, 16, 12)
+    solid = random_solid(dims, frac, 41)
+    f0 = O.random_state(lat, dims, 13, dtype, solid)
+    g = T.GridDims(*dims)
+    plane = dims[0] * dims[1]
+    L = T.lattice_of(lat)
+    slabs = [T.DeviceSolver(lat, g, 1.1, spec_of(faces), dtype, 1, solid, slab=s) for s in split(dims[2], parts)]
+    try:
+        assert all(s.schedule == "m" for s in slabs)
+        for sv, (z0, nzl) in zip(slabs, split(dims[2], parts)):
+            sv.upload_f(np.ascontiguousarray(f0[:, z0 * plane:(z0 + nzl) * plane]))
+        arr = (C.c_void_p * parts)(*[s.h.value for s in slabs])
+        _lib.call("tslb_cuda_link_local", arr, parts)
+        _lib.call("tslb_cuda_group_step", arr, parts, 5)
+        mo = np.concatenate([np.concatenate([s.download_field("rho")[None], s.download_field("mom").reshape(L.dim, -1),
+                                             s.download_field("pineq").reshape(L.npineq, -1)]) for s in slabs], axis=1)
+        f = np.concatenate([s.download_f() for s in slabs], axis=1)
+    finally:
+        for s in slabs:
+            s.close()
+    one = T.DeviceSolver(lat, g, 1.1, spec_of(faces), dtype, 1, solid)
+    try:
+        one.set_schedule("f1")
+        one.upload_f(f0)
+        one.step(5)
+        fo = one.download_f()
+        moo = np.concatenate([one.download_field("rho")[None], one.download_field("mom").reshape(L.dim, -1),
+                              one.download_field("pineq").reshape(L.npineq, -1)])
+    finally:
+        one.close()
+    assert_bitwise(f, fo, f"masked M slabs x{parts} f (all nodes)")
+    assert_bitwise(mo, moo, f"masked M slabs x{parts} moments (all nodes)")
+    ref = f0.copy()
+    rmo = np.zeros((O.moments_layout(lat), ref.shape[1]), dtype)
+    oracle_port.single_run(lat, dims, 1.1, faces, ref, rmo, 5, 0, solid)
+    fluid = solid == 0
+    assert_bitwise(f, ref, "masked M slabs f vs oracle", fluid)
+    assert_bitwise(mo, rmo, "masked M slabs moments vs oracle", fluid)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_nccl_self_exchange_masked(gpu, dtype, monkeypatch):
+    """The masked M slab on real NCCL (one-rank communicator, its own
+    neighbour): equals the periodic masked box of the slab's height."""
+    monkeypatch.setenv("TSLB_LZ", "2")
+    lat, nx, ny, nzl = "d3q19", 32, 16, 8
+    mask = random_solid((nx, ny, nzl), 0.15, 9)
+    f0 = O.random_state(lat, (nx, ny, nzl), 6, dtype, mask)
+    spec = spec_of(O.periodic())
+    ref = T.DeviceSolver(lat, T.GridDims(nx, ny, nzl), 1.2, spec, dtype, 1, mask)
+    slab = T.DeviceSolver(lat, T.GridDims(nx, ny, 2 * nzl), 1.2, spec, dtype, 1, np.concatenate([mask, mask]),
+                          slab=(0, nzl))
+    try:
+        assert slab.schedule == "m" and ref.schedule == "m"
+        uid = (C.c_char * 128)()
+        _lib.call("tslb_cuda_nccl_unique_id", uid)
+        _lib.call("tslb_cuda_attach_nccl", slab.h, uid, 1, 0)
+        for d in (ref, slab):
+            d.upload_f(f0)
+            d.step(7)
+        assert_bitwise(slab.download_f(), ref.download_f(), "masked NCCL self-exchange f")
+        for fld in ("rho", "mom", "pineq"):
+            assert_bitwise(slab.download_field(fld), ref.download_field(fld), f"masked NCCL self-exchange {fld}")
+    finally:
+        slab.close()
+        ref.close()
