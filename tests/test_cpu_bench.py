@@ -1,0 +1,40 @@
+"""bench.py's host-side accounting (no GPU): algorithmic bytes per lattice
+update (SURVEY.md §8(d) census rule 2 x arrays x s, and the M schedule's
+2 x moments x s), and the porous workload's geometry generator."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import bench  # noqa: E402
+from paper_2304_06437_b200 import tslb as T  # noqa: E402
+
+
+def test_census_bytes_per_update():
+    # bench.hpp:62-63: D2Q9 120 B, D3Q19 232 B, D3Q27 296 B at fp32 (F1)
+    for lat, b in (("d2q9", 120), ("d3q19", 232), ("d3q27", 296)):
+        assert bench.step_bytes(T.lattice_of(lat), 1, 4, "f1") == b
+    # M: 2 x (1 + D + D(D+1)/2) x s
+    assert bench.step_bytes(T.lattice_of("d3q19"), 1, 4, "m") == 80
+    assert bench.step_bytes(T.lattice_of("d2q9"), 1, 4, "m") == 48
+    assert bench.step_bytes(T.lattice_of("d3q19"), 1, 8, "m") == 160
+
+
+def test_masked_bytes_add_the_geometry():
+    L = T.lattice_of("d3q19")
+    plain, masked = bench.kernel_bytes(L, 1, 4), bench.kernel_bytes(L, 1, 4, True)
+    assert masked["mstep"] - plain["mstep"] == 4          # u32 solid bits
+    assert masked["moments"] - plain["moments"] == 1      # u8 solid mask
+    assert masked["streamcoll"] - plain["streamcoll"] == 5  # mask + u32 slow mask
+
+
+def test_sphere_pack_is_deterministic_and_hits_its_fraction():
+    a = bench.sphere_pack((96, 64, 48), 6.0, 0.25, 5)
+    b = bench.sphere_pack((96, 64, 48), 6.0, 0.25, 5)
+    assert a.dtype == np.uint8 and a.shape == (96 * 64 * 48,)
+    assert np.array_equal(a, b)
+    assert 0.2 < a.mean() < 0.3
+    # periodic: spheres wrap across every face
+    s = a.reshape(48, 64, 96)
+    assert s[:, :, 0].any() and s[:, :, -1].any() and s[0].any() and s[-1].any()
