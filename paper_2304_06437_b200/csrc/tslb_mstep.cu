@@ -1,5 +1,6 @@
 // Moment-resident single-pass step ("M" schedule) for
-// 3-D box geometries (periodic faces and walls, no solid mask).
+// 3-D grids: periodic faces, walls, slab ghost faces and (SOLID kernels)
+// solid masks.
 //
 // The F1 schedule (k_moments + k_streamcoll) moves the populations through
 // HBM twice per step: 2 (q + 1 + D + np) scalars per lattice update. Here the
@@ -31,9 +32,12 @@
 // is collided; the x-halo columns and wrapped rows come in by cp.async.
 // Slots live in per-direction plane rings sized by the direction's c_z (a
 // slot of destination plane d is written while the march is at plane
-// d - c_z, or at d for a bounce, and read after the march passed d), two
-// barriers per plane. Pure-z and rest directions never leave the thread:
-// they ride a register ring.
+// d - c_z, or at d for a bounce, and read after the march passed d): two
+// barriers per plane, or one with rings a plane deeper (SL<L, 1>). Pure-z
+// and rest directions never leave the thread: they ride a register ring.
+// Solid masks (SOLID): per-node solid bits (k_solid_bits) ride along with
+// the moments; solid nodes push nothing and carry their moments through,
+// a push towards a solid node is a bounce (see emit).
 // Ring nodes outside the tile (one-node x/y halo, the planes just below and
 // above the march) only rebuild the directions that land inside the tile;
 // they never bounce (a push that lands in the tile cannot cross a wall).
