@@ -359,3 +359,25 @@ def test_slice_sampler_matches_full_download(gpu, axis, sched):
             assert_bitwise(sl, want, f"slice {name} axis {axis}")
     finally:
         dev.close()
+
+
+def test_invalid_arguments_raise(gpu):
+    """EINVAL paths of the C-ABI (fields.hpp:84 / boundary.hpp:65-77 analogues
+    and the extension entry points): nothing is created, an exception is
+    raised, the error string names the problem."""
+    spec = T.BoundarySpec.all_periodic()
+    with pytest.raises(T.InvalidArgument):
+        T.DeviceSolver("d3q19", T.GridDims(8, 8, 0), 1.0, spec)
+    with pytest.raises(T.InvalidArgument):
+        T.DeviceSolver("d2q9", T.GridDims(8, 8, 3), 1.0, spec)  # 2-D lattice on a 3-D grid
+    for slab in ((4, 8), (-1, 2), (0, 0)):
+        with pytest.raises(T.InvalidArgument):
+            T.DeviceSolver("d3q19", T.GridDims(8, 8, 8), 1.0, spec, slab=slab)
+    dev = T.DeviceSolver("d3q19", T.GridDims(32, 8, 4), 1.0, spec, np.float32, 2, None, T.ColorParams())
+    try:
+        with pytest.raises(RuntimeError):
+            dev.set_schedule("m")  # the M schedule is single-fluid
+        with pytest.raises(RuntimeError):
+            dev.set_body_force(1e-5, 0.0, 0.0)  # forcing is a single-fluid extension
+    finally:
+        dev.close()
