@@ -222,7 +222,18 @@ def step_bytes(lat, comps, es, schedule="f1", solid=False):
     return sum(kb.values())
 
 
+def _json_stdout():
+    """stdout carries exactly one JSON line: anything else written to fd 1
+    (NCCL's version banner, library chatter) is sent to stderr; the returned
+    stream is the original stdout."""
+    sys.stdout.flush()
+    keep = os.dup(1)
+    os.dup2(2, 1)
+    return os.fdopen(keep, "w", buffering=1)
+
+
 def main():
+    out_stream = _json_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -236,6 +247,10 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sample-nz", type=int, default=16)
+    ap.add_argument("--nccl-self", action="store_true",
+                    help="N=1 probe of the multi-GPU step: the GPU's domain is a z slab of a twice-as-tall box on "
+                         "a one-rank NCCL communicator (its own up/down neighbour), so every step runs the "
+                         "boundary chunks, the NCCL halo exchange on the comm stream and the overlapped interior")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -247,8 +262,8 @@ def main():
         dims = (args.n, args.n, args.n)
     if args.dims and dims[2] > 1:
         dims = tuple(int(v) for v in args.dims.split(","))
-    default = args.workload == "tgv-d3q19"
-    metric = METRIC if default else f"GLUPS ({args.workload})"
+    default = args.workload == "tgv-d3q19" and not args.nccl_self
+    metric = METRIC if default else f"GLUPS ({args.workload}{', NCCL self-exchange probe' if args.nccl_self else ''})"
 
     if args.impl == "reference":
         if rank != 0:
@@ -264,7 +279,7 @@ def main():
                "cpu_baseline": {"value": round(glups, 6), "unit": "GLUPS", "cores": info["cores"],
                                 "kind": info["kind"], "sample": info["sample"]},
                "e2e": {"value": round(glups, 6), "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(out))
+        print(json.dumps(out), file=out_stream)
         return
 
     import torch
@@ -286,11 +301,12 @@ def main():
     if world > 1 and lat.dim != 3:
         raise SystemExit("multi-GPU slabs: 3-D workloads only")
     nx, ny, nzp = dims
-    nz_g = nzp * world
+    self_x = args.nccl_self and world == 1 and lat.dim == 3
+    nz_g = nzp * (2 if self_x else world)
     g = T.GridDims(nx, ny, nz_g)
     spec = spec_of(T, W["faces"])
     color = T.ColorParams(sigma=W.get("sigma", 0.01), beta=W.get("beta", 0.7)) if W["comps"] == 2 else None
-    slab = (rank * nzp, nzp) if world > 1 else None
+    slab = (rank * nzp, nzp) if world > 1 or self_x else None
     solid = None
     if "spheres" in W:
         if world > 1:
@@ -307,15 +323,16 @@ def main():
         sim.set_body_force(8.0 * nu * W["umax"] / float(ny) ** 2, 0.0, 0.0)
     if "force" in W:
         sim.set_body_force(*W["force"])
-    if world > 1:
+    if world > 1 or self_x:
         import ctypes as C
         uid = (C.c_char * 128)()
         if rank == 0:
             _lib.check(_lib.load().tslb_cuda_nccl_unique_id(uid))
-        obj = [bytes(uid)]
-        dist.broadcast_object_list(obj, src=0)
-        buf = (C.c_char * 128).from_buffer_copy(obj[0])
-        _lib.check(_lib.load().tslb_cuda_attach_nccl(sim.h, buf, world, rank))
+        if dist:
+            obj = [bytes(uid)]
+            dist.broadcast_object_list(obj, src=0)
+            uid = (C.c_char * 128).from_buffer_copy(obj[0])
+        _lib.check(_lib.load().tslb_cuda_attach_nccl(sim.h, uid, world, rank))
     if W["init"] == "droplet":
         sim.init_analytic("droplet", 0.0, W["radius"])
     else:
@@ -347,7 +364,7 @@ def main():
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    nodes = g.n()
+    nodes = nx * ny * nzp * world  # (the self-exchange probe steps one slab)
     glups = nodes * args.steps / (ms / 1e3) / 1e9
 
     # roofline of the dominant kernel: algorithmic bytes per launch / mean
@@ -362,7 +379,10 @@ def main():
     dom = max((k for k in per_node if k in prof), key=lambda k: prof[k][0])
     k_ms, k_n = prof[dom]
     local_nodes = nx * ny * nzp
-    achieved = per_node[dom] * local_nodes / (k_ms / k_n / 1e3) / 1e9
+    # algorithmic bytes over the class's summed launch time: one launch per
+    # step on a whole domain (= bytes per launch / mean launch time); slabs
+    # split the step into boundary and interior chunk launches
+    achieved = per_node[dom] * local_nodes * args.steps / (k_ms / 1e3) / 1e9
     hbm, peak_kind, _ = peaks()
     sched = sim.schedule if W["comps"] == 1 else "f1"
     sb = step_bytes(lat, W["comps"], es, sched, masked) if W["comps"] == 1 else sum(per_node.values())
@@ -382,6 +402,8 @@ def main():
             "traffic_source": tsrc, "limiter": limiter, "kernel": f"k_{dom}",
             "kernel_bytes_per_node": per_node[dom], "peak_kind": peak_kind,
             "per_kernel_ms": {k: round(v[0] / v[1], 4) for k, v in prof.items()},
+            "kernel_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in prof.items()},
+            "launches_per_step": {k: round(v[1] / args.steps, 2) for k, v in prof.items()},
             "step_bytes_per_lu": sb, "step_frac": round(step_bw / hbm, 4),
             "step_frac_of_8TBs": round(step_bw / 8000.0, 4)}
     if fp64_ops:
@@ -439,9 +461,11 @@ def main():
                                        else "colour moments + gradient + fused prepare/stream-collide-recolour"),
                           "l2": "state >> 126 MB L2, no flush needed" if nodes > 10 ** 7
                           else "L2-resident (correctness config)",
-                          "parallelism": f"z-slab x{world}" if world > 1 else "single GPU"},
+                          "parallelism": f"z-slab x{world}" if world > 1 else
+                          "one z slab on a 1-rank NCCL communicator (self halo exchange)" if self_x
+                          else "single GPU"},
                "roofline": roof, "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
-        print(json.dumps(out))
+        print(json.dumps(out), file=out_stream)
     sim.close()
     if dist:
         dist.destroy_process_group()

@@ -804,7 +804,11 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
     return r;
   };
   CK(cudaStreamCreateWithFlags(&h->s, cudaStreamNonBlocking));
-  CK(cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking));
+  // the halo stream runs at the highest priority: its NCCL kernels get SMs
+  // ahead of the queued CTAs of the interior chunks they overlap with
+  int prio_lo = 0, prio_hi = 0;
+  CK(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+  CK(cudaStreamCreateWithPriority(&h->cs, cudaStreamNonBlocking, prio_hi));
   CK(cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming));
   CK(cudaEventCreateWithFlags(&h->ev_c, cudaEventDisableTiming));
   CK(cudaEventCreate(&h->t0));
