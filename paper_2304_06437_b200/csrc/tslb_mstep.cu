@@ -420,9 +420,8 @@ __device__ __forceinline__ void push_ring(const Ring<L, T>& rg, int hdelta, int 
 
 // compute_moments of one node from its gathered slots (kernels.hpp:74-107;
 // same accumulation order and formulae as k_moments)
-template <class L, typename T, typename C>
-__device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, const T (&R)[L::q][3],
-                                         T* __restrict__ mo, int64_t idx) {
+template <class L, typename T, typename C, class Put>
+__device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, const T (&R)[L::q][3], const Put& put) {
   C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pzz = 0, pxy = 0, pxz = 0, pyz = 0;
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
@@ -451,17 +450,16 @@ __device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, con
   if constexpr (L::dim == 3) force_shift<C>(d, jx, jy, jz);
   else { C z0 = 0; force_shift<C>(d, jx, jy, z0); }
   const C c3 = cs2<C>();
-  const int64_t ms = d.mstride;
-  mo[idx] = T(r);
-  mo[ms + idx] = T(jx);
-  mo[2 * ms + idx] = T(jy);
-  mo[3 * ms + idx] = T(jz);
-  mo[4 * ms + idx] = T(pxx - c3 * r - jx * jx);
-  mo[5 * ms + idx] = T(pyy - c3 * r - jy * jy);
-  mo[6 * ms + idx] = T(pzz - c3 * r - jz * jz);
-  mo[7 * ms + idx] = T(pxy - jx * jy);
-  mo[8 * ms + idx] = T(pxz - jx * jz);
-  mo[9 * ms + idx] = T(pyz - jy * jz);
+  put(0, T(r));
+  put(1, T(jx));
+  put(2, T(jy));
+  put(3, T(jz));
+  put(4, T(pxx - c3 * r - jx * jx));
+  put(5, T(pyy - c3 * r - jy * jy));
+  put(6, T(pzz - c3 * r - jz * jz));
+  put(7, T(pxy - jx * jy));
+  put(8, T(pxz - jx * jz));
+  put(9, T(pyz - jy * jz));
 }
 
 template <class L, typename T, typename C, bool WALLS, bool SOLID, int MINB>
@@ -612,8 +610,11 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     __syncthreads();
     // compute_moments skips solid nodes (their moment arrays keep their values)
-    if (z - 1 >= za && !(SOLID && solid_prev))
-      finalize<L, T, C>(d, rg, R, mo, col + int64_t(z - 1) * d.plane);
+    if (z - 1 >= za && !(SOLID && solid_prev)) {
+      T* o = mo + col + int64_t(z - 1) * d.plane;
+      const int64_t ms = d.mstride;
+      finalize<L, T, C>(d, rg, R, [&](int c, T v) { o[c * ms] = v; });
+    }
     if constexpr (SOLID) solid_prev = (ct.sb & kSelfSolid) != 0;  // (ct.sb: plane z)
     if constexpr (L::rd == 0) __syncthreads();
 #pragma unroll
