@@ -305,3 +305,37 @@ def test_nccl_self_exchange_masked(gpu, dtype, monkeypatch):
     finally:
         slab.close()
         ref.close()
+
+
+@pytest.mark.parametrize("sched", ["m", "f1"])
+def test_survey_decomposition_512x256x256(gpu, sched):
+    """fields bit-identical for 1/2/4/8 slabs at
+    512x256x256 (per-plane FNV digests of every population array, D3Q19
+    periodic Taylor-Green, fp32 storage, fp64 node math), device-initialised
+    on each slab from the global coordinates."""
+    dims = (512, 256, 256)
+    g = T.GridDims(*dims)
+    spec = spec_of(O.periodic())
+    steps = 4
+    one = T.DeviceSolver("d3q19", g, 1.6, spec, np.float32)
+    try:
+        one.set_schedule(sched)
+        one.init_analytic("taylor_green", 0.03)
+        one.step(steps)
+        ref = one.plane_digests()
+    finally:
+        one.close()
+    for parts in (2, 4, 8):
+        slabs = [T.DeviceSolver("d3q19", g, 1.6, spec, np.float32, 1, None, slab=s) for s in split(dims[2], parts)]
+        try:
+            for s in slabs:
+                s.set_schedule(sched)
+                s.init_analytic("taylor_green", 0.03)
+            arr = (C.c_void_p * parts)(*[s.h.value for s in slabs])
+            _lib.call("tslb_cuda_link_local", arr, parts)
+            _lib.call("tslb_cuda_group_step", arr, parts, steps)
+            dig = np.concatenate([s.plane_digests() for s in slabs], axis=2)
+        finally:
+            for s in slabs:
+                s.close()
+        assert np.array_equal(dig, ref), f"{parts} slabs ({sched}): plane digests differ"
