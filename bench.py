@@ -170,6 +170,31 @@ def cpu_reference(steps, warmup, sample_nz=16, workers=None):
     return glups, dict(kind=kind, cores=cores, sample=sample, seconds=t)
 
 
+def host_info():
+    """CPU model, logical CPUs, sockets and physical cores (lscpu's fields,
+    read from /proc/cpuinfo)."""
+    model, phys = "", set()
+    cur = {}
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                k, _, v = line.partition(":")
+                k, v = k.strip(), v.strip()
+                if k == "model name" and not model:
+                    model = v
+                elif k in ("physical id", "core id"):
+                    cur[k] = v
+                elif not k and cur:
+                    phys.add((cur.get("physical id"), cur.get("core id")))
+                    cur = {}
+        if cur:
+            phys.add((cur.get("physical id"), cur.get("core id")))
+    except OSError:
+        pass
+    return {"model": model, "logical_cpus": os.cpu_count(), "sockets": len({p for p, _ in phys}) or None,
+            "physical_cores": len(phys) or None}
+
+
 # ---------------------------------------------------------------------------
 def spec_of(T, kind):
     if kind == "periodic":
@@ -270,6 +295,8 @@ def main():
             return
         steps, warm = args.steps, max(1, min(args.warmup, 2))
         glups, info = cpu_reference(steps, warm, args.sample_nz)
+        # the host, and a 1-worker row beside the all-cores one
+        g1, info1 = cpu_reference(1, 1, args.sample_nz, workers=1)
         out = {"metric": METRIC, "value": round(glups, 6), "unit": "GLUPS", "n_gpus": args.gpus, "steps": steps,
                "warmup": warm, "ms_per_step": round(info["seconds"] / steps * 1e3, 3), "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -278,7 +305,10 @@ def main():
                           "lattice": "d3q19", "storage": "f32", "sample": info["sample"]},
                "cpu_baseline": {"value": round(glups, 6), "unit": "GLUPS", "cores": info["cores"],
                                 "kind": info["kind"], "sample": info["sample"]},
-               "e2e": {"value": round(glups, 6), "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+               "e2e": {"value": round(glups, 6), "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+               "cpu_1worker": {"value": round(g1, 6), "unit": "GLUPS", "cores": info1["cores"],
+                               "kind": info1["kind"], "sample": info1["sample"]},
+               "host": host_info()}
         print(json.dumps(out), file=out_stream)
         return
 
@@ -437,7 +467,7 @@ def main():
         try:
             cg, info = cpu_reference(max(2, min(args.steps, 5)), 1, args.sample_nz)
             cpu = {"value": round(cg, 6), "unit": "GLUPS", "cores": info["cores"], "kind": info["kind"],
-                   "sample": info["sample"]}
+                   "sample": info["sample"], "host": host_info()}
         except Exception as e:  # report, never fake
             cpu = {"value": None, "unit": "GLUPS", "cores": 0, "kind": "unavailable", "sample": str(e)[:200]}
 
