@@ -170,6 +170,68 @@ def cpu_reference(steps, warmup, sample_nz=16, workers=None):
     return glups, dict(kind=kind, cores=cores, sample=sample, seconds=t)
 
 
+def cpu_reference_workload(name, W, dims, steps, warmup, sample_nz=16, workers=None):
+    """The reference CPU path (oracle/_ref: the reference headers, WorkerPool
+    over the host cores) on a bounded sample of a non-default workload:
+    2-D workloads whole, 3-D workloads as an nx x ny x sample_nz slab
+    (periodic in z) of the same faces / mask / colour state. The reference
+    has no D3Q27: the channel row times D3Q19 on the same slab (BASELINE.md
+    §3, C3). Returns (GLUPS, info) or raises."""
+    import ctypes as C
+
+    from oracle import oracle as O
+    if not os.path.exists(O.REF_SO):
+        raise FileNotFoundError("oracle/_ref not built")
+    workers = workers or os.cpu_count() or 1
+    lat = "d3q19" if W["lat"] == "d3q27" else W["lat"]
+    nx, ny, nz = dims
+    sdims = (nx, ny, nz) if nz == 1 else (nx, ny, min(sample_nz, nz))
+    n = int(np.prod(sdims))
+    steps = max(steps, min(2000, int(2e8 // n)))  # small grids: enough steps for a stable timing
+    dt = np.float32 if W["storage"] == "f32" else np.float64
+    faces = {"periodic": O.periodic(), "lid": O.lid_cavity(0.025)}.get(W["faces"])
+    if faces is None:  # channel: no-slip walls at y
+        faces = O.periodic()
+        faces[2] = ("wall", (0, 0, 0))
+        faces[3] = ("wall", (0, 0, 0))
+    kinds, uw = O.faces_arrays(faces)
+    info = O.lattice_info(lat)
+    o = O.Oracle("ref")
+    secs = C.c_double()
+    scalar = 0 if dt == np.float64 else 1
+    if W["comps"] == 2:
+        z0 = (nz - sdims[2]) // 2  # a slab through the droplet centre
+        k, j, i = np.meshgrid(np.arange(sdims[2]) + z0, np.arange(ny), np.arange(nx), indexing="ij")
+        r = np.sqrt((i - 0.5 * nx + 0.5) ** 2 + (j - 0.5 * ny + 0.5) ** 2 + (k - 0.5 * nz + 0.5) ** 2).ravel()
+        prof = 0.5 * (1 + np.tanh(W["radius"] - r))
+        st = np.zeros((5, n), dt)
+        st[0], st[1] = prof, 1 - prof
+        fr, fb = O.Oracle("port").init_colors(lat, sdims, st)
+        cp = np.array([W.get("sigma", 0.01), W.get("beta", 0.7), 0.0, 0.02, 1e-6], np.float64)
+        ip = np.array([3, 0], np.int32)
+        o._check(o.lib.tslbref_time_two(O.LATTICES[lat], scalar, *sdims, float(W["omega"]), O._ptr(cp),
+                                        O._ptr(ip), O._ptr(kinds), O._ptr(uw), O._ptr(fr), O._ptr(fb), int(steps),
+                                        int(warmup), int(workers), C.byref(secs)))
+    else:
+        solid = None
+        if "spheres" in W:
+            solid = np.ascontiguousarray(sphere_pack(dims, *W["spheres"])[:n])
+        f = np.repeat(info["t"].astype(dt)[:, None], n, axis=1)  # rest equilibrium
+        if solid is not None:
+            f[:, solid != 0] = 0
+        f = np.ascontiguousarray(f)
+        o._check(o.lib.tslbref_time_steps_ex(O.LATTICES[lat], scalar, *sdims, float(W["omega"]), O._ptr(kinds),
+                                             O._ptr(uw), O._ptr(solid), O._ptr(f), int(steps), int(warmup),
+                                             int(workers), C.byref(secs)))
+    t = secs.value
+    glups = n * steps / t / 1e9
+    what = "x".join(str(v) for v in sdims)
+    sample = (f"{lat.upper()} {what} sample of the {name} workload ({W['storage']}), {steps} steps after "
+              f"{warmup} warm-up, WorkerPool({workers})" + (" -- D3Q19 stands in: the reference has no D3Q27"
+                                                            if W["lat"] == "d3q27" else ""))
+    return glups, dict(kind="reference", cores=workers, sample=sample, seconds=t)
+
+
 def host_info():
     """CPU model, logical CPUs, sockets and physical cores (lscpu's fields,
     read from /proc/cpuinfo)."""
@@ -463,6 +525,13 @@ def main():
                                                            "full state per rank)"}
 
     cpu = None
+    if not default and rank == 0 and not args.no_cpu and world == 1 and not args.nccl_self:
+        try:
+            cg, info = cpu_reference_workload(args.workload, W, dims, max(2, min(args.steps, 5)), 1, args.sample_nz)
+            cpu = {"value": round(cg, 6), "unit": "GLUPS", "cores": info["cores"], "kind": info["kind"],
+                   "sample": info["sample"], "host": host_info()}
+        except Exception as e:  # report, never fake
+            cpu = {"value": None, "unit": "GLUPS", "cores": 0, "kind": "unavailable", "sample": str(e)[:200]}
     if default and rank == 0 and not args.no_cpu and world == 1:
         try:
             cg, info = cpu_reference(max(2, min(args.steps, 5)), 1, args.sample_nz)

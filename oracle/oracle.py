@@ -102,6 +102,8 @@ class Oracle:
             self._fn("census").argtypes = [i, i, vp, vp]
         else:
             self._fn("time_steps").argtypes = [i, i, i, i, i, d, vp, vp, vp, l, l, i, vp]
+            self._fn("time_steps_ex").argtypes = [i, i, i, i, i, d, vp, vp, vp, vp, l, l, i, vp]
+            self._fn("time_two").argtypes = [i, i, i, i, i, d, vp, vp, vp, vp, vp, vp, l, l, i, vp]
             self._fn("bench").argtypes = [i, i, i, i, i, d, l, l, i, vp, vp, vp]
 
     def _fn(self, name):

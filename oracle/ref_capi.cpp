@@ -314,6 +314,75 @@ int tslbref_time_steps(int lattice, int scalar, int nx, int ny, int nz,
   });
 }
 
+// The same on any face mix and an optional solid mask (bench.py's CPU rows
+// of the other workloads: cavity, channel, porous medium).
+int tslbref_time_steps_ex(int lattice, int scalar, int nx, int ny, int nz,
+                          double omega, const int* kinds, const double* uw,
+                          const std::uint8_t* solid, void* f, long steps,
+                          long warmup, int workers, double* seconds) {
+  return guarded([&] {
+    with_lattice(lattice, [&](auto L) {
+      using Lat = typename decltype(L)::type;
+      with_scalar(scalar, [&](auto z) {
+        using T = decltype(z);
+        const GridDims g{nx, ny, nz};
+        CollisionParams<T> prm;
+        prm.omega = T(omega);
+        std::unique_ptr<WorkerPool> pool;
+        if (workers > 1) pool = std::make_unique<WorkerPool>(workers);
+        SingleFluidSim<Lat, T> sim(g, prm, make_spec<T>(kinds, uw),
+                                   make_solid(solid, g.n()), pool.get());
+        load_arrays(sim.fields().f, static_cast<T*>(f), g.n());
+        sim.run(warmup);
+        const auto t0 = std::chrono::steady_clock::now();
+        sim.run(steps);
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+      });
+    });
+  });
+}
+
+// Time `steps` two_fluid_step calls (TwoFluidSim::run) on a caller-provided
+// colour state; cp / ip as tslbref_two_run.
+int tslbref_time_two(int lattice, int scalar, int nx, int ny, int nz,
+                     double omega, const double* cp, const int* ip,
+                     const int* kinds, const double* uw, const void* fr,
+                     const void* fb, long steps, long warmup, int workers,
+                     double* seconds) {
+  return guarded([&] {
+    with_lattice(lattice, [&](auto L) {
+      using Lat = typename decltype(L)::type;
+      with_scalar(scalar, [&](auto z) {
+        using T = decltype(z);
+        const GridDims g{nx, ny, nz};
+        const std::size_t n = g.n();
+        CollisionParams<T> prm;
+        prm.omega = T(omega);
+        ColorParams<T> c;
+        c.sigma = T(cp[0]);
+        c.beta = T(cp[1]);
+        c.nci_strength = T(cp[2]);
+        c.eps_bulk = T(cp[3]);
+        c.grad_threshold = T(cp[4]);
+        c.nci_reach = ip[0];
+        c.form = ip[1] ? PerturbationForm::Linear : PerturbationForm::Squared;
+        std::unique_ptr<WorkerPool> pool;
+        if (workers > 1) pool = std::make_unique<WorkerPool>(workers);
+        TwoFluidSim<Lat, T> sim(g, prm, c, make_spec<T>(kinds, uw), {},
+                                pool.get());
+        load_arrays(sim.fields().fr, static_cast<const T*>(fr), n);
+        load_arrays(sim.fields().fb, static_cast<const T*>(fb), n);
+        sim.run(warmup);
+        const auto t0 = std::chrono::steady_clock::now();
+        sim.run(steps);
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+      });
+    });
+  });
+}
+
 std::uint64_t tslbref_fnv1a(const void* data, std::size_t n, std::uint64_t h) {
   return fnv1a(data, n, h);
 }
