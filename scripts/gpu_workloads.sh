@@ -9,3 +9,5 @@ timeout 600 python bench.py --workload cavity-d2q9 --steps 2000 --warmup 64 > gp
 timeout 600 python bench.py --n 512 --steps 20 --warmup 3 --no-e2e --no-cpu > gpurun_out/${TAG}_tgv512.json 2> gpurun_out/${TAG}_tgv512.err
 timeout 600 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --math f32 > gpurun_out/${TAG}_tgv1024_f32.json 2> gpurun_out/${TAG}_tgv1024_f32.err
 timeout 600 python bench.py --steps 20 --warmup 3 --no-e2e --no-cpu --schedule f1 > gpurun_out/${TAG}_tgv1024_f1.json 2> gpurun_out/${TAG}_tgv1024_f1.err
+timeout 600 python bench.py --workload tgv-d2q9 --steps 20 --warmup 3 > gpurun_out/${TAG}_tgv2d.json 2> gpurun_out/${TAG}_tgv2d.err
+timeout 600 python bench.py --workload porous-d3q19 --steps 20 --warmup 3 > gpurun_out/${TAG}_porous.json 2> gpurun_out/${TAG}_porous.err
