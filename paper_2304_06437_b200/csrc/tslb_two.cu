@@ -451,8 +451,13 @@ __global__ void __launch_bounds__(BX2) k_cg_gradient_box(Dom d, TF<T> s) {
 // GRAD: compute grad phi in place from the phi stencil instead of reading
 // the gradient arrays (the step's gradient phase folded in; the host
 // mirror computes the arrays lazily when they are read)
+#ifdef TSLB_CG_MINB
+#define TSLB_CG_BOUNDS __launch_bounds__(BX2, TSLB_CG_MINB)
+#else
+#define TSLB_CG_BOUNDS __launch_bounds__(BX2)
+#endif
 template <class L, typename T, bool FOLD, bool WALLS, bool GRAD>
-__global__ void __launch_bounds__(BX2)
+__global__ void TSLB_CG_BOUNDS
     k_cg_streamcoll_box(Dom d, T* __restrict__ fr, T* __restrict__ fb, TF<T> s, T omega, T tau,
                         ColorParamsDev cp) {
   int i, j, k;
