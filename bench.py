@@ -482,7 +482,10 @@ def main():
     traffic, tsrc, limiter, fp64_ops = None, None, None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
-            tr = None if masked else json.load(fh).get(f"{lat.name}/{W['storage']}/{dom}")
+            # (masked geometries carry the solid bits: their own capture)
+            tr = json.load(fh).get(f"{lat.name}/{W['storage']}/{dom}{'+solid' if masked else ''}")
+        if tr and args.workload not in tr.get("workloads", [args.workload]):
+            tr = None
         if tr:
             traffic, tsrc = round(tr["bytes_per_node"] * local_nodes / 1e9, 3), tr["source"]
             limiter = tr.get("limiter")

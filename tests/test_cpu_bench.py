@@ -38,3 +38,32 @@ def test_sphere_pack_is_deterministic_and_hits_its_fraction():
     # periodic: spheres wrap across every face
     s = a.reshape(48, 64, 96)
     assert s[:, :, 0].any() and s[:, :, -1].any() and s[0].any() and s[-1].any()
+
+
+def test_traffic_captures_match_the_bench_accounting():
+    # profiles/traffic.json feeds roofline.traffic: every entry names a
+    # committed capture, a bench workload, and the algorithmic bytes that
+    # kernel_bytes assigns to the same kernel class
+    import json
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    t = json.load(open(os.path.join(root, "profiles", "traffic.json")))
+    for key, e in t.items():
+        if key.startswith("_"):
+            continue
+        lat, storage, kind = key.split("/")
+        masked = kind.endswith("+solid")
+        kind = kind.replace("+solid", "")
+        assert os.path.exists(os.path.join(root, e["source"].split(" ")[0])), key
+        assert e["workloads"] and all(w in bench.WORKLOADS for w in e["workloads"]), key
+        L = T.lattice_of(lat)
+        comps = 2 if kind.startswith("cg_") else 1
+        es = 4 if storage == "f32" else 8
+        kb = bench.kernel_bytes(L, comps, es, masked)
+        if kind == "cg_streamcoll":
+            # box geometries fold the gradient in: phi read instead of grad
+            npi = L.dim * (L.dim + 1) // 2
+            kb[kind] = (3 + L.dim + npi + 1 + 2 * L.q) * es
+        if kind in kb:
+            assert kb[kind] == e["algorithmic"], key
+        # measured DRAM bytes within 10 % of the algorithmic figure
+        assert 0.95 < e["bytes_per_node"] / e["algorithmic"] < 1.1, key
