@@ -570,20 +570,32 @@ int enqueue_step(tslb_cuda_sim* h) {
   int rc;
   if (h->comps == 2 && h->xmode == 1) {
     // two-fluid slab: colour moments, phi ghost planes, folded recolouring
-    // stream-collide, population halos of both species
+    // stream-collide, population halos of both species. As in F1, the two
+    // boundary planes go first and the population exchange on the comm
+    // stream overlaps the interior planes: the interior stream-collide
+    // reads phi of owned planes only and writes no slot the exchange
+    // sends or receives (one writer per slot)
     if ((rc = ph_cg_moments(h, h->s))) return rc;
     if ((rc = exchange_phi_nccl(h, h->s))) return rc;
-    {
+    auto scr = [&](int k0, int k1) {
+      if (k1 <= k0) return 0;
       Prof p(h, TSLB_K_CG_STREAMCOLL, h->s);
       ++h->launches;
-      rc = by_scalar(h, [&](auto z) {
+      const int r = by_scalar(h, [&](auto z) {
         using T = decltype(z);
-        return launch_cg_streamcoll_grad<T>(h->lat, h->range(0, h->nzl), static_cast<T*>(h->f[0]),
+        return launch_cg_streamcoll_grad<T>(h->lat, h->range(k0, k1), static_cast<T*>(h->f[0]),
                                             static_cast<T*>(h->f[1]), h->tf(), h->omega, h->cp, h->s);
       });
-      if (rc) return set_err(TSLB_ESTATE, "two-fluid slab step needs a box geometry without NCI");
-    }
-    if ((rc = exchange_nccl(h, h->s))) return rc;
+      return r ? set_err(TSLB_ESTATE, "two-fluid slab step needs a box geometry without NCI") : 0;
+    };
+    if ((rc = scr(0, 1))) return rc;
+    if (h->nzl > 1 && (rc = scr(h->nzl - 1, h->nzl))) return rc;
+    CK(cudaEventRecord(h->ev_b, h->s));
+    CK(cudaStreamWaitEvent(h->cs, h->ev_b, 0));
+    if ((rc = exchange_nccl(h, h->cs))) return rc;
+    CK(cudaEventRecord(h->ev_c, h->cs));
+    if ((rc = scr(1, h->nzl - 1))) return rc;
+    CK(cudaStreamWaitEvent(h->s, h->ev_c, 0));
     if ((rc = unpack(h, h->s))) return rc;
     h->grad_pending = true;
     h->stress_pending = true;
