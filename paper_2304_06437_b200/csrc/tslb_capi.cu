@@ -1303,6 +1303,36 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
     return set_err(TSLB_ESTATE, "slab solver has no halo transport attached");
   CK(cudaSetDevice(h->device));
   long done = 0;
+  // small 2-D domains under M: the whole run in persistent cooperative
+  // launches (grid barrier between passes) -- per-pass launch overhead is
+  // most of their step time; TSLB_PERSIST=0 selects the graph path instead
+  constexpr int64_t kPersistMaxNodes = int64_t(1) << 20;
+  const char* pe = std::getenv("TSLB_PERSIST");
+  const bool persist = !(pe && std::atoi(pe) == 0);
+  if (persist && h->sched == TSLB_SCHED_M && h->dim == 2 && h->comps == 1 && h->xmode == 0 && !h->decomposed &&
+      !h->d.has_solid && h->n() <= kPersistMaxNodes && nsteps >= 3) {
+    if (!h->fimplicit) {
+      if (int rc = enqueue_step(h)) return rc;
+      ++done;
+    }
+    while (nsteps - done >= 2) {
+      const int n = int(std::min<long>(nsteps - done, 1L << 20));
+      int rc;
+      {
+        Prof p(h, TSLB_K_MSTEP, h->s);
+        rc = by_scalar(h, [&](auto z) {
+          using T = decltype(z);
+          return launch_mstep2d_persist<T>(h->math, h->range(0, h->nzl), static_cast<T*>(h->mo),
+                                           static_cast<T*>(h->mo2), h->omega, n, h->s);
+        });
+      }
+      if (rc) break;  // not co-resident: the regular launches below
+      ++h->launches;
+      if (n & 1) std::swap(h->mo, h->mo2);
+      h->steps += n;
+      done += n;
+    }
+  }
   // small domains are launch bound: replay a captured graph of G steps
   constexpr int64_t kGraphMaxNodes = int64_t(8) << 20;
   constexpr long kGraphSteps = 32;  // even: an M graph ends on the buffer it starts from

@@ -57,6 +57,8 @@ int launch_solid_bits(int lat, const Dom& d, const uint8_t* solid, uint32_t* bit
 // D2Q9 form of the M step (tslb_mstep2d.cu; launched through launch_mstep)
 template <typename T>
 int launch_mstep2d(int math, const Dom& d, const T* mi, T* mo, double omega, cudaStream_t st);
+template <typename T>
+int launch_mstep2d_persist(int math, const Dom& d, T* m0, T* m1, double omega, int nsteps, cudaStream_t st);
 // slab f materialisation: pushes entering boundary plane `side` (0 below,
 // 1 above) rebuilt from the ghost moments
 template <typename T>

@@ -20,6 +20,9 @@
 // HBM traffic: 2 x 6 scalars per lattice update (48 B fp32) instead of F1's
 // 120 B; the row strips overlap by one halo row at each end (the rows just
 // outside the strip push only their c_y-inward directions).
+#include <cooperative_groups.h>
+
+#include <algorithm>
 #include <cstdint>
 #include <cstdlib>
 
@@ -29,6 +32,7 @@
 #include "tslb_pair.cuh"
 
 namespace tslb_cuda {
+namespace cg = cooperative_groups;
 namespace mstep2d {
 
 constexpr int OWN = 30;  // owned columns per warp (lanes 1..30)
@@ -46,16 +50,19 @@ __device__ __forceinline__ NodeMoments<C> prep(const T (&v)[6]) {
   return prepare_node<C>(C(v[0]), C(v[1]), C(v[2]), C(0), C(v[3]), C(v[4]), C(0), C(v[5]), C(0), C(0));
 }
 
-template <class L, typename T, typename C, bool WALLS>
-__global__ void __launch_bounds__(32 * WPB)
-    k_mstep2d(Dom d, const T* __restrict__ mi, T* __restrict__ mo, C om1, int rows) {
+// One warp's strip: columns strip * OWN - 1 .. + 31, rows ya .. ya + rows - 1.
+// COH: the moments are read through L2 (ld.global.cg) -- the persistent
+// kernel reads buffers that other SMs wrote before the last grid barrier,
+// where the non-coherent read-only path could return stale lines.
+template <class L, typename T, typename C, bool WALLS, bool COH>
+__device__ __forceinline__ void strip_pass(const Dom& d, const T* __restrict__ mi, T* __restrict__ mo, C om1,
+                                           int rows, int strip, int ya) {
   using Lat = L;
   const int lane = threadIdx.x & 31;
-  const int strip = int(blockIdx.x) * WPB + int(threadIdx.x >> 5);
   const int xg = strip * OWN - 1 + lane;  // this lane's column (may lie outside [0, nx))
   const int xs = xg > d.nx ? -1 : wrap_coord(xg, d.nx, d.mode[XMin], d.mode[XMax]);
   const bool owned = lane >= 1 && lane <= OWN && xg < d.nx;
-  const int ya = int(blockIdx.y) * rows, yb = min(ya + rows, d.ny);
+  const int yb = min(ya + rows, d.ny);
   // is the lane that pushes into this one along c_x = +1 / -1 a real node?
   const bool src = xs >= 0;
   const bool from_left = __shfl_up_sync(FULL, src, 1);
@@ -77,7 +84,7 @@ __global__ void __launch_bounds__(32 * WPB)
     }
     const int64_t idx = xs + int64_t(d.nx) * yy;
 #pragma unroll
-    for (int c = 0; c < 6; ++c) v[c] = __ldg(mi + c * ms + idx);
+    for (int c = 0; c < 6; ++c) v[c] = COH ? __ldcg(mi + c * ms + idx) : __ldg(mi + c * ms + idx);
   };
 
   T R[9][3];  // slot of direction a for destination rows y-1, y, y+1
@@ -181,6 +188,50 @@ __global__ void __launch_bounds__(32 * WPB)
   row(std::integral_constant<int, -1>{}, yb);
 }
 
+template <class L, typename T, typename C, bool WALLS>
+__global__ void __launch_bounds__(32 * WPB)
+    k_mstep2d(Dom d, const T* __restrict__ mi, T* __restrict__ mo, C om1, int rows) {
+  strip_pass<L, T, C, WALLS, false>(d, mi, mo, om1, rows, int(blockIdx.x) * WPB + int(threadIdx.x >> 5),
+                                    int(blockIdx.y) * rows);
+}
+
+// Persistent form for small (launch-bound) domains: one cooperative launch
+// runs nsteps M passes, ping-ponging m0 -> m1 -> m0 ..., with a grid barrier
+// between passes; each block loops over the (strip block, row block) items
+// of the regular grid. Same per-node arithmetic, so the same bits.
+template <class L, typename T, typename C, bool WALLS>
+__global__ void __launch_bounds__(32 * WPB)
+    k_mstep2d_persist(Dom d, T* m0, T* m1, C om1, int rows, int nsteps, int nbx, int nby) {
+  cg::grid_group grid = cg::this_grid();
+  const int items = nbx * nby;
+  for (int s = 0; s < nsteps; ++s) {
+    const T* src = (s & 1) ? m1 : m0;
+    T* dst = (s & 1) ? m0 : m1;
+    for (int it = int(blockIdx.x); it < items; it += int(gridDim.x)) {
+      const int bx = it % nbx, by = it / nbx;
+      strip_pass<L, T, C, WALLS, true>(d, src, dst, om1, rows, bx * WPB + int(threadIdx.x >> 5), by * rows);
+    }
+    grid.sync();
+  }
+}
+
+}  // namespace mstep2d
+
+namespace mstep2d {
+// rows per warp: 16 measured best at 4096^2 (72.8 GLUPS vs 67.5 at 64 and
+// 71.2 at 8: the two halo rows vs wave quantisation); small domains
+// (launch-bound, e.g. the 256^2 cavity) shorten strips for parallelism:
+// 256^2 kernel 8.6 us at 2 rows vs 9.5 at 4, 10.1 at 1, 10.6 at 8 (s28)
+inline int strip_rows(const Dom& d) {
+  const int strips = (d.nx + OWN - 1) / OWN;
+  int rows = 16;
+  while (rows > 2 && int64_t(strips) * ((d.ny + rows - 1) / rows) < 148 * 32) rows /= 2;
+  static const int rows_env = [] {
+    const char* e = std::getenv("TSLB_ROWS2D");
+    return e ? std::atoi(e) : 0;
+  }();
+  return rows_env > 0 ? rows_env : rows;
+}
 }  // namespace mstep2d
 
 template <typename T>
@@ -189,16 +240,7 @@ int launch_mstep2d(int math, const Dom& d, const T* mi, T* mo, double omega, cud
   if (d.has_solid || d.nz != 1 || d.ghost) return 1;
   const int strips = (d.nx + OWN - 1) / OWN;
   const unsigned bx = unsigned((strips + WPB - 1) / WPB);
-  // rows per warp: 16 measured best at 4096^2 (72.8 GLUPS vs 67.5 at 64 and
-  // 71.2 at 8: the two halo rows vs wave quantisation); small domains
-  // (launch-bound, e.g. the 256^2 cavity) shorten strips for parallelism
-  int rows = 16;
-  while (rows > 4 && int64_t(strips) * ((d.ny + rows - 1) / rows) < 148 * 32) rows /= 2;
-  static const int rows_env = [] {
-    const char* e = std::getenv("TSLB_ROWS2D");
-    return e ? std::atoi(e) : 0;
-  }();
-  if (rows_env > 0) rows = rows_env;
+  const int rows = strip_rows(d);
   const dim3 grid(bx, unsigned((d.ny + rows - 1) / rows));
   if (grid.y > 65535) return 1;
   bool walls = false;
@@ -215,7 +257,51 @@ int launch_mstep2d(int math, const Dom& d, const T* mi, T* mo, double omega, cud
   return 0;
 }
 
+// nsteps M passes in one cooperative launch (m0 holds m(t); the result is in
+// m0 for even nsteps, m1 for odd). Returns 1 (nothing launched) when the
+// domain does not qualify or the device refuses a co-resident grid.
+template <typename T>
+int launch_mstep2d_persist(int math, const Dom& d, T* m0, T* m1, double omega, int nsteps, cudaStream_t st) {
+  using namespace mstep2d;
+  if (d.has_solid || d.nz != 1 || d.ghost || nsteps < 1) return 1;
+  const int strips = (d.nx + OWN - 1) / OWN;
+  const int nbx = (strips + WPB - 1) / WPB;
+  const int rows = strip_rows(d);
+  const int nby = (d.ny + rows - 1) / rows;
+  bool walls = false;
+  for (int fc = 0; fc < 4; ++fc) walls |= d.mode[fc] == kWall;
+  int dev = 0, sms = 0, coop = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 1;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+  if (!coop) return 1;
+  auto go = [&](auto kern, auto om1) {
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * WPB, 0) != cudaSuccess || per_sm < 1)
+      return 1;
+    const int blocks = std::min(nbx * nby, per_sm * sms);
+    Dom dd = d;
+    T *a = m0, *b = m1;
+    int rr = rows, ns = nsteps, x = nbx, y = nby;
+    void* args[] = {&dd, &a, &b, &om1, &rr, &ns, &x, &y};
+    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(blocks), dim3(32 * WPB), args, 0, st) ==
+        cudaSuccess)
+      return 0;
+    cudaGetLastError();  // a refused launch is not sticky; clear it for the caller's checks
+    return 1;
+  };
+  if (math == kMathDouble) {
+    const double om1 = 1.0 - double(T(omega));
+    return walls ? go(k_mstep2d_persist<D2Q9, T, double, true>, om1)
+                 : go(k_mstep2d_persist<D2Q9, T, double, false>, om1);
+  }
+  const float om1 = 1.0f - float(omega);
+  return walls ? go(k_mstep2d_persist<D2Q9, T, float, true>, om1) : go(k_mstep2d_persist<D2Q9, T, float, false>, om1);
+}
+
 template int launch_mstep2d<float>(int, const Dom&, const float*, float*, double, cudaStream_t);
 template int launch_mstep2d<double>(int, const Dom&, const double*, double*, double, cudaStream_t);
+template int launch_mstep2d_persist<float>(int, const Dom&, float*, float*, double, int, cudaStream_t);
+template int launch_mstep2d_persist<double>(int, const Dom&, double*, double*, double, int, cudaStream_t);
 
 }  // namespace tslb_cuda

@@ -503,3 +503,31 @@ def test_mstep_solid_graph_and_switch(gpu, oracle_port, dtype):
     fluid = solid == 0
     assert_bitwise(fg, fo, "switch/graph M f", fluid)
     assert_bitwise(mg, mo, "switch/graph M moments", fluid)
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("nsteps", [2, 33, 100])
+def test_mstep2d_persistent_equals_per_pass_launches(gpu, dtype, nsteps, monkeypatch):
+    # small 2-D domains run under one cooperative launch per step() call
+    # (grid barrier between passes); TSLB_PERSIST=0 takes the per-pass
+    # launches / graph replay. Same bits, including odd pass counts (the
+    # ping-pong parity) and the first step after an upload (moments pass)
+    dims, faces = (256, 256, 1), O.lid_cavity(0.1)
+    f0 = O.random_state("d2q9", dims, 21, dtype)
+    out = {}
+    for mode in ("1", "0"):
+        monkeypatch.setenv("TSLB_PERSIST", mode)
+        dev = T.DeviceSolver("d2q9", T.GridDims(*dims), 1.4450867, spec_of(faces), dtype)
+        try:
+            dev.upload_f(f0)
+            l0 = dev.launch_count()
+            dev.step(nsteps)
+            launches = dev.launch_count() - l0
+            dev.step(nsteps + 1)
+            out[mode] = (_moments(dev, "d2q9"), dev.download_f(), launches)
+        finally:
+            dev.close()
+    assert_bitwise(out["1"][0], out["0"][0], "persistent vs per-pass moments")
+    assert_bitwise(out["1"][1], out["0"][1], "persistent vs per-pass f")
+    if nsteps >= 3:  # the moments pass after the upload, then one cooperative launch
+        assert out["1"][2] <= 3 < out["0"][2]
