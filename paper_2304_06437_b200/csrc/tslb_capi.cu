@@ -403,13 +403,15 @@ int materialize(tslb_cuda_sim* h) {
   });
 }
 
-int ph_cg_moments(tslb_cuda_sim* h, cudaStream_t st) {
+int ph_cg_moments(tslb_cuda_sim* h, cudaStream_t st, int k0 = 0, int k1 = -1) {
+  if (k1 < 0) k1 = h->nzl;
+  if (k1 <= k0) return 0;
   Prof p(h, TSLB_K_CG_MOMENTS, st);
   ++h->launches;
   h->stress_pending = false;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
-    return launch_cg_moments<T>(h->lat, h->range(0, h->nzl),
+    return launch_cg_moments<T>(h->lat, h->range(k0, k1),
                                 static_cast<const T*>(h->f[0]),
                                 static_cast<const T*>(h->f[1]), h->tf(), h->solid, st);
   });
@@ -575,8 +577,17 @@ int enqueue_step(tslb_cuda_sim* h) {
     // stream overlaps the interior planes: the interior stream-collide
     // reads phi of owned planes only and writes no slot the exchange
     // sends or receives (one writer per slot)
-    if ((rc = ph_cg_moments(h, h->s))) return rc;
-    if ((rc = exchange_phi_nccl(h, h->s))) return rc;
+    // colour moments of the two boundary planes first: their phi goes to
+    // the neighbours on the comm stream while the interior planes' colour
+    // moments run (they neither read nor write phi's boundary/ghost planes)
+    if ((rc = ph_cg_moments(h, h->s, 0, 1))) return rc;
+    if (h->nzl > 1 && (rc = ph_cg_moments(h, h->s, h->nzl - 1, h->nzl))) return rc;
+    CK(cudaEventRecord(h->ev_b, h->s));
+    CK(cudaStreamWaitEvent(h->cs, h->ev_b, 0));
+    if ((rc = exchange_phi_nccl(h, h->cs))) return rc;
+    CK(cudaEventRecord(h->ev_c, h->cs));
+    if ((rc = ph_cg_moments(h, h->s, 1, h->nzl - 1))) return rc;
+    CK(cudaStreamWaitEvent(h->s, h->ev_c, 0));
     auto scr = [&](int k0, int k1) {
       if (k1 <= k0) return 0;
       Prof p(h, TSLB_K_CG_STREAMCOLL, h->s);
