@@ -82,7 +82,11 @@ constexpr int NT = TX * TY;                // threads = tile columns
 constexpr int NH = 2 * TX + 2 * (TY + 2);  // halo ring nodes (x columns include the corners)
 constexpr int TR = TY + 2;                 // staged tile rows (with y halo)
 constexpr int TC = TR * TX;                // staged elements per moment array
-constexpr int kDefaultLz = 64;             // planes marched per CTA
+// planes marched per CTA: the march re-reads one halo plane below and above
+// per column, so longer columns amortise it; s28 sweep at 1024^3 (fp64 math,
+// same box): 32 / 64 / 128 / 256 / 512 -> 33.3 / 33.9 / 34.1 / 34.1-34.2 /
+// 33.7 GLUPS, D3Q27 channel 64 / 128 / 256 -> 20.56 / 20.61 / 20.73
+constexpr int kDefaultLz = 128;
 
 template <class L>
 __host__ __device__ constexpr bool is_reg(int a) {
