@@ -85,7 +85,8 @@ constexpr int TC = TR * TX;                // staged elements per moment array
 // planes marched per CTA: the march re-reads one halo plane below and above
 // per column, so longer columns amortise it; s28 sweep at 1024^3 (fp64 math,
 // same box): 32 / 64 / 128 / 256 / 512 -> 33.3 / 33.9 / 34.1 / 34.1-34.2 /
-// 33.7 GLUPS, D3Q27 channel 64 / 128 / 256 -> 20.56 / 20.61 / 20.73
+// 33.7 GLUPS, D3Q27 channel 64 / 128 / 256 -> 20.56 / 20.61 / 20.73; fp32
+// node math 64 / 128 -> 44.1-44.3 / 44.9
 constexpr int kDefaultLz = 128;
 
 template <class L>
