@@ -37,6 +37,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+L2_NOTE = "state >> 126 MB L2, no flush needed"
 METRIC = "GLUPS and % of HBM roofline (D3Q19 1024^3) at 1/2/4/8 B200 vs CPU ref"
 
 # per-GPU workloads (BASELINE.json configs)
@@ -60,6 +61,10 @@ WORKLOADS = {
     "cavity-d2q9": dict(lat="d2q9", dims=(256, 256, 1), faces="lid", comps=1, init="rest", amp=0.0,
                         omega=1 / (0.064 * 3 + 0.5), storage="f64",
                         desc="D2Q9 lid-driven cavity {n}, Re 100, fp64"),
+    # BASELINE config 5: one fixed domain split into N z slabs (strong scaling)
+    "tgv-c5": dict(lat="d3q19", dims=(2048, 1024, 1024), faces="periodic", comps=1, init="taylor_green",
+                   amp=0.03, omega=1.6, storage="f32", strong=True,
+                   desc="D3Q19 periodic Taylor-Green 2048x1024x1024 (BASELINE config 5), {n} z slab per GPU"),
 }
 
 
@@ -168,6 +173,48 @@ def cpu_reference(steps, warmup, sample_nz=16, workers=None):
     sample = (f"D3Q19 periodic Taylor-Green slab {dims[0]}x{dims[1]}x{dims[2]} fp32 (fp64 node math), {steps} steps "
               f"after {warmup} warm-up, WorkerPool({cores})")
     return glups, dict(kind=kind, cores=cores, sample=sample, seconds=t)
+
+
+def mem_available():
+    try:
+        with open("/proc/meminfo") as fh:
+            for line in fh:
+                if line.startswith("MemAvailable:"):
+                    return int(line.split()[1]) * 1024
+    except OSError:
+        pass
+    return 0
+
+
+def cpu_reference_full(dims, steps, warmup, workers=None):
+    """The reference CPU path on the WHOLE per-GPU workload: the reference's
+    fused_step (WorkerPool over every host core) on the nx x ny x nz
+    periodic Taylor-Green state of the reference's own
+    initialize_regularized (oracle/ref_capi.cpp tslbref_time_tgv).
+    Returns (GLUPS, info) or None when the host cannot hold the state."""
+    import ctypes as C
+
+    from oracle import oracle as O
+    if not os.path.exists(O.REF_SO):
+        return None
+    n = int(np.prod(dims))
+    need = n * (29 * 4 + 5)  # f + moments (fp32), slow mask, solid mask
+    if mem_available() < 1.08 * need:
+        return None
+    workers = workers or os.cpu_count() or 1
+    lib = C.CDLL(O.REF_SO)
+    fn = lib.tslbref_time_tgv
+    fn.argtypes = [C.c_int] * 4 + [C.c_double, C.c_double, C.c_long, C.c_long, C.c_int, C.c_int, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]
+    ti, ts, dg = C.c_double(), C.c_double(), C.c_uint64()
+    if fn(1, *dims, 1.6, 0.03, int(steps), int(warmup), int(workers), 0, C.byref(ti), C.byref(ts), C.byref(dg)):
+        lib.tslbref_last_error.restype = C.c_char_p
+        raise RuntimeError(lib.tslbref_last_error().decode())
+    what = "x".join(str(v) for v in dims)
+    sample = (f"the whole workload: D3Q19 periodic Taylor-Green {what} fp32 (fp64 node math), {steps} steps after "
+              f"{warmup} warm-up, WorkerPool({workers})")
+    return n * steps / ts.value / 1e9, dict(kind="reference", cores=workers, sample=sample, seconds=ts.value,
+                                            init_seconds=round(ti.value, 1), digest=f"{dg.value:016x}")
 
 
 def cpu_reference_workload(name, W, dims, steps, warmup, sample_nz=16, workers=None):
@@ -319,7 +366,48 @@ def _json_stdout():
     return os.fdopen(keep, "w", buffering=1)
 
 
+def _free_port():
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def _relaunch(n):
+    """`bench.py --gpus N` outside torchrun: re-run this command as N ranks
+    (one process per GPU) under torch.distributed.run and return its exit
+    code; rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+    env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
+    return subprocess.run(cmd, env=env).returncode
+
+
+def launch_check(world, rank):
+    """--launch-check: the ranks this command started, gathered over gloo
+    (CPU; no GPU needed) -- the test of the N-rank launch path."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+        ranks = [None] * world
+        dist.all_gather_object(ranks, (rank, os.getpid()))
+        dist.destroy_process_group()
+    else:
+        ranks = [(rank, os.getpid())]
+    return {"launch_check": True, "n_gpus": world, "ranks": [r for r, _ in ranks],
+            "pids_distinct": len({p for _, p in ranks}) == world}
+
+
 def main():
+    # --gpus N without a torchrun environment: one process per GPU
+    world_env = os.environ.get("WORLD_SIZE")
+    pre = argparse.ArgumentParser(add_help=False)
+    pre.add_argument("--gpus", type=int, default=1)
+    ngpus = pre.parse_known_args()[0].gpus
+    if world_env is None and ngpus > 1:
+        sys.exit(_relaunch(ngpus))
+    if world_env is not None and int(world_env) != ngpus:
+        raise SystemExit(f"bench.py: --gpus {ngpus} but WORLD_SIZE={world_env}: launch one rank per GPU")
     out_stream = _json_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -334,6 +422,11 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sample-nz", type=int, default=16)
+    ap.add_argument("--sample-only", action="store_true",
+                    help="--impl reference: time the 1024 x 1024 x sample_nz slab even if the host holds the "
+                         "whole workload")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="report the ranks this command launched (gloo, CPU) and exit")
     ap.add_argument("--nccl-self", action="store_true",
                     help="N=1 probe of the multi-GPU step: the GPU's domain is a z slab of a twice-as-tall box on "
                          "a one-rank NCCL communicator (its own up/down neighbour), so every step runs the "
@@ -343,34 +436,63 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.launch_check:
+        info = launch_check(world, rank)
+        if rank == 0:
+            print(json.dumps(info), file=out_stream)
+        return
     W = dict(WORKLOADS[args.workload])
     dims = W["dims"]
+    strong = W.get("strong", False)
     if args.n and dims[2] > 1:
         dims = (args.n, args.n, args.n)
     if args.dims and dims[2] > 1:
         dims = tuple(int(v) for v in args.dims.split(","))
+    if strong:
+        # the fixed global domain (--n / --dims: its extent), one z slab per rank
+        if dims[2] % world:
+            raise SystemExit(f"{args.workload}: nz = {dims[2]} does not split into {world} slabs")
+        dims = (dims[0], dims[1], dims[2] // world)
     default = args.workload == "tgv-d3q19" and not args.nccl_self
+    scaling = "strong" if strong else "weak"
     metric = METRIC if default else f"GLUPS ({args.workload}{', NCCL self-exchange probe' if args.nccl_self else ''})"
 
     if args.impl == "reference":
         if rank != 0:
             return
-        steps, warm = args.steps, max(1, min(args.warmup, 2))
-        glups, info = cpu_reference(steps, warm, args.sample_nz)
+        steps, warm = args.steps, args.warmup
+        # the whole per-GPU workload when the host holds it (1024^3: 130 GB),
+        # else a 1024 x 1024 x 16 slab sample of it
+        full = None
+        if default and not args.sample_only:
+            full = cpu_reference_full(dims, steps, warm)
+        if full:
+            glups, info = full
+        else:
+            warm = max(1, min(warm, 2))
+            glups, info = cpu_reference(steps, warm, args.sample_nz)
         # the host, and a 1-worker row beside the all-cores one
         g1, info1 = cpu_reference(1, 1, args.sample_nz, workers=1)
+        n_desc = "x".join(str(v) for v in dims)
+        cfg = ({"workload": WORKLOADS["tgv-d3q19"]["desc"].format(n=n_desc) + " per GPU", "lattice": "d3q19",
+                "nodes": int(np.prod(dims)), "storage": "f32", "node_math": "f64", "l2": L2_NOTE,
+                "parallelism": "single GPU"}
+               if full else
+               {"workload": f"D3Q19 periodic Taylor-Green, sample of the {dims[0]}^3 fp32 workload",
+                "lattice": "d3q19", "storage": "f32", "sample": info["sample"]})
         out = {"metric": METRIC, "value": round(glups, 6), "unit": "GLUPS", "n_gpus": args.gpus, "steps": steps,
                "warmup": warm, "ms_per_step": round(info["seconds"] / steps * 1e3, 3), "higher_is_better": True,
                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-               "impl": "reference",
-               "config": {"workload": f"D3Q19 periodic Taylor-Green, sample of the {dims[0]}^3 fp32 workload",
-                          "lattice": "d3q19", "storage": "f32", "sample": info["sample"]},
+               "impl": "reference", "same_config": bool(full),
+               "config": cfg,
                "cpu_baseline": {"value": round(glups, 6), "unit": "GLUPS", "cores": info["cores"],
                                 "kind": info["kind"], "sample": info["sample"]},
                "e2e": {"value": round(glups, 6), "unit": "GLUPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                "cpu_1worker": {"value": round(g1, 6), "unit": "GLUPS", "cores": info1["cores"],
                                "kind": info1["kind"], "sample": info1["sample"]},
                "host": host_info()}
+        if full:
+            out["reference_run"] = {"init_seconds": info["init_seconds"], "f_digest": info["digest"]}
         print(json.dumps(out), file=out_stream)
         return
 
@@ -547,25 +669,25 @@ def main():
         n_desc = f"{nx}x{ny}x{nzp}" if lat.dim == 3 else f"{nx}x{ny}"
         out = {"metric": metric, "value": round(glups, 4), "unit": "GLUPS", "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": round(ms / args.steps, 4), "higher_is_better": True,
-               "scaling": "weak", "vs_baseline": None,
+               "scaling": scaling, "vs_baseline": None,
                "dtype": ("f64" if args.math == "f64" else "f32") if W["comps"] == 1 else W["storage"],
                "data": "synthetic",
                "config": {"workload": W["desc"].format(n=n_desc) + (" per GPU" if lat.dim == 3 else "")
-                          + (f" (global {nx}x{ny}x{nz_g}, z slabs)" if world > 1 else ""),
+                          + (f" (global {nx}x{ny}x{nz_g}, {world} z slabs)" if world > 1 else ""),
                           "lattice": lat.name, "nodes": nodes, "storage": W["storage"],
                           **({"solid_fraction": round(float(solid.mean()), 4)} if masked else {}),
                           "node_math": (args.math if W["comps"] == 1 else W["storage"] + " (as the reference)"),
-                          "schedule": ({"m": "M: moment-resident single pass (populations rebuilt in shared "
-                                             "memory; f materialised on read)",
-                                        "f1": "F1: moments + fused stream-collide"}[sched] if W["comps"] == 1
-                                       else "colour moments + fused gradient/prepare/stream-collide-recolour"
-                                       if "cg_gradient" not in prof
-                                       else "colour moments + gradient + fused prepare/stream-collide-recolour"),
-                          "l2": "state >> 126 MB L2, no flush needed" if nodes > 10 ** 7
-                          else "L2-resident (correctness config)",
+                          "l2": L2_NOTE if nodes > 10 ** 7 else "L2-resident (correctness config)",
                           "parallelism": f"z-slab x{world}" if world > 1 else
                           "one z slab on a 1-rank NCCL communicator (self halo exchange)" if self_x
                           else "single GPU"},
+               # (how this arm computes the workload; `config` is what both arms run)
+               "schedule": ({"m": "M: moment-resident single pass (populations rebuilt in shared "
+                                  "memory; f materialised on read)",
+                             "f1": "F1: moments + fused stream-collide"}[sched] if W["comps"] == 1
+                            else "colour moments + fused gradient/prepare/stream-collide-recolour"
+                            if "cg_gradient" not in prof
+                            else "colour moments + gradient + fused prepare/stream-collide-recolour"),
                "roofline": roof, "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(out), file=out_stream)
     sim.close()

@@ -8,10 +8,13 @@
 // linear_index (fields.hpp:26-29). Scalars: 0 = double, 1 = float storage.
 // Lattices: 0 = D2Q9, 1 = D3Q19 (the reference has no D3Q27).
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <exception>
 #include <memory>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "tslb/bench.hpp"
@@ -142,7 +145,10 @@ void run_single(int nx, int ny, int nz, double omega, const int* kinds,
   if (moments) load_moments(s, moments);
   std::unique_ptr<WorkerPool> pool;
   if (workers > 1) pool = std::make_unique<WorkerPool>(workers);
-  auto scratch = s.f;
+  // the second population buffer only for the two-buffer modes (a full-size
+  // fused run -- tests/test_gpu_configs.py -- does not need the extra copy)
+  std::vector<FieldArray<T>> scratch;
+  if (mode == 1 || mode == 4) scratch = s.f;
   for (long k = 0; k < steps; ++k) {
     switch (mode) {
       case 0: fused_step<Lat, T>(s, geo, spec, prm, pool.get()); break;
@@ -379,6 +385,103 @@ int tslbref_time_two(int lattice, int scalar, int nx, int ny, int nz,
         const auto t1 = std::chrono::steady_clock::now();
         *seconds = std::chrono::duration<double>(t1 - t0).count();
       });
+    });
+  });
+}
+
+// The headline workload whole: D3Q19 periodic Taylor-Green on nx*ny*nz with
+// the reference's own SingleFluidSim and initialize_regularized
+// (kernels.hpp:296-311; the state bench.py's device init writes: rho =
+// 1 + 3 (U^2/16)(cos 2X + cos 2Y)(cos 2Z + 2), u = U (sin X cos Y cos Z,
+// -cos X sin Y cos Z, 0), Pi^neq = 0), `warmup` untimed steps, then `steps`
+// timed ones (bench.py --impl reference). *digest: fnv1a of f afterwards.
+// classify_full != 0: classify_nodes over the whole grid (the check of the
+// expansion, tests/test_cpu_oracle.py).
+int tslbref_time_tgv(int scalar, int nx, int ny, int nz, double omega, double amp, long steps, long warmup,
+                     int workers, int classify_full, double* init_seconds, double* seconds, std::uint64_t* digest) {
+  return guarded([&] {
+    with_scalar(scalar, [&](auto z) {
+      using T = decltype(z);
+      using Lat = D3Q19;
+      const GridDims g{nx, ny, nz};
+      CollisionParams<T> prm;
+      prm.omega = T(omega);
+      std::unique_ptr<WorkerPool> pool;
+      if (workers > 1) pool = std::make_unique<WorkerPool>(workers);
+      const auto t0 = std::chrono::steady_clock::now();
+      if (nx < 3 || ny < 3 || nz < 3) throw std::invalid_argument("tslbref_time_tgv: nx, ny, nz >= 3");
+      const auto spec = BoundarySpec<T>::all_periodic();
+      // classify_nodes (boundary.hpp:61-111) on 3x3x3 and expanded: without
+      // solids a node's slow mask only depends on whether it sits on the low
+      // face, inside, or on the high face of each axis (the serial loop over
+      // 10^9 nodes would take minutes)
+      const NodeGeometry g3 = classify_nodes<T, Lat>(GridDims{3, 3, 3}, spec);
+      NodeGeometry geo;
+      geo.dims = g;
+      geo.solid.assign(g.n(), 0);
+      geo.slow_mask.resize(g.n());
+      geo.n_fluid = g.n();
+      auto cls = [](int c, int n) { return c == 0 ? 0 : c == n - 1 ? 2 : 1; };
+      auto fill_geo = [&](int k) {
+        for (int j = 0; j < ny; ++j)
+          for (int i = 0; i < nx; ++i)
+            geo.slow_mask[linear_index(g, i, j, k)] =
+                g3.slow_mask[linear_index(GridDims{3, 3, 3}, cls(i, nx), cls(j, ny), cls(k, nz))];
+      };
+      auto par = [&](auto&& fn) {
+        const int nt = std::max(1, workers);
+        std::vector<std::thread> th;
+        for (int t = 0; t < nt; ++t)
+          th.emplace_back([&, t] {
+            for (int k = t; k < nz; k += nt) fn(k);
+          });
+        for (auto& x : th) x.join();
+      };
+      if (classify_full) geo = classify_nodes<T, Lat>(g, spec);
+      else par(fill_geo);
+      FieldSet<T> s = allocate_fields<T>(g, make_descriptor<T>(Lat::kind));
+      const auto tc = std::chrono::steady_clock::now();
+      // initialize_regularized's node loop (kernels.hpp:296-311), split over
+      // z planes on the worker threads (a 1024^3 state takes minutes on one
+      // thread); trig from per-axis tables
+      const double pi2 = 2.0 * 3.14159265358979323846;
+      auto tab = [&](int n, double (*fn)(double), double mul) {
+        std::vector<double> t(static_cast<std::size_t>(n));
+        for (int i = 0; i < n; ++i) t[std::size_t(i)] = fn(mul * pi2 * (i + 0.5) / n);
+        return t;
+      };
+      const auto sx = tab(nx, std::sin, 1), cx = tab(nx, std::cos, 1), c2x = tab(nx, std::cos, 2);
+      const auto sy = tab(ny, std::sin, 1), cy = tab(ny, std::cos, 1), c2y = tab(ny, std::cos, 2);
+      const auto cz = tab(nz, std::cos, 1), c2z = tab(nz, std::cos, 2);
+      auto plane = [&](int k) {
+        for (int j = 0; j < ny; ++j)
+          for (int i = 0; i < nx; ++i) {
+            const double rho = 1.0 + 3.0 * (amp * amp / 16.0) * (c2x[i] + c2y[j]) * (c2z[k] + 2.0);
+            const double ux = amp * sx[i] * cy[j] * cz[k];
+            const double uy = -amp * cx[i] * sy[j] * cz[k];
+            const NodeMoments<T> m = prepare_node<T>(T(rho), T(ux), T(uy), T(0), T(0), T(0), T(0), T(0), T(0), T(0));
+            const Eigen::Index idx = Eigen::Index(linear_index(g, i, j, k));
+            for_each_dir<Lat>([&](auto A) {
+              constexpr int a = A.value;
+              s.f[a][idx] = equilibrium_dir<Lat, a, T>(m) + regularized_dir<Lat, a, T>(m);
+            });
+          }
+      };
+      par(plane);
+      // SingleFluidSim::step (solver.hpp:87-90) is fused_step
+      const auto t1 = std::chrono::steady_clock::now();
+      for (long k = 0; k < warmup; ++k) fused_step<Lat, T>(s, geo, spec, prm, pool.get());
+      const auto t2 = std::chrono::steady_clock::now();
+      for (long k = 0; k < steps; ++k) fused_step<Lat, T>(s, geo, spec, prm, pool.get());
+      const auto t3 = std::chrono::steady_clock::now();
+      *init_seconds = std::chrono::duration<double>(t1 - t0).count();
+      if (std::getenv("TSLBREF_VERBOSE"))
+        std::fprintf(stderr, "tslbref_time_tgv: construct %.2f s, init %.2f s\n",
+                     std::chrono::duration<double>(tc - t0).count(), std::chrono::duration<double>(t1 - tc).count());
+      *seconds = std::chrono::duration<double>(t3 - t2).count();
+      std::uint64_t h = 0xcbf29ce484222325ull;
+      for (const auto& a : s.f) h = fnv1a(a.data(), std::size_t(a.size()) * sizeof(T), h);
+      *digest = h;
     });
   });
 }

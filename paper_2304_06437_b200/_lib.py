@@ -39,7 +39,8 @@ def load(path: str | None = None) -> C.CDLL:
     global _lib
     if _lib is not None:
         return _lib
-    p = path or LIB_PATH
+    # TSLB_LIB: a measurement variant (same-box A/B runs, scripts/gpu_ab_libs.sh)
+    p = path or os.environ.get("TSLB_LIB") or LIB_PATH
     if not os.path.exists(p):
         raise TslbCudaError(
             f"{p} is missing: build it with `python -m paper_2304_06437_b200.build` "

@@ -37,38 +37,50 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src, obj):
-    cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+def _compile(src, obj, extra=()):
+    cmd = [NVCC, *FLAGS, *extra, "-c", src, "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
     return obj
 
 
-def build(verbose: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(verbose: bool = False, out: str | None = None, defines: tuple = ()) -> str:
+    """Build the product library (default), or -- with `defines` -- a
+    measurement variant (-D flags) into `out` with its own object directory
+    (same-box A/B runs load it through TSLB_LIB; the product .so is untouched)."""
+    lib = out or LIB
+    obj_dir = OBJ if not defines else os.path.join(OBJ, "v_" + "_".join(d.replace("=", "-") for d in defines))
+    extra = [f"-D{d}" for d in defines]
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
     hdrs = _headers()
     jobs = []
     objs = []
     for s in srcs:
-        o = os.path.join(OBJ, os.path.basename(s)[:-3] + ".o")
+        o = os.path.join(obj_dir, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if _stale(o, [s, *hdrs]):
             jobs.append((s, o))
     if jobs:
         with cf.ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as ex:
-            for o in ex.map(lambda so: _compile(*so), jobs):
+            for o in ex.map(lambda so: _compile(*so, extra), jobs):
                 if verbose:
                     print("compiled", o, file=sys.stderr)
-    if jobs or _stale(LIB, objs):
-        cmd = [NVCC, "-shared", *GENCODE, "-Wno-deprecated-gpu-targets", "-o", LIB, *objs,
+    if jobs or _stale(lib, objs):
+        os.makedirs(os.path.dirname(os.path.abspath(lib)), exist_ok=True)
+        cmd = [NVCC, "-shared", *GENCODE, "-Wno-deprecated-gpu-targets", "-o", lib, *objs,
                "-lcudart_static", "-ldl", "-lrt", "-lpthread"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(verbose=True))
+    # python build.py [OUT.so -DNAME[=V] ...]: a measurement variant
+    args = sys.argv[1:]
+    if args:
+        print(build(verbose=True, out=args[0], defines=tuple(a[2:] for a in args[1:] if a.startswith("-D"))))
+    else:
+        print(build(verbose=True))

@@ -117,7 +117,9 @@ struct tslb_cuda_sim {
   InitSpec f0_spec{};
   int lz = 0;          // planes per CTA of the M kernel (0 = default; TSLB_LZ)
   void* mo2 = nullptr; // second moment buffer of the M schedule (ping-pong)
-  void* gm = nullptr;  // M on z slabs: neighbours' boundary-plane moments [NM][2][plane]
+  void* gm = nullptr;  // M on z slabs: neighbours' boundary-plane moments [2][NM][plane] (below, above)
+  void* sx = nullptr;  // M on z slabs: own boundary-plane moments to send [2][NM][plane] (plane 0, nzl - 1)
+  int lzb = 0;         // planes of each boundary chunk on slabs (0 = default; TSLB_LZB)
   void* graph_mo = nullptr;  // moment buffer the captured graph starts from
   MstepMaps* mmaps = nullptr;  // TMA tensor maps of the M kernel's inputs
   int vx = 0;          // nodes per thread in the vectorised kernel (0 = default; TSLB_VX)
@@ -302,46 +304,73 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
   });
 }
 
-// M schedule: m(t) in h->mo -> m(t+1) in h->mo2 for z chunks [c0, c0+n)
-// (n <= 0: all); the caller swaps the buffers once every chunk is done
-int ph_mstep(tslb_cuda_sim* h, cudaStream_t st, int c0 = 0, int n = 0) {
+// M schedule: m(t) in h->mo -> m(t+1) in h->mo2 for planes [z0, z1) (z1 <= 0:
+// to the end); the caller swaps the buffers once every plane is done. On
+// slabs the kernel also copies the new boundary planes into h->sx.
+int ph_mstep(tslb_cuda_sim* h, cudaStream_t st, int z0 = 0, int z1 = 0) {
   Prof p(h, TSLB_K_MSTEP, st);
   ++h->launches;
   int rc = by_scalar(h, [&](auto z) {
     using T = decltype(z);
     return launch_mstep<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<const T*>(h->mo),
-                           static_cast<const T*>(h->gm), static_cast<T*>(h->mo2), h->omega, h->lz, c0, n,
-                           h->mmaps, h->sbits ? h->sbits + size_t(h->d.ghost) * h->plane() : nullptr, st);
+                           static_cast<const T*>(h->gm), static_cast<T*>(h->mo2), static_cast<T*>(h->sx), h->omega,
+                           h->lz, z0, z1, h->mmaps,
+                           h->sbits ? h->sbits + size_t(h->d.ghost) * h->plane() : nullptr, st);
   });
+  if (rc < 0) return set_err(TSLB_ECUDA, "k_mstep launch: %s", cudaGetErrorString(cudaError_t(-rc)));
   if (rc) return set_err(TSLB_ESTATE, "M step not supported for this domain");
   return 0;
 }
 
-// M on slabs: ship the boundary planes of the moment buffer `buf` into the
-// neighbours' ghost planes (their `gm`), all 1+D+np arrays. Same grouping
-// as the F1 exchange: +z direction first, then -z, so every peer pair
-// matches its sends and receives in order (also when up == down).
-int exchange_moments_nccl(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
+// planes per boundary chunk of a slab step: thin, so the halo exchange
+// starts early and overlaps the interior chunks (TSLB_LZB overrides)
+constexpr int kBoundaryLz = 16;
+int boundary_planes(const tslb_cuda_sim* h) {
+  static const int env = [] {
+    const char* e = std::getenv("TSLB_LZB");
+    return e ? std::atoi(e) : 0;
+  }();
+  const int b = h->lzb > 0 ? h->lzb : env > 0 ? env : kBoundaryLz;
+  return std::min(b, h->nzl);
+}
+
+size_t moment_plane_block(const tslb_cuda_sim* h) {  // bytes of NM planes
+  return size_t(1 + h->dim + h->np) * size_t(h->plane()) * h->esz;
+}
+
+// the boundary planes of the moment buffer `buf` into the send buffer (the
+// first step of a run, whose moments come from the moments pass; later
+// steps have the M kernel write them)
+int pack_moments(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
+  const size_t pb = size_t(h->plane()) * h->esz;
+  const int nm = 1 + h->dim + h->np;
+  for (int side = 0; side < 2; ++side) {
+    const int k = side ? h->nzl - 1 : 0;
+    const char* src = static_cast<const char*>(buf) + size_t(k) * pb;
+    char* dst = static_cast<char*>(h->sx) + size_t(side) * moment_plane_block(h);
+    CK(cudaMemcpy2DAsync(dst, pb, src, size_t(h->d.mstride) * h->esz, pb, size_t(nm), cudaMemcpyDeviceToDevice, st));
+  }
+  return 0;
+}
+
+// M on slabs: the packed boundary planes (h->sx, all 1+D+np arrays in one
+// block per face) into the neighbours' ghost planes (their `gm`): one send
+// and one receive per face. Same grouping as the F1 exchange: +z direction
+// first, then -z, so every peer pair matches its sends and receives in order
+// (also when up == down).
+int exchange_moments_nccl(tslb_cuda_sim* h, cudaStream_t st) {
   NcclApi& N = nccl();
   const ncclDataType_t ty = h->scalar == TSLB_F64 ? ncclFloat64 : ncclFloat32;
-  const size_t cnt = size_t(h->plane());
-  const int nm = 1 + h->dim + h->np;
-  auto arr = [&](int c, int k) {
-    return static_cast<const char*>(buf) + (size_t(c) * h->d.mstride + size_t(k) * h->plane()) * h->esz;
-  };
-  auto ghost = [&](int c, int side) {
-    return static_cast<char*>(h->gm) + (size_t(2 * c + side) * h->plane()) * h->esz;
-  };
+  const size_t cnt = size_t(1 + h->dim + h->np) * size_t(h->plane());
+  const size_t blk = moment_plane_block(h);
+  char* sx = static_cast<char*>(h->sx);
+  char* gm = static_cast<char*>(h->gm);
   Prof p(h, TSLB_K_EXCHANGE, st);
   N.GroupStart();
-  if (h->up >= 0)
-    for (int c = 0; c < nm; ++c) N.Send(arr(c, h->nzl - 1), cnt, ty, h->up, h->comm, st);
-  if (h->down >= 0)
-    for (int c = 0; c < nm; ++c) N.Recv(ghost(c, 0), cnt, ty, h->down, h->comm, st);
-  if (h->down >= 0)
-    for (int c = 0; c < nm; ++c) N.Send(arr(c, 0), cnt, ty, h->down, h->comm, st);
-  if (h->up >= 0)
-    for (int c = 0; c < nm; ++c) N.Recv(ghost(c, 1), cnt, ty, h->up, h->comm, st);
+  if (h->up >= 0) N.Send(sx + blk, cnt, ty, h->up, h->comm, st);
+  if (h->down >= 0) N.Recv(gm, cnt, ty, h->down, h->comm, st);
+  if (h->down >= 0) N.Send(sx, cnt, ty, h->down, h->comm, st);
+  if (h->up >= 0) N.Recv(gm + blk, cnt, ty, h->up, h->comm, st);
   ncclResult_t r = N.GroupEnd();
   if (r != ncclSuccess)
     return set_err(TSLB_ECUDA, "NCCL moment halo exchange: %s", N.ErrStr ? N.ErrStr(r) : "error");
@@ -349,22 +378,13 @@ int exchange_moments_nccl(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
 }
 
 // local transport of the same (single-device verification)
-int exchange_moments_local(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
-  const size_t bytes = size_t(h->plane()) * h->esz;
-  const int nm = 1 + h->dim + h->np;
-  auto arr = [&](int c, int k) {
-    return static_cast<const char*>(buf) + (size_t(c) * h->d.mstride + size_t(k) * h->plane()) * h->esz;
-  };
-  auto ghost = [&](tslb_cuda_sim* p, int c, int side) {
-    return static_cast<char*>(p->gm) + (size_t(2 * c + side) * p->plane()) * p->esz;
-  };
+int exchange_moments_local(tslb_cuda_sim* h, cudaStream_t st) {
+  const size_t blk = moment_plane_block(h);
   Prof p(h, TSLB_K_EXCHANGE, st);
-  for (int c = 0; c < nm; ++c) {
-    if (h->up_peer)
-      CK(cudaMemcpyAsync(ghost(h->up_peer, c, 0), arr(c, h->nzl - 1), bytes, cudaMemcpyDeviceToDevice, st));
-    if (h->down_peer)
-      CK(cudaMemcpyAsync(ghost(h->down_peer, c, 1), arr(c, 0), bytes, cudaMemcpyDeviceToDevice, st));
-  }
+  if (h->up_peer)
+    CK(cudaMemcpyAsync(h->up_peer->gm, static_cast<char*>(h->sx) + blk, blk, cudaMemcpyDeviceToDevice, st));
+  if (h->down_peer)
+    CK(cudaMemcpyAsync(static_cast<char*>(h->down_peer->gm) + blk, h->sx, blk, cudaMemcpyDeviceToDevice, st));
   return 0;
 }
 
@@ -641,23 +661,30 @@ int enqueue_step(tslb_cuda_sim* h) {
       // first step from stored populations: the moments pass (and, on
       // slabs, the ghost planes of m(t)); the stream-collide is deferred
       if ((rc = first_moments(h, h->s))) return rc;
-      if (h->xmode == 1 && (rc = exchange_moments_nccl(h, h->mo, h->s))) return rc;
+      if (h->xmode == 1) {
+        if ((rc = pack_moments(h, h->mo, h->s))) return rc;
+        if ((rc = exchange_moments_nccl(h, h->s))) return rc;
+      }
       h->fimplicit = true;
     } else if (h->xmode == 1) {
-      // slab: the two boundary chunks first, their new boundary planes go to
-      // the neighbours on the comm stream while the interior chunks run
-      const int nzc = mstep_chunks(h->range(0, h->nzl), h->lz);
-      if (nzc <= 2) {
+      // slab: the two thin boundary chunks run on the (high-priority) comm
+      // stream and write the new boundary planes into the send buffer; the
+      // exchange follows them there, while the interior chunk runs on the
+      // solver stream at the same time. The boundary chunks start once the
+      // previous step is complete on both streams; the solver stream joins
+      // the exchange before the next step.
+      const int b = boundary_planes(h);
+      if (h->nzl <= 2 * b) {
         if ((rc = ph_mstep(h, h->s))) return rc;
-        if ((rc = exchange_moments_nccl(h, h->mo2, h->s))) return rc;
+        if ((rc = exchange_moments_nccl(h, h->s))) return rc;
       } else {
-        if ((rc = ph_mstep(h, h->s, 0, 1))) return rc;
-        if ((rc = ph_mstep(h, h->s, nzc - 1, 1))) return rc;
         CK(cudaEventRecord(h->ev_b, h->s));
         CK(cudaStreamWaitEvent(h->cs, h->ev_b, 0));
-        if ((rc = exchange_moments_nccl(h, h->mo2, h->cs))) return rc;
+        if ((rc = ph_mstep(h, h->cs, 0, b))) return rc;
+        if ((rc = ph_mstep(h, h->cs, h->nzl - b, h->nzl))) return rc;
+        if ((rc = exchange_moments_nccl(h, h->cs))) return rc;
         CK(cudaEventRecord(h->ev_c, h->cs));
-        if ((rc = ph_mstep(h, h->s, 1, nzc - 2))) return rc;
+        if ((rc = ph_mstep(h, h->s, b, h->nzl - b))) return rc;
         CK(cudaStreamWaitEvent(h->s, h->ev_c, 0));
       }
       std::swap(h->mo, h->mo2);
@@ -892,15 +919,17 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
     // M needs a second moment buffer (and ghost planes on slabs); where HBM
     // cannot hold it (e.g. D3Q27 1024^3 fp32) the solver stays on F1
     if (!(e && !std::strcmp(e, "f1"))) {
+      // (slabs: the ghost planes and the packed send buffer, [2][NM][plane] each)
       const size_t gb = decomposed ? size_t(d.plane) * 2 * (1 + h->dim + h->np) * h->esz : 0;
       // masked geometries: 4 B of solid bits per node (+ the ghost planes)
       const size_t sb = d.has_solid ? size_t(d.plane) * (nzl + 2 * d.ghost) * 4 : 0;
       if (cudaMalloc(&h->mo2, mbytes) == cudaSuccess &&
-          (!gb || cudaMalloc(&h->gm, gb) == cudaSuccess) &&
+          (!gb || cudaMalloc(&h->gm, gb) == cudaSuccess) && (!gb || cudaMalloc(&h->sx, gb) == cudaSuccess) &&
           (!sb || cudaMalloc(reinterpret_cast<void**>(&h->sbits), sb) == cudaSuccess)) {
-        h->bytes += mbytes + gb + sb;
+        h->bytes += mbytes + 2 * gb + sb;
         CK(cudaMemsetAsync(h->mo2, 0, mbytes, h->s));
         if (gb) CK(cudaMemsetAsync(h->gm, 0, gb, h->s));
+        if (gb) CK(cudaMemsetAsync(h->sx, 0, gb, h->s));
         if (sb && launch_solid_bits(lattice, d, h->solid, h->sbits, h->s))
           return fail(set_err(TSLB_ECUDA, "solid bits: launch failed"));
         h->sched = TSLB_SCHED_M;
@@ -908,8 +937,10 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
         cudaGetLastError();  // clear the allocation failure
         if (h->mo2) cudaFree(h->mo2);
         if (h->gm) cudaFree(h->gm);
+        if (h->sx) cudaFree(h->sx);
         h->mo2 = nullptr;
         h->gm = nullptr;
+        h->sx = nullptr;
       }
     }
   }
@@ -1013,7 +1044,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   if (h->s) cudaStreamSynchronize(h->s);
   if (h->cs) cudaStreamSynchronize(h->cs);
   if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
-  void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->phig, h->two, h->flag, h->solid, h->slow,
+  void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->sx, h->phig, h->two, h->flag, h->solid, h->slow,
                   h->sbits, h->scratch, h->red, h->dig, h->recv_lo, h->recv_hi};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1057,7 +1088,9 @@ int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
     if (h->decomposed && !h->gm) {
       const size_t gb = size_t(h->plane()) * 2 * (1 + h->dim + h->np) * h->esz;
       if (int rc = alloc(h, &h->gm, gb)) return rc;
+      if (int rc = alloc(h, &h->sx, gb)) return rc;
       CK(cudaMemsetAsync(h->gm, 0, gb, h->s));
+      CK(cudaMemsetAsync(h->sx, 0, gb, h->s));
     }
     if (h->d.has_solid && !h->sbits) {
       if (int rc = alloc(h, reinterpret_cast<void**>(&h->sbits),
@@ -1337,6 +1370,7 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
                                            static_cast<T*>(h->mo2), h->omega, n, h->s);
         });
       }
+      if (rc < 0) return set_err(TSLB_ECUDA, "k_mstep2d_persist launch: %s", cudaGetErrorString(cudaError_t(-rc)));
       if (rc) break;  // not co-resident: the regular launches below
       ++h->launches;
       if (n & 1) std::swap(h->mo, h->mo2);
@@ -1347,15 +1381,16 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
   // small domains are launch bound: replay a captured graph of G steps
   constexpr int64_t kGraphMaxNodes = int64_t(8) << 20;
   constexpr long kGraphSteps = 32;  // even: an M graph ends on the buffer it starts from
-  if (h->graphs_ok && !h->prof && h->xmode == 0 && h->n() <= kGraphMaxNodes && nsteps >= kGraphSteps) {
+  // (steps still owed only: the persistent path above may have run them all)
+  if (h->graphs_ok && !h->prof && h->xmode == 0 && h->n() <= kGraphMaxNodes && nsteps - done >= kGraphSteps) {
     // an M graph replays M passes only: leave the stored-f state first, and
     // start from the moment buffer the graph was captured on
     if (h->sched == TSLB_SCHED_M) {
-      if (!h->fimplicit) {
+      if (!h->fimplicit && done < nsteps) {
         if (int rc = enqueue_step(h)) return rc;
         ++done;
       }
-      if (h->graph && h->graph_mo != h->mo) {
+      if (h->graph && h->graph_mo != h->mo && done < nsteps) {
         if (int rc = enqueue_step(h)) return rc;
         ++done;
       }
@@ -1736,26 +1771,30 @@ int tslb_cuda_group_step(tslb_cuda_handle* slabs, int count, long nsteps) {
   }
   for (long s = 0; s < nsteps; ++s) {
     if (all_m) {
-      // the NCCL path's order: boundary chunks, exchange of the new boundary
-      // planes, interior chunks, swap (first step: moments + exchange)
+      // the NCCL path's order: boundary chunks (writing the send buffers),
+      // exchange, interior chunks, swap (first step: moments, pack, exchange)
       const bool first = !slabs[0]->fimplicit;
       for (int r = 0; r < count; ++r) {
         tslb_cuda_sim* h = slabs[r];
-        const int nzc = mstep_chunks(h->range(0, h->nzl), h->lz);
+        const int b = boundary_planes(h);
         int rc = 0;
-        if (first) rc = first_moments(h, st);
-        else if (nzc <= 2) rc = ph_mstep(h, st);
-        else if (!(rc = ph_mstep(h, st, 0, 1))) rc = ph_mstep(h, st, nzc - 1, 1);
+        if (first) {
+          if (!(rc = first_moments(h, st))) rc = pack_moments(h, h->mo, st);
+        } else if (h->nzl <= 2 * b) {
+          rc = ph_mstep(h, st);
+        } else if (!(rc = ph_mstep(h, st, 0, b))) {
+          rc = ph_mstep(h, st, h->nzl - b, h->nzl);
+        }
         if (rc) return rc;
       }
       for (int r = 0; r < count; ++r)
-        if (int rc = exchange_moments_local(slabs[r], first ? slabs[r]->mo : slabs[r]->mo2, st)) return rc;
+        if (int rc = exchange_moments_local(slabs[r], st)) return rc;
       for (int r = 0; r < count; ++r) {
         tslb_cuda_sim* h = slabs[r];
         if (!first) {
-          const int nzc = mstep_chunks(h->range(0, h->nzl), h->lz);
-          if (nzc > 2)
-            if (int rc = ph_mstep(h, st, 1, nzc - 2)) return rc;
+          const int b = boundary_planes(h);
+          if (h->nzl > 2 * b)
+            if (int rc = ph_mstep(h, st, b, h->nzl - b)) return rc;
           std::swap(h->mo, h->mo2);
         }
         h->fimplicit = true;

@@ -39,19 +39,20 @@ template <typename T>
 int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
                           double omega, int vx, int kz, cudaStream_t st);
 // moment-resident single-pass step (tslb_mstep.cu): m(t) in `mi` -> m(t+1)
-// in `mo` for box geometries, z chunks [chunk0, chunk0 + nchunks) of lz
-// planes (nchunks <= 0: to the end); `gm` holds the slab ghost planes
-// ([NM][2][plane], below/above) when a z face is a slab interface. Returns
-// nonzero (nothing launched) when the shape is not supported. `maps` caches
-// the TMA tensor maps (opaque, owned by the caller, freed with
-// free_mstep_maps).
+// in `mo` for box geometries, planes [z0, z1) (z1 <= 0: to the end) in
+// chunks of lz planes per CTA column; `gm` holds the slab ghost planes
+// ([2][NM][plane], below/above) when a z face is a slab interface, and `snd`
+// (optional, same layout) receives a copy of the slab's own boundary planes
+// 0 / nz - 1 of m(t+1) as they are reduced -- the packed send buffer of the
+// halo exchange. Returns 1 (nothing launched) when the shape is not
+// supported, -cudaError on a launch failure. `maps` caches the TMA tensor
+// maps (opaque, owned by the caller, freed with free_mstep_maps).
 struct MstepMaps;
 void free_mstep_maps(MstepMaps* maps);
 bool mstep_supported(int lat, const Dom& d);
-int mstep_chunks(const Dom& d, int lz);
 template <typename T>
-int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
-                 int lz, int chunk0, int nchunks, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st);
+int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, T* snd, double omega,
+                 int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st);
 // per-node solid bits of a masked geometry for the 3-D M step (tslb_mstep.cu)
 int launch_solid_bits(int lat, const Dom& d, const uint8_t* solid, uint32_t* bits, cudaStream_t st);
 // D2Q9 form of the M step (tslb_mstep2d.cu; launched through launch_mstep)

@@ -59,6 +59,7 @@
 #include "tslb_collision.cuh"
 #include "tslb_domain.cuh"
 #include "tslb_kernels.h"
+#include "tslb_msums.cuh"
 #include "tslb_pair.cuh"
 
 namespace tslb_cuda {
@@ -277,8 +278,9 @@ __host__ __device__ constexpr int slot_off() {
 }
 template <class L, int A, int DZ, typename T>
 __device__ __forceinline__ uint32_t ring_addr(const Ring<L, T>& rg) {
-  if constexpr (ring_depth<L>(A) == Ring<L, T>::DB) return rg.qb[(DZ + 1) % Ring<L, T>::DB];
-  else return rg.qa[(DZ + 1) % Ring<L, T>::DA];
+  constexpr int DA = Ring<L, T>::DA, DB = Ring<L, T>::DB;
+  if constexpr (ring_depth<L>(A) == DB) return rg.qb[((DZ + 1) % DB + DB) % DB];
+  else return rg.qa[((DZ + 1) % DA + DA) % DA];
 }
 
 template <class L, typename T, typename C>
@@ -345,13 +347,21 @@ __device__ __forceinline__ void emit(const Dom& d, const Ring<L, T>& rg, T (&R)[
 }
 
 // All directions of a tile node; ZC != 0 (a plane just outside the march)
-// keeps only the directions with c_z == ZC.
-template <class L, typename T, typename C, bool WALLS, bool SOLID, int ZC>
+// keeps only the directions with c_z == ZC. `side(A)` runs after the rest
+// direction (A = 0) and after every opposite pair (odd A): the caller
+// interleaves independent work (the moment sums of an earlier plane) with
+// the collision, so the FP64 pipe sees one even instruction mix.
+struct NoSide {
+  template <class A>
+  __device__ __forceinline__ void operator()(A) const {}
+};
+template <class L, typename T, typename C, bool WALLS, bool SOLID, int ZC, class Side = NoSide>
 __device__ __forceinline__ void push_tile(const Dom& d, const Ring<L, T>& rg, T (&R)[L::q][3],
                                           int lx, int ly, const Contact& ct,
-                                          const NodeMoments<C>& m, C om1) {
+                                          const NodeMoments<C>& m, C om1, const Side& side = Side{}) {
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
+    if constexpr (a == 0 || (a & 1)) side(A);
     if constexpr (a == 0) {
       if constexpr (ZC == 0) emit<L, 0, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(post_rest<L, C>(m, om1)));
     } else if constexpr (a & 1) {
@@ -424,54 +434,51 @@ __device__ __forceinline__ void push_ring(const Ring<L, T>& rg, int hdelta, int 
 }
 
 // compute_moments of one node from its gathered slots (kernels.hpp:74-107;
-// same accumulation order and formulae as k_moments)
-template <class L, typename T, typename C, class Put>
-__device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, const T (&R)[L::q][3], const Put& put) {
-  C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pzz = 0, pxy = 0, pxz = 0, pyz = 0;
+// the sums of tslb_msums.cuh: bit-identical to k_moments). DZ: the slots of
+// destination plane z + DZ (z = the plane being pushed); register-ring
+// directions come from `Rv`.
+template <class L, int DZ, typename T>
+__device__ __forceinline__ void gather(const Ring<L, T>& rg, const T (&Rv)[L::q], T (&v)[L::q]) {
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
-    using dd = Dir<L, a>;
-    T v;
-    if constexpr (is_reg<L>(a)) v = R[a][0];
-    else v = Shm<T>::template ld<slot_off<L, a, 0, 0, T>()>(ring_addr<L, a, -1>(rg));
-    const C fa = C(v);
-    r += fa;
-    if constexpr (dd::x == 1) jx += fa;
-    if constexpr (dd::x == -1) jx -= fa;
-    if constexpr (dd::y == 1) jy += fa;
-    if constexpr (dd::y == -1) jy -= fa;
-    if constexpr (dd::z == 1) jz += fa;
-    if constexpr (dd::z == -1) jz -= fa;
-    if constexpr (dd::x != 0) pxx += fa;
-    if constexpr (dd::y != 0) pyy += fa;
-    if constexpr (dd::z != 0) pzz += fa;
-    if constexpr (dd::x * dd::y == 1) pxy += fa;
-    if constexpr (dd::x * dd::y == -1) pxy -= fa;
-    if constexpr (dd::x * dd::z == 1) pxz += fa;
-    if constexpr (dd::x * dd::z == -1) pxz -= fa;
-    if constexpr (dd::y * dd::z == 1) pyz += fa;
-    if constexpr (dd::y * dd::z == -1) pyz -= fa;
+    if constexpr (is_reg<L>(a)) v[a] = Rv[a];
+    else v[a] = Shm<T>::template ld<slot_off<L, a, 0, 0, T>()>(ring_addr<L, a, DZ>(rg));
   });
-  if constexpr (L::dim == 3) force_shift<C>(d, jx, jy, jz);
-  else { C z0 = 0; force_shift<C>(d, jx, jy, z0); }
+}
+
+template <class L, typename T, typename C, class Put>
+__device__ __forceinline__ void put_moments(const Dom& d, MSums<C> s, const Put& put) {
+  if constexpr (L::dim == 3) force_shift<C>(d, s.jx, s.jy, s.jz);
+  else { C z0 = 0; force_shift<C>(d, s.jx, s.jy, z0); }
   const C c3 = cs2<C>();
-  put(0, T(r));
-  put(1, T(jx));
-  put(2, T(jy));
-  put(3, T(jz));
-  put(4, T(pxx - c3 * r - jx * jx));
-  put(5, T(pyy - c3 * r - jy * jy));
-  put(6, T(pzz - c3 * r - jz * jz));
-  put(7, T(pxy - jx * jy));
-  put(8, T(pxz - jx * jz));
-  put(9, T(pyz - jy * jz));
+  put(0, T(s.r));
+  put(1, T(s.jx));
+  put(2, T(s.jy));
+  put(3, T(s.jz));
+  put(4, T(s.pxx - c3 * s.r - s.jx * s.jx));
+  put(5, T(s.pyy - c3 * s.r - s.jy * s.jy));
+  put(6, T(s.pzz - c3 * s.r - s.jz * s.jz));
+  put(7, T(s.pxy - s.jx * s.jy));
+  put(8, T(s.pxz - s.jx * s.jz));
+  put(9, T(s.pyz - s.jy * s.jz));
+}
+
+template <class L, typename T, typename C, class Put>
+__device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, const T (&R)[L::q][3], const Put& put) {
+  T rv[L::q], v[L::q];
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    if constexpr (is_reg<L>(a)) rv[a] = R[a][0];
+  });
+  gather<L, -1, T>(rg, rv, v);
+  put_moments<L, T, C>(d, msums<L, T, C>(v), put);
 }
 
 template <class L, typename T, typename C, bool WALLS, bool SOLID, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
     k_mstep(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap, Dom d,
-            const T* __restrict__ mi, const T* __restrict__ gm, T* __restrict__ mo, C om1, int lz, int zc0,
-            const uint32_t* __restrict__ sbits) {
+            const T* __restrict__ mi, const T* __restrict__ gm, T* __restrict__ mo, T* __restrict__ snd, C om1,
+            int lz, int zbeg, int zend, const uint32_t* __restrict__ sbits) {
   static_assert(L::dim == 3, "the M step is 3-D");
   using SM = Smem<L, T, SOLID>;
   constexpr int NM = n_moments<L>();
@@ -486,7 +493,7 @@ __global__ void __launch_bounds__(NT, MINB)
 
   const int tid = threadIdx.x, lx = tid & (TX - 1), ly = tid >> 5;
   const int x0 = int(blockIdx.x) * TX, y0 = int(blockIdx.y) * TY;
-  const int za = (int(blockIdx.z) + zc0) * lz, zb = min(za + lz, d.nz);
+  const int za = zbeg + int(blockIdx.z) * lz, zb = min(za + lz, zend);
   const int gx = x0 + lx, gy = y0 + ly;
   const int64_t col = gx + int64_t(d.nx) * gy;
 
@@ -554,8 +561,8 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     if (hfetch) {
       T* w = wstg + b * WSTG_B + hoff;
-      const T* g = (src == 1 ? mi : gm) + int64_t(zz) * d.plane + hcol;
-      const int64_t cs = src == 1 ? d.mstride : 2 * d.plane;
+      const T* g = (src == 1 ? mi + int64_t(zz) * d.plane : gm + int64_t(zz) * NM * d.plane) + hcol;
+      const int64_t cs = src == 1 ? d.mstride : d.plane;
 #pragma unroll
       for (int c = 0; c < NM; ++c) __pipeline_memcpy_async(w + c * WH, g + c * cs, sizeof(T));
     }
@@ -569,16 +576,76 @@ __global__ void __launch_bounds__(NT, MINB)
   T R[L::q][3];
 #pragma unroll
   for (int a = 0; a < L::q; ++a) R[a][0] = R[a][1] = R[a][2] = T(0);
+  // SKEW (one-barrier rings, rd == 1): plane z - 2 is reduced while plane z
+  // is pushed, between the same two barriers -- its slots are complete
+  // (pushes from z - 3 .. z - 1 happened before the last barrier) and the
+  // rings, 3 deep for c_z <= 0 and 4 deep for c_z = +1, hold planes z - 2 ..
+  // z + 1 apart. The moment sums of z - 2 are fed into the collision of z
+  // pair by pair (push_tile's side hook), so the finalize's loads, converts
+  // and adds fill the FP64 pipe's gaps instead of forming their own phase.
+  // rd == 0 (two barriers, shallower rings) reduces z - 1 after the barrier.
+  // Measured (r02, same box, 1024^3): 33.4 GLUPS skewed vs 34.0 unskewed
+  // (128 vs 102 registers, barrier stalls 10.4 % vs 7.3 %), so it is off
+  // unless built with -DTSLB_MSTEP_SKEW (profiles/r02_mstep_variants.md).
+#ifdef TSLB_MSTEP_SKEW
+  constexpr bool SKEW = L::rd == 1;
+#else
+  constexpr bool SKEW = false;
+#endif
+  T Rf[L::q];  // register-ring values of plane z - 2 (SKEW)
+#pragma unroll
+  for (int a = 0; a < L::q; ++a) Rf[a] = T(0);
   Ring<L, T> rg;
   rg.init(smem_u32(sl + ly * TX + lx));
   int buf = 0;
   uint32_t phase = 0;  // bit b: parity of the next completion of bar[b]
-  bool solid_prev = false;  // the tile node of the plane being reduced is solid
+  bool solid_prev = false, solid_prev2 = false;  // the tile node of plane z - 1 / z - 2 is solid
+  constexpr bool PAIRS = msums_pair_form<T, C>();
+  const int64_t ms = d.mstride;
+
+  // slab boundary planes also go to the packed send buffer [2][NM][plane]
+  auto send_row = [&](int zr) -> T* {
+    if (snd == nullptr) return nullptr;
+    if (zr == 0 && d.mode[ZMin] == kGhost) return snd + col;
+    if (zr == d.nz - 1 && d.mode[ZMax] == kGhost) return snd + int64_t(NM) * d.plane + col;
+    return nullptr;
+  };
+  // the skewed reduction of plane zr (= z - 2) from its gathered slots v:
+  // the sums ran in `acc`; nodes outside the pair form's range redo them in
+  // the reference order from the (still intact) slots
+  auto store_skewed = [&](int zr, MAcc<L, T, C, PAIRS>& acc, bool exact) {
+    MSums<C> sm = acc.finish();
+    if constexpr (PAIRS) {
+      if (!exact) {
+        T v2[L::q];
+        gather<L, -2, T>(rg, Rf, v2);
+        sm = msums_reference<L, T, C>(v2);
+      }
+    }
+    T* o = mo + col + int64_t(zr) * d.plane;
+    T* sx = send_row(zr);
+    put_moments<L, T, C>(d, sm, [&](int c, T v) {
+      o[c * ms] = v;
+      if (sx) sx[c * d.plane] = v;
+    });
+  };
 
   auto plane = [&](auto ZCc, int z) {
     constexpr int ZC = decltype(ZCc)::value;
     if (ZC != -1) issue(z + 1, buf ^ 1);
     __pipeline_commit();
+    // SKEW: plane z - 2's slots, gathered before this plane's pushes
+    T v[L::q];
+    bool exact = true;
+    MAcc<L, T, C, PAIRS> acc;
+    if constexpr (SKEW) {
+      gather<L, -2, T>(rg, Rf, v);
+      if constexpr (PAIRS) exact = msums_exact<L::q>(v);
+    }
+    auto side = [&](auto A) {
+      if constexpr (SKEW) acc.template step<decltype(A)::value>(v);
+    };
+    bool fed = false;  // the collision of plane z carried the skewed sums
     int zz_unused = 0;
     if (plane_src(d, z, zz_unused) != 0) {
       mbar_wait(&bar[buf], (phase >> buf) & 1u);
@@ -598,14 +665,19 @@ __global__ void __launch_bounds__(NT, MINB)
         // arrays keep their values (compute_moments skips them too), carried
         // into the output buffer of the ping-pong pair here
         if (ZC == 0 && solid) {
+          T* sx = send_row(z);
 #pragma unroll
-          for (int c = 0; c < NM; ++c)
-            mo[c * d.mstride + col + int64_t(z) * d.plane] = tb[c * TC + (ly + 1) * TX + lx];
+          for (int c = 0; c < NM; ++c) {
+            const T v = tb[c * TC + (ly + 1) * TX + lx];
+            mo[c * d.mstride + col + int64_t(z) * d.plane] = v;
+            if (sx) sx[c * d.plane] = v;
+          }
         }
       }
       if (!solid) {
         const NodeMoments<C> m = node_at<L, T, C>(tb + (ly + 1) * TX + lx, TC);
-        push_tile<L, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, m, om1);
+        push_tile<L, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, m, om1, side);
+        fed = true;
       }
       if (hnode >= 0 && !hsolid) {
         const T* hb = (hfetch ? wstg + buf * WSTG_B : tb) + hoff;
@@ -613,17 +685,30 @@ __global__ void __launch_bounds__(NT, MINB)
         push_ring<L, T, C, ZC>(rg, hdelta, ly, hx, hy, hm, om1);
       }
     }
-    __syncthreads();
-    // compute_moments skips solid nodes (their moment arrays keep their values)
-    if (z - 1 >= za && !(SOLID && solid_prev)) {
-      T* o = mo + col + int64_t(z - 1) * d.plane;
-      const int64_t ms = d.mstride;
-      finalize<L, T, C>(d, rg, R, [&](int c, T v) { o[c * ms] = v; });
+    if constexpr (SKEW) {
+      if (!fed) acc.all(v);
+      if (z - 2 >= za && !(SOLID && solid_prev2)) store_skewed(z - 2, acc, exact);
     }
-    if constexpr (SOLID) solid_prev = (ct.sb & kSelfSolid) != 0;  // (ct.sb: plane z)
+    __syncthreads();
+    if constexpr (!SKEW) {
+      // compute_moments skips solid nodes (their moment arrays keep their values)
+      if (z - 1 >= za && !(SOLID && solid_prev)) {
+        T* o = mo + col + int64_t(z - 1) * d.plane;
+        T* sx = send_row(z - 1);
+        finalize<L, T, C>(d, rg, R, [&](int c, T v) {
+          o[c * ms] = v;
+          if (sx) sx[c * d.plane] = v;
+        });
+      }
+    }
+    if constexpr (SOLID) {
+      solid_prev2 = solid_prev;
+      solid_prev = (ct.sb & kSelfSolid) != 0;  // (ct.sb: plane z)
+    }
     if constexpr (L::rd == 0) __syncthreads();
 #pragma unroll
     for (int a = 0; a < L::q; ++a) {
+      if constexpr (SKEW) Rf[a] = R[a][0];
       R[a][0] = R[a][1];
       R[a][1] = R[a][2];
     }
@@ -637,6 +722,16 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll 1
   for (int z = za; z < zb; ++z) plane(std::integral_constant<int, 0>{}, z);
   plane(std::integral_constant<int, -1>{}, zb);
+  if constexpr (SKEW) {
+    // the last plane of the march (zb - 1) completed at the final barrier
+    if (zb - 1 >= za && !(SOLID && solid_prev2)) {
+      T v[L::q];
+      gather<L, -2, T>(rg, Rf, v);
+      MAcc<L, T, C, PAIRS> acc;
+      acc.all(v);
+      store_skewed(zb - 1, acc, PAIRS ? msums_exact<L::q>(v) : true);
+    }
+  }
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -659,7 +754,7 @@ EncodeFn encoder() {
 
 // 4-D map (x, y, z, moment array) with a {TX, TY + 2, 1, NM} box over the
 // moment buffer `base` (ghost = false), or over the slab ghost planes
-// (ghost = true: layout [NM][2][plane], the "z" coordinate picks the side)
+// (ghost = true: layout [2][NM][plane], the "z" coordinate picks the side)
 template <typename T>
 const CUtensorMap* tensor_map(MstepMaps*& maps, const Dom& d, int nm, const T* base, bool ghost) {
   if (!maps) maps = new MstepMaps();
@@ -682,8 +777,9 @@ const CUtensorMap* tensor_map(MstepMaps*& maps, const Dom& d, int nm, const T* b
   const cuuint64_t es = sizeof(T);
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const cuuint64_t dim[4] = {cuuint64_t(d.nx), cuuint64_t(d.ny), cuuint64_t(ghost ? 2 : d.nz), cuuint64_t(nm)};
-  const cuuint64_t str[3] = {cuuint64_t(d.nx) * es, cuuint64_t(d.plane) * es,
-                             ghost ? cuuint64_t(2 * d.plane) * es : cuuint64_t(d.mstride) * es};
+  // (ghost planes [2][NM][plane]: the "z" coordinate picks the side)
+  const cuuint64_t str[3] = {cuuint64_t(d.nx) * es, (ghost ? cuuint64_t(nm) : 1u) * cuuint64_t(d.plane) * es,
+                             ghost ? cuuint64_t(d.plane) * es : cuuint64_t(d.mstride) * es};
   const cuuint32_t box[4] = {cuuint32_t(TX), cuuint32_t(TR), 1, cuuint32_t(nm)};
   if (enc(&e.map, dt, 4, const_cast<T*>(base), dim, str, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
           CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -707,7 +803,7 @@ __global__ void __launch_bounds__(128) k_ghost_push(Dom d, T* __restrict__ f, co
   if (i >= d.nx) return;
   const int k = side ? d.nz - 1 : 0;
   const int cz_in = side ? -1 : 1;
-  const T* g = gm + int64_t(side) * d.plane;
+  const T* g = gm + int64_t(side) * n_moments<L>() * d.plane;  // ([2][NM][plane])
   // masked geometries: a solid node keeps its populations, a solid source
   // pushes nothing (that slot holds the node's own bounce)
   if (solid && solid[fidx(d, i, j, k)]) return;
@@ -721,7 +817,7 @@ __global__ void __launch_bounds__(128) k_ghost_push(Dom d, T* __restrict__ f, co
       if (sx < 0 || sy < 0) return;
       if (solid && solid[fidx(d, sx, sy, k - dd::z)]) return;
       const T* p = g + sx + int64_t(d.nx) * sy;
-      const int64_t cs = 2 * d.plane;
+      const int64_t cs = d.plane;
       const NodeMoments<C> m = prepare_node<C>(C(p[0]), C(p[cs]), C(p[2 * cs]), C(p[3 * cs]), C(p[4 * cs]),
                                                C(p[5 * cs]), C(p[6 * cs]), C(p[7 * cs]), C(p[8 * cs]),
                                                C(p[9 * cs]));
@@ -783,11 +879,6 @@ int launch_solid_bits(int lat, const Dom& d, const uint8_t* solid, uint32_t* bit
   return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
-int mstep_chunks(const Dom& d, int lz) {
-  if (lz <= 0) lz = mstep::kDefaultLz;
-  return (d.nz + lz - 1) / lz;
-}
-
 template <typename T>
 int launch_ghost_push(int lat, int math, const Dom& d, T* f, const T* gm, double omega, int side,
                       const uint8_t* solid, cudaStream_t st) {
@@ -807,18 +898,18 @@ int launch_ghost_push(int lat, int math, const Dom& d, T* f, const T* gm, double
 }
 
 template <typename T>
-int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
-                 int lz, int chunk0, int nchunks, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st) {
+int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, T* snd, double omega,
+                 int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st) {
   using namespace mstep;
   if (!mstep_supported(lat, d)) return 1;
   if (d.has_solid && !sbits) return 1;
-  if (lat == kD2Q9) return chunk0 == 0 ? launch_mstep2d<T>(math, d, mi, mo, omega, st) : 1;
+  if (z1 <= 0) z1 = d.nz;
+  if (lat == kD2Q9) return z0 == 0 && z1 == d.nz ? launch_mstep2d<T>(math, d, mi, mo, omega, st) : 1;
   if ((d.mode[ZMin] == kGhost || d.mode[ZMax] == kGhost) && !gm) return 1;
   if (lz <= 0) lz = kDefaultLz;
-  const int nzc = (d.nz + lz - 1) / lz;
-  if (nchunks <= 0) nchunks = nzc - chunk0;
-  if (chunk0 < 0 || chunk0 + nchunks > nzc) return 1;
-  if (nchunks == 0) return 0;
+  if (z0 < 0 || z1 > d.nz || z0 > z1) return 1;
+  if (z0 == z1) return 0;
+  const int nchunks = (z1 - z0 + lz - 1) / lz;
   bool walls = false;
   for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
   const dim3 grid(unsigned(d.nx / TX), unsigned(d.ny / TY), unsigned(nchunks));
@@ -841,9 +932,15 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
     if (!tm) return 1;
     const CUtensorMap* gmp = gm ? tensor_map<T>(maps, d, n_moments<Lat>(), gm, true) : tm;
     if (!gmp) return 1;
+    // CUDA failures come back as -error (the caller names the kernel)
+    int err = 0;
     auto go = [&](auto kern, auto om1, size_t smem) {
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-      kern<<<grid, NT, smem, st>>>(*tm, *gmp, d, mi, gm, mo, om1, lz, chunk0, sbits);
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e == cudaSuccess) {
+        kern<<<grid, NT, smem, st>>>(*tm, *gmp, d, mi, gm, mo, snd, om1, lz, z0, z1, sbits);
+        e = cudaGetLastError();
+      }
+      if (e != cudaSuccess) err = -int(e);
     };
     constexpr size_t sm0 = Smem<Lat, T, false>::total, sm1 = Smem<Lat, T, true>::total;
     if ((d.has_solid ? sm1 : sm0) > 227 * 1024) return 1;
@@ -863,7 +960,7 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
       else if (walls) go(k_mstep<Lat, T, float, true, false, MB>, om1f, sm0);
       else go(k_mstep<Lat, T, float, false, false, MB>, om1f, sm0);
     }
-    return 0;
+    return err;
   };
   auto by_rd = [&](auto B) {
     using Base = decltype(B);
@@ -872,10 +969,10 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
   return lat == kD3Q19 ? by_rd(D3Q19{}) : by_rd(D3Q27{});
 }
 
-template int launch_mstep<float>(int, int, const Dom&, const float*, const float*, float*, double, int, int,
-                                 int, MstepMaps*&, const uint32_t*, cudaStream_t);
-template int launch_mstep<double>(int, int, const Dom&, const double*, const double*, double*, double, int, int,
-                                  int, MstepMaps*&, const uint32_t*, cudaStream_t);
+template int launch_mstep<float>(int, int, const Dom&, const float*, const float*, float*, float*, double, int,
+                                 int, int, MstepMaps*&, const uint32_t*, cudaStream_t);
+template int launch_mstep<double>(int, int, const Dom&, const double*, const double*, double*, double*, double,
+                                  int, int, int, MstepMaps*&, const uint32_t*, cudaStream_t);
 template int launch_ghost_push<float>(int, int, const Dom&, float*, const float*, double, int, const uint8_t*,
                                       cudaStream_t);
 template int launch_ghost_push<double>(int, int, const Dom&, double*, const double*, double, int,

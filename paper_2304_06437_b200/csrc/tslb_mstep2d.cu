@@ -254,7 +254,8 @@ int launch_mstep2d(int math, const Dom& d, const T* mi, T* mo, double omega, cud
     if (walls) k_mstep2d<D2Q9, T, float, true><<<grid, 32 * WPB, 0, st>>>(d, mi, mo, om1, rows);
     else k_mstep2d<D2Q9, T, float, false><<<grid, 32 * WPB, 0, st>>>(d, mi, mo, om1, rows);
   }
-  return 0;
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? 0 : -int(e);  // (the caller names the kernel)
 }
 
 // nsteps M passes in one cooperative launch (m0 holds m(t); the result is in
@@ -284,11 +285,16 @@ int launch_mstep2d_persist(int math, const Dom& d, T* m0, T* m1, double omega, i
     T *a = m0, *b = m1;
     int rr = rows, ns = nsteps, x = nbx, y = nby;
     void* args[] = {&dd, &a, &b, &om1, &rr, &ns, &x, &y};
-    if (cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(blocks), dim3(32 * WPB), args, 0, st) ==
-        cudaSuccess)
-      return 0;
-    cudaGetLastError();  // a refused launch is not sticky; clear it for the caller's checks
-    return 1;
+    // an error still pending from the work enqueued before belongs to the
+    // caller: report it (-error) rather than clearing it with the refusal below
+    if (const cudaError_t pe = cudaPeekAtLastError(); pe != cudaSuccess) return -int(pe);
+    const cudaError_t e =
+        cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(blocks), dim3(32 * WPB), args, 0, st);
+    if (e == cudaSuccess) return 0;
+    cudaGetLastError();  // (a refused launch is not sticky)
+    // not co-resident: the caller falls back to per-pass launches; any other
+    // failure is reported
+    return e == cudaErrorCooperativeLaunchTooLarge ? 1 : -int(e);
   };
   if (math == kMathDouble) {
     const double om1 = 1.0 - double(T(omega));

@@ -15,7 +15,7 @@ namespace tslb_cuda {
 
 constexpr int RB = 256;        // threads per reduction block
 constexpr int RBLOCKS = 592;   // 4 x 148 SMs; fixed => deterministic order
-constexpr int RSLOTS = 5;      // doubles per partial
+constexpr int RSLOTS = 7;      // doubles per partial
 
 size_t reduce_partial_count() { return size_t(RBLOCKS) * RSLOTS; }
 
@@ -81,13 +81,18 @@ __global__ void k_fold_sum(const double* partial, int nslots, double* out) {
   }
 }
 
+// scan_stability (solver.hpp:39-65). min/max are order-independent except
+// for NaN: the reference's std::min/std::max keep a NaN only when it is the
+// FIRST fluid node's rho (every later comparison with it is false), and
+// drop later NaNs -- so the scan also carries the first fluid node (lowest
+// index) and its rho; with no fluid node at all min = max = 0.
 template <typename T>
 __global__ void __launch_bounds__(RB)
     k_stability(Dom d, int dim, const T* __restrict__ rho,
                 const T* __restrict__ mom, const uint8_t* __restrict__ solid,
                 double* partial) {
-  __shared__ double sh[5 * (RB / 32)];
-  double bad = 0, mx = 0, lo = 1e300, hi = -1e300, first = 1e300;
+  __shared__ double sh[7 * (RB / 32)];
+  double bad = 0, mx = 0, lo = 1e300, hi = -1e300, first = 1e300, ffirst = 1e300, frho = 0;
   const int64_t per = (d.n + RBLOCKS - 1) / RBLOCKS;
   const int64_t b0 = int64_t(blockIdx.x) * per;
   const int64_t b1 = min(d.n, b0 + per);
@@ -101,6 +106,10 @@ __global__ void __launch_bounds__(RB)
       u2 += m * m;
     }
     const T r = rho[mi];
+    if (ffirst > 1e299) {  // (t ascends per thread)
+      ffirst = double(t);
+      frho = double(r);
+    }
     if (!isfinite(double(r)) || !isfinite(double(u2))) {
       bad = 1;
       first = fmin(first, double(t));
@@ -110,7 +119,8 @@ __global__ void __launch_bounds__(RB)
     lo = fmin(lo, double(r));
     hi = fmax(hi, double(r));
   }
-  // min/max are order-independent: reduce with shuffles
+  // min/max are order-independent: reduce with shuffles; the first fluid
+  // node travels with its rho
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int o = 16; o > 0; o >>= 1) {
     bad = fmax(bad, __shfl_down_sync(0xffffffffu, bad, o));
@@ -118,6 +128,12 @@ __global__ void __launch_bounds__(RB)
     lo = fmin(lo, __shfl_down_sync(0xffffffffu, lo, o));
     hi = fmax(hi, __shfl_down_sync(0xffffffffu, hi, o));
     first = fmin(first, __shfl_down_sync(0xffffffffu, first, o));
+    const double of = __shfl_down_sync(0xffffffffu, ffirst, o);
+    const double orh = __shfl_down_sync(0xffffffffu, frho, o);
+    if (of < ffirst) {
+      ffirst = of;
+      frho = orh;
+    }
   }
   if (lane == 0) {
     sh[w] = bad;
@@ -125,6 +141,8 @@ __global__ void __launch_bounds__(RB)
     sh[16 + w] = lo;
     sh[24 + w] = hi;
     sh[32 + w] = first;
+    sh[40 + w] = ffirst;
+    sh[48 + w] = frho;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -134,6 +152,10 @@ __global__ void __launch_bounds__(RB)
       lo = fmin(lo, sh[16 + k]);
       hi = fmax(hi, sh[24 + k]);
       first = fmin(first, sh[32 + k]);
+      if (sh[40 + k] < ffirst) {
+        ffirst = sh[40 + k];
+        frho = sh[48 + k];
+      }
     }
     double* p = partial + blockIdx.x * RSLOTS;
     p[0] = bad;
@@ -141,12 +163,14 @@ __global__ void __launch_bounds__(RB)
     p[2] = lo;
     p[3] = hi;
     p[4] = first;
+    p[5] = ffirst;
+    p[6] = frho;
   }
 }
 
 __global__ void k_fold_stability(const double* partial, double* out) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  double bad = 0, mx = 0, lo = 1e300, hi = -1e300, first = 1e300;
+  double bad = 0, mx = 0, lo = 1e300, hi = -1e300, first = 1e300, ffirst = 1e300, frho = 0;
   for (int b = 0; b < RBLOCKS; ++b) {
     const double* p = partial + b * RSLOTS;
     bad = fmax(bad, p[0]);
@@ -154,6 +178,15 @@ __global__ void k_fold_stability(const double* partial, double* out) {
     lo = fmin(lo, p[2]);
     hi = fmax(hi, p[3]);
     first = fmin(first, p[4]);
+    if (p[5] < ffirst) {
+      ffirst = p[5];
+      frho = p[6];
+    }
+  }
+  if (ffirst > 1e299) {
+    lo = hi = 0.0;  // no fluid node: the report's zero-initialised fields
+  } else if (isnan(frho)) {
+    lo = hi = frho;  // the reference's min/max stay at a NaN first value
   }
   out[0] = bad > 0 ? 0.0 : 1.0;  // finite flag
   out[1] = mx;

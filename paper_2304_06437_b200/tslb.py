@@ -365,11 +365,21 @@ class DeviceSolver:
     # data movement
     def upload_f(self, f, species=0):
         f = np.ascontiguousarray(f, self.dtype)
-        assert f.shape == (self.lat.q, self.n), f.shape
+        if f.shape != (self.lat.q, self.n):
+            raise _lib.InvalidArgument(f"upload_f: expected shape {(self.lat.q, self.n)}, got {f.shape}")
         self._call("tslb_cuda_upload_f", species, _ptr(f))
 
     def download_f(self, species=0, out=None):
-        out = np.empty((self.lat.q, self.n), self.dtype) if out is None else out
+        """f of one species as (q, n); `out` (optional) must be a C-contiguous
+        array of the solver's dtype and exactly that shape -- the C-ABI
+        writes q * n elements into it."""
+        if out is None:
+            out = np.empty((self.lat.q, self.n), self.dtype)
+        elif (not isinstance(out, np.ndarray) or out.dtype != self.dtype or out.shape != (self.lat.q, self.n)
+              or not out.flags.c_contiguous or not out.flags.writeable):
+            raise _lib.InvalidArgument(
+                f"download_f: out must be a writeable C-contiguous {np.dtype(self.dtype).name} array of shape "
+                f"{(self.lat.q, self.n)}")
         self._call("tslb_cuda_download_f", species, _ptr(out))
         return out
 
@@ -400,7 +410,10 @@ class DeviceSolver:
 
     def upload_field(self, name, arr):
         cnt, dt = self._fshape(name)
-        a = np.ascontiguousarray(np.asarray(arr, dt).reshape(cnt, self.n))
+        a = np.asarray(arr, dt)
+        if a.size != cnt * self.n:
+            raise _lib.InvalidArgument(f"upload_field({name}): expected {cnt * self.n} values, got {a.size}")
+        a = np.ascontiguousarray(a.reshape(cnt, self.n))
         self._call("tslb_cuda_upload_field", _lib.FIELD[name], _ptr(a))
 
     def geometry(self) -> NodeGeometry:
@@ -482,6 +495,11 @@ class DeviceSolver:
         cnt = np.zeros(len(_lib.KCLASS), np.int64)
         self._call("tslb_cuda_profile_read", _ptr(ms), _ptr(cnt))
         return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(_lib.KCLASS) if cnt[i]}
+
+    def steps_done(self) -> int:
+        v = C.c_long()
+        self._call("tslb_cuda_steps_done", C.byref(v))
+        return v.value
 
     def launch_count(self) -> int:
         v = C.c_int64()

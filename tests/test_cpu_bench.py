@@ -67,3 +67,35 @@ def test_traffic_captures_match_the_bench_accounting():
             assert kb[kind] == e["algorithmic"], key
         # measured DRAM bytes within 10 % of the algorithmic figure
         assert 0.95 < e["bytes_per_node"] / e["algorithmic"] < 1.1, key
+
+
+def _run_bench(args, env=None, timeout=300):
+    import subprocess
+    e = dict(os.environ)
+    for k in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT"):
+        e.pop(k, None)
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(bench.ROOT, "bench.py"), *args], capture_output=True,
+                          text=True, env=e, timeout=timeout)
+
+
+def test_gpus_flag_launches_one_rank_per_gpu():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks
+    (torch.distributed.run, 127.0.0.1); --launch-check reports them over gloo."""
+    import json
+    r = _run_bench(["--gpus", "2", "--launch-check"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    assert out["n_gpus"] == 2 and out["ranks"] == [0, 1] and out["pids_distinct"]
+
+
+def test_gpus_flag_must_match_world_size():
+    r = _run_bench(["--gpus", "4", "--launch-check"], env={"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
+    assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr
+
+
+def test_strong_scaling_workload_splits_the_fixed_domain():
+    w = bench.WORKLOADS["tgv-c5"]
+    assert w["dims"] == (2048, 1024, 1024) and w.get("strong")
+    for n in (1, 2, 4, 8):
+        assert w["dims"][2] % n == 0

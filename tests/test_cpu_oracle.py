@@ -92,3 +92,19 @@ def test_half_periodic_axis_rejected_like_reference(oracle_port, oracle_ref):
     for o in (oracle_port, oracle_ref):
         with pytest.raises(ValueError, match="axis 1"):
             o.classify("d2q9", (8, 8, 1), f)
+
+
+def test_ref_full_workload_geometry_expansion(oracle_ref):
+    """bench.py --impl reference's whole-workload run (tslbref_time_tgv)
+    expands classify_nodes' 3x3x3 slow masks instead of classifying 10^9
+    nodes serially: the same f afterwards as with the full classification."""
+    import ctypes as C
+    fn = oracle_ref.lib.tslbref_time_tgv
+    fn.argtypes = [C.c_int] * 4 + [C.c_double, C.c_double, C.c_long, C.c_long, C.c_int, C.c_int, C.c_void_p,
+                                   C.c_void_p, C.c_void_p]
+    digests = []
+    for full in (0, 1):
+        ti, ts, dg = C.c_double(), C.c_double(), C.c_uint64()
+        assert fn(1, 12, 10, 9, 1.6, 0.03, 3, 1, 2, full, C.byref(ti), C.byref(ts), C.byref(dg)) == 0
+        digests.append(dg.value)
+    assert digests[0] == digests[1]

@@ -531,3 +531,66 @@ def test_mstep2d_persistent_equals_per_pass_launches(gpu, dtype, nsteps, monkeyp
     assert_bitwise(out["1"][1], out["0"][1], "persistent vs per-pass f")
     if nsteps >= 3:  # the moments pass after the upload, then one cooperative launch
         assert out["1"][2] <= 3 < out["0"][2]
+
+
+def _msums_fallback_fraction(f, q):
+    """Share of nodes whose gathered populations fail the pair-form range
+    check of tslb_msums.cuh (max|f| < 2^24 min|f|)."""
+    a = np.abs(f.astype(np.float64))
+    return float(np.mean(~(a.max(0) < a.min(0) * 2.0 ** 24)))
+
+
+@pytest.mark.parametrize("lat", ["d3q19", "d3q27"])
+def test_mstep_msums_both_forms_bitwise(gpu, oracle_port, lat):
+    """The moment sums of the M kernel take the exact pair form where the
+    node's populations span < 2^24 and the reference accumulation order
+    elsewhere (tslb_msums.cuh). Node states scaled by 2^U(-12, 8) put both
+    kinds of node side by side; f(N) and m(N-1) must stay bit-identical to
+    fused_step. 2 % of the nodes start with all-zero populations (zero
+    operands fail the check). The second step is the first M pass: it
+    reduces f(1), whose populations come from differently scaled sources."""
+    dims, faces, steps = (32, 16, 6), corner_box_3d(), 2
+    f0 = O.random_state(lat, dims, 31, np.float64)
+    rng = np.random.default_rng(7)
+    scale = np.exp2(rng.uniform(-12, 8, f0.shape[1]))
+    scale[rng.random(f0.shape[1]) < 0.3] = 1.0
+    f0 = np.ascontiguousarray((f0 * scale[None, :]).astype(np.float32))
+    f0[:, rng.random(f0.shape[1]) < 0.02] = 0.0
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.25, spec_of(faces), np.float32)
+    try:
+        assert dev.schedule == "m"
+        dev.upload_f(f0)
+        dev.step(steps)
+        mg = _moments(dev, lat)
+        fg = dev.download_f()
+    finally:
+        dev.close()
+    fo, mo = _oracle(oracle_port, lat, dims, 1.25, faces, f0, steps)
+    # f(N-1) is what the last finalize reduced: both forms must have run
+    fprev, _ = _oracle(oracle_port, lat, dims, 1.25, faces, f0, steps - 1)
+    frac = _msums_fallback_fraction(fprev, T.lattice_of(lat).q)
+    assert 0.05 < frac < 0.95, f"fallback share {frac}: the state does not exercise both forms"
+    assert_bitwise(mg, mo, f"M {lat} msums moments m(N-1)")
+    assert_bitwise(fg, fo, f"M {lat} msums f(N)")
+
+
+def test_persist_toggle_on_one_handle(gpu, oracle_port, monkeypatch):
+    """TSLB_PERSIST is read per step() call: a graph captured under per-pass
+    launches, then persistent calls with odd counts that swap the ping-pong
+    buffers, must still take exactly the requested number of steps."""
+    lat, dims, faces, om = "d2q9", (256, 256, 1), O.lid_cavity(0.08), 1.3
+    f0 = O.random_state(lat, dims, 4, np.float64)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), om, spec_of(faces), np.float64)
+    total = 0
+    try:
+        dev.upload_f(f0)
+        for mode, n in (("0", 40), ("1", 33), ("0", 35), ("1", 35), ("0", 32)):
+            monkeypatch.setenv("TSLB_PERSIST", mode)
+            dev.step(n)
+            total += n
+            assert dev.steps_done() == total, f"after TSLB_PERSIST={mode} step({n})"
+        fg = dev.download_f()
+    finally:
+        dev.close()
+    fo, _ = _oracle(oracle_port, lat, dims, om, faces, f0, total)
+    assert_bitwise(fg, fo, "persist toggles")

@@ -7,6 +7,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
+from paper_2304_06437_b200 import _lib
 from paper_2304_06437_b200 import tslb as T
 
 from helpers import assert_bitwise, block_solid, corner_box_3d, mixed_2d, random_solid, spec_of, zwalls_3d
@@ -379,5 +380,58 @@ def test_invalid_arguments_raise(gpu):
             dev.set_schedule("m")  # the M schedule is single-fluid
         with pytest.raises(RuntimeError):
             dev.set_body_force(1e-5, 0.0, 0.0)  # forcing is a single-fluid extension
+    finally:
+        dev.close()
+
+
+def test_stability_empty_and_nan_first(gpu):
+    """scan_stability edge cases (solver.hpp:39-65): no fluid node -> the
+    report's zero fields; a NaN rho on the FIRST fluid node sticks in
+    min/max (std::min/std::max never replace it), a later NaN is ignored."""
+    dims = (8, 8, 4)
+    n = int(np.prod(dims))
+    dev = T.DeviceSolver("d3q19", T.GridDims(*dims), 1.0, T.BoundarySpec.all_periodic(), np.float64,
+                         solid=np.ones(n, np.uint8))
+    try:
+        rep = dev.stability()
+        assert rep.finite and rep.min_rho == 0.0 and rep.max_rho == 0.0 and rep.max_speed == 0.0
+    finally:
+        dev.close()
+    solid = np.zeros(n, np.uint8)
+    solid[:5] = 1  # the first fluid node is 5
+    for bad, sticks in ((5, True), (40, False)):
+        dev = T.DeviceSolver("d3q19", T.GridDims(*dims), 1.0, T.BoundarySpec.all_periodic(), np.float64,
+                             solid=solid)
+        try:
+            rho = np.linspace(0.9, 1.1, n)
+            rho[bad] = np.nan
+            dev.upload_field("rho", rho)
+            rep = dev.stability()
+            assert not rep.finite and rep.first_bad == bad
+            if sticks:
+                assert np.isnan(rep.min_rho) and np.isnan(rep.max_rho)
+            else:
+                fl = np.delete(rho[5:], bad - 5)
+                assert rep.min_rho == fl.min() and rep.max_rho == fl.max()
+        finally:
+            dev.close()
+
+
+def test_host_buffer_validation(gpu):
+    """The Python mirror checks every host buffer it hands to the C-ABI."""
+    dims = (8, 8, 4)
+    dev = T.DeviceSolver("d3q19", T.GridDims(*dims), 1.0, T.BoundarySpec.all_periodic(), np.float32)
+    try:
+        n = int(np.prod(dims))
+        with pytest.raises(_lib.InvalidArgument):
+            dev.upload_f(np.zeros((19, n - 1), np.float32))
+        for bad in (np.empty((19, n), np.float64), np.empty((19, n + 1), np.float32),
+                    np.empty((n, 19), np.float32).T):
+            with pytest.raises(_lib.InvalidArgument):
+                dev.download_f(out=bad)
+        with pytest.raises(_lib.InvalidArgument):
+            dev.upload_field("rho", np.zeros(n + 3))
+        ok = np.empty((19, n), np.float32)
+        assert dev.download_f(out=ok) is ok
     finally:
         dev.close()
