@@ -64,7 +64,7 @@ WORKLOADS = {
     # BASELINE config 5: one fixed domain split into N z slabs (strong scaling)
     "tgv-c5": dict(lat="d3q19", dims=(2048, 1024, 1024), faces="periodic", comps=1, init="taylor_green",
                    amp=0.03, omega=1.6, storage="f32", strong=True,
-                   desc="D3Q19 periodic Taylor-Green 2048x1024x1024 (BASELINE config 5), {n} z slab per GPU"),
+                   desc="D3Q19 periodic Taylor-Green 2048x1024x1024 (BASELINE config 5): {n}"),
 }
 
 

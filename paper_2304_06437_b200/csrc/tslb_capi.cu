@@ -171,7 +171,10 @@ struct tslb_cuda_sim {
   tslb_cuda_sim* down_peer = nullptr;
   void* recv_lo = nullptr;  // staging (masked geometries), per species
   void* recv_hi = nullptr;
-  void* phig = nullptr;     // two-fluid slabs: phi with a ghost plane below and above
+  void* phig = nullptr;     // two-fluid slabs: phi with pgz ghost planes below and above
+  int pgz = 1;              // two-fluid slabs: ghost planes of phi (and of the NCI flags): max(1, nci_reach) with NCI
+  uint8_t* flagg = nullptr; // two-fluid slabs with NCI: flag allocation with pgz ghost planes each side
+  uint8_t* rflag = nullptr; // two-fluid slabs with NCI: received neighbour flag planes [2][pgz plane]
   int zp[9], zm[9], nzp = 0, nzm = 0;  // directions with c_z = +1 / -1
   int zpx[9], zpy[9], zmx[9], zmy[9];
 
@@ -193,7 +196,7 @@ struct tslb_cuda_sim {
     t.pin = m_arr(1 + dim);
     t.rho_r = t_arr(0);
     t.rho_b = t_arr(1);
-    t.phi = phig ? static_cast<char*>(phig) + size_t(plane()) * esz : t_arr(2);
+    t.phi = phig ? static_cast<char*>(phig) + size_t(pgz) * size_t(plane()) * esz : t_arr(2);
     t.grad = t_arr(3);
     t.flag = flag;
     return t;
@@ -253,6 +256,11 @@ int by_scalar(const tslb_cuda_sim* h, F&& f) {
   return f(float(0));
 }
 
+// the near-contact scan runs (gradient_and_nci: cp.nci_strength != T(0))
+bool nci_on(const tslb_cuda_sim* h) {
+  return h->scalar == TSLB_F64 ? h->cp.nci_strength != 0.0 : float(h->cp.nci_strength) != 0.0f;
+}
+
 // -- phases -------------------------------------------------------------------
 // the single-fluid population buffer, allocated on first use under M and
 // filled with the pending analytic f(0) if there is one
@@ -305,16 +313,14 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
 }
 
 // M schedule: m(t) in h->mo -> m(t+1) in h->mo2 for planes [z0, z1) (z1 <= 0:
-// to the end); the caller swaps the buffers once every plane is done. On
-// slabs the kernel also copies the new boundary planes into h->sx.
+// to the end); the caller swaps the buffers once every plane is done.
 int ph_mstep(tslb_cuda_sim* h, cudaStream_t st, int z0 = 0, int z1 = 0) {
   Prof p(h, TSLB_K_MSTEP, st);
   ++h->launches;
   int rc = by_scalar(h, [&](auto z) {
     using T = decltype(z);
     return launch_mstep<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<const T*>(h->mo),
-                           static_cast<const T*>(h->gm), static_cast<T*>(h->mo2), static_cast<T*>(h->sx), h->omega,
-                           h->lz, z0, z1, h->mmaps,
+                           static_cast<const T*>(h->gm), static_cast<T*>(h->mo2), h->omega, h->lz, z0, z1, h->mmaps,
                            h->sbits ? h->sbits + size_t(h->d.ghost) * h->plane() : nullptr, st);
   });
   if (rc < 0) return set_err(TSLB_ECUDA, "k_mstep launch: %s", cudaGetErrorString(cudaError_t(-rc)));
@@ -338,9 +344,8 @@ size_t moment_plane_block(const tslb_cuda_sim* h) {  // bytes of NM planes
   return size_t(1 + h->dim + h->np) * size_t(h->plane()) * h->esz;
 }
 
-// the boundary planes of the moment buffer `buf` into the send buffer (the
-// first step of a run, whose moments come from the moments pass; later
-// steps have the M kernel write them)
+// the boundary planes of the moment buffer `buf` into the packed send
+// buffer h->sx: two strided 2-D copies (NM planes each)
 int pack_moments(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
   const size_t pb = size_t(h->plane()) * h->esz;
   const int nm = 1 + h->dim + h->np;
@@ -555,18 +560,20 @@ int exchange_local(tslb_cuda_sim* h, cudaStream_t st) {
   return 0;
 }
 
-// two-fluid slabs: phi boundary planes -> the neighbours' phi ghost planes
-// (the gradient stencil of the boundary planes), same grouping as above
+// two-fluid slabs: phi's pgz boundary planes -> the neighbours' phi ghost
+// planes (the gradient stencil and the near-contact probes), same grouping
+// as above
 int exchange_phi_nccl(tslb_cuda_sim* h, cudaStream_t st) {
   NcclApi& N = nccl();
   const ncclDataType_t ty = h->scalar == TSLB_F64 ? ncclFloat64 : ncclFloat32;
-  const size_t cnt = size_t(h->plane());
+  const int g = h->pgz;
+  const size_t cnt = size_t(g) * size_t(h->plane());
   char* phi = static_cast<char*>(h->tf().phi);
   auto pl = [&](int k) { return phi + (int64_t(k) * h->plane()) * h->esz; };
   Prof p(h, TSLB_K_EXCHANGE, st);
   N.GroupStart();
-  if (h->up >= 0) N.Send(pl(h->nzl - 1), cnt, ty, h->up, h->comm, st);
-  if (h->down >= 0) N.Recv(pl(-1), cnt, ty, h->down, h->comm, st);
+  if (h->up >= 0) N.Send(pl(h->nzl - g), cnt, ty, h->up, h->comm, st);
+  if (h->down >= 0) N.Recv(pl(-g), cnt, ty, h->down, h->comm, st);
   if (h->down >= 0) N.Send(pl(0), cnt, ty, h->down, h->comm, st);
   if (h->up >= 0) N.Recv(pl(h->nzl), cnt, ty, h->up, h->comm, st);
   ncclResult_t r = N.GroupEnd();
@@ -576,20 +583,115 @@ int exchange_phi_nccl(tslb_cuda_sim* h, cudaStream_t st) {
 }
 
 int exchange_phi_local(tslb_cuda_sim* h, cudaStream_t st) {
-  const size_t bytes = size_t(h->plane()) * h->esz;
+  const int g = h->pgz;
+  const size_t bytes = size_t(g) * size_t(h->plane()) * h->esz;
   auto pl = [&](const tslb_cuda_sim* x, int k) {
     return static_cast<char*>(x->tf().phi) + (int64_t(k) * x->plane()) * x->esz;
   };
   Prof p(h, TSLB_K_EXCHANGE, st);
-  if (h->up_peer) CK(cudaMemcpyAsync(pl(h->up_peer, -1), pl(h, h->nzl - 1), bytes, cudaMemcpyDeviceToDevice, st));
+  if (h->up_peer) CK(cudaMemcpyAsync(pl(h->up_peer, -g), pl(h, h->nzl - g), bytes, cudaMemcpyDeviceToDevice, st));
   if (h->down_peer)
     CK(cudaMemcpyAsync(pl(h->down_peer, h->down_peer->nzl), pl(h, 0), bytes, cudaMemcpyDeviceToDevice, st));
   return 0;
 }
 
+// two-fluid slabs with NCI: flags the scan set in the ghost planes belong
+// to the neighbours' nodes -- ship them (lower ghosts to the slab below,
+// upper to the slab above) into the receiver's staging planes, which
+// fold_flags ORs into its own boundary planes
+int exchange_flags_nccl(tslb_cuda_sim* h, cudaStream_t st) {
+  NcclApi& N = nccl();
+  const size_t gp = size_t(h->pgz) * size_t(h->plane());
+  Prof p(h, TSLB_K_EXCHANGE, st);
+  N.GroupStart();
+  if (h->up >= 0) N.Send(h->flag + int64_t(h->nzl) * h->plane(), gp, ncclUint8, h->up, h->comm, st);
+  if (h->down >= 0) N.Recv(h->rflag, gp, ncclUint8, h->down, h->comm, st);
+  if (h->down >= 0) N.Send(h->flagg, gp, ncclUint8, h->down, h->comm, st);
+  if (h->up >= 0) N.Recv(h->rflag + gp, gp, ncclUint8, h->up, h->comm, st);
+  ncclResult_t r = N.GroupEnd();
+  if (r != ncclSuccess)
+    return set_err(TSLB_ECUDA, "NCCL NCI flag exchange: %s", N.ErrStr ? N.ErrStr(r) : "error");
+  return 0;
+}
+
+int exchange_flags_local(tslb_cuda_sim* h, cudaStream_t st) {
+  const size_t gp = size_t(h->pgz) * size_t(h->plane());
+  Prof p(h, TSLB_K_EXCHANGE, st);
+  if (h->up_peer)
+    CK(cudaMemcpyAsync(h->up_peer->rflag, h->flag + int64_t(h->nzl) * h->plane(), gp, cudaMemcpyDeviceToDevice, st));
+  if (h->down_peer) CK(cudaMemcpyAsync(h->down_peer->rflag + gp, h->flagg, gp, cudaMemcpyDeviceToDevice, st));
+  return 0;
+}
+
+// received flags -> OR into the boundary planes they describe (from below:
+// planes [0, pgz); from above: [nzl - pgz, nzl)); then clear the ghost flags
+// for the next scan
+int fold_flags(tslb_cuda_sim* h, cudaStream_t st) {
+  const int64_t gp = int64_t(h->pgz) * h->plane();
+  h->launches += 2;
+  if (h->down >= 0 || h->down_peer)
+    if (launch_flag_or(h->flag, h->rflag, gp, st)) return set_err(TSLB_ECUDA, "k_flag_or launch failed");
+  if (h->up >= 0 || h->up_peer)
+    if (launch_flag_or(h->flag + int64_t(h->nzl) * h->plane() - gp, h->rflag + gp, gp, st))
+      return set_err(TSLB_ECUDA, "k_flag_or launch failed");
+  CK(cudaMemsetAsync(h->flagg, 0, size_t(gp), st));
+  CK(cudaMemsetAsync(h->flag + int64_t(h->nzl) * h->plane(), 0, size_t(gp), st));
+  return 0;
+}
+
+// gradient + near-contact scan of a slab (box geometry, ghost planes)
+int ph_cg_gradient_slab(tslb_cuda_sim* h, cudaStream_t st) {
+  Prof p(h, TSLB_K_CG_GRADIENT, st);
+  h->launches += nci_on(h) ? 2 : 1;
+  h->grad_pending = false;
+  const int rc = by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_cg_gradient_nci_box<T>(h->lat, h->range(0, h->nzl), h->tf(), h->cp, st);
+  });
+  return rc ? set_err(TSLB_ESTATE, "two-fluid slab step needs a box geometry") : 0;
+}
+
+// the recolouring stream-collide of planes [k0, k1) from the stored
+// gradient arrays and flags (prepare_stress folded in)
+int ph_cg_streamcoll_range(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
+  if (k1 <= k0) return 0;
+  Prof p(h, TSLB_K_CG_STREAMCOLL, st);
+  ++h->launches;
+  return by_scalar(h, [&](auto z) {
+    using T = decltype(z);
+    return launch_cg_streamcoll<T>(h->lat, h->range(k0, k1), static_cast<T*>(h->f[0]), static_cast<T*>(h->f[1]),
+                                   h->tf(), h->solid, h->slow, h->omega, h->cp, 1, st);
+  });
+}
+
 // One fused step (fused_step / two_fluid_step) enqueued on h->s.
 int enqueue_step(tslb_cuda_sim* h) {
   int rc;
+  if (h->comps == 2 && h->xmode == 1 && nci_on(h)) {
+    // two-fluid slab with the near-contact scan: colour moments, phi's
+    // nci_reach boundary planes to the neighbours, gradient + scan (probes
+    // run into the ghost planes and may flag the neighbours' nodes), the
+    // ghost flags ORed into their owners' planes, then the recolouring
+    // stream-collide from the stored gradient and flags -- boundary planes
+    // first, population exchange overlapped with the interior as below
+    if ((rc = ph_cg_moments(h, h->s))) return rc;
+    if ((rc = exchange_phi_nccl(h, h->s))) return rc;
+    if ((rc = ph_cg_gradient_slab(h, h->s))) return rc;
+    if ((rc = exchange_flags_nccl(h, h->s))) return rc;
+    if ((rc = fold_flags(h, h->s))) return rc;
+    if ((rc = ph_cg_streamcoll_range(h, 0, 1, h->s))) return rc;
+    if (h->nzl > 1 && (rc = ph_cg_streamcoll_range(h, h->nzl - 1, h->nzl, h->s))) return rc;
+    CK(cudaEventRecord(h->ev_b, h->s));
+    CK(cudaStreamWaitEvent(h->cs, h->ev_b, 0));
+    if ((rc = exchange_nccl(h, h->cs))) return rc;
+    CK(cudaEventRecord(h->ev_c, h->cs));
+    if ((rc = ph_cg_streamcoll_range(h, 1, h->nzl - 1, h->s))) return rc;
+    CK(cudaStreamWaitEvent(h->s, h->ev_c, 0));
+    if ((rc = unpack(h, h->s))) return rc;
+    h->stress_pending = true;
+    ++h->steps;
+    return 0;
+  }
   if (h->comps == 2 && h->xmode == 1) {
     // two-fluid slab: colour moments, phi ghost planes, folded recolouring
     // stream-collide, population halos of both species. As in F1, the two
@@ -676,12 +778,14 @@ int enqueue_step(tslb_cuda_sim* h) {
       const int b = boundary_planes(h);
       if (h->nzl <= 2 * b) {
         if ((rc = ph_mstep(h, h->s))) return rc;
+        if ((rc = pack_moments(h, h->mo2, h->s))) return rc;
         if ((rc = exchange_moments_nccl(h, h->s))) return rc;
       } else {
         CK(cudaEventRecord(h->ev_b, h->s));
         CK(cudaStreamWaitEvent(h->cs, h->ev_b, 0));
         if ((rc = ph_mstep(h, h->cs, 0, b))) return rc;
         if ((rc = ph_mstep(h, h->cs, h->nzl - b, h->nzl))) return rc;
+        if ((rc = pack_moments(h, h->mo2, h->cs))) return rc;
         if ((rc = exchange_moments_nccl(h, h->cs))) return rc;
         CK(cudaEventRecord(h->ev_c, h->cs));
         if ((rc = ph_mstep(h, h->s, b, h->nzl - b))) return rc;
@@ -757,8 +861,6 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   if (!kinds || !uw) return set_err(TSLB_EINVAL, "face arrays are required");
   if (int rc = check_axes(kinds)) return rc;
   const bool decomposed = nzl != nz;
-  if (decomposed && components == 2 && color && color[2] != 0.0)
-    return set_err(TSLB_EINVAL, "two-fluid slabs: the near-contact force (NCI) is not decomposed");
   CK(cudaSetDevice(device));
 
   auto* h = new tslb_cuda_sim();
@@ -871,13 +973,28 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
     const size_t tb = size_t(d.mstride) * (3 + h->dim) * h->esz;
     if ((rc = alloc(h, &h->two, tb))) return fail(rc);
     CK(cudaMemsetAsync(h->two, 0, tb, h->s));
+    const bool nci = nci_on(h);
     if (decomposed) {
-      const size_t pg = size_t(d.plane) * (nzl + 2) * h->esz;
+      // the near-contact scan probes nci_reach nodes along +-c: phi (and the
+      // flags it may set) need that many ghost planes on each side
+      h->pgz = nci ? std::max(1, h->cp.nci_reach) : 1;
+      if (nzl < h->pgz)
+        return fail(set_err(TSLB_EINVAL, "two-fluid slab of %d planes is thinner than nci_reach = %d", nzl, h->pgz));
+      const size_t pg = size_t(d.plane) * (nzl + 2 * h->pgz) * h->esz;
       if ((rc = alloc(h, &h->phig, pg))) return fail(rc);
       CK(cudaMemsetAsync(h->phig, 0, pg, h->s));
     }
-    if ((rc = alloc(h, reinterpret_cast<void**>(&h->flag), size_t(d.mstride)))) return fail(rc);
-    CK(cudaMemsetAsync(h->flag, 0, size_t(d.mstride), h->s));
+    if (decomposed && nci) {
+      const size_t gp = size_t(h->pgz) * size_t(d.plane);
+      const size_t fb = 2 * gp + size_t(d.mstride);
+      if ((rc = alloc(h, reinterpret_cast<void**>(&h->flagg), fb))) return fail(rc);
+      CK(cudaMemsetAsync(h->flagg, 0, fb, h->s));
+      h->flag = h->flagg + gp;
+      if ((rc = alloc(h, reinterpret_cast<void**>(&h->rflag), 2 * gp))) return fail(rc);
+    } else {
+      if ((rc = alloc(h, reinterpret_cast<void**>(&h->flag), size_t(d.mstride)))) return fail(rc);
+      CK(cudaMemsetAsync(h->flag, 0, size_t(d.mstride), h->s));
+    }
   }
   // solid mask with ghost planes (always present: 1 B/node)
   const size_t sbytes = size_t(d.fstride);
@@ -1044,7 +1161,8 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   if (h->s) cudaStreamSynchronize(h->s);
   if (h->cs) cudaStreamSynchronize(h->cs);
   if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
-  void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->sx, h->phig, h->two, h->flag, h->solid, h->slow,
+  void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->sx, h->phig, h->two,
+                  h->flagg ? h->flagg : h->flag, h->rflag, h->solid, h->slow,
                   h->sbits, h->scratch, h->red, h->dig, h->recv_lo, h->recv_hi};
   for (void* b : bufs)
     if (b) cudaFree(b);
@@ -1740,6 +1858,33 @@ int tslb_cuda_group_step(tslb_cuda_handle* slabs, int count, long nsteps) {
     any_m = any_m || slabs[r]->sched == TSLB_SCHED_M;
   }
   if (any_m && !all_m) return set_err(TSLB_ESTATE, "linked slabs must share one step schedule");
+  if (slabs[0]->comps == 2 && nci_on(slabs[0])) {
+    // the NCCL path's phases (NCI), serialised
+    for (long s = 0; s < nsteps; ++s) {
+      for (int r = 0; r < count; ++r)
+        if (int rc = ph_cg_moments(slabs[r], st)) return rc;
+      for (int r = 0; r < count; ++r)
+        if (int rc = exchange_phi_local(slabs[r], st)) return rc;
+      for (int r = 0; r < count; ++r)
+        if (int rc = ph_cg_gradient_slab(slabs[r], st)) return rc;
+      for (int r = 0; r < count; ++r)
+        if (int rc = exchange_flags_local(slabs[r], st)) return rc;
+      for (int r = 0; r < count; ++r)
+        if (int rc = fold_flags(slabs[r], st)) return rc;
+      for (int r = 0; r < count; ++r)
+        if (int rc = ph_cg_streamcoll_range(slabs[r], 0, slabs[r]->nzl, st)) return rc;
+      for (int r = 0; r < count; ++r)
+        if (int rc = exchange_local(slabs[r], st)) return rc;
+      for (int r = 0; r < count; ++r) {
+        if (int rc = unpack(slabs[r], st)) return rc;
+        slabs[r]->stress_pending = true;
+        ++slabs[r]->steps;
+      }
+    }
+    CK(cudaStreamSynchronize(st));
+    CK(cudaGetLastError());
+    return 0;
+  }
   if (slabs[0]->comps == 2) {
     for (long s = 0; s < nsteps; ++s) {
       for (int r = 0; r < count; ++r)
@@ -1785,6 +1930,7 @@ int tslb_cuda_group_step(tslb_cuda_handle* slabs, int count, long nsteps) {
         } else if (!(rc = ph_mstep(h, st, 0, b))) {
           rc = ph_mstep(h, st, h->nzl - b, h->nzl);
         }
+        if (!rc && !first) rc = pack_moments(h, h->mo2, st);
         if (rc) return rc;
       }
       for (int r = 0; r < count; ++r)

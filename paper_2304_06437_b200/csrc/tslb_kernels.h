@@ -41,17 +41,15 @@ int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
 // moment-resident single-pass step (tslb_mstep.cu): m(t) in `mi` -> m(t+1)
 // in `mo` for box geometries, planes [z0, z1) (z1 <= 0: to the end) in
 // chunks of lz planes per CTA column; `gm` holds the slab ghost planes
-// ([2][NM][plane], below/above) when a z face is a slab interface, and `snd`
-// (optional, same layout) receives a copy of the slab's own boundary planes
-// 0 / nz - 1 of m(t+1) as they are reduced -- the packed send buffer of the
-// halo exchange. Returns 1 (nothing launched) when the shape is not
-// supported, -cudaError on a launch failure. `maps` caches the TMA tensor
-// maps (opaque, owned by the caller, freed with free_mstep_maps).
+// ([2][NM][plane], below/above) when a z face is a slab interface. Returns
+// 1 (nothing launched) when the shape is not supported, -cudaError on a
+// launch failure. `maps` caches the TMA tensor maps (opaque, owned by the
+// caller, freed with free_mstep_maps).
 struct MstepMaps;
 void free_mstep_maps(MstepMaps* maps);
 bool mstep_supported(int lat, const Dom& d);
 template <typename T>
-int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, T* snd, double omega,
+int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
                  int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st);
 // per-node solid bits of a masked geometry for the 3-D M step (tslb_mstep.cu)
 int launch_solid_bits(int lat, const Dom& d, const uint8_t* solid, uint32_t* bits, cudaStream_t st);
@@ -115,6 +113,13 @@ template <typename T>
 int launch_init_colors(int lat, const Dom& d, T* fr, T* fb,
                        const uint8_t* solid, const InitSpec& s,
                        cudaStream_t st);
+// gradient_and_nci on a box geometry that may be a z slab (phi and the NCI
+// flags carry nci_reach ghost planes; hits there are ORed into the
+// neighbours' flags with launch_flag_or)
+template <typename T>
+int launch_cg_gradient_nci_box(int lat, const Dom& d, const TwoFields& s, const ColorParamsDev& cp,
+                               cudaStream_t st);
+int launch_flag_or(uint8_t* dst, const uint8_t* src, int64_t n, cudaStream_t st);
 
 // ---- reductions / digest (tslb_reduce.cu)
 // totals: out[0] = mass, out[1..3] = momentum (fp64 deterministic tree)

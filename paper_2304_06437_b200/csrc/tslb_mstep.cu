@@ -477,8 +477,8 @@ __device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, con
 template <class L, typename T, typename C, bool WALLS, bool SOLID, int MINB>
 __global__ void __launch_bounds__(NT, MINB)
     k_mstep(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap, Dom d,
-            const T* __restrict__ mi, const T* __restrict__ gm, T* __restrict__ mo, T* __restrict__ snd, C om1,
-            int lz, int zbeg, int zend, const uint32_t* __restrict__ sbits) {
+            const T* __restrict__ mi, const T* __restrict__ gm, T* __restrict__ mo, C om1, int lz, int zbeg,
+            int zend, const uint32_t* __restrict__ sbits) {
   static_assert(L::dim == 3, "the M step is 3-D");
   using SM = Smem<L, T, SOLID>;
   constexpr int NM = n_moments<L>();
@@ -603,13 +603,6 @@ __global__ void __launch_bounds__(NT, MINB)
   constexpr bool PAIRS = msums_pair_form<T, C>();
   const int64_t ms = d.mstride;
 
-  // slab boundary planes also go to the packed send buffer [2][NM][plane]
-  auto send_row = [&](int zr) -> T* {
-    if (snd == nullptr) return nullptr;
-    if (zr == 0 && d.mode[ZMin] == kGhost) return snd + col;
-    if (zr == d.nz - 1 && d.mode[ZMax] == kGhost) return snd + int64_t(NM) * d.plane + col;
-    return nullptr;
-  };
   // the skewed reduction of plane zr (= z - 2) from its gathered slots v:
   // the sums ran in `acc`; nodes outside the pair form's range redo them in
   // the reference order from the (still intact) slots
@@ -623,11 +616,7 @@ __global__ void __launch_bounds__(NT, MINB)
       }
     }
     T* o = mo + col + int64_t(zr) * d.plane;
-    T* sx = send_row(zr);
-    put_moments<L, T, C>(d, sm, [&](int c, T v) {
-      o[c * ms] = v;
-      if (sx) sx[c * d.plane] = v;
-    });
+    put_moments<L, T, C>(d, sm, [&](int c, T v) { o[c * ms] = v; });
   };
 
   auto plane = [&](auto ZCc, int z) {
@@ -665,13 +654,9 @@ __global__ void __launch_bounds__(NT, MINB)
         // arrays keep their values (compute_moments skips them too), carried
         // into the output buffer of the ping-pong pair here
         if (ZC == 0 && solid) {
-          T* sx = send_row(z);
 #pragma unroll
-          for (int c = 0; c < NM; ++c) {
-            const T v = tb[c * TC + (ly + 1) * TX + lx];
-            mo[c * d.mstride + col + int64_t(z) * d.plane] = v;
-            if (sx) sx[c * d.plane] = v;
-          }
+          for (int c = 0; c < NM; ++c)
+            mo[c * d.mstride + col + int64_t(z) * d.plane] = tb[c * TC + (ly + 1) * TX + lx];
         }
       }
       if (!solid) {
@@ -694,11 +679,7 @@ __global__ void __launch_bounds__(NT, MINB)
       // compute_moments skips solid nodes (their moment arrays keep their values)
       if (z - 1 >= za && !(SOLID && solid_prev)) {
         T* o = mo + col + int64_t(z - 1) * d.plane;
-        T* sx = send_row(z - 1);
-        finalize<L, T, C>(d, rg, R, [&](int c, T v) {
-          o[c * ms] = v;
-          if (sx) sx[c * d.plane] = v;
-        });
+        finalize<L, T, C>(d, rg, R, [&](int c, T v) { o[c * ms] = v; });
       }
     }
     if constexpr (SOLID) {
@@ -898,7 +879,7 @@ int launch_ghost_push(int lat, int math, const Dom& d, T* f, const T* gm, double
 }
 
 template <typename T>
-int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, T* snd, double omega,
+int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
                  int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st) {
   using namespace mstep;
   if (!mstep_supported(lat, d)) return 1;
@@ -937,7 +918,7 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
     auto go = [&](auto kern, auto om1, size_t smem) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e == cudaSuccess) {
-        kern<<<grid, NT, smem, st>>>(*tm, *gmp, d, mi, gm, mo, snd, om1, lz, z0, z1, sbits);
+        kern<<<grid, NT, smem, st>>>(*tm, *gmp, d, mi, gm, mo, om1, lz, z0, z1, sbits);
         e = cudaGetLastError();
       }
       if (e != cudaSuccess) err = -int(e);
@@ -969,10 +950,10 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
   return lat == kD3Q19 ? by_rd(D3Q19{}) : by_rd(D3Q27{});
 }
 
-template int launch_mstep<float>(int, int, const Dom&, const float*, const float*, float*, float*, double, int,
-                                 int, int, MstepMaps*&, const uint32_t*, cudaStream_t);
-template int launch_mstep<double>(int, int, const Dom&, const double*, const double*, double*, double*, double,
-                                  int, int, int, MstepMaps*&, const uint32_t*, cudaStream_t);
+template int launch_mstep<float>(int, int, const Dom&, const float*, const float*, float*, double, int, int, int,
+                                 MstepMaps*&, const uint32_t*, cudaStream_t);
+template int launch_mstep<double>(int, int, const Dom&, const double*, const double*, double*, double, int, int,
+                                  int, MstepMaps*&, const uint32_t*, cudaStream_t);
 template int launch_ghost_push<float>(int, int, const Dom&, float*, const float*, double, int, const uint8_t*,
                                       cudaStream_t);
 template int launch_ghost_push<double>(int, int, const Dom&, double*, const double*, double, int,

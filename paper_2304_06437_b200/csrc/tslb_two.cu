@@ -448,6 +448,81 @@ __global__ void __launch_bounds__(BX2) k_cg_gradient_box(Dom d, TF<T> s) {
   if constexpr (L::dim == 3) s.grad[2 * ms + mi] = gz;
 }
 
+// Near-contact scan (gradient_and_nci's second half, multicomponent.hpp:
+// 202-238) on a box geometry that may be a z slab: a probe that crosses a
+// slab face continues into phi's ghost planes (the solver keeps nci_reach of
+// them on each side), and a hit there flags the node in the flag buffer's
+// matching ghost plane -- the neighbour owning that node ORs it into its own
+// flags (k_flag_or). Set-only flags commute, so the merged result equals the
+// single-domain scan. Owned flags were cleared by k_cg_moments.
+template <class L, typename T>
+__global__ void __launch_bounds__(BX2) k_cg_nci_box(Dom d, TF<T> s, ColorParamsDev cp) {
+  int i, j, k;
+  if (!node_coords<BX2>(d, i, j, k)) return;
+  const T bulk_cut = T(-1) + T(cp.eps_bulk);
+  if (!(s.phi[midx(d, i, j, k)] < bulk_cut)) return;
+  const int nd[3] = {d.nx, d.ny, d.nz};
+  // detail::advance (multicomponent.hpp:126-143): wrap periodic axes, stop
+  // at walls; slab faces lead into the ghost planes
+  auto advance = [&](int cx, int cy, int cz, int (&c)[3]) {
+    const int dc[3] = {cx, cy, cz};
+    int tc[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+      tc[ax] = c[ax] + dc[ax];
+      if (tc[ax] < 0 || tc[ax] >= nd[ax]) {
+        const int m = d.mode[2 * ax + (tc[ax] < 0 ? 0 : 1)];
+        if (m == kWrap) tc[ax] += tc[ax] < 0 ? nd[ax] : -nd[ax];
+        else if (m != kGhost) return false;
+      }
+    }
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) c[ax] = tc[ax];
+    return true;
+  };
+  unroll<L::q>([&](auto A) {
+    constexpr int a = decltype(A)::value;
+    using dd = Dir<L, a>;
+    if constexpr (a > 0 && dd::opp > a) {  // one probe per +-c pair
+      int64_t hit_p = 0, hit_m = 0;
+      bool found = false;
+      int c[3] = {i, j, k};
+      for (int st = 0; st < cp.nci_reach; ++st) {
+        if (!advance(dd::x, dd::y, dd::z, c)) break;
+        const int64_t t = midx(d, c[0], c[1], c[2]);
+        if (s.phi[t] >= bulk_cut) {
+          hit_p = t;
+          found = true;
+          break;
+        }
+      }
+      if (!found) return;
+      found = false;
+      c[0] = i;
+      c[1] = j;
+      c[2] = k;
+      for (int st = 0; st < cp.nci_reach; ++st) {
+        if (!advance(-dd::x, -dd::y, -dd::z, c)) break;
+        const int64_t t = midx(d, c[0], c[1], c[2]);
+        if (s.phi[t] >= bulk_cut) {
+          hit_m = t;
+          found = true;
+          break;
+        }
+      }
+      if (!found) return;
+      s.flag[hit_p] = 1;
+      s.flag[hit_m] = 1;
+    }
+  });
+}
+
+__global__ void __launch_bounds__(256) k_flag_or(uint8_t* __restrict__ dst, const uint8_t* __restrict__ src,
+                                                 int64_t n) {
+  const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  if (i < n) dst[i] |= src[i];
+}
+
 // GRAD: compute grad phi in place from the phi stencil instead of reading
 // the gradient arrays (the step's gradient phase folded in; the host
 // mirror computes the arrays lazily when they are read)
@@ -710,6 +785,27 @@ int launch_cg_streamcoll_grad(int lat, const Dom& d, T* fr, T* fb, const TwoFiel
   });
 }
 
+// gradient_and_nci on a box geometry / z slab: the gradient kernel (phi
+// stencil through the ghost planes) and the near-contact scan
+template <typename T>
+int launch_cg_gradient_nci_box(int lat, const Dom& d, const TwoFields& s, const ColorParamsDev& cp,
+                               cudaStream_t st) {
+  if (d.has_solid) return 1;
+  bool walls = false;
+  for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
+  return with_lat2(lat, [&](auto L) {
+    if (walls) k_cg_gradient_box<decltype(L), T, true><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s));
+    else k_cg_gradient_box<decltype(L), T, false><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s));
+    if (T(cp.nci_strength) != T(0)) k_cg_nci_box<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s), cp);
+  });
+}
+
+int launch_flag_or(uint8_t* dst, const uint8_t* src, int64_t n, cudaStream_t st) {
+  if (n <= 0) return 0;
+  k_flag_or<<<unsigned((n + 255) / 256), 256, 0, st>>>(dst, src, n);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 template <typename T>
 int launch_init_colors(int lat, const Dom& d, T* fr, T* fb,
                        const uint8_t* solid, const InitSpec& sp,
@@ -741,7 +837,9 @@ int launch_init_colors(int lat, const Dom& d, T* fr, T* fb,
                                             cudaStream_t);                    \
   template int launch_init_colors<T>(int, const Dom&, T*, T*,                 \
                                      const uint8_t*, const InitSpec&,         \
-                                     cudaStream_t);
+                                     cudaStream_t);                           \
+  template int launch_cg_gradient_nci_box<T>(int, const Dom&, const TwoFields&, \
+                                             const ColorParamsDev&, cudaStream_t);
 TSLB_INST2(float)
 TSLB_INST2(double)
 #undef TSLB_INST2

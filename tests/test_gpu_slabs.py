@@ -339,3 +339,102 @@ def test_survey_decomposition_512x256x256(gpu, sched):
             for s in slabs:
                 s.close()
         assert np.array_equal(dig, ref), f"{parts} slabs ({sched}): plane digests differ"
+
+
+# --- two-fluid slabs with the near-contact scan (NCI): phi and the flags keep
+# nci_reach ghost planes; probes cross slab faces; ghost flags are ORed into
+# their owners (multicomponent.hpp:202-238, 249-266) ---
+def _nci_cp():
+    return T.ColorParams(sigma=0.02, beta=0.7, nci_strength=0.01, nci_reach=3)
+
+
+def _nci_film(dims, dtype):
+    """Two red layers (cut to a disc) with thin blue films between them and
+    across the periodic z wrap: the scan flags nodes in most planes,
+    including the planes next to every slab face of 2 / 3 / 4 slabs."""
+    nx, ny, nz = dims
+    k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+
+    def layer(z0, z1, w=0.6):
+        return 0.5 * (np.tanh((k - z0) / w) - np.tanh((k - z1) / w))
+    red = (layer(3.5, 6.6) + layer(9.4, 12.5)) * (np.hypot(i - (nx - 1) / 2, j - (ny - 1) / 2) < 5)
+    phi = (2 * np.clip(red, 0, 1) - 1).ravel()
+    st = np.zeros((5, phi.size))
+    st[0], st[1], st[2], st[3] = 0.5 * (1 + phi), 0.5 * (1 - phi), 0.003, -0.002
+    return Oracle_port().init_colors("d3q19", dims, st.astype(dtype))
+
+
+NCI_FIELDS = ("phi", "gradphi", "rho", "nci_flag", "mom", "pineq")
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("parts", [2, 3, 4])
+@pytest.mark.parametrize("name,faces", TWO_FACES[:2], ids=[t[0] for t in TWO_FACES[:2]])
+def test_two_fluid_nci_slabs_equal_single_domain(gpu, oracle_port, name, faces, parts, dtype):
+    dims, steps = (16, 12, 16), 4
+    fr, fb = _nci_film(dims, dtype)
+    plane = dims[0] * dims[1]
+    one = T.DeviceSolver("d3q19", T.GridDims(*dims), 1.25, spec_of(faces), dtype, 2, None, _nci_cp())
+    try:
+        one.upload_f(fr, 0)
+        one.upload_f(fb, 1)
+        one.step(steps)
+        ref = {"fr": one.download_f(0), "fb": one.download_f(1)}
+        ref.update({k: one.download_field(k) for k in NCI_FIELDS})
+    finally:
+        one.close()
+    assert ref["nci_flag"].sum() > 50, "the state should trigger the near-contact scan"
+    slabs = [T.DeviceSolver("d3q19", T.GridDims(*dims), 1.25, spec_of(faces), dtype, 2, None, _nci_cp(), slab=s)
+             for s in split(dims[2], parts)]
+    try:
+        for sv, (z0, nzl) in zip(slabs, split(dims[2], parts)):
+            sv.upload_f(np.ascontiguousarray(fr[:, z0 * plane:(z0 + nzl) * plane]), 0)
+            sv.upload_f(np.ascontiguousarray(fb[:, z0 * plane:(z0 + nzl) * plane]), 1)
+        arr = (C.c_void_p * parts)(*[s.h.value for s in slabs])
+        _lib.call("tslb_cuda_link_local", arr, parts)
+        _lib.call("tslb_cuda_group_step", arr, parts, steps)
+        got = {"fr": np.concatenate([s.download_f(0) for s in slabs], axis=1),
+               "fb": np.concatenate([s.download_f(1) for s in slabs], axis=1)}
+        for k in NCI_FIELDS:
+            parts_k = [s.download_field(k) for s in slabs]
+            got[k] = np.concatenate(parts_k, axis=-1)
+    finally:
+        for s in slabs:
+            s.close()
+    for k in got:
+        assert_bitwise(got[k], ref[k], f"NCI {parts} slabs {k}")
+    # and the single domain against the oracle (the reference restatement)
+    fro, fbo = fr.copy(), fb.copy()
+    cd = dict(sigma=0.02, beta=0.7, nci_strength=0.01, nci_reach=3)
+    res = oracle_port.two_run("d3q19", dims, 1.25, cd, faces, fro, fbo, steps)
+    assert_bitwise(ref["fr"], fro, "NCI single domain vs oracle fr")
+    assert_bitwise(ref["nci_flag"], res["nci_flag"], "NCI single domain vs oracle flags")
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_two_fluid_nci_nccl_self_exchange(gpu, dtype):
+    """NCI slab on a one-rank NCCL communicator (its own neighbour above and
+    below) == the periodic box: phi ghost planes of depth nci_reach, the
+    probes across both faces and the flag OR exchange all go through NCCL."""
+    dims = (16, 12, 16)
+    fr, fb = _nci_film(dims, dtype)
+    spec = spec_of(O.periodic())
+    ref = T.DeviceSolver("d3q19", T.GridDims(*dims), 1.25, spec, dtype, 2, None, _nci_cp())
+    slab = T.DeviceSolver("d3q19", T.GridDims(dims[0], dims[1], 2 * dims[2]), 1.25, spec, dtype, 2, None, _nci_cp(),
+                          slab=(0, dims[2]))
+    try:
+        uid = (C.c_char * 128)()
+        _lib.call("tslb_cuda_nccl_unique_id", uid)
+        _lib.call("tslb_cuda_attach_nccl", slab.h, uid, 1, 0)
+        for d in (ref, slab):
+            d.upload_f(fr, 0)
+            d.upload_f(fb, 1)
+            d.step(5)
+        for sp in (0, 1):
+            assert_bitwise(slab.download_f(sp), ref.download_f(sp), f"NCI NCCL self-exchange species {sp}")
+        for k in NCI_FIELDS:
+            assert_bitwise(slab.download_field(k), ref.download_field(k), f"NCI NCCL self-exchange {k}")
+        assert ref.download_field("nci_flag").sum() > 50
+    finally:
+        slab.close()
+        ref.close()
