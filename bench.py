@@ -3,23 +3,30 @@
 "GLUPS and % of HBM roofline (D3Q19 1024^3) at 1/2/4/8 B200 vs CPU ref").
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload tgv-d3q19|channel-d3q27|droplet-d3q19|cavity-d2q9]
+                    [--workload tgv-d3q19|tgv-c5|channel-d3q27|droplet-d3q19|tgv-d2q9|porous-d3q19|cavity-d2q9]
+                    [--math f64|f32] [--schedule auto|m|f1]
 
 Default workload (the metric's): D3Q19 single-phase periodic Taylor-Green
 vortex, 1024^3 nodes per GPU, fp32 storage, fp64 node arithmetic (the
-reference's float build, bit for bit), F1 step = moments kernel + fused
-stream-collide kernel. N > 1 (torchrun, one rank per GPU): weak scaling, one
-1024^3 z slab per GPU of a 1024 x 1024 x (1024 N) periodic box, NCCL halo
-exchange overlapped with the interior stream-collide. The state (125.6 GB
-per GPU) is far larger than the 126 MB L2, so no L2 flush is needed.
+reference's float build, bit for bit), M step = ONE moment-resident kernel
+per step (k_mstep: populations rebuilt and streamed in shared memory, 80 B
+per lattice update). `--gpus N` without a torchrun environment re-launches
+this command as N ranks (one process per GPU, torch.distributed.run on
+127.0.0.1); under torchrun WORLD_SIZE must equal N. N > 1: weak scaling, one
+1024^3 z slab per GPU of a 1024 x 1024 x (1024 N) periodic box, boundary
+chunks + NCCL halo exchange on the comm stream overlapped with the interior
+chunk. `--workload tgv-c5` is BASELINE config 5 (strong scaling: the fixed
+2048 x 1024 x 1024 domain split into N slabs). The state (86 GB per GPU) is
+far larger than the 126 MB L2, so no L2 flush is needed.
 
-The other workloads are BASELINE.json's configs 1, 3 and 4, for the record
-(DESIGN.md); the driver's headline is the default.
+The other workloads are BASELINE.json's configs 1, 3 and 4 and extra cases,
+for the record; the driver's headline is the default.
 
 --impl reference times the reference's own CPU implementation
 (oracle/_ref/libtslb_ref.so = the unmodified tslb headers, WorkerPool over
-all host cores; the plain-C oracle port if that build is absent) on a
-bounded sample of the same workload.
+all host cores; the plain-C oracle port if that build is absent): the WHOLE
+per-GPU workload when the host has the memory (1024^3: 130 GB), else a
+1024 x 1024 x 16 slab sample of it.
 """
 from __future__ import annotations
 
@@ -642,7 +649,7 @@ def main():
 
     e2e = None
     if default and not args.no_e2e and world == 1:
-        e2e = run_e2e(sim, lat, nx * ny * nzp, args.steps, dtype)
+        e2e = run_e2e(sim, lat, (nx, ny, nzp), args.steps, dtype, W.get("amp", 0.03))
     elif default and not args.no_e2e:
         # the loop stages each rank's whole state in pinned host memory
         # (~99 GB per 1024^3 slab): not attempted N times on one host
@@ -695,32 +702,65 @@ def main():
         dist.destroy_process_group()
 
 
-def run_e2e(sim, lat, nn, steps, dtype):
+def tgv_state_host(dims, amp, tdt):
+    """The Taylor-Green node states (rho, u[3], Pi^neq[6] = 0 -- the
+    prepare_node arguments of initialize_regularized) of an nx*ny*nz box in
+    a pinned host tensor (1 + D + np, n), computed on the device plane chunk
+    by plane chunk (untimed set-up of the e2e loop)."""
+    import torch
+    nx, ny, nz = dims
+    plane = nx * ny
+    st = torch.zeros((10, plane * nz), dtype=tdt, pin_memory=True)
+    dev = torch.device("cuda")
+    two_pi = 2.0 * np.pi
+    X = two_pi * (torch.arange(nx, device=dev, dtype=torch.float64) + 0.5) / nx
+    Y = two_pi * (torch.arange(ny, device=dev, dtype=torch.float64) + 0.5) / ny
+    sx, cx, c2x = torch.sin(X), torch.cos(X), torch.cos(2 * X)
+    sy, cy, c2y = torch.sin(Y), torch.cos(Y), torch.cos(2 * Y)
+    step = max(1, (1 << 26) // plane)
+    for k0 in range(0, nz, step):
+        k1 = min(nz, k0 + step)
+        Z = two_pi * (torch.arange(k0, k1, device=dev, dtype=torch.float64) + 0.5) / nz
+        cz, c2z = torch.cos(Z)[:, None, None], torch.cos(2 * Z)[:, None, None]
+        rho = 1.0 + 3.0 * (amp * amp / 16.0) * (c2x[None, None, :] + c2y[None, :, None]) * (c2z + 2.0)
+        ux = amp * sx[None, None, :] * cy[None, :, None] * cz
+        uy = -amp * cx[None, None, :] * sy[None, :, None] * cz
+        sl = slice(k0 * plane, k1 * plane)
+        st[0, sl].copy_(rho.reshape(-1).to(tdt))
+        st[1, sl].copy_(ux.reshape(-1).to(tdt))
+        st[2, sl].copy_(uy.reshape(-1).to(tdt))
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    return st
+
+
+def run_e2e(sim, lat, dims, steps, dtype, amp):
     """The reference driver loop (tslb_main.cpp run_single) through the public
-    C-ABI with HOST buffers: upload f from pinned host memory, `steps` steps
-    each followed by a totals() sample read back to the host, then refresh
-    and download rho and u (the output frame). Host wall time around it."""
+    C-ABI with HOST buffers: the initial node states go up from pinned host
+    memory into the device initialize_regularized (tslb_cuda_init_state:
+    chunked upload overlapped with the initialisation), `steps` steps each
+    followed by a totals() sample read back to the host, then refresh and
+    download rho and u (the output frame). Host wall time around it."""
     import ctypes as C
 
     import torch
 
     from paper_2304_06437_b200 import _lib
-    q = lat.q
+    nn = int(np.prod(dims))
     esz = np.dtype(dtype).itemsize
     tdt = torch.float32 if esz == 4 else torch.float64
+    nm = 1 + lat.dim + lat.dim * (lat.dim + 1) // 2
     try:
-        host_f = torch.empty((q, nn), dtype=tdt, pin_memory=True)
+        host_state = tgv_state_host(dims, amp, tdt)
         out = torch.empty((1 + lat.dim, nn), dtype=tdt, pin_memory=True)
     except Exception as e:
         return {"value": None, "unit": "GLUPS", "error": f"pinned host alloc failed: {e}"[:200]}
     lib = _lib.load()
-    # untimed: the host holds the initial state
-    _lib.check(lib.tslb_cuda_download_f(sim.h, 0, C.c_void_p(host_f.data_ptr())))
     mass = C.c_double()
     mom = (C.c_double * 3)()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    _lib.check(lib.tslb_cuda_upload_f(sim.h, 0, C.c_void_p(host_f.data_ptr())))
+    _lib.check(lib.tslb_cuda_init_state(sim.h, C.c_void_p(host_state.data_ptr())))
     for _ in range(steps):
         _lib.check(lib.tslb_cuda_step(sim.h, 1))
         _lib.check(lib.tslb_cuda_totals(sim.h, C.byref(mass), mom))
@@ -728,11 +768,12 @@ def run_e2e(sim, lat, nn, steps, dtype):
     _lib.check(lib.tslb_cuda_download_field(sim.h, 0, C.c_void_p(out.data_ptr())))
     _lib.check(lib.tslb_cuda_download_field(sim.h, 1, C.c_void_p(out[1:].data_ptr())))
     t = time.perf_counter() - t0
-    h2d = q * nn * esz
+    h2d = nm * nn * esz
     d2h = (1 + lat.dim) * nn * esz + steps * 32
     return {"value": round(nn * steps / t / 1e9, 4), "unit": "GLUPS", "h2d_bytes_per_step": int(h2d / steps),
             "d2h_bytes_per_step": int(d2h / steps), "seconds": round(t, 3),
-            "loop": "upload f (pinned) -> steps x (step + totals readback) -> refresh, download rho,u"}
+            "loop": "node states (pinned) -> init_state (device initialize_regularized, upload overlapped) -> "
+                    "steps x (step + totals readback) -> refresh, download rho,u"}
 
 
 if __name__ == "__main__":

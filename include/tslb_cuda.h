@@ -125,10 +125,12 @@ int tslb_cuda_create_slab(int lattice, int scalar, int components, int nx,
 
 int tslb_cuda_destroy(tslb_cuda_handle h);
 int tslb_cuda_set_math(tslb_cuda_handle h, int math);
-/* Select the single-fluid step schedule (default: M where supported --
- * D3Q19/D3Q27, no solid mask, single domain, nx % 32 == 0, ny % 8 == 0 --
- * else F1). TSLB_EINVAL if M is requested where it is not supported. Same
- * results either way (fused_step, kernels.hpp:209-215). */
+/* Select the single-fluid step schedule (default: M where supported -- 3-D:
+ * D3Q19/D3Q27 with nx * sizeof(scalar) a multiple of 16 bytes (the TMA row
+ * pitch; any nx, ny otherwise: partial tiles at the grid edges), with or
+ * without a solid mask, whole domains and z slabs; 2-D: D2Q9 whole domains
+ * without solids -- else F1). TSLB_EINVAL if M is requested where it is not
+ * supported. Same results either way (fused_step, kernels.hpp:209-215). */
 int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule);
 int tslb_cuda_get_schedule(tslb_cuda_handle h, int* schedule);
 /* Single-fluid body force F (EXTENSION: the reference has no single-fluid
@@ -158,6 +160,14 @@ int tslb_cuda_download_geometry(tslb_cuda_handle h, uint8_t* solid,
                                 uint32_t* slow_mask, uint64_t* n_fluid);
 int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
                             double radius);
+/* initialize_regularized (kernels.hpp:296-311; the drop-in's
+ * initialize_regularized(FieldSet, NodeGeometry, node_state)) from HOST node
+ * states: (1 + D + D(D+1)/2) arrays of n_local storage-type scalars, the
+ * prepare_node arguments rho, u[D], Pi[np] per node (solid nodes are
+ * skipped). The upload is chunked and overlapped with the device
+ * initialisation; pinned host memory gives full PCIe bandwidth. Single fluid
+ * only (TSLB_EINVAL otherwise). Same f(0) bits as the host routine. */
+int tslb_cuda_init_state(tslb_cuda_handle h, const void* host_state);
 
 /* time stepping */
 int tslb_cuda_step(tslb_cuda_handle h, long nsteps);

@@ -38,12 +38,16 @@ int set_err(int code, const char* fmt, ...) {
   return code;
 }
 
+// (a failed call's error is reported here and cleared, so a later
+// cudaGetLastError() does not report it a second time against another call)
 #define CK(call)                                                              \
   do {                                                                        \
     cudaError_t e_ = (call);                                                  \
-    if (e_ != cudaSuccess)                                                    \
+    if (e_ != cudaSuccess) {                                                  \
+      cudaGetLastError();                                                     \
       return set_err(TSLB_ECUDA, "%s: %s (%s:%d)", #call,                     \
                      cudaGetErrorString(e_), __FILE__, __LINE__);             \
+    }                                                                         \
   } while (0)
 
 // ---- NCCL, loaded at run time (torch's copy if already mapped) -------------
@@ -138,6 +142,7 @@ struct tslb_cuda_sim {
   uint32_t* slow = nullptr;
   uint32_t* sbits = nullptr;  // M on a masked geometry: per-node solid bits (with ghost planes)
   void* scratch = nullptr;
+  void* state_buf = nullptr;  // tslb_cuda_init_state: the node states [1+D+np][mstride] (f(0) pending on them)
   double* red = nullptr;  // partials + outputs
   uint64_t* dig = nullptr;
   size_t dig_bytes = 0;
@@ -265,6 +270,13 @@ bool nci_on(const tslb_cuda_sim* h) {
 // the single-fluid population buffer, allocated on first use under M and
 // filled with the pending analytic f(0) if there is one
 int ensure_f(tslb_cuda_sim* h) {
+  // node states of tslb_cuda_init_state that no pending f(0) refers to any
+  // more: their memory goes before the populations are allocated
+  if (h->state_buf && !h->f0_pending) {
+    CK(cudaFree(h->state_buf));
+    h->state_buf = nullptr;
+    h->bytes -= size_t(h->d.mstride) * (1 + h->dim + h->np) * h->esz;
+  }
   if (!h->f[0]) {
     const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
     if (int rc = alloc(h, &h->f[0], fbytes)) return rc;
@@ -1031,7 +1043,7 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
     if ((rc = alloc(h, &h->recv_lo, pb))) return fail(rc);
     if ((rc = alloc(h, &h->recv_hi, pb))) return fail(rc);
   }
-  if (components == 1 && mstep_supported(lattice, d)) {
+  if (components == 1 && mstep_supported(lattice, d, h->esz)) {
     const char* e = std::getenv("TSLB_SCHEDULE");
     // M needs a second moment buffer (and ghost planes on slabs); where HBM
     // cannot hold it (e.g. D3Q27 1024^3 fp32) the solver stays on F1
@@ -1163,7 +1175,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
   void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->sx, h->phig, h->two,
                   h->flagg ? h->flagg : h->flag, h->rflag, h->solid, h->slow,
-                  h->sbits, h->scratch, h->red, h->dig, h->recv_lo, h->recv_hi};
+                  h->sbits, h->scratch, h->state_buf, h->red, h->dig, h->recv_lo, h->recv_hi};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -1195,10 +1207,10 @@ int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
   if (schedule == h->sched) return 0;
   CK(cudaSetDevice(h->device));
   if (schedule == TSLB_SCHED_M) {
-    if (h->comps != 1 || !mstep_supported(h->lat, h->d))
+    if (h->comps != 1 || !mstep_supported(h->lat, h->d, h->esz))
       return set_err(TSLB_EINVAL,
-                     "M schedule needs a single-fluid D3Q19/D3Q27 domain with nx %% 32 == 0 "
-                     "and ny %% 8 == 0 (or D2Q9 without solids); solid masks only on whole domains");
+                     "M schedule needs a single-fluid D3Q19/D3Q27 domain whose x rows are a multiple of "
+                     "16 bytes (or D2Q9 whole domains without solids)");
     if (!h->mo2) {
       const size_t mbytes = size_t(h->d.mstride) * (1 + h->dim + h->np) * h->esz;
       if (int rc = alloc(h, &h->mo2, mbytes)) return rc;
@@ -1457,6 +1469,72 @@ int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
   });
   if (rc) return rc;
   return sync(h);
+}
+
+// initialize_regularized (kernels.hpp:296-311) on the device from HOST node
+// states: the state planes travel in z chunks on the copy (comm) stream and
+// each chunk's kernel runs as soon as its planes have landed, so the PCIe
+// transfer overlaps the initialisation. Under M (box geometry) the kernel
+// writes the first step's moments directly and f(0) stays pending on the
+// uploaded states (materialised only if read); otherwise f(0) is stored.
+int tslb_cuda_init_state(tslb_cuda_handle h, const void* host) {
+  if (!host) return set_err(TSLB_EINVAL, "init_state: null state");
+  if (h->comps != 1)
+    return set_err(TSLB_EINVAL, "init_state: single-fluid node states (two-fluid: initialize_colors + upload_f)");
+  CK(cudaSetDevice(h->device));
+  const int nm = 1 + h->dim + h->np;
+  const bool m_path = h->sched == TSLB_SCHED_M && !h->d.has_solid;
+  h->fimplicit = false;
+  h->f0_pending = false;
+  h->m0_ready = false;
+  // (ensure_f releases an earlier state buffer: allocate this one after it)
+  if (!m_path)
+    if (int rc = ensure_f(h)) return rc;
+  if (!h->state_buf)
+    if (int rc = alloc(h, &h->state_buf, size_t(h->d.mstride) * nm * h->esz)) return rc;
+  InitSpec sp{};
+  sp.kind = kInitState;
+  sp.nx_g = h->nx;
+  sp.ny_g = h->ny;
+  sp.nz_g = h->nzg;
+  sp.z0 = h->z0;
+  sp.state = h->state_buf;
+  sp.sstride = h->d.mstride;
+  // ~32 MB of each state array per chunk
+  const int64_t plane = h->plane();
+  const int cz = int(std::max<int64_t>(1, (int64_t(32) << 20) / (plane * h->esz)));
+  const size_t pitch_h = size_t(h->n()) * h->esz, pitch_d = size_t(h->d.mstride) * h->esz;
+  CK(cudaEventRecord(h->ev_b, h->s));  // (the buffers are free once earlier work is done)
+  CK(cudaStreamWaitEvent(h->cs, h->ev_b, 0));
+  for (int k0 = 0; k0 < h->nzl; k0 += cz) {
+    const int k1 = std::min(h->nzl, k0 + cz);
+    const size_t off = size_t(k0) * plane * h->esz;
+    CK(cudaMemcpy2DAsync(static_cast<char*>(h->state_buf) + off, pitch_d, static_cast<const char*>(host) + off,
+                         pitch_h, size_t(k1 - k0) * plane * h->esz, size_t(nm), cudaMemcpyHostToDevice, h->cs));
+    CK(cudaEventRecord(h->ev_c, h->cs));
+    CK(cudaStreamWaitEvent(h->s, h->ev_c, 0));
+    ++h->launches;
+    const int rc = by_scalar(h, [&](auto z) {
+      using T = decltype(z);
+      if (m_path)
+        return launch_init_moments<T>(h->lat, h->math, h->range(k0, k1), static_cast<T*>(h->mo2), sp, h->s);
+      return launch_init_analytic<T>(h->lat, h->range(k0, k1), static_cast<T*>(h->f[0]),
+                                     h->d.has_solid ? h->solid : nullptr, sp, h->s);
+    });
+    if (rc) return set_err(TSLB_EINVAL, "init_state: bad lattice");
+  }
+  if (m_path) {
+    h->f0_spec = sp;
+    h->f0_pending = true;
+    h->m0_ready = true;
+    return sync(h);
+  }
+  // f(0) is stored: the states are no longer needed
+  if (int rc = sync(h)) return rc;
+  CK(cudaFree(h->state_buf));
+  h->state_buf = nullptr;
+  h->bytes -= size_t(h->d.mstride) * nm * h->esz;
+  return 0;
 }
 
 int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {

@@ -11,7 +11,9 @@ namespace tslb_cuda {
 
 enum MathMode : int { kMathDouble = 0, kMathFloat = 1 };
 
-enum InitKind : int { kInitRest = 0, kInitShear = 1, kInitTaylorGreen = 2, kInitDroplet = 3 };
+// kInitState: node states (the prepare_node arguments rho, u[D], Pi[np] of
+// initialize_regularized, kernels.hpp:296-311) read from device arrays
+enum InitKind : int { kInitRest = 0, kInitShear = 1, kInitTaylorGreen = 2, kInitDroplet = 3, kInitState = 4 };
 
 struct InitSpec {
   int kind;
@@ -19,6 +21,8 @@ struct InitSpec {
   int z0;                // global z of local plane 0
   double amp;            // shear / Taylor-Green velocity amplitude
   double cx, cy, cz, radius, width;  // droplet
+  const void* state;     // kInitState: [1 + D + np][sstride] of the storage type
+  int64_t sstride;
 };
 
 struct ColorParamsDev {
@@ -47,7 +51,7 @@ int launch_streamcoll_vec(int lat, int math, const Dom& d, T* f, const T* mo,
 // caller, freed with free_mstep_maps).
 struct MstepMaps;
 void free_mstep_maps(MstepMaps* maps);
-bool mstep_supported(int lat, const Dom& d);
+bool mstep_supported(int lat, const Dom& d, int esz);
 template <typename T>
 int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
                  int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st);

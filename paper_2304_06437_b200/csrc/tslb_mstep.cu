@@ -495,7 +495,13 @@ __global__ void __launch_bounds__(NT, MINB)
   const int x0 = int(blockIdx.x) * TX, y0 = int(blockIdx.y) * TY;
   const int za = zbeg + int(blockIdx.z) * lz, zb = min(za + lz, zend);
   const int gx = x0 + lx, gy = y0 + ly;
-  const int64_t col = gx + int64_t(d.nx) * gy;
+  // partial tiles at the high x / y edge of a grid that does not tile: the
+  // tile is tw x th nodes, its right halo column and upper halo row sit
+  // right after it; lanes beyond it push and store nothing (the TMA box
+  // reads zeros there)
+  const int tw = min(TX, d.nx - x0), th = min(TY, d.ny - y0);
+  const bool active = lx < tw && ly < th;
+  const int64_t col = active ? gx + int64_t(d.nx) * gy : 0;
 
   // halo task of this warp (see push_ring): side = warp / 2 (row below, row
   // above, column left, column right; the columns run from y0-1 to y0+TY and
@@ -506,12 +512,14 @@ __global__ void __launch_bounds__(NT, MINB)
   const int side = ly >> 1, half = ly & 1;
   int hnode = -1, hx = 0, hy = 0;
   if (side < 2) {
-    hnode = side * TX + lx;
-    hx = lx;
-    hy = side == 0 ? -1 : TY;
-  } else if (lx < TY + 2) {
+    if (lx < tw) {
+      hnode = side * TX + lx;
+      hx = lx;
+      hy = side == 0 ? -1 : th;
+    }
+  } else if (lx < th + 2) {
     hnode = 2 * TX + (side - 2) * (TY + 2) + lx;
-    hx = side == 2 ? -1 : TX;
+    hx = side == 2 ? -1 : tw;
     hy = lx - 1;
   }
   int64_t hcol = 0;
@@ -653,13 +661,13 @@ __global__ void __launch_bounds__(NT, MINB)
         // solid nodes push nothing (stream_collide skips them); their moment
         // arrays keep their values (compute_moments skips them too), carried
         // into the output buffer of the ping-pong pair here
-        if (ZC == 0 && solid) {
+        if (ZC == 0 && solid && active) {
 #pragma unroll
           for (int c = 0; c < NM; ++c)
             mo[c * d.mstride + col + int64_t(z) * d.plane] = tb[c * TC + (ly + 1) * TX + lx];
         }
       }
-      if (!solid) {
+      if (!solid && active) {
         const NodeMoments<C> m = node_at<L, T, C>(tb + (ly + 1) * TX + lx, TC);
         push_tile<L, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, m, om1, side);
         fed = true;
@@ -672,12 +680,12 @@ __global__ void __launch_bounds__(NT, MINB)
     }
     if constexpr (SKEW) {
       if (!fed) acc.all(v);
-      if (z - 2 >= za && !(SOLID && solid_prev2)) store_skewed(z - 2, acc, exact);
+      if (active && z - 2 >= za && !(SOLID && solid_prev2)) store_skewed(z - 2, acc, exact);
     }
     __syncthreads();
     if constexpr (!SKEW) {
       // compute_moments skips solid nodes (their moment arrays keep their values)
-      if (z - 1 >= za && !(SOLID && solid_prev)) {
+      if (active && z - 1 >= za && !(SOLID && solid_prev)) {
         T* o = mo + col + int64_t(z - 1) * d.plane;
         finalize<L, T, C>(d, rg, R, [&](int c, T v) { o[c * ms] = v; });
       }
@@ -700,12 +708,15 @@ __global__ void __launch_bounds__(NT, MINB)
   issue(za - 1, 0);
   __pipeline_commit();
   plane(std::integral_constant<int, 1>{}, za - 1);
-#pragma unroll 1
+#ifndef TSLB_MSTEP_UNROLL
+#define TSLB_MSTEP_UNROLL 1
+#endif
+#pragma unroll TSLB_MSTEP_UNROLL
   for (int z = za; z < zb; ++z) plane(std::integral_constant<int, 0>{}, z);
   plane(std::integral_constant<int, -1>{}, zb);
   if constexpr (SKEW) {
     // the last plane of the march (zb - 1) completed at the final barrier
-    if (zb - 1 >= za && !(SOLID && solid_prev2)) {
+    if (active && zb - 1 >= za && !(SOLID && solid_prev2)) {
       T v[L::q];
       gather<L, -2, T>(rg, Rf, v);
       MAcc<L, T, C, PAIRS> acc;
@@ -844,10 +855,12 @@ __global__ void __launch_bounds__(128)
 
 }  // namespace mstep
 
-bool mstep_supported(int lat, const Dom& d) {
+// 3-D: any nx, ny whose rows the TMA tensor map can address (row pitch a
+// multiple of 16 bytes); partial tiles at the high x / y edges
+bool mstep_supported(int lat, const Dom& d, int esz) {
   if (lat == kD2Q9) return !d.has_solid && d.nz == 1 && d.ghost == 0;  // tslb_mstep2d.cu
-  return (lat == kD3Q19 || lat == kD3Q27) && d.nx % mstep::TX == 0 &&
-         d.ny % mstep::TY == 0 && mstep::encoder() != nullptr;
+  return (lat == kD3Q19 || lat == kD3Q27) && (int64_t(d.nx) * esz) % 16 == 0 && d.nx >= 2 && d.ny >= 2 &&
+         mstep::encoder() != nullptr;
 }
 
 int launch_solid_bits(int lat, const Dom& d, const uint8_t* solid, uint32_t* bits, cudaStream_t st) {
@@ -882,7 +895,7 @@ template <typename T>
 int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
                  int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st) {
   using namespace mstep;
-  if (!mstep_supported(lat, d)) return 1;
+  if (!mstep_supported(lat, d, int(sizeof(T)))) return 1;
   if (d.has_solid && !sbits) return 1;
   if (z1 <= 0) z1 = d.nz;
   if (lat == kD2Q9) return z0 == 0 && z1 == d.nz ? launch_mstep2d<T>(math, d, mi, mo, omega, st) : 1;
@@ -893,7 +906,7 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
   const int nchunks = (z1 - z0 + lz - 1) / lz;
   bool walls = false;
   for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
-  const dim3 grid(unsigned(d.nx / TX), unsigned(d.ny / TY), unsigned(nchunks));
+  const dim3 grid(unsigned((d.nx + TX - 1) / TX), unsigned((d.ny + TY - 1) / TY), unsigned(nchunks));
   if (grid.y > 65535 || grid.z > 65535) return 1;
   const double om1d = 1.0 - double(T(omega));
   const float om1f = 1.0f - float(omega);

@@ -319,6 +319,15 @@ __global__ void __launch_bounds__(BX)
 // node state of the analytic initialisers (rest, shear, Taylor-Green)
 template <class L, typename T>
 __device__ __forceinline__ NodeMoments<T> init_state(const InitSpec& s, int i, int j, int k) {
+  if (s.kind == kInitState) {  // user node states, already in T
+    const T* p = static_cast<const T*>(s.state) + (int64_t(i) + int64_t(s.nx_g) * (int64_t(j) + int64_t(s.ny_g) * k));
+    const int64_t q = s.sstride;
+    if constexpr (L::dim == 3)
+      return prepare_node<T>(p[0], p[q], p[2 * q], p[3 * q], p[4 * q], p[5 * q], p[6 * q], p[7 * q], p[8 * q],
+                             p[9 * q]);
+    else
+      return prepare_node<T>(p[0], p[q], p[2 * q], T(0), p[3 * q], p[4 * q], T(0), p[5 * q], T(0), T(0));
+  }
   const double two_pi = 6.283185307179586476925286766559;
   double rho = 1.0, ux = 0.0, uy = 0.0, uz = 0.0;
   const int kg = k + s.z0;

@@ -463,6 +463,23 @@ class DeviceSolver:
     def init_analytic(self, kind: str, amplitude=0.0, radius=0.0):
         self._call("tslb_cuda_init_analytic", _lib.INIT[kind], float(amplitude), float(radius))
 
+    def init_state(self, state):
+        """initialize_regularized on the device from host node states: an
+        array (1 + D + np, n) of the storage dtype -- rho, u[D], Pi[np] per
+        node (kernels.hpp:296-311). Pinned host memory (e.g. a torch tensor
+        with pin_memory) is taken as is, by pointer."""
+        nm = 1 + self.lat.dim + self.lat.npineq
+        if hasattr(state, "data_ptr"):  # a torch tensor (pinned host buffer)
+            if tuple(state.shape) != (nm, self.n) or not state.is_contiguous() or state.element_size() != \
+                    np.dtype(self.dtype).itemsize or state.is_cuda:
+                raise _lib.InvalidArgument(f"init_state: expected a contiguous host tensor of shape {(nm, self.n)}")
+            self._call("tslb_cuda_init_state", C.c_void_p(state.data_ptr()))
+            return
+        a = np.ascontiguousarray(state, self.dtype)
+        if a.shape != (nm, self.n):
+            raise _lib.InvalidArgument(f"init_state: expected shape {(nm, self.n)}, got {a.shape}")
+        self._call("tslb_cuda_init_state", _ptr(a))
+
     # diagnostics
     def totals(self):
         mass = C.c_double()

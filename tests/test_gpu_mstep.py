@@ -221,6 +221,13 @@ def test_schedule_rules(gpu):
         assert dev.schedule == "m"  # the 2-D M kernel (tslb_mstep2d.cu)
     finally:
         dev.close()
+    # 3-D rows of a multiple of 16 bytes tile partially: M
+    for nx, dt in ((36, np.float32), (30, np.float64), (1000, np.float32)):
+        dev = T.DeviceSolver("d3q19", T.GridDims(nx, 9, 3), 1.0, spec, dt)
+        try:
+            assert dev.schedule == "m", (nx, dt)
+        finally:
+            dev.close()
 
 
 @pytest.mark.parametrize("dtype", DT)
@@ -594,3 +601,52 @@ def test_persist_toggle_on_one_handle(gpu, oracle_port, monkeypatch):
         dev.close()
     fo, _ = _oracle(oracle_port, lat, dims, om, faces, f0, total)
     assert_bitwise(fg, fo, "persist toggles")
+
+
+PARTIAL = [
+    ("periodic-36x13", (36, 13, 7), O.periodic()),
+    ("corners-44x10", (44, 10, 5), corner_box_3d()),
+    ("xwalls-20x9", (20, 9, 6), xwalls_3d()),
+    ("ylid-100x11", (100, 11, 4), ylid_3d()),
+]
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("lat", ["d3q19", "d3q27"])
+@pytest.mark.parametrize("case", PARTIAL, ids=lambda c: c[0])
+def test_mstep_partial_tiles_bitwise(gpu, oracle_port, case, lat, dtype):
+    """Grids that do not tile 32 x 8 run the M kernel with partial tiles at
+    the high x / y edges (halo column / row right after the last node,
+    inactive lanes push nothing) -- bit-identical to fused_step."""
+    name, dims, faces = case
+    f0 = O.random_state(lat, dims, 23, dtype)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 0.93, spec_of(faces), dtype)
+    try:
+        assert dev.schedule == "m", "partial tiles should run the M schedule"
+        dev.upload_f(f0)
+        dev.step(5)
+        mg = _moments(dev, lat)
+        fg = dev.download_f()
+    finally:
+        dev.close()
+    fo, mo = _oracle(oracle_port, lat, dims, 0.93, faces, f0, 5)
+    assert_bitwise(mg, mo, f"M partial {lat}/{name} moments")
+    assert_bitwise(fg, fo, f"M partial {lat}/{name} f")
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_mstep_partial_tiles_solid(gpu, oracle_port, dtype):
+    lat, dims, faces = "d3q19", (44, 13, 6), zwalls_3d()
+    solid = random_solid(dims, 0.2, 9)
+    f0 = O.random_state(lat, dims, 29, dtype, solid)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.1, spec_of(faces), dtype, 1, solid)
+    try:
+        assert dev.schedule == "m"
+        dev.upload_f(f0)
+        dev.step(4)
+        fg = dev.download_f()
+    finally:
+        dev.close()
+    fo = f0.copy()
+    oracle_port.single_run(lat, dims, 1.1, faces, fo, None, 4, 0, solid)
+    assert_bitwise(fg, fo, "M partial tiles, solid mask", solid == 0)

@@ -435,3 +435,44 @@ def test_host_buffer_validation(gpu):
         assert dev.download_f(out=ok) is ok
     finally:
         dev.close()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("lat,dims,sched,masked", [
+    ("d3q19", (32, 16, 6), "m", False), ("d3q19", (32, 16, 6), "f1", False), ("d3q27", (32, 8, 5), "m", False),
+    ("d2q9", (45, 17, 1), "m", False), ("d3q19", (12, 10, 9), "f1", True)])
+def test_init_state_matches_host_initialize_regularized(gpu, oracle_port, lat, dims, sched, masked, dtype):
+    """tslb_cuda_init_state: initialize_regularized on the device from host
+    node states (the e2e input path) == the port's initialize_regularized,
+    bit for bit, then the same fused steps -- with f(0) pending under M
+    (downloaded before the first step) and stored under F1."""
+    L = T.lattice_of(lat)
+    n = int(np.prod(dims))
+    nm = 1 + L.dim + L.npineq
+    rng = np.random.default_rng(17)
+    st = rng.uniform(-0.02, 0.02, (nm, n))
+    st[0] += 1.0
+    st[1 + L.dim:] *= 0.01
+    st = st.astype(dtype)
+    solid = random_solid(dims, 0.15, 3) if masked else None
+    state10 = st if L.dim == 3 else np.concatenate([st[:3], np.zeros((1, n), dtype), st[3:5], np.zeros((1, n), dtype),
+                                                    st[5:6], np.zeros((2, n), dtype)])
+    f0 = oracle_port.init_regularized(lat, dims, state10, solid)
+    faces = zwalls_3d() if L.dim == 3 else O.lid_cavity(0.05)
+    for read_first in (True, False):
+        dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.3, spec_of(faces), dtype, 1, solid)
+        try:
+            if dev.schedule != sched:
+                dev.set_schedule(sched)
+            dev.init_state(st)
+            if read_first:
+                fluid = np.ones(n, bool) if solid is None else solid == 0
+                assert_bitwise(dev.download_f(), f0, f"{lat} {sched} f(0)", fluid)
+            dev.step(4)
+            fg = dev.download_f()
+        finally:
+            dev.close()
+        fo = f0.copy()
+        oracle_port.single_run(lat, dims, 1.3, faces, fo, None, 4, 0, solid)
+        fluid = np.ones(n, bool) if solid is None else solid == 0
+        assert_bitwise(fg, fo, f"{lat} {sched} f(4) after init_state (read f(0) first: {read_first})", fluid)
