@@ -708,10 +708,12 @@ __global__ void __launch_bounds__(NT, MINB)
   issue(za - 1, 0);
   __pipeline_commit();
   plane(std::integral_constant<int, 1>{}, za - 1);
-#ifndef TSLB_MSTEP_UNROLL
-#define TSLB_MSTEP_UNROLL 1
+#ifdef TSLB_MSTEP_UNROLL  // (measurement switch)
+  constexpr int kUnroll = TSLB_MSTEP_UNROLL;
+#else
+  constexpr int kUnroll = 1;
 #endif
-#pragma unroll TSLB_MSTEP_UNROLL
+#pragma unroll kUnroll
   for (int z = za; z < zb; ++z) plane(std::integral_constant<int, 0>{}, z);
   plane(std::integral_constant<int, -1>{}, zb);
   if constexpr (SKEW) {
