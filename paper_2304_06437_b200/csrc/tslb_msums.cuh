@@ -180,26 +180,41 @@ __host__ __device__ constexpr bool msums_pair_form() {
 #endif
 }
 
-/// M < m * 2^24 over |v| (false for zeros, infinities, NaNs)
+/// M < m * 2^24 over |v| (false for zeros, infinities, NaNs): three-input
+/// |.| min / max (FMNMX3) as a tree of depth 3 for q <= 27; .NaN makes a NaN
+/// win the max
+namespace msums_detail {
+__device__ __forceinline__ float amax3(float a, float b, float c) {
+  float r;
+  asm("max.NaN.abs.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+__device__ __forceinline__ float amin3(float a, float b, float c) {
+  float r;
+  asm("min.abs.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
+  return r;
+}
+// reduce v[I0 .. I0 + N) with F, three at a time
+template <int I0, int N, bool MAX, int Q>
+__device__ __forceinline__ float red3(const float (&v)[Q]) {
+  if constexpr (N == 1) {
+    return fabsf(v[I0]);
+  } else if constexpr (N == 2) {
+    return MAX ? amax3(v[I0], v[I0 + 1], v[I0 + 1]) : amin3(v[I0], v[I0 + 1], v[I0 + 1]);
+  } else if constexpr (N == 3) {
+    return MAX ? amax3(v[I0], v[I0 + 1], v[I0 + 2]) : amin3(v[I0], v[I0 + 1], v[I0 + 2]);
+  } else {
+    constexpr int A = (N + 2) / 3, B = (N - A + 1) / 2, C = N - A - B;
+    const float x = red3<I0, A, MAX>(v), y = red3<I0 + A, B, MAX>(v), z = red3<I0 + A + B, C, MAX>(v);
+    return MAX ? amax3(x, y, z) : amin3(x, y, z);
+  }
+}
+}  // namespace msums_detail
+
 template <int Q>
 __device__ __forceinline__ bool msums_exact(const float (&v)[Q]) {
-  float mx = v[0], mn = v[0];
-  int i = 1;
-  // three-input |.| min / max (FMNMX3); .NaN makes a NaN win the max
-#pragma unroll
-  for (; i + 1 < Q; i += 2) {
-    asm("max.NaN.abs.f32 %0, %0, %1, %2;" : "+f"(mx) : "f"(v[i]), "f"(v[i + 1]));
-    asm("min.abs.f32 %0, %0, %1, %2;" : "+f"(mn) : "f"(v[i]), "f"(v[i + 1]));
-  }
-#pragma unroll
-  for (; i < Q; ++i) {
-    asm("max.NaN.abs.f32 %0, %0, %1;" : "+f"(mx) : "f"(v[i]));
-    asm("min.abs.f32 %0, %0, %1;" : "+f"(mn) : "f"(v[i]));
-  }
-  if (Q == 1) {
-    mx = fabsf(mx);
-    mn = fabsf(mn);
-  }
+  const float mx = msums_detail::red3<0, Q, true>(v);
+  const float mn = msums_detail::red3<0, Q, false>(v);
   return mx < mn * 16777216.0f;
 }
 
@@ -214,7 +229,12 @@ __device__ __forceinline__ bool msums_exact(const double (&)[Q]) {
 template <class L, typename T, typename C>
 __device__ __forceinline__ MSums<C> msums(const T (&v)[L::q]) {
   if constexpr (msums_pair_form<T, C>()) {
-    if (msums_exact<L::q>(v)) return msums_pairs<L, T, C>(v);
+    // speculative: the pair sums and the range check are independent, so
+    // they overlap; nodes that fail the check redo the sums in the
+    // reference order
+    MSums<C> s = msums_pairs<L, T, C>(v);
+    if (!msums_exact<L::q>(v)) s = msums_reference<L, T, C>(v);
+    return s;
   }
   return msums_reference<L, T, C>(v);
 }

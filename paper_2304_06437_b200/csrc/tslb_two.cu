@@ -29,6 +29,26 @@ struct TF {
   uint8_t* flag;
 };
 
+// base pointer of every population array of both species (kernel
+// parameters, read through the constant cache): a push then costs one
+// 32-bit index and one wide multiply-add for its address instead of a
+// running 64-bit pointer per species and direction
+template <typename T>
+struct PopBases {
+  T* r[27];
+  T* b[27];
+};
+
+template <typename T>
+__host__ PopBases<T> pop_bases(T* fr, T* fb, const Dom& d, int q) {
+  PopBases<T> p{};
+  for (int a = 0; a < q; ++a) {
+    p.r[a] = fr + int64_t(a) * d.fstride;
+    p.b[a] = fb + int64_t(a) * d.fstride;
+  }
+  return p;
+}
+
 template <typename T>
 __host__ TF<T> tf_of(const TwoFields& s) {
   return TF<T>{static_cast<T*>(s.rho_r), static_cast<T*>(s.rho_b),
@@ -533,7 +553,7 @@ __global__ void __launch_bounds__(256) k_flag_or(uint8_t* __restrict__ dst, cons
 #endif
 template <class L, typename T, bool FOLD, bool WALLS, bool GRAD>
 __global__ void TSLB_CG_BOUNDS
-    k_cg_streamcoll_box(Dom d, T* __restrict__ fr, T* __restrict__ fb, TF<T> s, T omega, T tau,
+    k_cg_streamcoll_box(Dom d, const __grid_constant__ PopBases<T> pop, TF<T> s, T omega, T tau,
                         ColorParamsDev cp) {
   int i, j, k;
   if (!node_coords<BX2>(d, i, j, k)) return;
@@ -579,12 +599,8 @@ __global__ void TSLB_CG_BOUNDS
   const T inv_gn = interface ? T(1) / gn : T(0);
   const T nhx = gx * inv_gn, nhy = gy * inv_gn, nhz = gz * inv_gn;
   const bool linear = cp.linear != 0;
-  // per-thread slot pointers of the direction being written, advanced by one
-  // array stride per direction (directions are visited in order): one 64-bit
-  // add per direction and species instead of a fresh a * fstride product
-  T* pr = fr + fi;
-  T* pb = fb + fi;
-  const int64_t fs = d.fstride;
+  // (a population array holds < 2^32 elements: 32-bit slot indices)
+  const uint32_t fi32 = uint32_t(fi);
 
   // one direction: perturbation + recolouring (reference order), then push
   // or bounce (multicomponent.hpp:340-398). IFACE is the node's interface
@@ -630,15 +646,13 @@ __global__ void TSLB_CG_BOUNDS
       if constexpr (dd::z == -1) add(st.bm[2], ZMin);
       const T corr = bounce_correction<L, a, T>(wx, wy, wz);
       const T corr_r = red_frac * corr;
-      constexpr int so = dd::opp - a;  // the opposite array is the neighbouring one
-      pr[so * fs] = fr_out - corr_r;
-      pb[so * fs] = fb_out - (corr - corr_r);
+      pop.r[dd::opp][fi32] = fr_out - corr_r;
+      pop.b[dd::opp][fi32] = fb_out - (corr - corr_r);
     } else {
-      pr[delta] = fr_out;
-      pb[delta] = fb_out;
+      const uint32_t t = fi32 + uint32_t(delta);
+      pop.r[a][t] = fr_out;
+      pop.b[a][t] = fb_out;
     }
-    pr += fs;
-    pb += fs;
   };
   auto all_dirs = [&](auto IF) {
     unroll<L::q>([&](auto A) {
@@ -753,9 +767,11 @@ int launch_cg_streamcoll(int lat, const Dom& d, T* fr, T* fb,
       bool walls = false;
       for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
       if (walls)
-        k_cg_streamcoll_box<decltype(L), T, true, true, false><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
+        k_cg_streamcoll_box<decltype(L), T, true, true, false>
+            <<<grid2(d), BX2, 0, st>>>(d, pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
       else
-        k_cg_streamcoll_box<decltype(L), T, true, false, false><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
+        k_cg_streamcoll_box<decltype(L), T, true, false, false>
+            <<<grid2(d), BX2, 0, st>>>(d, pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
       return;
     }
     if (fold_prepare)
@@ -779,9 +795,11 @@ int launch_cg_streamcoll_grad(int lat, const Dom& d, T* fr, T* fb, const TwoFiel
   for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
   return with_lat2(lat, [&](auto L) {
     if (walls)
-      k_cg_streamcoll_box<decltype(L), T, true, true, true><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
+      k_cg_streamcoll_box<decltype(L), T, true, true, true>
+          <<<grid2(d), BX2, 0, st>>>(d, pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
     else
-      k_cg_streamcoll_box<decltype(L), T, true, false, true><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), om, tau, cp);
+      k_cg_streamcoll_box<decltype(L), T, true, false, true>
+          <<<grid2(d), BX2, 0, st>>>(d, pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
   });
 }
 
