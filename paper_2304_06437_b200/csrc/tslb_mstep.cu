@@ -363,19 +363,19 @@ __device__ __forceinline__ void push_tile(const Dom& d, const Ring<L, T>& rg, T 
     constexpr int a = decltype(A)::value;
     if constexpr (a == 0 || (a & 1)) side(A);
     if constexpr (a == 0) {
-      if constexpr (ZC == 0) emit<L, 0, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(post_rest<L, C>(m, om1)));
+      if constexpr (ZC == 0) emit<L, 0, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(sf_post<L, 0, C>(m, om1)));
     } else if constexpr (a & 1) {
       constexpr bool ua = ZC == 0 || Dir<L, a>::z == ZC;
       constexpr bool ub = ZC == 0 || Dir<L, a + 1>::z == ZC;
       if constexpr (ua && ub) {
         C ra, rb;
-        post_pair<L, a, C>(m, om1, ra, rb);
+        sf_pair<L, a, C>(m, om1, ra, rb);
         emit<L, a, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(ra));
         emit<L, a + 1, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(rb));
       } else if constexpr (ua) {
-        emit<L, a, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(post_single<L, a, C>(m, om1)));
+        emit<L, a, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(sf_post<L, a, C>(m, om1)));
       } else if constexpr (ub) {
-        emit<L, a + 1, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(post_single<L, a + 1, C>(m, om1)));
+        emit<L, a + 1, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(sf_post<L, a + 1, C>(m, om1)));
       }
     }
   });
@@ -413,7 +413,7 @@ __device__ __forceinline__ void push_halo(const Ring<L, T>& rg, int hdelta, int 
       if constexpr (SX == 0 && dd::x != 0) in = unsigned(tx) < unsigned(TX);
       if constexpr (SY == 0) in = in && unsigned(ty) < unsigned(TY);  // x columns carry the corners
       Shm<T>::template st_if<slot_off<L, a, dd::x, dd::y, T>()>(ring_addr<L, a, dd::z>(rg) + hdelta, 
-                                                                 T(post_single<L, a, C>(m, om1)), in);
+                                                                 T(sf_post<L, a, C>(m, om1)), in);
     }
   });
 }
@@ -447,23 +447,6 @@ __device__ __forceinline__ void gather(const Ring<L, T>& rg, const T (&Rv)[L::q]
 }
 
 template <class L, typename T, typename C, class Put>
-__device__ __forceinline__ void put_moments(const Dom& d, MSums<C> s, const Put& put) {
-  if constexpr (L::dim == 3) force_shift<C>(d, s.jx, s.jy, s.jz);
-  else { C z0 = 0; force_shift<C>(d, s.jx, s.jy, z0); }
-  const C c3 = cs2<C>();
-  put(0, T(s.r));
-  put(1, T(s.jx));
-  put(2, T(s.jy));
-  put(3, T(s.jz));
-  put(4, T(s.pxx - c3 * s.r - s.jx * s.jx));
-  put(5, T(s.pyy - c3 * s.r - s.jy * s.jy));
-  put(6, T(s.pzz - c3 * s.r - s.jz * s.jz));
-  put(7, T(s.pxy - s.jx * s.jy));
-  put(8, T(s.pxz - s.jx * s.jz));
-  put(9, T(s.pyz - s.jy * s.jz));
-}
-
-template <class L, typename T, typename C, class Put>
 __device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, const T (&R)[L::q][3], const Put& put) {
   T rv[L::q], v[L::q];
   unroll<L::q>([&](auto A) {
@@ -471,7 +454,7 @@ __device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, con
     if constexpr (is_reg<L>(a)) rv[a] = R[a][0];
   });
   gather<L, -1, T>(rg, rv, v);
-  put_moments<L, T, C>(d, msums<L, T, C>(v), put);
+  moment_tail<L, T, C>(d, msums<L, T, C>(v), put);
 }
 
 template <class L, typename T, typename C, bool WALLS, bool SOLID, int MINB>
@@ -624,7 +607,7 @@ __global__ void __launch_bounds__(NT, MINB)
       }
     }
     T* o = mo + col + int64_t(zr) * d.plane;
-    put_moments<L, T, C>(d, sm, [&](int c, T v) { o[c * ms] = v; });
+    moment_tail<L, T, C>(d, sm, [&](int c, T v) { o[c * ms] = v; });
   };
 
   auto plane = [&](auto ZCc, int z) {
@@ -817,7 +800,7 @@ __global__ void __launch_bounds__(128) k_ghost_push(Dom d, T* __restrict__ f, co
       const NodeMoments<C> m = prepare_node<C>(C(p[0]), C(p[cs]), C(p[2 * cs]), C(p[3 * cs]), C(p[4 * cs]),
                                                C(p[5 * cs]), C(p[6 * cs]), C(p[7 * cs]), C(p[8 * cs]),
                                                C(p[9 * cs]));
-      f[a * d.fstride + fidx(d, i, j, k)] = T(post_collision<L, a, C>(m, om1));
+      f[a * d.fstride + fidx(d, i, j, k)] = T(sf_post_ref<L, a, C>(m, om1));
     }
   });
 }

@@ -129,19 +129,19 @@ __device__ __forceinline__ void strip_pass(const Dom& d, const T* __restrict__ m
       unroll<9>([&](auto A) {
         constexpr int a = decltype(A)::value;
         if constexpr (a == 0) {
-          if constexpr (ZC == 0) push(A, T(post_rest<Lat, C>(m, om1)));
+          if constexpr (ZC == 0) push(A, T(sf_post<Lat, 0, C>(m, om1)));
         } else if constexpr (a & 1) {
           constexpr bool ua = ZC == 0 || Dir<Lat, a>::y == ZC;
           constexpr bool ub = ZC == 0 || Dir<Lat, a + 1>::y == ZC;
           if constexpr (ua && ub) {
             C ra, rb;
-            post_pair<Lat, a, C>(m, om1, ra, rb);
+            sf_pair<Lat, a, C>(m, om1, ra, rb);
             push(A, T(ra));
             push(std::integral_constant<int, a + 1>{}, T(rb));
           } else if constexpr (ua) {
-            push(A, T(post_single<Lat, a, C>(m, om1)));
+            push(A, T(sf_post<Lat, a, C>(m, om1)));
           } else if constexpr (ub) {
-            push(std::integral_constant<int, a + 1>{}, T(post_single<Lat, a + 1, C>(m, om1)));
+            push(std::integral_constant<int, a + 1>{}, T(sf_post<Lat, a + 1, C>(m, om1)));
           }
         }
       });

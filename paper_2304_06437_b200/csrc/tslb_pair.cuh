@@ -3,6 +3,8 @@
 // (exact rewrites, see tslb_streamcoll_vec.cu header for the argument).
 #pragma once
 
+#include <type_traits>
+
 #include "tslb_collision.cuh"
 #include "tslb_domain.cuh"
 
@@ -117,6 +119,84 @@ __device__ __forceinline__ C post_single(const NodeMoments<C>& m, C om1) {
   const C cu = dot_noseed<d::x, d::y, d::z, C>(m.ux, m.uy, m.uz);
   const C e = t * (m.rho + C(3) * cu + C(4.5) * cu * cu - m.usq15);
   return e + om1 * regularized_noseed<L, A, C>(m);
+}
+
+// ---------------------------------------------------------------------------
+// fp32 node arithmetic (the opt-in tolerance mode): the same
+// regularised collision in fused multiply-adds with the node constants
+// folded -- f_a = t (rho - 1.5 u^2) + 3t c.u + 4.5t (c.u)^2
+// + (1 - omega) 4.5t (Q_a : Pi^neq - cs2 tr Pi). Every single-fluid kernel
+// takes these forms when C = float (mstep, mstep2d, F1 vector / scalar,
+// collide, ghost push), so the schedules agree bit for bit with each other;
+// the reference parity of fp64 node math and the two-fluid kernels (which
+// compute in T as the reference does) never go through them.
+template <class L, int A>
+__device__ __forceinline__ float reg_arg(const NodeMoments<float>& m) {
+  using d = Dir<L, A>;
+  float s = 0.0f;
+  bool first = true;
+  auto add = [&](bool on, int sign, float v) {
+    if (!on) return;
+    if (first) {
+      s = sign > 0 ? v : -v;
+      first = false;
+    } else {
+      s = sign > 0 ? s + v : s - v;
+    }
+  };
+  add(d::x != 0, 1, m.pxx);
+  add(d::y != 0, 1, m.pyy);
+  add(d::z != 0, 1, m.pzz);
+  add(d::x * d::y != 0, d::x * d::y, m.pxy2);
+  add(d::x * d::z != 0, d::x * d::z, m.pxz2);
+  add(d::y * d::z != 0, d::y * d::z, m.pyz2);
+  return first ? -m.trcs2 : s - m.trcs2;
+}
+
+template <class L, int A>
+__device__ __forceinline__ float fast_post(const NodeMoments<float>& m, float om1) {
+  using d = Dir<L, A>;
+  constexpr float t = d::template t<float>();
+  const float tbase = t * (m.rho - m.usq15);
+  const float k = om1 * (4.5f * t);
+  if constexpr (d::x == 0 && d::y == 0 && d::z == 0) return fmaf(k, reg_arg<L, A>(m), tbase);
+  const float cu = dot_noseed<d::x, d::y, d::z, float>(m.ux, m.uy, m.uz);
+  const float e = fmaf((4.5f * t) * cu, cu, fmaf(3.0f * t, cu, tbase));
+  return fmaf(k, reg_arg<L, A>(m), e);
+}
+
+template <class L, int A>
+__device__ __forceinline__ void fast_pair(const NodeMoments<float>& m, float om1, float& out_a, float& out_b) {
+  using d = Dir<L, A>;
+  constexpr float t = d::template t<float>();
+  const float tbase = t * (m.rho - m.usq15);
+  const float k = om1 * (4.5f * t);
+  const float cu = dot_noseed<d::x, d::y, d::z, float>(m.ux, m.uy, m.uz);
+  const float h = (4.5f * t) * cu;
+  const float r = reg_arg<L, A>(m);
+  out_a = fmaf(k, r, fmaf(h, cu, fmaf(3.0f * t, cu, tbase)));
+  out_b = fmaf(k, r, fmaf(h, cu, fmaf(-3.0f * t, cu, tbase)));
+}
+
+// the single-fluid entry points: fp32 node math -> the fused forms, fp64 ->
+// the exact rewrites above (post_rest / post_pair / post_single)
+template <class L, int A, typename C>
+__device__ __forceinline__ C sf_post(const NodeMoments<C>& m, C om1) {
+  if constexpr (std::is_same_v<C, float>) return fast_post<L, A>(m, om1);
+  else if constexpr (A == 0) return post_rest<L, C>(m, om1);
+  else return post_single<L, A, C>(m, om1);
+}
+template <class L, int A, typename C>
+__device__ __forceinline__ void sf_pair(const NodeMoments<C>& m, C om1, C& out_a, C& out_b) {
+  if constexpr (std::is_same_v<C, float>) fast_pair<L, A>(m, om1, out_a, out_b);
+  else post_pair<L, A, C>(m, om1, out_a, out_b);
+}
+// the reference-order single direction (post_collision) for fp64 node math;
+// the fused form for fp32
+template <class L, int A, typename C>
+__device__ __forceinline__ C sf_post_ref(const NodeMoments<C>& m, C om1) {
+  if constexpr (std::is_same_v<C, float>) return fast_post<L, A>(m, om1);
+  else return post_collision<L, A, C>(m, om1);
 }
 
 // Bounce of direction A at node fi: f[opp][fi] = T(C(out) - 6 t (c.u_wall))

@@ -21,6 +21,8 @@
 #include "tslb_collision.cuh"
 #include "tslb_domain.cuh"
 #include "tslb_kernels.h"
+#include "tslb_msums.cuh"
+#include "tslb_pair.cuh"
 
 namespace tslb_cuda {
 
@@ -40,49 +42,13 @@ __global__ void __launch_bounds__(BX) k_moments(Dom d, const T* __restrict__ f,
   if constexpr (SOLID) {
     if (solid[fi]) return;
   }
-  C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pzz = 0, pxy = 0,
-    pxz = 0, pyz = 0;
-  unroll<L::q>([&](auto A) {
-    constexpr int a = decltype(A)::value;
-    using dd = Dir<L, a>;
-    const C fa = C(__ldg(f + a * d.fstride + fi));
-    r += fa;
-    if constexpr (dd::x == 1) jx += fa;
-    if constexpr (dd::x == -1) jx -= fa;
-    if constexpr (dd::y == 1) jy += fa;
-    if constexpr (dd::y == -1) jy -= fa;
-    if constexpr (dd::z == 1) jz += fa;
-    if constexpr (dd::z == -1) jz -= fa;
-    if constexpr (dd::x != 0) pxx += fa;
-    if constexpr (dd::y != 0) pyy += fa;
-    if constexpr (dd::z != 0) pzz += fa;
-    if constexpr (dd::x * dd::y == 1) pxy += fa;
-    if constexpr (dd::x * dd::y == -1) pxy -= fa;
-    if constexpr (dd::x * dd::z == 1) pxz += fa;
-    if constexpr (dd::x * dd::z == -1) pxz -= fa;
-    if constexpr (dd::y * dd::z == 1) pyz += fa;
-    if constexpr (dd::y * dd::z == -1) pyz -= fa;
-  });
-  if constexpr (L::dim == 3) force_shift<C>(d, jx, jy, jz);
-  else { C z0 = 0; force_shift<C>(d, jx, jy, z0); }
-  const C c3 = cs2<C>();
+  // compute_moments' sums and finish (tslb_msums.cuh: bit-identical to the
+  // reference order for fp64 node math; the same forms as the M kernel)
+  T v[L::q];
+#pragma unroll
+  for (int a = 0; a < L::q; ++a) v[a] = __ldg(f + a * d.fstride + fi);
   const int64_t ms = d.mstride;
-  mo[mi] = T(r);
-  mo[ms + mi] = T(jx);
-  mo[2 * ms + mi] = T(jy);
-  if constexpr (L::dim == 3) {
-    mo[3 * ms + mi] = T(jz);
-    mo[4 * ms + mi] = T(pxx - c3 * r - jx * jx);
-    mo[5 * ms + mi] = T(pyy - c3 * r - jy * jy);
-    mo[6 * ms + mi] = T(pzz - c3 * r - jz * jz);
-    mo[7 * ms + mi] = T(pxy - jx * jy);
-    mo[8 * ms + mi] = T(pxz - jx * jz);
-    mo[9 * ms + mi] = T(pyz - jy * jz);
-  } else {
-    mo[3 * ms + mi] = T(pxx - c3 * r - jx * jx);
-    mo[4 * ms + mi] = T(pyy - c3 * r - jy * jy);
-    mo[5 * ms + mi] = T(pxy - jx * jy);
-  }
+  moment_tail<L, T, C>(d, msums<L, T, C>(v), [&](int c, T x) { mo[c * ms + mi] = x; });
 }
 
 // load_node_moments (kernels.hpp:109-125)
@@ -161,7 +127,7 @@ __global__ void __launch_bounds__(BX)
     unroll<L::q>([&](auto A) {
       constexpr int a = decltype(A)::value;
       using dd = Dir<L, a>;
-      const T out = T(post_collision<L, a, C>(m, om1));
+      const T out = T(sf_post_ref<L, a, C>(m, om1));
       if ((sm >> a) & 1u) {
         int64_t target = 0;
         T wx, wy, wz;
@@ -184,7 +150,7 @@ __global__ void __launch_bounds__(BX)
     unroll<L::q>([&](auto A) {
       constexpr int a = decltype(A)::value;
       using dd = Dir<L, a>;
-      const T out = T(post_collision<L, a, C>(m, om1));
+      const T out = T(sf_post_ref<L, a, C>(m, om1));
       int64_t delta = 0;
       bool bounce = false;
       if constexpr (dd::x == 1) { delta += st.dp[0]; bounce |= st.bp[0]; }
@@ -234,7 +200,7 @@ __global__ void __launch_bounds__(BX)
   const NodeMoments<C> m = load_node<L, T, C>(d, mo, midx(d, i, j, k));
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
-    f[a * d.fstride + fi] = T(post_collision<L, a, C>(m, om1));
+    f[a * d.fstride + fi] = T(sf_post_ref<L, a, C>(m, om1));
   });
 }
 
@@ -385,48 +351,13 @@ __global__ void __launch_bounds__(BX)
   if (!node_coords<BX>(d, i, j, k)) return;
   const int64_t mi = midx(d, i, j, k);
   const NodeMoments<T> m = init_state<L, T>(s, i, j, k);
-  C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pzz = 0, pxy = 0, pxz = 0, pyz = 0;
+  T v[L::q];
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
-    using dd = Dir<L, a>;
-    const C fa = C(init_population<L, a, T>(m));
-    r += fa;
-    if constexpr (dd::x == 1) jx += fa;
-    if constexpr (dd::x == -1) jx -= fa;
-    if constexpr (dd::y == 1) jy += fa;
-    if constexpr (dd::y == -1) jy -= fa;
-    if constexpr (dd::z == 1) jz += fa;
-    if constexpr (dd::z == -1) jz -= fa;
-    if constexpr (dd::x != 0) pxx += fa;
-    if constexpr (dd::y != 0) pyy += fa;
-    if constexpr (dd::z != 0) pzz += fa;
-    if constexpr (dd::x * dd::y == 1) pxy += fa;
-    if constexpr (dd::x * dd::y == -1) pxy -= fa;
-    if constexpr (dd::x * dd::z == 1) pxz += fa;
-    if constexpr (dd::x * dd::z == -1) pxz -= fa;
-    if constexpr (dd::y * dd::z == 1) pyz += fa;
-    if constexpr (dd::y * dd::z == -1) pyz -= fa;
+    v[a] = init_population<L, a, T>(m);
   });
-  if constexpr (L::dim == 3) force_shift<C>(d, jx, jy, jz);
-  else { C z0 = 0; force_shift<C>(d, jx, jy, z0); }
-  const C c3 = cs2<C>();
   const int64_t ms = d.mstride;
-  mo[mi] = T(r);
-  mo[ms + mi] = T(jx);
-  mo[2 * ms + mi] = T(jy);
-  if constexpr (L::dim == 3) {
-    mo[3 * ms + mi] = T(jz);
-    mo[4 * ms + mi] = T(pxx - c3 * r - jx * jx);
-    mo[5 * ms + mi] = T(pyy - c3 * r - jy * jy);
-    mo[6 * ms + mi] = T(pzz - c3 * r - jz * jz);
-    mo[7 * ms + mi] = T(pxy - jx * jy);
-    mo[8 * ms + mi] = T(pxz - jx * jz);
-    mo[9 * ms + mi] = T(pyz - jy * jz);
-  } else {
-    mo[3 * ms + mi] = T(pxx - c3 * r - jx * jx);
-    mo[4 * ms + mi] = T(pyy - c3 * r - jy * jy);
-    mo[5 * ms + mi] = T(pxy - jx * jy);
-  }
+  moment_tail<L, T, C>(d, msums<L, T, C>(v), [&](int c, T x) { mo[c * ms + mi] = x; });
 }
 
 // ---------------------------------------------------------------------------

@@ -195,18 +195,18 @@ __device__ __forceinline__ void all_dirs(const Dom& d, T* __restrict__ f,
       T o[VX];
 #pragma unroll
       for (int x = 0; x < VX; ++x)
-        o[x] = EXACT ? T(post_collision<L, 0, C>(m[x], om1)) : T(post_rest<L, C>(m[x], om1));
+        o[x] = EXACT ? T(sf_post_ref<L, 0, C>(m[x], om1)) : T(sf_post<L, 0, C>(m[x], om1));
       if (active) push_dir<L, 0, T, C, VX, WALLS>(d, f, g, fi, i0, seg_start, seg_end, o);
     } else if constexpr (a & 1) {
       T oa[VX], ob[VX];
 #pragma unroll
       for (int x = 0; x < VX; ++x) {
         if constexpr (EXACT) {
-          oa[x] = T(post_collision<L, a, C>(m[x], om1));
-          ob[x] = T(post_collision<L, a + 1, C>(m[x], om1));
+          oa[x] = T(sf_post_ref<L, a, C>(m[x], om1));
+          ob[x] = T(sf_post_ref<L, a + 1, C>(m[x], om1));
         } else {
           C ra, rb;
-          post_pair<L, a, C>(m[x], om1, ra, rb);
+          sf_pair<L, a, C>(m[x], om1, ra, rb);
           oa[x] = T(ra);
           ob[x] = T(rb);
         }
