@@ -426,6 +426,8 @@ def main():
     ap.add_argument("--dims", default="", help="override the per-GPU extent nx,ny,nz (3D)")
     ap.add_argument("--math", default="f64", choices=["f64", "f32"])
     ap.add_argument("--schedule", default="auto", choices=["auto", "m", "f1"])
+    ap.add_argument("--storage", default="native", choices=["native", "f16"],
+                    help="f16: the M steps keep the moments as scaled fp16 (mixed precision, fp32 node math)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--sample-nz", type=int, default=16)
@@ -536,6 +538,9 @@ def main():
     sim = T.DeviceSolver(lat, g, W["omega"], spec, dtype, W["comps"], solid, color, dev_id, slab=slab)
     if args.math == "f32":
         sim.set_math(_lib.MATH_F32)
+    if args.storage == "f16":
+        sim.set_moment_storage("f16")  # (fp32 node math with it)
+        args.math = "f32"
     if args.schedule != "auto" and W["comps"] == 1:
         sim.set_schedule(args.schedule)
     if "umax" in W:
@@ -592,6 +597,8 @@ def main():
     # launch duration (CUDA events on the solver stream, timed region)
     masked = solid is not None
     per_node = kernel_bytes(lat, W["comps"], es, masked)
+    if args.storage == "f16":  # fp16 moments in and out of the M step
+        per_node["mstep"] = 2 * (1 + lat.dim + lat.dim * (lat.dim + 1) // 2) * 2
     if W["comps"] == 2 and "cg_gradient" not in prof:
         # gradient folded into the recolouring stream-collide: it reads phi
         # (its stencil from cache) instead of the stored gradient
@@ -607,6 +614,8 @@ def main():
     hbm, peak_kind, _ = peaks()
     sched = sim.schedule if W["comps"] == 1 else "f1"
     sb = step_bytes(lat, W["comps"], es, sched, masked) if W["comps"] == 1 else sum(per_node.values())
+    if args.storage == "f16":
+        sb = per_node["mstep"]
     step_bw = glups * sb / world  # per-GPU GB/s of the whole step
     traffic, tsrc, limiter, fp64_ops = None, None, None, None
     try:
@@ -681,7 +690,9 @@ def main():
                "data": "synthetic",
                "config": {"workload": W["desc"].format(n=n_desc) + (" per GPU" if lat.dim == 3 else "")
                           + (f" (global {nx}x{ny}x{nz_g}, {world} z slabs)" if world > 1 else ""),
-                          "lattice": lat.name, "nodes": nodes, "storage": W["storage"],
+                          "lattice": lat.name, "nodes": nodes,
+                          "storage": W["storage"] if args.storage == "native"
+                          else "f16 moments (scaled), f32 populations",
                           **({"solid_fraction": round(float(solid.mean()), 4)} if masked else {}),
                           "node_math": (args.math if W["comps"] == 1 else W["storage"] + " (as the reference)"),
                           "l2": L2_NOTE if nodes > 10 ** 7 else "L2-resident (correctness config)",

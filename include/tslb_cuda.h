@@ -56,7 +56,7 @@
 extern "C" {
 #endif
 
-#define TSLB_CUDA_ABI_VERSION 2
+#define TSLB_CUDA_ABI_VERSION 3
 
 typedef struct tslb_cuda_sim* tslb_cuda_handle;
 
@@ -133,6 +133,15 @@ int tslb_cuda_set_math(tslb_cuda_handle h, int math);
  * supported. Same results either way (fused_step, kernels.hpp:209-215). */
 int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule);
 int tslb_cuda_get_schedule(tslb_cuda_handle h, int* schedule);
+/* Moment storage of the M schedule. TSLB_STORE_NATIVE (default): the
+ * storage scalar. TSLB_STORE_F16 (EXTENSION, the paper's mixed-precision
+ * outlook): the steps keep the ten moment arrays as scaled
+ * IEEE fp16 (40 B per lattice update instead of 80) with fp32 node
+ * arithmetic (switched on with it); every other call sees fp32 moments
+ * decoded from them. Tolerance mode, not reference-exact. Needs a fp32
+ * single-fluid D3Q19/D3Q27 whole domain on M without solids, nx % 8 == 0. */
+enum tslb_store { TSLB_STORE_NATIVE = 0, TSLB_STORE_F16 = 1 };
+int tslb_cuda_set_moment_storage(tslb_cuda_handle h, int kind);
 /* Single-fluid body force F (EXTENSION: the reference has no single-fluid
  * forcing; used for the Poiseuille channel of BASELINE config 3). Velocity
  * shift of the reference's two-fluid prepare_stress (multicomponent.hpp:

@@ -21,6 +21,7 @@ FIELD = dict(rho=0, mom=1, pineq=2, rho_r=3, rho_b=4, phi=5, gradphi=6, nci_flag
 INIT = dict(rest=0, shear=1, taylor_green=2, droplet=3)
 KCLASS = ["moments", "streamcoll", "cg_moments", "cg_gradient", "cg_streamcoll", "exchange", "mstep"]
 SCHED_F1, SCHED_M = 0, 1
+STORE_NATIVE, STORE_F16 = 0, 1
 
 
 class TslbCudaError(RuntimeError):
@@ -69,6 +70,7 @@ def load(path: str | None = None) -> C.CDLL:
         "tslb_cuda_download_geometry": ([H, vp, vp, vp], i),
         "tslb_cuda_init_analytic": ([H, i, d, d], i),
         "tslb_cuda_init_state": ([H, vp], i),
+        "tslb_cuda_set_moment_storage": ([H, i], i),
         "tslb_cuda_step": ([H, l], i),
         "tslb_cuda_step_async": ([H, l], i),
         "tslb_cuda_synchronize": ([H], i),
@@ -99,7 +101,7 @@ def load(path: str | None = None) -> C.CDLL:
         fn = getattr(lib, name)
         fn.argtypes = args
         fn.restype = res
-    if lib.tslb_cuda_abi_version() != 2:
+    if lib.tslb_cuda_abi_version() != 3:
         raise TslbCudaError("libtslb_cuda.so ABI version mismatch")
     _lib = lib
     return lib

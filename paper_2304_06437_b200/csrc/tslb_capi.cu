@@ -143,6 +143,14 @@ struct tslb_cuda_sim {
   uint32_t* sbits = nullptr;  // M on a masked geometry: per-node solid bits (with ghost planes)
   void* scratch = nullptr;
   void* state_buf = nullptr;  // tslb_cuda_init_state: the node states [1+D+np][mstride] (f(0) pending on them)
+  // mixed-precision moment storage (tslb_cuda_set_moment_storage): the M
+  // steps run on fp16 moments mh/mh2 (tslb_store16.cuh); every other API
+  // works on the fp32 moments mo, decoded on demand (m32_valid) and encoded
+  // again before the next step once an fp32 path changed them (m16_valid)
+  int store16 = 0;
+  void* mh = nullptr;
+  void* mh2 = nullptr;
+  bool m16_valid = false, m32_valid = true;
   double* red = nullptr;  // partials + outputs
   uint64_t* dig = nullptr;
   size_t dig_bytes = 0;
@@ -266,6 +274,17 @@ bool nci_on(const tslb_cuda_sim* h) {
   return h->scalar == TSLB_F64 ? h->cp.nci_strength != 0.0 : float(h->cp.nci_strength) != 0.0f;
 }
 
+// mixed precision: the fp32 moments mo are needed (decode the fp16 state)
+int sync32(tslb_cuda_sim* h) {
+  if (!h->store16 || h->m32_valid) return 0;
+  ++h->launches;
+  if (launch_moments_codec16(h->range(0, h->nzl), 1 + h->dim + h->np, static_cast<float*>(h->mo),
+                             static_cast<__half*>(h->mh), 0, h->s))
+    return set_err(TSLB_ECUDA, "fp16 moment decode launch failed");
+  h->m32_valid = true;
+  return 0;
+}
+
 // -- phases -------------------------------------------------------------------
 // the single-fluid population buffer, allocated on first use under M and
 // filled with the pending analytic f(0) if there is one
@@ -297,6 +316,7 @@ int ensure_f(tslb_cuda_sim* h) {
 int ph_moments(tslb_cuda_sim* h, cudaStream_t st) {
   if (h->comps == 1)
     if (int rc = ensure_f(h)) return rc;
+  h->m16_valid = false;
   Prof p(h, TSLB_K_MOMENTS, st);
   ++h->launches;
   return by_scalar(h, [&](auto z) {
@@ -407,6 +427,7 @@ int exchange_moments_local(tslb_cuda_sim* h, cudaStream_t st) {
 
 // the first step's moments pass: precomputed by the M initialiser, or from f
 int first_moments(tslb_cuda_sim* h, cudaStream_t st) {
+  h->m16_valid = false;
   if (h->m0_ready) {
     std::swap(h->mo, h->mo2);
     h->m0_ready = false;
@@ -423,6 +444,7 @@ int first_moments(tslb_cuda_sim* h, cudaStream_t st) {
 // ghost moments instead of exchanged
 int materialize(tslb_cuda_sim* h) {
   if (!h->fimplicit) return 0;
+  if (int rc = sync32(h)) return rc;
   h->fimplicit = false;
   if (int rc = ph_streamcoll(h, 0, h->nzl, h->s)) return rc;
   if (!h->decomposed) return 0;
@@ -804,6 +826,25 @@ int enqueue_step(tslb_cuda_sim* h) {
         CK(cudaStreamWaitEvent(h->s, h->ev_c, 0));
       }
       std::swap(h->mo, h->mo2);
+    } else if (h->store16) {
+      // mixed precision: fp16 moments in and out (40 B per update)
+      if (!h->m16_valid) {
+        ++h->launches;
+        if (launch_moments_codec16(h->range(0, h->nzl), 1 + h->dim + h->np, static_cast<float*>(h->mo),
+                                   static_cast<__half*>(h->mh), 1, h->s))
+          return set_err(TSLB_ECUDA, "fp16 moment encode launch failed");
+        h->m16_valid = true;
+      }
+      {
+        Prof p(h, TSLB_K_MSTEP, h->s);
+        ++h->launches;
+        const int r = launch_mstep16(h->lat, h->range(0, h->nzl), static_cast<const __half*>(h->mh),
+                                     static_cast<__half*>(h->mh2), h->omega, h->lz, h->mmaps, h->s);
+        if (r < 0) return set_err(TSLB_ECUDA, "k_mstep (fp16) launch: %s", cudaGetErrorString(cudaError_t(-r)));
+        if (r) return set_err(TSLB_ESTATE, "fp16 M step not supported for this domain");
+      }
+      std::swap(h->mh, h->mh2);
+      h->m32_valid = false;
     } else {
       if ((rc = ph_mstep(h, h->s))) return rc;
       std::swap(h->mo, h->mo2);
@@ -1175,7 +1216,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
   void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->sx, h->phig, h->two,
                   h->flagg ? h->flagg : h->flag, h->rflag, h->solid, h->slow,
-                  h->sbits, h->scratch, h->state_buf, h->red, h->dig, h->recv_lo, h->recv_hi};
+                  h->sbits, h->scratch, h->state_buf, h->mh, h->mh2, h->red, h->dig, h->recv_lo, h->recv_hi};
   for (void* b : bufs)
     if (b) cudaFree(b);
   if (h->graph) cudaGraphExecDestroy(h->graph);
@@ -1191,6 +1232,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
 }
 
 int tslb_cuda_set_math(tslb_cuda_handle h, int math) {
+  if (int rc = sync32(h)) return rc;
   if (math != kMathDouble && math != kMathFloat) return set_err(TSLB_EINVAL, "bad math mode");
   CK(cudaSetDevice(h->device));
   // a pending f(t+1) belongs to the step that was taken with the old mode
@@ -1202,6 +1244,7 @@ int tslb_cuda_set_math(tslb_cuda_handle h, int math) {
 }
 
 int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
+  if (int rc = sync32(h)) return rc;
   if (schedule != TSLB_SCHED_F1 && schedule != TSLB_SCHED_M)
     return set_err(TSLB_EINVAL, "bad schedule %d", schedule);
   if (schedule == h->sched) return 0;
@@ -1239,6 +1282,7 @@ int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
 }
 
 int tslb_cuda_set_body_force(tslb_cuda_handle h, const double* force) {
+  if (int rc = sync32(h)) return rc;
   if (!force) return set_err(TSLB_EINVAL, "null force");
   if (h->comps != 1) return set_err(TSLB_EINVAL, "the body force is a single-fluid extension");
   CK(cudaSetDevice(h->device));
@@ -1287,6 +1331,8 @@ int tslb_cuda_memory_bytes(tslb_cuda_handle h, uint64_t* bytes) {
 }
 
 int tslb_cuda_upload_f(tslb_cuda_handle h, int species, const void* host) {
+  if (int rc = sync32(h)) return rc;
+  h->m16_valid = false;
   CK(cudaSetDevice(h->device));
   char* base;
   if (species == 0) h->fimplicit = false;  // every owned slot is overwritten
@@ -1346,6 +1392,8 @@ int field_desc(tslb_cuda_sim* h, int field, void** base, int* count, int* eb,
 }  // namespace
 
 int tslb_cuda_upload_field(tslb_cuda_handle h, int field, const void* host) {
+  if (int rc = sync32(h)) return rc;
+  h->m16_valid = false;
   void* base; int cnt, eb; int64_t stride;
   if (int rc = field_desc(h, field, &base, &cnt, &eb, &stride, true)) return rc;
   CK(cudaSetDevice(h->device));
@@ -1362,6 +1410,7 @@ int tslb_cuda_upload_field(tslb_cuda_handle h, int field, const void* host) {
 }
 
 int tslb_cuda_download_field(tslb_cuda_handle h, int field, void* host) {
+  if (int rc = sync32(h)) return rc;
   CK(cudaSetDevice(h->device));
   if (int rc = finish_gradient(h)) return rc;
   // two-fluid: after a step the host-visible mom/pineq are u_eq / Pi^neq
@@ -1390,6 +1439,7 @@ int tslb_cuda_download_field(tslb_cuda_handle h, int field, void* host) {
 }
 
 int tslb_cuda_download_slice(tslb_cuda_handle h, int field, int axis, int index, void* host) {
+  if (int rc = sync32(h)) return rc;
   if (axis < 0 || axis > 2) return set_err(TSLB_EINVAL, "slice axis must be 0, 1 or 2");
   const int ext[3] = {h->nx, h->ny, h->nzl};
   if (index < 0 || index >= ext[axis]) return set_err(TSLB_EINVAL, "slice index %d outside [0, %d)", index, ext[axis]);
@@ -1431,6 +1481,8 @@ int tslb_cuda_download_geometry(tslb_cuda_handle h, uint8_t* solid,
 
 int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
                             double radius) {
+  if (int rc = sync32(h)) return rc;
+  h->m16_valid = false;
   CK(cudaSetDevice(h->device));
   InitSpec s{};
   s.kind = kind;
@@ -1478,6 +1530,8 @@ int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
 // writes the first step's moments directly and f(0) stays pending on the
 // uploaded states (materialised only if read); otherwise f(0) is stored.
 int tslb_cuda_init_state(tslb_cuda_handle h, const void* host) {
+  if (int rc = sync32(h)) return rc;
+  h->m16_valid = false;
   if (!host) return set_err(TSLB_EINVAL, "init_state: null state");
   if (h->comps != 1)
     return set_err(TSLB_EINVAL, "init_state: single-fluid node states (two-fluid: initialize_colors + upload_f)");
@@ -1534,6 +1588,40 @@ int tslb_cuda_init_state(tslb_cuda_handle h, const void* host) {
   CK(cudaFree(h->state_buf));
   h->state_buf = nullptr;
   h->bytes -= size_t(h->d.mstride) * nm * h->esz;
+  return 0;
+}
+
+int tslb_cuda_set_moment_storage(tslb_cuda_handle h, int kind) {
+  if (kind != TSLB_STORE_NATIVE && kind != TSLB_STORE_F16) return set_err(TSLB_EINVAL, "bad moment storage %d", kind);
+  CK(cudaSetDevice(h->device));
+  if (kind == h->store16) return 0;
+  if (kind == TSLB_STORE_NATIVE) {
+    if (int rc = sync32(h)) return rc;
+    CK(cudaStreamSynchronize(h->s));
+    const size_t hb = size_t(h->d.mstride) * (1 + h->dim + h->np) * sizeof(__half);
+    CK(cudaFree(h->mh));
+    CK(cudaFree(h->mh2));
+    h->mh = h->mh2 = nullptr;
+    h->bytes -= 2 * hb;
+    h->store16 = 0;
+    return 0;
+  }
+  if (h->comps != 1 || h->scalar != TSLB_F32 || h->sched != TSLB_SCHED_M || h->decomposed ||
+      !mstep16_supported(h->lat, h->d))
+    return set_err(TSLB_EINVAL,
+                   "fp16 moment storage needs a single-fluid fp32 D3Q19/D3Q27 whole domain on the M schedule, "
+                   "without solids, nx %% 8 == 0");
+  // fp16 storage is paired with fp32 node arithmetic
+  if (h->math != kMathFloat)
+    if (int rc = tslb_cuda_set_math(h, kMathFloat)) return rc;
+  const size_t hb = size_t(h->d.mstride) * (1 + h->dim + h->np) * sizeof(__half);
+  if (int rc = alloc(h, &h->mh, hb)) return rc;
+  if (int rc = alloc(h, &h->mh2, hb)) return rc;
+  drop_graph(h);
+  h->graphs_ok = false;  // (the encode of the first fp16 step must not be replayed)
+  h->store16 = 1;
+  h->m16_valid = false;
+  h->m32_valid = true;
   return 0;
 }
 
@@ -1656,6 +1744,7 @@ int tslb_cuda_time_steps(tslb_cuda_handle h, long nsteps, double* ms) {
 }
 
 int tslb_cuda_compute_moments(tslb_cuda_handle h) {
+  if (int rc = sync32(h)) return rc;
   if (h->comps != 1) return set_err(TSLB_EINVAL, "compute_moments is single-fluid");
   CK(cudaSetDevice(h->device));
   if (int rc = materialize(h)) return rc;
@@ -1664,6 +1753,7 @@ int tslb_cuda_compute_moments(tslb_cuda_handle h) {
 }
 
 int tslb_cuda_stream_collide(tslb_cuda_handle h) {
+  if (int rc = sync32(h)) return rc;
   if (h->comps != 1) return set_err(TSLB_EINVAL, "stream_collide_fused is single-fluid");
   if (h->decomposed) return set_err(TSLB_ESTATE, "use step() on slab solvers");
   CK(cudaSetDevice(h->device));
@@ -1674,6 +1764,7 @@ int tslb_cuda_stream_collide(tslb_cuda_handle h) {
 }
 
 int tslb_cuda_reference_step(tslb_cuda_handle h, long nsteps) {
+  if (int rc = sync32(h)) return rc;
   if (h->comps != 1 || h->decomposed)
     return set_err(TSLB_EINVAL, "reference_step: single-fluid, single domain only");
   CK(cudaSetDevice(h->device));
@@ -1700,6 +1791,7 @@ int tslb_cuda_reference_step(tslb_cuda_handle h, long nsteps) {
 }
 
 int tslb_cuda_stream_only(tslb_cuda_handle h) {
+  if (int rc = sync32(h)) return rc;
   if (h->comps != 1 || h->decomposed)
     return set_err(TSLB_EINVAL, "stream_only: single-fluid, single domain only");
   CK(cudaSetDevice(h->device));
@@ -1753,6 +1845,7 @@ int tslb_cuda_stream_collide_recolor(tslb_cuda_handle h) {
 }
 
 int tslb_cuda_refresh_moments(tslb_cuda_handle h) {
+  if (int rc = sync32(h)) return rc;
   CK(cudaSetDevice(h->device));
   if (h->comps == 1) {
     if (int rc = materialize(h)) return rc;
@@ -1765,6 +1858,7 @@ int tslb_cuda_refresh_moments(tslb_cuda_handle h) {
 }
 
 int tslb_cuda_totals(tslb_cuda_handle h, double* mass, double* momentum3) {
+  if (int rc = sync32(h)) return rc;
   CK(cudaSetDevice(h->device));
   double* part = h->red;
   double* out = h->red + reduce_partial_count();
@@ -1784,6 +1878,7 @@ int tslb_cuda_totals(tslb_cuda_handle h, double* mass, double* momentum3) {
 
 int tslb_cuda_stability(tslb_cuda_handle h, int* finite, double* max_speed,
                         double* min_rho, double* max_rho, int64_t* first_bad) {
+  if (int rc = sync32(h)) return rc;
   CK(cudaSetDevice(h->device));
   if (int rc = finish_gradient(h)) return rc;
   if (h->comps == 2 && h->stress_pending)
@@ -1828,6 +1923,7 @@ int tslb_cuda_color_masses(tslb_cuda_handle h, double* red, double* blue) {
 }
 
 int tslb_cuda_plane_digests(tslb_cuda_handle h, uint64_t* out) {
+  if (int rc = sync32(h)) return rc;
   CK(cudaSetDevice(h->device));
   if (int rc = materialize(h)) return rc;
   if (h->comps == 1)

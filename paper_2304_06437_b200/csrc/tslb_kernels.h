@@ -1,6 +1,7 @@
 // Internal launcher declarations shared by the kernel TUs and the C-ABI TU.
 #pragma once
 
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -55,6 +56,13 @@ bool mstep_supported(int lat, const Dom& d, int esz);
 template <typename T>
 int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
                  int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st);
+// mixed-precision M step (tslb_mstep.cu, tslb_store16.cuh): fp16 moments,
+// fp32 populations and arithmetic, whole domains without solids, nx % 8 == 0
+bool mstep16_supported(int lat, const Dom& d);
+int launch_mstep16(int lat, const Dom& d, const __half* mi, __half* mo, double omega, int lz, MstepMaps*& maps,
+                   cudaStream_t st);
+// fp32 moments <-> fp16 storage (to16 = 1: encode m32 into m16)
+int launch_moments_codec16(const Dom& d, int nm, float* m32, __half* m16, int to16, cudaStream_t st);
 // per-node solid bits of a masked geometry for the 3-D M step (tslb_mstep.cu)
 int launch_solid_bits(int lat, const Dom& d, const uint8_t* solid, uint32_t* bits, cudaStream_t st);
 // D2Q9 form of the M step (tslb_mstep2d.cu; launched through launch_mstep)

@@ -61,6 +61,7 @@
 #include "tslb_kernels.h"
 #include "tslb_msums.cuh"
 #include "tslb_pair.cuh"
+#include "tslb_store16.cuh"
 
 namespace tslb_cuda {
 
@@ -125,11 +126,11 @@ __host__ __device__ constexpr int n_moments() {
 __host__ __device__ constexpr size_t align128(size_t b) { return (b + 127) / 128 * 128; }
 
 // dynamic shared memory: [tile buf 0 | tile buf 1 | wstg 0 | wstg 1 | slots | mbarriers]
-template <class L, typename T, bool SOLID = false>
+template <class L, typename T, bool SOLID = false, typename TM = T>
 struct Smem {
-  static constexpr size_t tile = align128(size_t(n_moments<L>()) * TC * sizeof(T));
+  static constexpr size_t tile = align128(size_t(n_moments<L>()) * TC * sizeof(TM));
   // one copy of the ring per halo task half (see push_ring)
-  static constexpr size_t wstg = align128(size_t(n_moments<L>()) * 2 * NH * sizeof(T));
+  static constexpr size_t wstg = align128(size_t(n_moments<L>()) * 2 * NH * sizeof(typename MStore<TM>::W));
   static constexpr size_t slots = size_t(slot_planes<L>()) * NT * sizeof(T);
   // solid geometries: the per-node solid bits of the tile and of the halo
   // ring (cp.async, double buffered) -- [2][NT + 2 NH] u32
@@ -283,14 +284,24 @@ __device__ __forceinline__ uint32_t ring_addr(const Ring<L, T>& rg) {
   else return rg.qa[((DZ + 1) % DA + DA) % DA];
 }
 
-template <class L, typename T, typename C>
-__device__ __forceinline__ NodeMoments<C> node_at(const T* s, int stride) {
+template <class L, typename TM, typename C>
+__device__ __forceinline__ NodeMoments<C> node_at(const TM* s, int stride) {
   constexpr int NM = n_moments<L>();
-  T v[NM];
+  C v[NM];
 #pragma unroll
-  for (int c = 0; c < NM; ++c) v[c] = s[c * stride];
-  return prepare_node<C>(C(v[0]), C(v[1]), C(v[2]), C(v[3]), C(v[4]), C(v[5]), C(v[6]), C(v[7]), C(v[8]),
-                         C(v[9]));
+  for (int c = 0; c < NM; ++c) v[c] = C(MStore<TM>::dec(c, s[c * stride]));
+  return prepare_node<C>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9]);
+}
+
+// a lane-fetched halo node: staged words (MStore<TM>::W), `sel` picks the
+// half of a 2-byte element inside its aligned 4-byte word
+template <class L, typename TM, typename C>
+__device__ __forceinline__ NodeMoments<C> staged_at(const typename MStore<TM>::W* s, int stride, int sel) {
+  constexpr int NM = n_moments<L>();
+  C v[NM];
+#pragma unroll
+  for (int c = 0; c < NM; ++c) v[c] = C(MStore<TM>::dec(c, MStore<TM>::pick(s[c * stride], sel)));
+  return prepare_node<C>(v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7], v[8], v[9]);
 }
 
 // per-thread wall contact of the tile node (only for WALLS kernels) and,
@@ -347,21 +358,13 @@ __device__ __forceinline__ void emit(const Dom& d, const Ring<L, T>& rg, T (&R)[
 }
 
 // All directions of a tile node; ZC != 0 (a plane just outside the march)
-// keeps only the directions with c_z == ZC. `side(A)` runs after the rest
-// direction (A = 0) and after every opposite pair (odd A): the caller
-// interleaves independent work (the moment sums of an earlier plane) with
-// the collision, so the FP64 pipe sees one even instruction mix.
-struct NoSide {
-  template <class A>
-  __device__ __forceinline__ void operator()(A) const {}
-};
-template <class L, typename T, typename C, bool WALLS, bool SOLID, int ZC, class Side = NoSide>
+// keeps only the directions with c_z == ZC.
+template <class L, typename T, typename C, bool WALLS, bool SOLID, int ZC>
 __device__ __forceinline__ void push_tile(const Dom& d, const Ring<L, T>& rg, T (&R)[L::q][3],
                                           int lx, int ly, const Contact& ct,
-                                          const NodeMoments<C>& m, C om1, const Side& side = Side{}) {
+                                          const NodeMoments<C>& m, C om1) {
   unroll<L::q>([&](auto A) {
     constexpr int a = decltype(A)::value;
-    if constexpr (a == 0 || (a & 1)) side(A);
     if constexpr (a == 0) {
       if constexpr (ZC == 0) emit<L, 0, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, T(sf_post<L, 0, C>(m, om1)));
     } else if constexpr (a & 1) {
@@ -457,22 +460,26 @@ __device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, con
   moment_tail<L, T, C>(d, msums<L, T, C>(v), put);
 }
 
-template <class L, typename T, typename C, bool WALLS, bool SOLID, int MINB>
+// TM: the storage type of the moment arrays (T, or __half: the scaled fp16
+// moments of the mixed-precision mode, tslb_store16.cuh); the populations
+// are rounded to T in the slots either way
+template <class L, typename T, typename C, bool WALLS, bool SOLID, int MINB, typename TM = T>
 __global__ void __launch_bounds__(NT, MINB)
     k_mstep(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap, Dom d,
-            const T* __restrict__ mi, const T* __restrict__ gm, T* __restrict__ mo, C om1, int lz, int zbeg,
+            const TM* __restrict__ mi, const TM* __restrict__ gm, TM* __restrict__ mo, C om1, int lz, int zbeg,
             int zend, const uint32_t* __restrict__ sbits) {
   static_assert(L::dim == 3, "the M step is 3-D");
-  using SM = Smem<L, T, SOLID>;
+  using SM = Smem<L, T, SOLID, TM>;
+  using W = typename MStore<TM>::W;
   constexpr int NM = n_moments<L>();
   extern __shared__ __align__(128) unsigned char smraw[];
-  T* tile = reinterpret_cast<T*>(smraw);                  // [2][NM][TR][TX]
-  T* wstg = reinterpret_cast<T*>(smraw + SM::off_wstg);   // [2][NM][2 NH]
+  TM* tile = reinterpret_cast<TM*>(smraw);                // [2][NM][TR][TX]
+  W* wstg = reinterpret_cast<W*>(smraw + SM::off_wstg);   // [2][NM][2 NH]
   T* sl = reinterpret_cast<T*>(smraw + SM::off_slots);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smraw + SM::off_bar);
   uint32_t* bstg = reinterpret_cast<uint32_t*>(smraw + SM::off_bits);  // [2][NT + 2 NH]
   constexpr int BITS_B = NT + 2 * NH;
-  constexpr int TILE_B = int(SM::tile / sizeof(T)), WSTG_B = int(SM::wstg / sizeof(T));
+  constexpr int TILE_B = int(SM::tile / sizeof(TM)), WSTG_B = int(SM::wstg / sizeof(W));
 
   const int tid = threadIdx.x, lx = tid & (TX - 1), ly = tid >> 5;
   const int x0 = int(blockIdx.x) * TX, y0 = int(blockIdx.y) * TY;
@@ -507,7 +514,8 @@ __global__ void __launch_bounds__(NT, MINB)
   }
   int64_t hcol = 0;
   bool hfetch = false;  // this lane loads its halo node itself
-  int hoff = 0, hstride = TC;  // where the halo node's moments are staged
+  int hoff = 0;         // where the halo node's moments are staged
+  int hsel = 0;         // (2-byte moments: which half of the fetched word)
   if (hnode >= 0) {
     const int hgx = wrap_coord(x0 + hx, d.nx, d.mode[XMin], d.mode[XMax]);
     const int hgy = wrap_coord(y0 + hy, d.ny, d.mode[YMin], d.mode[YMax]);
@@ -518,7 +526,7 @@ __global__ void __launch_bounds__(NT, MINB)
       hfetch = side >= 2 || hgy != y0 + hy;
       if (hfetch) {
         hoff = half * NH + hnode;
-        hstride = WH;
+        hsel = MStore<TM>::sel(hcol);
       } else {
         hoff = (hy + 1) * TX + hx;
       }
@@ -540,7 +548,7 @@ __global__ void __launch_bounds__(NT, MINB)
   }
   __syncthreads();
 
-  constexpr uint32_t kTileBytes = uint32_t(NM * TC * sizeof(T));
+  constexpr uint32_t kTileBytes = uint32_t(NM * TC * sizeof(TM));
   auto issue = [&](int z, int b) {
     int zz = 0;
     const int src = plane_src(d, z, zz);
@@ -551,11 +559,11 @@ __global__ void __launch_bounds__(NT, MINB)
       tma_load_4d(tile + b * TILE_B, src == 1 ? &tmap : &gmap, &bar[b], x0, y0 - 1, zz, 0);
     }
     if (hfetch) {
-      T* w = wstg + b * WSTG_B + hoff;
-      const T* g = (src == 1 ? mi + int64_t(zz) * d.plane : gm + int64_t(zz) * NM * d.plane) + hcol;
+      W* w = wstg + b * WSTG_B + hoff;
+      const TM* g = (src == 1 ? mi + int64_t(zz) * d.plane : gm + int64_t(zz) * NM * d.plane) + hcol;
       const int64_t cs = src == 1 ? d.mstride : d.plane;
 #pragma unroll
-      for (int c = 0; c < NM; ++c) __pipeline_memcpy_async(w + c * WH, g + c * cs, sizeof(T));
+      for (int c = 0; c < NM; ++c) __pipeline_memcpy_async(w + c * WH, MStore<TM>::word(g + c * cs), sizeof(W));
     }
     if constexpr (SOLID) {  // sbits points at plane 0; slab ghost planes at z = -1, nz
       const uint32_t* gb = sbits + int64_t(src == 1 ? zz : z) * d.plane;
@@ -567,71 +575,23 @@ __global__ void __launch_bounds__(NT, MINB)
   T R[L::q][3];
 #pragma unroll
   for (int a = 0; a < L::q; ++a) R[a][0] = R[a][1] = R[a][2] = T(0);
-  // SKEW (one-barrier rings, rd == 1): plane z - 2 is reduced while plane z
-  // is pushed, between the same two barriers -- its slots are complete
-  // (pushes from z - 3 .. z - 1 happened before the last barrier) and the
-  // rings, 3 deep for c_z <= 0 and 4 deep for c_z = +1, hold planes z - 2 ..
-  // z + 1 apart. The moment sums of z - 2 are fed into the collision of z
-  // pair by pair (push_tile's side hook), so the finalize's loads, converts
-  // and adds fill the FP64 pipe's gaps instead of forming their own phase.
-  // rd == 0 (two barriers, shallower rings) reduces z - 1 after the barrier.
-  // Measured (r02, same box, 1024^3): 33.4 GLUPS skewed vs 34.0 unskewed
-  // (128 vs 102 registers, barrier stalls 10.4 % vs 7.3 %), so it is off
-  // unless built with -DTSLB_MSTEP_SKEW (profiles/r02_mstep_variants.md).
-#ifdef TSLB_MSTEP_SKEW
-  constexpr bool SKEW = L::rd == 1;
-#else
-  constexpr bool SKEW = false;
-#endif
-  T Rf[L::q];  // register-ring values of plane z - 2 (SKEW)
-#pragma unroll
-  for (int a = 0; a < L::q; ++a) Rf[a] = T(0);
   Ring<L, T> rg;
   rg.init(smem_u32(sl + ly * TX + lx));
   int buf = 0;
   uint32_t phase = 0;  // bit b: parity of the next completion of bar[b]
-  bool solid_prev = false, solid_prev2 = false;  // the tile node of plane z - 1 / z - 2 is solid
-  constexpr bool PAIRS = msums_pair_form<T, C>();
+  bool solid_prev = false;  // the tile node of the plane being reduced is solid
   const int64_t ms = d.mstride;
-
-  // the skewed reduction of plane zr (= z - 2) from its gathered slots v:
-  // the sums ran in `acc`; nodes outside the pair form's range redo them in
-  // the reference order from the (still intact) slots
-  auto store_skewed = [&](int zr, MAcc<L, T, C, PAIRS>& acc, bool exact) {
-    MSums<C> sm = acc.finish();
-    if constexpr (PAIRS) {
-      if (!exact) {
-        T v2[L::q];
-        gather<L, -2, T>(rg, Rf, v2);
-        sm = msums_reference<L, T, C>(v2);
-      }
-    }
-    T* o = mo + col + int64_t(zr) * d.plane;
-    moment_tail<L, T, C>(d, sm, [&](int c, T v) { o[c * ms] = v; });
-  };
 
   auto plane = [&](auto ZCc, int z) {
     constexpr int ZC = decltype(ZCc)::value;
     if (ZC != -1) issue(z + 1, buf ^ 1);
     __pipeline_commit();
-    // SKEW: plane z - 2's slots, gathered before this plane's pushes
-    T v[L::q];
-    bool exact = true;
-    MAcc<L, T, C, PAIRS> acc;
-    if constexpr (SKEW) {
-      gather<L, -2, T>(rg, Rf, v);
-      if constexpr (PAIRS) exact = msums_exact<L::q>(v);
-    }
-    auto side = [&](auto A) {
-      if constexpr (SKEW) acc.template step<decltype(A)::value>(v);
-    };
-    bool fed = false;  // the collision of plane z carried the skewed sums
     int zz_unused = 0;
     if (plane_src(d, z, zz_unused) != 0) {
       mbar_wait(&bar[buf], (phase >> buf) & 1u);
       phase ^= 1u << buf;
       __pipeline_wait_prior(1);
-      const T* tb = tile + buf * TILE_B;
+      const TM* tb = tile + buf * TILE_B;
       if constexpr (WALLS) {
         ct.zlo = z == 0 && d.mode[ZMin] == kWall;
         ct.zhi = z == d.nz - 1 && d.mode[ZMax] == kWall;
@@ -651,36 +611,27 @@ __global__ void __launch_bounds__(NT, MINB)
         }
       }
       if (!solid && active) {
-        const NodeMoments<C> m = node_at<L, T, C>(tb + (ly + 1) * TX + lx, TC);
-        push_tile<L, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, m, om1, side);
-        fed = true;
+        const NodeMoments<C> m = node_at<L, TM, C>(tb + (ly + 1) * TX + lx, TC);
+        push_tile<L, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, m, om1);
       }
       if (hnode >= 0 && !hsolid) {
-        const T* hb = (hfetch ? wstg + buf * WSTG_B : tb) + hoff;
-        const NodeMoments<C> hm = node_at<L, T, C>(hb, hstride);
+        const NodeMoments<C> hm = hfetch ? staged_at<L, TM, C>(wstg + buf * WSTG_B + hoff, WH, hsel)
+                                         : node_at<L, TM, C>(tb + hoff, TC);
         push_ring<L, T, C, ZC>(rg, hdelta, ly, hx, hy, hm, om1);
       }
     }
-    if constexpr (SKEW) {
-      if (!fed) acc.all(v);
-      if (active && z - 2 >= za && !(SOLID && solid_prev2)) store_skewed(z - 2, acc, exact);
-    }
+#ifndef TSLB_MSTEP_NOBAR  // (timing probe only: results are wrong without it)
     __syncthreads();
-    if constexpr (!SKEW) {
-      // compute_moments skips solid nodes (their moment arrays keep their values)
-      if (active && z - 1 >= za && !(SOLID && solid_prev)) {
-        T* o = mo + col + int64_t(z - 1) * d.plane;
-        finalize<L, T, C>(d, rg, R, [&](int c, T v) { o[c * ms] = v; });
-      }
+#endif
+    // compute_moments skips solid nodes (their moment arrays keep their values)
+    if (active && z - 1 >= za && !(SOLID && solid_prev)) {
+      TM* o = mo + col + int64_t(z - 1) * d.plane;
+      finalize<L, T, C>(d, rg, R, [&](int c, T v) { o[c * ms] = MStore<TM>::enc(c, v); });
     }
-    if constexpr (SOLID) {
-      solid_prev2 = solid_prev;
-      solid_prev = (ct.sb & kSelfSolid) != 0;  // (ct.sb: plane z)
-    }
+    if constexpr (SOLID) solid_prev = (ct.sb & kSelfSolid) != 0;  // (ct.sb: plane z)
     if constexpr (L::rd == 0) __syncthreads();
 #pragma unroll
     for (int a = 0; a < L::q; ++a) {
-      if constexpr (SKEW) Rf[a] = R[a][0];
       R[a][0] = R[a][1];
       R[a][1] = R[a][2];
     }
@@ -701,16 +652,6 @@ __global__ void __launch_bounds__(NT, MINB)
 #pragma unroll kUnroll
   for (int z = za; z < zb; ++z) plane(std::integral_constant<int, 0>{}, z);
   plane(std::integral_constant<int, -1>{}, zb);
-  if constexpr (SKEW) {
-    // the last plane of the march (zb - 1) completed at the final barrier
-    if (active && zb - 1 >= za && !(SOLID && solid_prev2)) {
-      T v[L::q];
-      gather<L, -2, T>(rg, Rf, v);
-      MAcc<L, T, C, PAIRS> acc;
-      acc.all(v);
-      store_skewed(zb - 1, acc, PAIRS ? msums_exact<L::q>(v) : true);
-    }
-  }
 }
 
 using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -752,7 +693,9 @@ const CUtensorMap* tensor_map(MstepMaps*& maps, const Dom& d, int nm, const T* b
   EncodeFn enc = encoder();
   if (!enc) return nullptr;
   auto& e = ghost ? maps->e[2] : maps->e[maps->next];
-  const CUtensorMapDataType dt = sizeof(T) == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64;
+  const CUtensorMapDataType dt = sizeof(T) == 4   ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                                 : sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64
+                                                  : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
   const cuuint64_t es = sizeof(T);
   const cuuint32_t estr[4] = {1, 1, 1, 1};
   const cuuint64_t dim[4] = {cuuint64_t(d.nx), cuuint64_t(d.ny), cuuint64_t(ghost ? 2 : d.nz), cuuint64_t(nm)};
@@ -948,6 +891,68 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
     return deep ? by_lat(SL<Base, 1>{}) : by_lat(SL<Base, 0>{});
   };
   return lat == kD3Q19 ? by_rd(D3Q19{}) : by_rd(D3Q27{});
+}
+
+// The mixed-precision M step: fp16 moments (MStore<__half>), fp32
+// populations and node arithmetic; whole domains without solids.
+int launch_mstep16(int lat, const Dom& d, const __half* mi, __half* mo, double omega, int lz, MstepMaps*& maps,
+                   cudaStream_t st) {
+  using namespace mstep;
+  if (!mstep16_supported(lat, d)) return 1;
+  if (lz <= 0) lz = kDefaultLz;
+  const int nchunks = (d.nz + lz - 1) / lz;
+  bool walls = false;
+  for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
+  const dim3 grid(unsigned((d.nx + TX - 1) / TX), unsigned((d.ny + TY - 1) / TY), unsigned(nchunks));
+  if (grid.y > 65535 || grid.z > 65535) return 1;
+  const float om1 = 1.0f - float(omega);
+  int err = 0;
+  auto by_lat = [&](auto L) {
+    using Lat = decltype(L);
+    const CUtensorMap* tm = tensor_map<__half>(maps, d, n_moments<Lat>(), mi, false);
+    if (!tm) return 1;
+    constexpr size_t smem = Smem<Lat, float, false, __half>::total;
+    auto go = [&](auto kern) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e == cudaSuccess) {
+        kern<<<grid, NT, smem, st>>>(*tm, *tm, d, mi, nullptr, mo, om1, lz, 0, d.nz, nullptr);
+        e = cudaGetLastError();
+      }
+      if (e != cudaSuccess) err = -int(e);
+    };
+    if (walls) go(k_mstep<Lat, float, float, true, false, 2, __half>);
+    else go(k_mstep<Lat, float, float, false, false, 2, __half>);
+    return err;
+  };
+  return lat == kD3Q19 ? by_lat(SL<D3Q19, 1>{}) : by_lat(SL<D3Q27, 0>{});
+}
+
+bool mstep16_supported(int lat, const Dom& d) {
+  return (lat == kD3Q19 || lat == kD3Q27) && d.nx % 8 == 0 && d.nx >= 2 && d.ny >= 2 && !d.has_solid &&
+         d.ghost == 0 && mstep::encoder() != nullptr;
+}
+
+namespace {
+// fp32 moment arrays <-> the fp16 storage codec (MStore<__half>)
+__global__ void __launch_bounds__(256) k_moments_to16(const float* __restrict__ src, __half* __restrict__ dst,
+                                                      int64_t n, int64_t stride, int nm) {
+  const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  const int c = int(blockIdx.y);
+  if (i < n && c < nm) dst[c * stride + i] = MStore<__half>::enc(c, src[c * stride + i]);
+}
+__global__ void __launch_bounds__(256) k_moments_from16(const __half* __restrict__ src, float* __restrict__ dst,
+                                                        int64_t n, int64_t stride, int nm) {
+  const int64_t i = int64_t(blockIdx.x) * 256 + threadIdx.x;
+  const int c = int(blockIdx.y);
+  if (i < n && c < nm) dst[c * stride + i] = MStore<__half>::dec(c, src[c * stride + i]);
+}
+}  // namespace
+
+int launch_moments_codec16(const Dom& d, int nm, float* m32, __half* m16, int to16, cudaStream_t st) {
+  const dim3 grid(unsigned((d.n + 255) / 256), unsigned(nm));
+  if (to16) k_moments_to16<<<grid, 256, 0, st>>>(m32, m16, d.n, d.mstride, nm);
+  else k_moments_from16<<<grid, 256, 0, st>>>(m16, m32, d.n, d.mstride, nm);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
 }
 
 template int launch_mstep<float>(int, int, const Dom&, const float*, const float*, float*, double, int, int, int,

@@ -449,6 +449,12 @@ class DeviceSolver:
         single pass); same results bit for bit."""
         self._call("tslb_cuda_set_schedule", {"f1": _lib.SCHED_F1, "m": _lib.SCHED_M}[schedule])
 
+    def set_moment_storage(self, kind: str):
+        """"f16": the M steps keep the moments as scaled fp16 (40 B per
+        lattice update) with fp32 node arithmetic -- a tolerance mode
+        (tslb_cuda.h); "native": the storage scalar."""
+        self._call("tslb_cuda_set_moment_storage", {"native": _lib.STORE_NATIVE, "f16": _lib.STORE_F16}[kind])
+
     def set_body_force(self, fx=0.0, fy=0.0, fz=0.0):
         """Single-fluid body force (extension)."""
         f = np.array([fx, fy, fz], np.float64)

@@ -14,7 +14,7 @@ def test_library_exports_every_declared_symbol():
     assert len(names) >= 40
     missing = [n for n in names if not hasattr(lib, n)]
     assert not missing, missing
-    assert _lib.load().tslb_cuda_abi_version() == 2
+    assert _lib.load().tslb_cuda_abi_version() == 3
 
 
 def test_library_is_sm100a_native():

@@ -650,3 +650,100 @@ def test_mstep_partial_tiles_solid(gpu, oracle_port, dtype):
     fo = f0.copy()
     oracle_port.single_run(lat, dims, 1.1, faces, fo, None, 4, 0, solid)
     assert_bitwise(fg, fo, "M partial tiles, solid mask", solid == 0)
+
+
+# --- mixed precision: fp16 moment storage, fp32 node arithmetic -------------
+def _tgv_f0(dims, dtype, amp=0.04):
+    """Taylor-Green f(0) through the oracle's initialize_regularized."""
+    nx, ny, nz = dims
+    k, j, i = np.meshgrid(np.arange(nz), np.arange(ny), np.arange(nx), indexing="ij")
+    X, Y, Z = (2 * np.pi * (a.ravel() + 0.5) / n for a, n in ((i, nx), (j, ny), (k, nz)))
+    st = np.zeros((10, X.size))
+    st[0] = 1 + 3 * (amp * amp / 16) * (np.cos(2 * X) + np.cos(2 * Y)) * (np.cos(2 * Z) + 2)
+    st[1] = amp * np.sin(X) * np.cos(Y) * np.cos(Z)
+    st[2] = -amp * np.cos(X) * np.sin(Y) * np.cos(Z)
+    return O.Oracle("port").init_regularized("d3q19", dims, st.astype(dtype))
+
+
+@pytest.mark.parametrize("lat", ["d3q19", "d3q27"])
+def test_f16_moment_storage_within_tolerance(gpu, oracle_port, lat):
+    """Mixed precision (fp16 moments, fp32 arithmetic; tslb_store16.cuh)
+    against the fp64 reference arithmetic after 300 steps (D3Q19: a
+    decaying Taylor-Green vortex; D3Q27: a random near-equilibrium state):
+    stated tolerance max|drho| <= 2e-5, max|du| <= 2e-3 * max|u| (measured
+    r02: fp16 storage 5.7e-6 / 8.1e-4, fp32 storage + fp32 math 4.6e-6 /
+    9.9e-5). The fp32-storage run must sit inside it as well."""
+    dims, steps, om = (32, 32, 16), 300, 1.6
+    faces = O.periodic()
+    f0 = _tgv_f0(dims, np.float64) if lat == "d3q19" else O.random_state(lat, dims, 3, np.float64)
+    fo, mo = f0.copy(), np.zeros((O.moments_layout(lat), f0.shape[1]))
+    oracle_port.single_run(lat, dims, om, faces, fo, mo, steps, 0)
+    oracle_port.single_run(lat, dims, om, faces, fo, mo, 1, 2)  # refresh: moments of f(N)
+    D = T.lattice_of(lat).dim
+    umax = np.max(np.abs(mo[1:1 + D]))
+    errs = {}
+    for storage in ("f16", "native"):
+        dev = T.DeviceSolver(lat, T.GridDims(*dims), om, spec_of(faces), np.float32)
+        try:
+            if storage == "f16":
+                dev.set_moment_storage("f16")
+            else:
+                dev.set_math(_lib.MATH_F32)
+            dev.upload_f(f0.astype(np.float32))
+            dev.step(steps)
+            dev.phase("refresh_moments")
+            rho, mom = dev.download_field("rho").astype(np.float64), dev.download_field("mom").astype(np.float64)
+        finally:
+            dev.close()
+        errs[storage] = (np.max(np.abs(rho - mo[0])), np.max(np.abs(mom - mo[1:1 + D])) / umax)
+    print("f16 / fp32 errors:", errs)
+    for storage, (drho, du) in errs.items():
+        assert drho <= 2e-5, (storage, drho)
+        assert du <= 2e-3, (storage, du)
+
+
+def test_f16_moment_storage_reads_are_consistent(gpu):
+    """In fp16 storage the host sees fp32 moments decoded from the fp16 state
+    and f(t+1) = stream_collide(decoded m(t)) -- the F1 fp32-math phase on
+    the same moments gives the same populations bit for bit; switching back
+    to native storage continues from the decoded state."""
+    lat, dims, om = "d3q19", (32, 16, 8), 1.3
+    f0 = O.random_state(lat, dims, 13, np.float32)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), om, spec_of(zwalls_3d()), np.float32)
+    f1 = T.DeviceSolver(lat, T.GridDims(*dims), om, spec_of(zwalls_3d()), np.float32)
+    try:
+        dev.set_moment_storage("f16")
+        dev.upload_f(f0)
+        dev.step(7)
+        m = _moments(dev, lat)
+        fg = dev.download_f()
+        f1.set_schedule("f1")
+        f1.set_math(_lib.MATH_F32)
+        f1.upload_field("rho", m[0])
+        f1.upload_field("mom", m[1:4])
+        f1.upload_field("pineq", m[4:])
+        f1.phase("stream_collide")
+        assert_bitwise(fg, f1.download_f(), "f16 storage: f = stream_collide(decoded moments)")
+        assert np.all(np.isfinite(m))
+        dev.set_moment_storage("native")
+        dev.step(3)
+        assert np.all(np.isfinite(dev.download_f()))
+    finally:
+        dev.close()
+        f1.close()
+
+
+def test_f16_moment_storage_rules(gpu):
+    spec = spec_of(O.periodic())
+    for args, ok in ((("d3q19", (32, 8, 4), np.float32), True), (("d3q19", (36, 8, 4), np.float32), False),
+                     (("d3q19", (32, 8, 4), np.float64), False), (("d2q9", (32, 8, 1), np.float32), False)):
+        lat, dims, dt = args
+        dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.0, spec, dt)
+        try:
+            if ok:
+                dev.set_moment_storage("f16")
+            else:
+                with pytest.raises(_lib.InvalidArgument):
+                    dev.set_moment_storage("f16")
+        finally:
+            dev.close()
