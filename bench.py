@@ -621,7 +621,8 @@ def main():
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             # (masked geometries carry the solid bits: their own capture)
-            tr = json.load(fh).get(f"{lat.name}/{W['storage']}/{dom}{'+solid' if masked else ''}")
+            skey = W["storage"] if args.storage == "native" else "f16"
+            tr = json.load(fh).get(f"{lat.name}/{skey}/{dom}{'+solid' if masked else ''}")
         if tr and args.workload not in tr.get("workloads", [args.workload]):
             tr = None
         if tr:

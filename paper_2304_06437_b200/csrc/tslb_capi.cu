@@ -147,6 +147,10 @@ struct tslb_cuda_sim {
   // steps run on fp16 moments mh/mh2 (tslb_store16.cuh); every other API
   // works on the fp32 moments mo, decoded on demand (m32_valid) and encoded
   // again before the next step once an fp32 path changed them (m16_valid)
+  // refreshed under M: the moments of the current f(t+1) are in mo2 (one M
+  // pass), mo still holds m(t) that f(t+1) is implicit in; the next step is
+  // just the swap (tslb_cuda_refresh_moments)
+  bool mvis2 = false;
   int store16 = 0;
   void* mh = nullptr;
   void* mh2 = nullptr;
@@ -196,8 +200,8 @@ struct tslb_cuda_sim {
   void* fa(int sp, int a) const {
     return static_cast<char*>(f[sp]) + size_t(a) * d.fstride * esz;
   }
-  void* m_arr(int c) const {
-    return static_cast<char*>(mo) + size_t(c) * d.mstride * esz;
+  void* m_arr(int c) const {  // the host-visible moment arrays
+    return static_cast<char*>(mvis2 ? mo2 : mo) + size_t(c) * d.mstride * esz;
   }
   void* t_arr(int c) const {
     return static_cast<char*>(two) + size_t(c) * d.mstride * esz;
@@ -285,6 +289,18 @@ int sync32(tslb_cuda_sim* h) {
   return 0;
 }
 
+// leave the refreshed-under-M state for a standard one: f(t+1) stored (from
+// m(t)), the moment arrays = m(t+1) (what refresh_moments promised)
+int unvis(tslb_cuda_sim* h);
+
+// API prologue: decode fp16 moments if needed; unless the caller only reads
+// the host-visible moments, leave the refreshed-under-M state
+int settle(tslb_cuda_sim* h, bool visible_ok = false) {
+  if (int rc = sync32(h)) return rc;
+  if (!visible_ok && h->mvis2) return unvis(h);
+  return 0;
+}
+
 // -- phases -------------------------------------------------------------------
 // the single-fluid population buffer, allocated on first use under M and
 // filled with the pending analytic f(0) if there is one
@@ -317,6 +333,7 @@ int ph_moments(tslb_cuda_sim* h, cudaStream_t st) {
   if (h->comps == 1)
     if (int rc = ensure_f(h)) return rc;
   h->m16_valid = false;
+  h->mvis2 = false;
   Prof p(h, TSLB_K_MOMENTS, st);
   ++h->launches;
   return by_scalar(h, [&](auto z) {
@@ -428,6 +445,7 @@ int exchange_moments_local(tslb_cuda_sim* h, cudaStream_t st) {
 // the first step's moments pass: precomputed by the M initialiser, or from f
 int first_moments(tslb_cuda_sim* h, cudaStream_t st) {
   h->m16_valid = false;
+  h->mvis2 = false;
   if (h->m0_ready) {
     std::swap(h->mo, h->mo2);
     h->m0_ready = false;
@@ -460,6 +478,14 @@ int materialize(tslb_cuda_sim* h) {
     }
     return 0;
   });
+}
+
+int unvis(tslb_cuda_sim* h) {
+  if (!h->mvis2) return 0;
+  if (int rc = materialize(h)) return rc;  // f(t+1) from m(t) in mo
+  std::swap(h->mo, h->mo2);                // the refreshed m(t+1)
+  h->mvis2 = false;
+  return 0;
 }
 
 int ph_cg_moments(tslb_cuda_sim* h, cudaStream_t st, int k0 = 0, int k1 = -1) {
@@ -1232,7 +1258,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
 }
 
 int tslb_cuda_set_math(tslb_cuda_handle h, int math) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   if (math != kMathDouble && math != kMathFloat) return set_err(TSLB_EINVAL, "bad math mode");
   CK(cudaSetDevice(h->device));
   // a pending f(t+1) belongs to the step that was taken with the old mode
@@ -1244,7 +1270,7 @@ int tslb_cuda_set_math(tslb_cuda_handle h, int math) {
 }
 
 int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   if (schedule != TSLB_SCHED_F1 && schedule != TSLB_SCHED_M)
     return set_err(TSLB_EINVAL, "bad schedule %d", schedule);
   if (schedule == h->sched) return 0;
@@ -1282,7 +1308,7 @@ int tslb_cuda_set_schedule(tslb_cuda_handle h, int schedule) {
 }
 
 int tslb_cuda_set_body_force(tslb_cuda_handle h, const double* force) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   if (!force) return set_err(TSLB_EINVAL, "null force");
   if (h->comps != 1) return set_err(TSLB_EINVAL, "the body force is a single-fluid extension");
   CK(cudaSetDevice(h->device));
@@ -1331,7 +1357,7 @@ int tslb_cuda_memory_bytes(tslb_cuda_handle h, uint64_t* bytes) {
 }
 
 int tslb_cuda_upload_f(tslb_cuda_handle h, int species, const void* host) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   h->m16_valid = false;
   CK(cudaSetDevice(h->device));
   char* base;
@@ -1392,7 +1418,7 @@ int field_desc(tslb_cuda_sim* h, int field, void** base, int* count, int* eb,
 }  // namespace
 
 int tslb_cuda_upload_field(tslb_cuda_handle h, int field, const void* host) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   h->m16_valid = false;
   void* base; int cnt, eb; int64_t stride;
   if (int rc = field_desc(h, field, &base, &cnt, &eb, &stride, true)) return rc;
@@ -1410,7 +1436,7 @@ int tslb_cuda_upload_field(tslb_cuda_handle h, int field, const void* host) {
 }
 
 int tslb_cuda_download_field(tslb_cuda_handle h, int field, void* host) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h, true)) return rc;
   CK(cudaSetDevice(h->device));
   if (int rc = finish_gradient(h)) return rc;
   // two-fluid: after a step the host-visible mom/pineq are u_eq / Pi^neq
@@ -1439,7 +1465,7 @@ int tslb_cuda_download_field(tslb_cuda_handle h, int field, void* host) {
 }
 
 int tslb_cuda_download_slice(tslb_cuda_handle h, int field, int axis, int index, void* host) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h, true)) return rc;
   if (axis < 0 || axis > 2) return set_err(TSLB_EINVAL, "slice axis must be 0, 1 or 2");
   const int ext[3] = {h->nx, h->ny, h->nzl};
   if (index < 0 || index >= ext[axis]) return set_err(TSLB_EINVAL, "slice index %d outside [0, %d)", index, ext[axis]);
@@ -1481,7 +1507,7 @@ int tslb_cuda_download_geometry(tslb_cuda_handle h, uint8_t* solid,
 
 int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
                             double radius) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   h->m16_valid = false;
   CK(cudaSetDevice(h->device));
   InitSpec s{};
@@ -1530,7 +1556,7 @@ int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
 // writes the first step's moments directly and f(0) stays pending on the
 // uploaded states (materialised only if read); otherwise f(0) is stored.
 int tslb_cuda_init_state(tslb_cuda_handle h, const void* host) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   h->m16_valid = false;
   if (!host) return set_err(TSLB_EINVAL, "init_state: null state");
   if (h->comps != 1)
@@ -1631,6 +1657,16 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
     return set_err(TSLB_ESTATE, "slab solver has no halo transport attached");
   CK(cudaSetDevice(h->device));
   long done = 0;
+  if (h->mvis2 && nsteps > 0) {
+    // refreshed under M: the next step's moment pass already ran (mo2 =
+    // m(t+1)); afterwards f(t+2) is implicit in it, whether or not f(t+1)
+    // was materialised meanwhile
+    std::swap(h->mo, h->mo2);
+    h->mvis2 = false;
+    h->fimplicit = true;
+    ++h->steps;
+    ++done;
+  }
   // small 2-D domains under M: the whole run in persistent cooperative
   // launches (grid barrier between passes) -- per-pass launch overhead is
   // most of their step time; TSLB_PERSIST=0 selects the graph path instead
@@ -1744,7 +1780,7 @@ int tslb_cuda_time_steps(tslb_cuda_handle h, long nsteps, double* ms) {
 }
 
 int tslb_cuda_compute_moments(tslb_cuda_handle h) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   if (h->comps != 1) return set_err(TSLB_EINVAL, "compute_moments is single-fluid");
   CK(cudaSetDevice(h->device));
   if (int rc = materialize(h)) return rc;
@@ -1753,7 +1789,7 @@ int tslb_cuda_compute_moments(tslb_cuda_handle h) {
 }
 
 int tslb_cuda_stream_collide(tslb_cuda_handle h) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   if (h->comps != 1) return set_err(TSLB_EINVAL, "stream_collide_fused is single-fluid");
   if (h->decomposed) return set_err(TSLB_ESTATE, "use step() on slab solvers");
   CK(cudaSetDevice(h->device));
@@ -1764,7 +1800,7 @@ int tslb_cuda_stream_collide(tslb_cuda_handle h) {
 }
 
 int tslb_cuda_reference_step(tslb_cuda_handle h, long nsteps) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   if (h->comps != 1 || h->decomposed)
     return set_err(TSLB_EINVAL, "reference_step: single-fluid, single domain only");
   CK(cudaSetDevice(h->device));
@@ -1791,7 +1827,7 @@ int tslb_cuda_reference_step(tslb_cuda_handle h, long nsteps) {
 }
 
 int tslb_cuda_stream_only(tslb_cuda_handle h) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   if (h->comps != 1 || h->decomposed)
     return set_err(TSLB_EINVAL, "stream_only: single-fluid, single domain only");
   CK(cudaSetDevice(h->device));
@@ -1847,6 +1883,15 @@ int tslb_cuda_stream_collide_recolor(tslb_cuda_handle h) {
 int tslb_cuda_refresh_moments(tslb_cuda_handle h) {
   if (int rc = sync32(h)) return rc;
   CK(cudaSetDevice(h->device));
+  if (h->mvis2) return 0;  // (already refreshed)
+  if (h->comps == 1 && h->sched == TSLB_SCHED_M && h->fimplicit && !h->decomposed && !h->store16) {
+    // M: the moments of f(t+1) are one more moment-resident pass from m(t)
+    // (80 B per node instead of storing f and re-reading it); mo keeps m(t)
+    // for f(t+1), the host sees mo2 until the next step takes it over
+    if (int rc = ph_mstep(h, h->s)) return rc;
+    h->mvis2 = true;
+    return sync(h);
+  }
   if (h->comps == 1) {
     if (int rc = materialize(h)) return rc;
     if (int rc = ph_moments(h, h->s)) return rc;
@@ -1858,7 +1903,7 @@ int tslb_cuda_refresh_moments(tslb_cuda_handle h) {
 }
 
 int tslb_cuda_totals(tslb_cuda_handle h, double* mass, double* momentum3) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h, true)) return rc;
   CK(cudaSetDevice(h->device));
   double* part = h->red;
   double* out = h->red + reduce_partial_count();
@@ -1878,7 +1923,7 @@ int tslb_cuda_totals(tslb_cuda_handle h, double* mass, double* momentum3) {
 
 int tslb_cuda_stability(tslb_cuda_handle h, int* finite, double* max_speed,
                         double* min_rho, double* max_rho, int64_t* first_bad) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h, true)) return rc;
   CK(cudaSetDevice(h->device));
   if (int rc = finish_gradient(h)) return rc;
   if (h->comps == 2 && h->stress_pending)
@@ -1923,7 +1968,7 @@ int tslb_cuda_color_masses(tslb_cuda_handle h, double* red, double* blue) {
 }
 
 int tslb_cuda_plane_digests(tslb_cuda_handle h, uint64_t* out) {
-  if (int rc = sync32(h)) return rc;
+  if (int rc = settle(h)) return rc;
   CK(cudaSetDevice(h->device));
   if (int rc = materialize(h)) return rc;
   if (h->comps == 1)

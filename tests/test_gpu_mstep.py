@@ -747,3 +747,60 @@ def test_f16_moment_storage_rules(gpu):
                     dev.set_moment_storage("f16")
         finally:
             dev.close()
+
+
+@pytest.mark.parametrize("lat,dims", [("d3q19", (32, 8, 6)), ("d2q9", (45, 17, 1))])
+def test_refresh_under_m_is_one_moment_pass(gpu, oracle_port, lat, dims):
+    """refresh_moments under M runs one more moment-resident pass (no stored
+    f): the host sees moments(f(t+1)); the next step takes them over without
+    a kernel; any other call first leaves that state. Every transition
+    against fused_step + compute_moments."""
+    faces, om, dt = (corner_box_3d() if lat == "d3q19" else O.lid_cavity(0.05)), 1.3, np.float64
+    f0 = O.random_state(lat, dims, 41, dt)
+    ref = f0.copy()
+    rmo = np.zeros((O.moments_layout(lat), ref.shape[1]), dt)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), om, spec_of(faces), dt)
+
+    def oracle(n, mode=0):
+        oracle_port.single_run(lat, dims, om, faces, ref, rmo, n, mode)
+
+    try:
+        assert dev.schedule == "m"
+        dev.upload_f(f0)
+        dev.step(5)
+        oracle(5)
+        launches = dev.launch_count()
+        dev.phase("refresh_moments")
+        dev.phase("refresh_moments")  # idempotent
+        assert dev.launch_count() - launches == 1, "one moment pass, no f materialised"
+        oracle(1, 2)
+        assert_bitwise(_moments(dev, lat), rmo, "refreshed moments")
+        mass, _ = dev.totals()
+        assert abs(mass - rmo[0].sum()) <= 1e-12 * abs(mass)
+        # the next step takes the refreshed moments over
+        l0 = dev.launch_count()
+        dev.step(1)
+        assert dev.launch_count() == l0, "the step after a refresh is a swap"
+        oracle(1)
+        assert dev.steps_done() == 6
+        dev.step(2)
+        oracle(2)
+        assert_bitwise(dev.download_f(), ref, "f after refresh + steps")
+        assert_bitwise(_moments(dev, lat), rmo, "lagged moments after refresh + steps")
+        # refresh, then read f (materialised from m(t)), then step
+        dev.phase("refresh_moments")
+        oracle(1, 2)
+        assert_bitwise(dev.download_f(), ref, "f read after refresh")
+        assert_bitwise(_moments(dev, lat), rmo, "moments after refresh + f read")
+        dev.step(2)
+        oracle(2)
+        assert_bitwise(dev.download_f(), ref, "f after refresh, f read, steps")
+        # refresh, then overwrite a moment array and step: the step
+        # recomputes the moments from f, as fused_step does
+        dev.phase("refresh_moments")
+        dev.upload_field("rho", np.full(ref.shape[1], 3.0))
+        dev.step(2)
+        oracle(2)
+        assert_bitwise(dev.download_f(), ref, "f after refresh, moment upload, steps")
+    finally:
+        dev.close()
