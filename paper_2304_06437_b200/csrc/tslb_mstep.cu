@@ -642,12 +642,14 @@ __global__ void __launch_bounds__(NT, MINB)
   issue(za - 1, 0);
   __pipeline_commit();
   plane(std::integral_constant<int, 1>{}, za - 1);
-  // two planes per loop iteration: the ping-pong tile buffer index and part
-  // of the ring rotation become static (r02: 34.0 vs 33.4 GLUPS; 4: 32.9)
+  // D3Q19: two planes per loop iteration -- the ping-pong tile buffer index
+  // and part of the ring rotation become static (r02: 34.0 vs 33.4 GLUPS;
+  // 4: 32.9). D3Q27 keeps one: its twice as large loop body missed the
+  // instruction cache (no-instruction stalls 23 %, channel 17.6 vs 20.7)
 #ifdef TSLB_MSTEP_UNROLL  // (measurement switch)
   constexpr int kUnroll = TSLB_MSTEP_UNROLL;
 #else
-  constexpr int kUnroll = 2;
+  constexpr int kUnroll = L::q <= 19 ? 2 : 1;
 #endif
 #pragma unroll kUnroll
   for (int z = za; z < zb; ++z) plane(std::integral_constant<int, 0>{}, z);

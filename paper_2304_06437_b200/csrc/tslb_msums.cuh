@@ -196,27 +196,31 @@ __device__ __forceinline__ float amin3(float a, float b, float c) {
   asm("min.abs.f32 %0, %1, %2, %3;" : "=f"(r) : "f"(a), "f"(b), "f"(c));
   return r;
 }
-// reduce v[I0 .. I0 + N) with F, three at a time
-template <int I0, int N, bool MAX, int Q>
-__device__ __forceinline__ float red3(const float (&v)[Q]) {
+// reduce N values level by level, three at a time: ceil((N - 1) / 2)
+// FMNMX3 in depth ceil(log3 N) (19 -> 7 -> 3 -> 1: 9 instructions)
+template <int N, bool MAX>
+__device__ __forceinline__ float red3(const float* v) {
   if constexpr (N == 1) {
-    return fabsf(v[I0]);
-  } else if constexpr (N == 2) {
-    return MAX ? amax3(v[I0], v[I0 + 1], v[I0 + 1]) : amin3(v[I0], v[I0 + 1], v[I0 + 1]);
-  } else if constexpr (N == 3) {
-    return MAX ? amax3(v[I0], v[I0 + 1], v[I0 + 2]) : amin3(v[I0], v[I0 + 1], v[I0 + 2]);
+    return MAX ? amax3(v[0], v[0], v[0]) : amin3(v[0], v[0], v[0]);
   } else {
-    constexpr int A = (N + 2) / 3, B = (N - A + 1) / 2, C = N - A - B;
-    const float x = red3<I0, A, MAX>(v), y = red3<I0 + A, B, MAX>(v), z = red3<I0 + A + B, C, MAX>(v);
-    return MAX ? amax3(x, y, z) : amin3(x, y, z);
+    constexpr int M = (N + 2) / 3;  // values after this level
+    float w[M];
+#pragma unroll
+    for (int g = 0; g < M; ++g) {
+      const int a = 3 * g, b = min(3 * g + 1, N - 1), c = min(3 * g + 2, N - 1);
+      if (3 * g + 1 >= N) w[g] = v[a];  // a lone leftover moves up unchanged
+      else w[g] = MAX ? amax3(v[a], v[b], v[c]) : amin3(v[a], v[b], v[c]);
+    }
+    if constexpr (M == 1) return w[0];
+    else return red3<M, MAX>(w);
   }
 }
 }  // namespace msums_detail
 
 template <int Q>
 __device__ __forceinline__ bool msums_exact(const float (&v)[Q]) {
-  const float mx = msums_detail::red3<0, Q, true>(v);
-  const float mn = msums_detail::red3<0, Q, false>(v);
+  const float mx = msums_detail::red3<Q, true>(v);
+  const float mn = msums_detail::red3<Q, false>(v);
   return mx < mn * 16777216.0f;
 }
 
