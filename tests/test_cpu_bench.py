@@ -57,7 +57,7 @@ def test_traffic_captures_match_the_bench_accounting():
         assert e["workloads"] and all(w in bench.WORKLOADS for w in e["workloads"]), key
         L = T.lattice_of(lat)
         comps = 2 if kind.startswith("cg_") else 1
-        es = 4 if storage == "f32" else 8
+        es = {"f32": 4, "f64": 8, "f16": 2}[storage]
         kb = bench.kernel_bytes(L, comps, es, masked)
         if kind == "cg_streamcoll":
             # box geometries fold the gradient in: phi read instead of grad
