@@ -84,3 +84,20 @@ def accept_mask(nx: int, ny: int, cx: int, cy: int, modes, src_solid_plane=None,
     if dst_solid_plane is not None:
         ok &= ~np.asarray(dst_solid_plane, bool).reshape(ny, nx)
     return ok
+
+
+# --- M schedule: the exchange is the slabs' boundary moment planes ----------
+def pack_moment_planes(mo: np.ndarray, nm: int, plane: int, nzl: int) -> np.ndarray:
+    """The send buffer of the M-step halo exchange (the device's h->sx,
+    csrc/tslb_capi.cu pack_moments): [2][NM][plane] -- every moment array's
+    plane 0 (for the slab below) and plane nzl - 1 (for the slab above) --
+    one contiguous message per face."""
+    m = np.asarray(mo).reshape(nm, -1)[:, :nzl * plane].reshape(nm, nzl, plane)
+    return np.ascontiguousarray(np.stack([m[:, 0], m[:, nzl - 1]]))
+
+
+def moment_ghost_messages(packed: np.ndarray) -> tuple[np.ndarray, np.ndarray]:
+    """(to the slab below, to the slab above): the receiver stores the first
+    as its upper ghost planes gm[1], the second as its lower gm[0]
+    (layout [2][NM][plane], below / above)."""
+    return packed[0], packed[1]

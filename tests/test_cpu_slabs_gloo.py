@@ -158,3 +158,122 @@ def test_split_and_modes():
     up, dn = S.exchange_dirs(T.D3Q19)
     assert len(up) == len(dn) == 5
     assert len(S.exchange_dirs(T.D3Q27)[0]) == 9
+
+
+# --- the M schedule's plan: moment ghost planes, one packed message per face
+def _rank_main_m(rank, world, port, case, steps, out_q):
+    """One rank of the M-schedule plan: the slab keeps its moments m(t) and
+    the neighbours' boundary moment planes (gm, [2][NM][plane]); a step is
+    f(t+1) = stream_collide(m(t)) over [ghost below] owned [ghost above]
+    (only owned planes kept), m(t+1) = compute_moments(f(t+1)), then the
+    packed boundary planes go to the neighbours. The oracle's phases stand in
+    for the M kernel (tests/test_gpu_slabs.py runs the device one)."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lat, dims, faces, solid, seed = case
+        nx, ny, nz = dims
+        plane = nx * ny
+        L = T.lattice_of(lat)
+        nm = O.moments_layout(lat)
+        kinds = [T.FaceKind.Periodic if k == "periodic" else T.FaceKind.NoSlipWall if k == "wall"
+                 else T.FaceKind.MovingWall for k, _ in faces]
+        z0, nzl = S.split(nz, world)[rank]
+        modes = S.face_modes(kinds, z0, nzl, nz)
+        down, up = S.neighbours(modes, rank, world)
+        glo, ghi = modes[4] == S.GHOST, modes[5] == S.GHOST
+        planes = ([z0 - 1] if glo else []) + list(range(z0, z0 + nzl)) + ([z0 + nzl] if ghi else [])
+        zl, owned0 = len(planes), (1 if glo else 0)
+        gsolid = np.zeros(nx * ny * nz, np.uint8) if solid is None else solid
+        sol = np.concatenate([gsolid[(p % nz) * plane:(p % nz + 1) * plane] for p in planes]).copy()
+        ext_faces = list(faces)
+        zghost = ("periodic" if (glo and ghi) else "wall", (0.0, 0.0, 0.0))
+        if glo:
+            ext_faces[4] = zghost
+        if ghi:
+            ext_faces[5] = zghost
+        edims = (nx, ny, zl)
+        orc = O.Oracle("port")
+        ssol = sol if solid is not None else None
+        own = slice(owned0 * plane, (owned0 + nzl) * plane)
+        f0 = O.random_state(lat, dims, seed, np.float64, solid)
+        fe = np.concatenate([f0[:, (p % nz) * plane:(p % nz + 1) * plane] for p in planes], axis=1).copy()
+        me = np.zeros((nm, zl * plane))
+        gm = np.zeros((2, nm, plane))
+
+        def exchange():
+            packed = S.pack_moment_planes(np.ascontiguousarray(me[:, own]), nm, plane, nzl)
+            to_dn, to_up = S.moment_ghost_messages(packed)
+            reqs = []
+            if ghi:
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(to_up)), dst=up, tag=1))
+            if glo:
+                reqs.append(dist.isend(torch.from_numpy(np.ascontiguousarray(to_dn)), dst=down, tag=2))
+            rlo, rhi = torch.zeros((nm, plane), dtype=torch.float64), torch.zeros((nm, plane), dtype=torch.float64)
+            if glo:
+                reqs.append(dist.irecv(rlo, src=down, tag=1))
+            if ghi:
+                reqs.append(dist.irecv(rhi, src=up, tag=2))
+            for r in reqs:
+                r.wait()
+            gm[0], gm[1] = rlo.numpy(), rhi.numpy()
+            if glo:
+                me[:, :plane] = gm[0]
+            if ghi:
+                me[:, (zl - 1) * plane:] = gm[1]
+
+        # first step's moments pass (m(0) of the owned planes) + exchange
+        orc.single_run(lat, edims, 0.9, ext_faces, fe, me, 1, 2, ssol)
+        exchange()
+        for _ in range(steps - 1):
+            orc.single_run(lat, edims, 0.9, ext_faces, fe, me, 1, 3, ssol)  # f(t+1) = stream_collide(m(t))
+            orc.single_run(lat, edims, 0.9, ext_faces, fe, me, 1, 2, ssol)  # m(t+1)
+            exchange()
+        m_lag = np.ascontiguousarray(me[:, own])            # the lagged moments m(steps - 1)
+        orc.single_run(lat, edims, 0.9, ext_faces, fe, me, 1, 3, ssol)  # f(steps), materialised
+        out_q.put((rank, z0, nzl, np.ascontiguousarray(fe[:, own]), m_lag))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("case", CASES, ids=lambda c: f"{c[0]}-{c[2]}-{c[3]}")
+def test_m_slab_plan_with_gloo_ranks(case, world):
+    """The M-schedule decomposition (packed moment planes per face, the
+    device's exchange_moments_nccl) with real gloo ranks: f(N) and the
+    lagged moments gathered over the slabs equal the undivided fused_step."""
+    lat, dims, fk, frac, seed = case
+    faces = {None: O.periodic(), "periodic": O.periodic(), "zwalls": zwalls_3d(), "box": O.closed_box()}[fk]
+    solid = random_solid(dims, frac, seed) if frac else None
+    steps = 4
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main_m, args=(r, world, port, (lat, dims, faces, solid, seed), steps, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    parts = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    parts.sort(key=lambda t: t[1])
+    got_f = np.concatenate([p[3] for p in parts], axis=1)
+    got_m = np.concatenate([p[4] for p in parts], axis=1)
+    ref = O.random_state(lat, dims, seed, np.float64, solid)
+    mo = np.zeros((O.moments_layout(lat), ref.shape[1]))
+    O.Oracle("port").single_run(lat, dims, 0.9, faces, ref, mo, steps, 0, solid)
+    fluid = np.ones(ref.shape[1], bool) if solid is None else solid == 0
+    assert np.array_equal(got_f[:, fluid].view(np.uint64), ref[:, fluid].view(np.uint64))
+    assert np.array_equal(got_m[:, fluid].view(np.uint64), mo[:, fluid].view(np.uint64))
+
+
+def test_pack_moment_planes_layout():
+    nm, plane, nzl = 10, 6, 4
+    mo = np.arange(nm * nzl * plane, dtype=np.float64).reshape(nm, nzl * plane)
+    p = S.pack_moment_planes(mo, nm, plane, nzl)
+    assert p.shape == (2, nm, plane)
+    assert np.array_equal(p[0], mo[:, :plane]) and np.array_equal(p[1], mo[:, (nzl - 1) * plane:])
+    dn, upm = S.moment_ghost_messages(p)
+    assert np.array_equal(dn, p[0]) and np.array_equal(upm, p[1])
