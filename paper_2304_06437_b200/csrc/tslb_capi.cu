@@ -381,12 +381,7 @@ int ph_mstep(tslb_cuda_sim* h, cudaStream_t st, int z0 = 0, int z1 = 0) {
 // starts early and overlaps the interior chunks (TSLB_LZB overrides)
 constexpr int kBoundaryLz = 16;
 int boundary_planes(const tslb_cuda_sim* h) {
-  static const int env = [] {
-    const char* e = std::getenv("TSLB_LZB");
-    return e ? std::atoi(e) : 0;
-  }();
-  const int b = h->lzb > 0 ? h->lzb : env > 0 ? env : kBoundaryLz;
-  return std::min(b, h->nzl);
+  return std::min(h->lzb > 0 ? h->lzb : kBoundaryLz, h->nzl);
 }
 
 size_t moment_plane_block(const tslb_cuda_sim* h) {  // bytes of NM planes
@@ -979,6 +974,7 @@ int create_impl(int lattice, int scalar, int components, int nx, int ny,
   if (const char* e = std::getenv("TSLB_KZ")) h->kz = std::atoi(e);
   if (const char* e = std::getenv("TSLB_GRAPHS")) h->graphs_ok = std::atoi(e) != 0;
   if (const char* e = std::getenv("TSLB_LZ")) h->lz = std::atoi(e);
+  if (const char* e = std::getenv("TSLB_LZB")) h->lzb = std::atoi(e);
   std::memcpy(h->kinds, kinds, sizeof h->kinds);
   if (color) {
     h->cp.sigma = color[0];

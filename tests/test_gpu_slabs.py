@@ -83,8 +83,9 @@ def test_mstep_slabs_equal_oracle(gpu, oracle_port, name, faces, lat, parts, dty
     """M-schedule slabs (boundary chunks, ghost-plane exchange, interior
     chunks; f rebuilt from ghost moments on download) are bit-identical to
     fused_step on the undivided domain, for any slab count."""
-    if lz:
+    if lz:  # several chunks, and 1-plane boundary chunks (boundary / exchange / interior)
         monkeypatch.setenv("TSLB_LZ", lz)
+        monkeypatch.setenv("TSLB_LZB", "1")
     dims = (32, 16, 12)
     f0 = O.random_state(lat, dims, 77, dtype)
     g = T.GridDims(*dims)
@@ -113,14 +114,17 @@ def test_mstep_slabs_equal_oracle(gpu, oracle_port, name, faces, lat, parts, dty
 # --- the NCCL transport itself, on one device: a single-rank communicator ---
 @pytest.mark.parametrize("sched", ["m", "f1"])
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-def test_nccl_self_exchange_equals_periodic_box(gpu, sched, dtype, monkeypatch):
+@pytest.mark.parametrize("lzb", ["", "2"])
+def test_nccl_self_exchange_equals_periodic_box(gpu, sched, dtype, lzb, monkeypatch):
     """One slab [0, nzl) of a 2*nzl box attached to a ONE-rank NCCL
     communicator: its up and down neighbour is itself, so every step ships
     its boundary planes (moment planes under M, pushed populations under F1)
     through ncclSend/ncclRecv to itself -- exactly a periodic box of height
     nzl. This exercises the multi-GPU step (boundary chunks, exchange on the
     comm stream, interior chunks, join) on real NCCL with one GPU."""
-    monkeypatch.setenv("TSLB_LZ", "2")  # several z chunks: boundary / interior split
+    monkeypatch.setenv("TSLB_LZ", "2")  # several z chunks per launch
+    if lzb:  # M: 2-plane boundary chunks on the comm stream, the interior overlapped
+        monkeypatch.setenv("TSLB_LZB", lzb)
     lat, nx, ny, nzl = "d3q19", 32, 16, 8
     f0 = O.random_state(lat, (nx, ny, nzl), 5, dtype)
     spec = spec_of(O.periodic())
@@ -435,6 +439,40 @@ def test_two_fluid_nci_nccl_self_exchange(gpu, dtype):
         for k in NCI_FIELDS:
             assert_bitwise(slab.download_field(k), ref.download_field(k), f"NCI NCCL self-exchange {k}")
         assert ref.download_field("nci_flag").sum() > 50
+    finally:
+        slab.close()
+        ref.close()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_init_state_on_a_slab(gpu, oracle_port, dtype, monkeypatch):
+    """tslb_cuda_init_state on a slab (the local planes' node states) with
+    the M step over a one-rank NCCL communicator == the periodic box
+    initialised the same way, and == the oracle's initialize_regularized +
+    fused_step."""
+    monkeypatch.setenv("TSLB_LZB", "2")
+    lat, nx, ny, nzl = "d3q19", 32, 8, 8
+    n = nx * ny * nzl
+    rng = np.random.default_rng(3)
+    st = rng.uniform(-0.02, 0.02, (10, n))
+    st[0] += 1.0
+    st[4:] *= 0.01
+    st = st.astype(dtype)
+    spec = spec_of(O.periodic())
+    ref = T.DeviceSolver(lat, T.GridDims(nx, ny, nzl), 1.2, spec, dtype)
+    slab = T.DeviceSolver(lat, T.GridDims(nx, ny, 2 * nzl), 1.2, spec, dtype, 1, None, slab=(0, nzl))
+    try:
+        uid = (C.c_char * 128)()
+        _lib.call("tslb_cuda_nccl_unique_id", uid)
+        _lib.call("tslb_cuda_attach_nccl", slab.h, uid, 1, 0)
+        for d in (ref, slab):
+            d.init_state(st)
+            d.step(6)
+        fs = slab.download_f()
+        assert_bitwise(fs, ref.download_f(), "init_state slab vs box f")
+        fo = oracle_port.init_regularized(lat, (nx, ny, nzl), st)
+        oracle_port.single_run(lat, (nx, ny, nzl), 1.2, O.periodic(), fo, None, 6, 0)
+        assert_bitwise(fs, fo, "init_state slab vs oracle f")
     finally:
         slab.close()
         ref.close()
