@@ -773,17 +773,22 @@ def run_e2e(sim, lat, dims, steps, dtype, amp):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     _lib.check(lib.tslb_cuda_init_state(sim.h, C.c_void_p(host_state.data_ptr())))
+    t1 = time.perf_counter()
     for _ in range(steps):
         _lib.check(lib.tslb_cuda_step(sim.h, 1))
         _lib.check(lib.tslb_cuda_totals(sim.h, C.byref(mass), mom))
+    t2 = time.perf_counter()
     _lib.check(lib.tslb_cuda_refresh_moments(sim.h))
+    t3 = time.perf_counter()
     _lib.check(lib.tslb_cuda_download_field(sim.h, 0, C.c_void_p(out.data_ptr())))
     _lib.check(lib.tslb_cuda_download_field(sim.h, 1, C.c_void_p(out[1:].data_ptr())))
     t = time.perf_counter() - t0
+    phases = {"init_state": round(t1 - t0, 3), "steps_and_totals": round(t2 - t1, 3), "refresh": round(t3 - t2, 3),
+              "download": round(t0 + t - t3, 3)}
     h2d = nm * nn * esz
     d2h = (1 + lat.dim) * nn * esz + steps * 32
     return {"value": round(nn * steps / t / 1e9, 4), "unit": "GLUPS", "h2d_bytes_per_step": int(h2d / steps),
-            "d2h_bytes_per_step": int(d2h / steps), "seconds": round(t, 3),
+            "d2h_bytes_per_step": int(d2h / steps), "seconds": round(t, 3), "phase_seconds": phases,
             "loop": "node states (pinned) -> init_state (device initialize_regularized, upload overlapped) -> "
                     "steps x (step + totals readback) -> refresh, download rho,u"}
 
