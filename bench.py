@@ -715,14 +715,14 @@ def main():
 
 
 def tgv_state_host(dims, amp, tdt):
-    """The Taylor-Green node states (rho, u[3], Pi^neq[6] = 0 -- the
-    prepare_node arguments of initialize_regularized) of an nx*ny*nz box in
-    a pinned host tensor (1 + D + np, n), computed on the device plane chunk
-    by plane chunk (untimed set-up of the e2e loop)."""
+    """The Taylor-Green node states (rho, u[3]; Pi^neq = 0 as in the
+    reference driver's prepare_node(rho, u, 0, ...), tslb_main.cpp:115-122)
+    of an nx*ny*nz box in a pinned host tensor (1 + D, n), computed on the
+    device plane chunk by plane chunk (untimed set-up of the e2e loop)."""
     import torch
     nx, ny, nz = dims
     plane = nx * ny
-    st = torch.zeros((10, plane * nz), dtype=tdt, pin_memory=True)
+    st = torch.zeros((4, plane * nz), dtype=tdt, pin_memory=True)
     dev = torch.device("cuda")
     two_pi = 2.0 * np.pi
     X = two_pi * (torch.arange(nx, device=dev, dtype=torch.float64) + 0.5) / nx
@@ -748,9 +748,11 @@ def tgv_state_host(dims, amp, tdt):
 
 def run_e2e(sim, lat, dims, steps, dtype, amp):
     """The reference driver loop (tslb_main.cpp run_single) through the public
-    C-ABI with HOST buffers: the initial node states go up from pinned host
-    memory into the device initialize_regularized (tslb_cuda_init_state:
-    chunked upload overlapped with the initialisation), `steps` steps each
+    C-ABI with HOST buffers: the initial rho and u go up from pinned host
+    memory into the device initialize_regularized with Pi^neq = 0
+    (tslb_cuda_init_equilibrium -- the reference driver's start,
+    tslb_main.cpp:115-122 -- chunked upload overlapped with the
+    initialisation), `steps` steps each
     followed by a totals() sample read back to the host, then refresh and
     download rho and u (the output frame). Host wall time around it."""
     import ctypes as C
@@ -761,7 +763,7 @@ def run_e2e(sim, lat, dims, steps, dtype, amp):
     nn = int(np.prod(dims))
     esz = np.dtype(dtype).itemsize
     tdt = torch.float32 if esz == 4 else torch.float64
-    nm = 1 + lat.dim + lat.dim * (lat.dim + 1) // 2
+    nm = 1 + lat.dim
     try:
         host_state = tgv_state_host(dims, amp, tdt)
         out = torch.empty((1 + lat.dim, nn), dtype=tdt, pin_memory=True)
@@ -772,7 +774,7 @@ def run_e2e(sim, lat, dims, steps, dtype, amp):
     mom = (C.c_double * 3)()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    _lib.check(lib.tslb_cuda_init_state(sim.h, C.c_void_p(host_state.data_ptr())))
+    _lib.check(lib.tslb_cuda_init_equilibrium(sim.h, C.c_void_p(host_state.data_ptr())))
     t1 = time.perf_counter()
     for _ in range(steps):
         _lib.check(lib.tslb_cuda_step(sim.h, 1))
@@ -783,13 +785,14 @@ def run_e2e(sim, lat, dims, steps, dtype, amp):
     _lib.check(lib.tslb_cuda_download_field(sim.h, 0, C.c_void_p(out.data_ptr())))
     _lib.check(lib.tslb_cuda_download_field(sim.h, 1, C.c_void_p(out[1:].data_ptr())))
     t = time.perf_counter() - t0
-    phases = {"init_state": round(t1 - t0, 3), "steps_and_totals": round(t2 - t1, 3), "refresh": round(t3 - t2, 3),
+    phases = {"init_equilibrium": round(t1 - t0, 3), "steps_and_totals": round(t2 - t1, 3), "refresh": round(t3 - t2, 3),
               "download": round(t0 + t - t3, 3)}
     h2d = nm * nn * esz
     d2h = (1 + lat.dim) * nn * esz + steps * 32
     return {"value": round(nn * steps / t / 1e9, 4), "unit": "GLUPS", "h2d_bytes_per_step": int(h2d / steps),
             "d2h_bytes_per_step": int(d2h / steps), "seconds": round(t, 3), "phase_seconds": phases,
-            "loop": "node states (pinned) -> init_state (device initialize_regularized, upload overlapped) -> "
+            "loop": "rho, u (pinned) -> init_equilibrium (device initialize_regularized, Pi^neq = 0, upload "
+                    "overlapped) -> "
                     "steps x (step + totals readback) -> refresh, download rho,u"}
 
 

@@ -177,6 +177,10 @@ int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
  * initialisation; pinned host memory gives full PCIe bandwidth. Single fluid
  * only (TSLB_EINVAL otherwise). Same f(0) bits as the host routine. */
 int tslb_cuda_init_state(tslb_cuda_handle h, const void* host_state);
+/* The same from rho and u alone, Pi^neq = 0 (prepare_node(rho, u, 0, ...): the
+ * equilibrium start of the reference driver, tslb_main.cpp:115-122): (1 + D)
+ * arrays of n_local storage-type scalars. */
+int tslb_cuda_init_equilibrium(tslb_cuda_handle h, const void* host_rho_u);
 
 /* time stepping */
 int tslb_cuda_step(tslb_cuda_handle h, long nsteps);

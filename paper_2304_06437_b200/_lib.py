@@ -70,6 +70,7 @@ def load(path: str | None = None) -> C.CDLL:
         "tslb_cuda_download_geometry": ([H, vp, vp, vp], i),
         "tslb_cuda_init_analytic": ([H, i, d, d], i),
         "tslb_cuda_init_state": ([H, vp], i),
+        "tslb_cuda_init_equilibrium": ([H, vp], i),
         "tslb_cuda_set_moment_storage": ([H, i], i),
         "tslb_cuda_step": ([H, l], i),
         "tslb_cuda_step_async": ([H, l], i),

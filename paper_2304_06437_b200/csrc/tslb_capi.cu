@@ -142,7 +142,8 @@ struct tslb_cuda_sim {
   uint32_t* slow = nullptr;
   uint32_t* sbits = nullptr;  // M on a masked geometry: per-node solid bits (with ghost planes)
   void* scratch = nullptr;
-  void* state_buf = nullptr;  // tslb_cuda_init_state: the node states [1+D+np][mstride] (f(0) pending on them)
+  void* state_buf = nullptr;  // tslb_cuda_init_state: the node states [state_nm][mstride] (f(0) pending on them)
+  int state_nm = 0;            // arrays in state_buf: 1+D+np (init_state) or 1+D (init_equilibrium)
   // mixed-precision moment storage (tslb_cuda_set_moment_storage): the M
   // steps run on fp16 moments mh/mh2 (tslb_store16.cuh); every other API
   // works on the fp32 moments mo, decoded on demand (m32_valid) and encoded
@@ -310,7 +311,7 @@ int ensure_f(tslb_cuda_sim* h) {
   if (h->state_buf && !h->f0_pending) {
     CK(cudaFree(h->state_buf));
     h->state_buf = nullptr;
-    h->bytes -= size_t(h->d.mstride) * (1 + h->dim + h->np) * h->esz;
+    h->bytes -= size_t(h->d.mstride) * h->state_nm * h->esz;
   }
   if (!h->f[0]) {
     const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
@@ -1551,14 +1552,16 @@ int tslb_cuda_init_analytic(tslb_cuda_handle h, int kind, double amplitude,
 // transfer overlaps the initialisation. Under M (box geometry) the kernel
 // writes the first step's moments directly and f(0) stays pending on the
 // uploaded states (materialised only if read); otherwise f(0) is stored.
-int tslb_cuda_init_state(tslb_cuda_handle h, const void* host) {
+// with_pi: the host states carry Pi^neq (1+D+np arrays); without, they are
+// rho and u only and Pi^neq = 0 (1+D arrays).
+static int init_state(tslb_cuda_sim* h, const void* host, bool with_pi) {
   if (int rc = settle(h)) return rc;
   h->m16_valid = false;
   if (!host) return set_err(TSLB_EINVAL, "init_state: null state");
   if (h->comps != 1)
     return set_err(TSLB_EINVAL, "init_state: single-fluid node states (two-fluid: initialize_colors + upload_f)");
   CK(cudaSetDevice(h->device));
-  const int nm = 1 + h->dim + h->np;
+  const int nm = 1 + h->dim + (with_pi ? h->np : 0);
   const bool m_path = h->sched == TSLB_SCHED_M && !h->d.has_solid;
   h->fimplicit = false;
   h->f0_pending = false;
@@ -1566,8 +1569,15 @@ int tslb_cuda_init_state(tslb_cuda_handle h, const void* host) {
   // (ensure_f releases an earlier state buffer: allocate this one after it)
   if (!m_path)
     if (int rc = ensure_f(h)) return rc;
-  if (!h->state_buf)
+  if (h->state_buf && h->state_nm != nm) {
+    CK(cudaFree(h->state_buf));
+    h->state_buf = nullptr;
+    h->bytes -= size_t(h->d.mstride) * h->state_nm * h->esz;
+  }
+  if (!h->state_buf) {
     if (int rc = alloc(h, &h->state_buf, size_t(h->d.mstride) * nm * h->esz)) return rc;
+    h->state_nm = nm;
+  }
   InitSpec sp{};
   sp.kind = kInitState;
   sp.nx_g = h->nx;
@@ -1576,6 +1586,7 @@ int tslb_cuda_init_state(tslb_cuda_handle h, const void* host) {
   sp.z0 = h->z0;
   sp.state = h->state_buf;
   sp.sstride = h->d.mstride;
+  sp.spi = with_pi ? 1 : 0;
   // ~32 MB of each state array per chunk
   const int64_t plane = h->plane();
   const int cz = int(std::max<int64_t>(1, (int64_t(32) << 20) / (plane * h->esz)));
@@ -1612,6 +1623,10 @@ int tslb_cuda_init_state(tslb_cuda_handle h, const void* host) {
   h->bytes -= size_t(h->d.mstride) * nm * h->esz;
   return 0;
 }
+
+int tslb_cuda_init_state(tslb_cuda_handle h, const void* host) { return init_state(h, host, true); }
+
+int tslb_cuda_init_equilibrium(tslb_cuda_handle h, const void* host) { return init_state(h, host, false); }
 
 int tslb_cuda_set_moment_storage(tslb_cuda_handle h, int kind) {
   if (kind != TSLB_STORE_NATIVE && kind != TSLB_STORE_F16) return set_err(TSLB_EINVAL, "bad moment storage %d", kind);

@@ -22,8 +22,9 @@ struct InitSpec {
   int z0;                // global z of local plane 0
   double amp;            // shear / Taylor-Green velocity amplitude
   double cx, cy, cz, radius, width;  // droplet
-  const void* state;     // kInitState: [1 + D + np][sstride] of the storage type
+  const void* state;     // kInitState: [1 + D (+ np)][sstride] of the storage type
   int64_t sstride;
+  int spi;               // kInitState: the states carry Pi^neq (else Pi^neq = 0)
 };
 
 struct ColorParamsDev {

@@ -49,22 +49,31 @@ __device__ __forceinline__ void owned(const Dom& d, int64_t t, int64_t& mi,
   fi = t + int64_t(d.ghost) * d.plane;
 }
 
-template <typename T>
+template <typename T, int DIM>
 __global__ void __launch_bounds__(RB)
-    k_totals(Dom d, int dim, const T* __restrict__ rho, const T* __restrict__ mom,
+    k_totals(Dom d, const T* __restrict__ rho, const T* __restrict__ mom,
              const uint8_t* __restrict__ solid, double* partial) {
   __shared__ double sh[4 * (RB / 32)];
   double v[4] = {0, 0, 0, 0};
-  // contiguous chunk per block, strided per thread: fixed assignment
+  // contiguous chunk per block, strided per thread: fixed assignment. The
+  // loads are unconditional (solid nodes are skipped in the sums only), so
+  // with the unrolled loop four iterations' loads are in flight together
   const int64_t per = (d.n + RBLOCKS - 1) / RBLOCKS;
   const int64_t b0 = int64_t(blockIdx.x) * per;
   const int64_t b1 = min(d.n, b0 + per);
+#pragma unroll 4
   for (int64_t t = b0 + threadIdx.x; t < b1; t += RB) {
     int64_t mi, fi;
     owned(d, t, mi, fi);
-    if (solid[fi]) continue;
-    v[0] += double(rho[mi]);
-    for (int c = 0; c < dim; ++c) v[1 + c] += double(mom[c * d.mstride + mi]);
+    const bool sol = solid[fi] != 0;
+    const double r = double(rho[mi]);
+    double m[DIM];
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) m[c] = double(mom[c * d.mstride + mi]);
+    if (sol) continue;
+    v[0] += r;
+#pragma unroll
+    for (int c = 0; c < DIM; ++c) v[1 + c] += m[c];
   }
   block_sum<4>(v, sh);
   if (threadIdx.x == 0)
@@ -96,6 +105,9 @@ __global__ void __launch_bounds__(RB)
   const int64_t per = (d.n + RBLOCKS - 1) / RBLOCKS;
   const int64_t b0 = int64_t(blockIdx.x) * per;
   const int64_t b1 = min(d.n, b0 + per);
+  // (unrolled: the loads of four iterations are in flight together; the
+  // accumulation order is unchanged)
+#pragma unroll 4
   for (int64_t t = b0 + threadIdx.x; t < b1; t += RB) {
     int64_t mi, fi;
     owned(d, t, mi, fi);
@@ -199,7 +211,8 @@ template <typename T>
 int launch_totals(const Dom& d, int dim, const T* rho, const T* mom,
                   const uint8_t* solid, double* partial, double* out,
                   cudaStream_t st) {
-  k_totals<T><<<RBLOCKS, RB, 0, st>>>(d, dim, rho, mom, solid, partial);
+  if (dim == 3) k_totals<T, 3><<<RBLOCKS, RB, 0, st>>>(d, rho, mom, solid, partial);
+  else k_totals<T, 2><<<RBLOCKS, RB, 0, st>>>(d, rho, mom, solid, partial);
   k_fold_sum<<<1, 32, 0, st>>>(partial, 4, out);
   return 0;
 }

@@ -288,6 +288,12 @@ __device__ __forceinline__ NodeMoments<T> init_state(const InitSpec& s, int i, i
   if (s.kind == kInitState) {  // user node states, already in T
     const T* p = static_cast<const T*>(s.state) + (int64_t(i) + int64_t(s.nx_g) * (int64_t(j) + int64_t(s.ny_g) * k));
     const int64_t q = s.sstride;
+    if (!s.spi) {  // rho and u only: the prepare_node(rho, u, 0) of tslb_main.cpp:115-122
+      if constexpr (L::dim == 3)
+        return prepare_node<T>(p[0], p[q], p[2 * q], p[3 * q], T(0), T(0), T(0), T(0), T(0), T(0));
+      else
+        return prepare_node<T>(p[0], p[q], p[2 * q], T(0), T(0), T(0), T(0), T(0), T(0), T(0));
+    }
     if constexpr (L::dim == 3)
       return prepare_node<T>(p[0], p[q], p[2 * q], p[3 * q], p[4 * q], p[5 * q], p[6 * q], p[7 * q], p[8 * q],
                              p[9 * q]);

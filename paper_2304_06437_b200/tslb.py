@@ -474,17 +474,26 @@ class DeviceSolver:
         array (1 + D + np, n) of the storage dtype -- rho, u[D], Pi[np] per
         node (kernels.hpp:296-311). Pinned host memory (e.g. a torch tensor
         with pin_memory) is taken as is, by pointer."""
-        nm = 1 + self.lat.dim + self.lat.npineq
+        self._init_states("tslb_cuda_init_state", state, 1 + self.lat.dim + self.lat.npineq)
+
+    def init_equilibrium(self, state):
+        """The same from rho and u alone, Pi^neq = 0 (the reference driver's
+        prepare_node(rho, u, 0, ...), tslb_main.cpp:115-122): an array
+        (1 + D, n) of the storage dtype."""
+        self._init_states("tslb_cuda_init_equilibrium", state, 1 + self.lat.dim)
+
+    def _init_states(self, fn, state, nm):
+        name = fn[len("tslb_cuda_"):]
         if hasattr(state, "data_ptr"):  # a torch tensor (pinned host buffer)
             if tuple(state.shape) != (nm, self.n) or not state.is_contiguous() or state.element_size() != \
                     np.dtype(self.dtype).itemsize or state.is_cuda:
-                raise _lib.InvalidArgument(f"init_state: expected a contiguous host tensor of shape {(nm, self.n)}")
-            self._call("tslb_cuda_init_state", C.c_void_p(state.data_ptr()))
+                raise _lib.InvalidArgument(f"{name}: expected a contiguous host tensor of shape {(nm, self.n)}")
+            self._call(fn, C.c_void_p(state.data_ptr()))
             return
         a = np.ascontiguousarray(state, self.dtype)
         if a.shape != (nm, self.n):
-            raise _lib.InvalidArgument(f"init_state: expected shape {(nm, self.n)}, got {a.shape}")
-        self._call("tslb_cuda_init_state", _ptr(a))
+            raise _lib.InvalidArgument(f"{name}: expected shape {(nm, self.n)}, got {a.shape}")
+        self._call(fn, _ptr(a))
 
     # diagnostics
     def totals(self):

@@ -476,3 +476,50 @@ def test_init_state_matches_host_initialize_regularized(gpu, oracle_port, lat, d
         oracle_port.single_run(lat, dims, 1.3, faces, fo, None, 4, 0, solid)
         fluid = np.ones(n, bool) if solid is None else solid == 0
         assert_bitwise(fg, fo, f"{lat} {sched} f(4) after init_state (read f(0) first: {read_first})", fluid)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("lat,dims,sched", [
+    ("d3q19", (32, 16, 6), "m"), ("d3q19", (32, 16, 6), "f1"), ("d3q27", (32, 8, 5), "m"), ("d2q9", (45, 17, 1), "m")])
+def test_init_equilibrium_is_init_state_with_zero_pi(gpu, oracle_port, lat, dims, sched, dtype):
+    """tslb_cuda_init_equilibrium (rho and u only, Pi^neq = 0: the reference
+    driver's start, tslb_main.cpp:115-122) == the port's initialize_regularized
+    of the same states with zero Pi, bit for bit, before and after steps; on
+    one handle after a full init_state (the state buffer changes size) and
+    the other way round."""
+    L = T.lattice_of(lat)
+    n = int(np.prod(dims))
+    nm = 1 + L.dim + L.npineq
+    rng = np.random.default_rng(23)
+    st = rng.uniform(-0.02, 0.02, (nm, n))
+    st[0] += 1.0
+    st[1 + L.dim:] *= 0.01
+    st = st.astype(dtype)
+    st0 = st.copy()
+    st0[1 + L.dim:] = 0
+    zero = np.zeros((1, n), dtype)
+    state10 = st0 if L.dim == 3 else np.concatenate([st0[:3], zero, st0[3:5], zero, st0[5:6], zero, zero])
+    f0 = oracle_port.init_regularized(lat, dims, state10, None)
+    faces = zwalls_3d() if L.dim == 3 else O.lid_cavity(0.05)
+    fo = f0.copy()
+    oracle_port.single_run(lat, dims, 1.3, faces, fo, None, 3, 0, None)
+    dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.3, spec_of(faces), dtype, 1, None)
+    try:
+        if dev.schedule != sched:
+            dev.set_schedule(sched)
+        for order in ("state first", "equilibrium first"):
+            if order == "state first":
+                dev.init_state(st)
+                dev.step(1)
+                dev.init_equilibrium(np.ascontiguousarray(st[:1 + L.dim]))
+            else:
+                dev.init_equilibrium(np.ascontiguousarray(st[:1 + L.dim]))
+                dev.step(2)
+                dev.init_state(st0)
+            assert_bitwise(dev.download_f(), f0, f"{lat} {sched} f(0), {order}")
+            dev.step(3)
+            assert_bitwise(dev.download_f(), fo, f"{lat} {sched} f(3), {order}")
+        with pytest.raises(_lib.InvalidArgument):
+            dev.init_equilibrium(st)
+    finally:
+        dev.close()
