@@ -593,7 +593,13 @@ __global__ void __launch_bounds__(NT, MINB)
       }
       if (!solid && active) {
         const NodeMoments<C> m = node_at<L, TM, C>(tb + (ly + 1) * TX + lx, TC);
-        push_tile<L, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, m, om1);
+        // the per-direction wall tests only for nodes on a wall face (whole
+        // rows or planes: a warp-uniform branch); every other node pushes
+        // without them
+        if (WALLS && ZC == 0 && (ct.xlo || ct.xhi || ct.ylo || ct.yhi || ct.zlo || ct.zhi))
+          push_tile<L, T, C, WALLS, SOLID, ZC>(d, rg, R, lx, ly, ct, m, om1);
+        else
+          push_tile<L, T, C, false, SOLID, ZC>(d, rg, R, lx, ly, ct, m, om1);
       }
       if (hnode >= 0 && !hsolid) {
         const NodeMoments<C> hm = hfetch ? staged_at<L, TM, C>(wstg + buf * WSTG_B + hoff, WH, hsel)
