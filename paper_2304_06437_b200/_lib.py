@@ -97,6 +97,8 @@ def load(path: str | None = None) -> C.CDLL:
         "tslb_cuda_attach_nccl": ([H, vp, i, i], i),
         "tslb_cuda_link_local": ([vp, i], i),
         "tslb_cuda_group_step": ([vp, i, l], i),
+        "tslb_cuda_ipc_handle": ([H, vp], i),
+        "tslb_cuda_attach_ipc": ([H, vp, vp], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)

@@ -182,7 +182,17 @@ struct tslb_cuda_sim {
   size_t pool_used = 0;
   int64_t launches = 0;
   // exchange
-  int xmode = 0;  // 0 none, 1 nccl, 2 local
+  int xmode = 0;  // 0 none, 1 nccl, 2 local, 3 peer memory (CUDA IPC)
+  // peer-memory transport (xmode 3, M steps): the exported block holds two
+  // flag words (exchange numbers from below / from above) and the ghost
+  // planes [2][NM][plane] twice (exchange parity); the neighbours' blocks
+  // are mapped (or, for a face that wraps onto this rank, the own block)
+  char* ipc_blk = nullptr;
+  size_t ipc_gb = 0;
+  char* ipc_up = nullptr;
+  char* ipc_down = nullptr;
+  bool ipc_up_mapped = false, ipc_down_mapped = false;
+  uint64_t xcount = 0;  // exchanges issued
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1, up = -1, down = -1;
   tslb_cuda_sim* up_peer = nullptr;
@@ -438,6 +448,47 @@ int exchange_moments_local(tslb_cuda_sim* h, cudaStream_t st) {
   return 0;
 }
 
+// peer-memory transport: the new boundary planes of the moment buffer `buf`
+// straight into the neighbours' ghost buffers of this exchange's parity (one
+// strided 2-D copy per face, over NVLink between GPUs), then the exchange
+// number into their flag words. Double buffering by parity makes the flags
+// the only synchronisation: a neighbour can only write parity p again after
+// it has received this rank's next exchange, which is issued after this
+// rank's reads of parity p (stream order).
+constexpr size_t kIpcFlags = 256;
+int exchange_moments_ipc(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
+  const uint64_t e = ++h->xcount;
+  const size_t par = size_t(e & 1) * h->ipc_gb;
+  const size_t pb = size_t(h->plane()) * h->esz, blk = moment_plane_block(h);
+  const int nm = 1 + h->dim + h->np;
+  const size_t spitch = size_t(h->d.mstride) * h->esz;
+  const char* src = static_cast<const char*>(buf);
+  Prof p(h, TSLB_K_EXCHANGE, st);
+  if (h->ipc_up)  // top plane -> the up neighbour's "below" ghost planes
+    CK(cudaMemcpy2DAsync(h->ipc_up + kIpcFlags + par, pb, src + size_t(h->nzl - 1) * pb, spitch, pb, size_t(nm),
+                         cudaMemcpyDeviceToDevice, st));
+  if (h->ipc_down)  // bottom plane -> the down neighbour's "above" ghost planes
+    CK(cudaMemcpy2DAsync(h->ipc_down + kIpcFlags + par + blk, pb, src, spitch, pb, size_t(nm),
+                         cudaMemcpyDeviceToDevice, st));
+  ++h->launches;
+  if (launch_ipc_signal(h->ipc_up ? reinterpret_cast<uint64_t*>(h->ipc_up) : nullptr,
+                        h->ipc_down ? reinterpret_cast<uint64_t*>(h->ipc_down) + 1 : nullptr, e, st))
+    return set_err(TSLB_ECUDA, "k_ipc_signal launch failed");
+  return 0;
+}
+
+// before the ghost planes of the current moments are read on `st`: wait for
+// the neighbours' latest exchange and point gm at its parity
+int ipc_ghosts(tslb_cuda_sim* h, cudaStream_t st) {
+  if (h->xmode != 3 || h->xcount == 0) return 0;
+  const uint64_t* fl = reinterpret_cast<const uint64_t*>(h->ipc_blk);
+  ++h->launches;
+  if (launch_ipc_wait(h->ipc_down ? fl : nullptr, h->ipc_up ? fl + 1 : nullptr, h->xcount, st))
+    return set_err(TSLB_ECUDA, "k_ipc_wait launch failed");
+  h->gm = h->ipc_blk + kIpcFlags + size_t(h->xcount & 1) * h->ipc_gb;
+  return 0;
+}
+
 // the first step's moments pass: precomputed by the M initialiser, or from f
 int first_moments(tslb_cuda_sim* h, cudaStream_t st) {
   h->m16_valid = false;
@@ -462,6 +513,7 @@ int materialize(tslb_cuda_sim* h) {
   h->fimplicit = false;
   if (int rc = ph_streamcoll(h, 0, h->nzl, h->s)) return rc;
   if (!h->decomposed) return 0;
+  if (int rc = ipc_ghosts(h, h->s)) return rc;
   return by_scalar(h, [&](auto z) {
     using T = decltype(z);
     for (int side = 0; side < 2; ++side) {
@@ -722,6 +774,8 @@ int ph_cg_streamcoll_range(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
 
 // One fused step (fused_step / two_fluid_step) enqueued on h->s.
 int enqueue_step(tslb_cuda_sim* h) {
+  if (h->xmode == 3 && !(h->comps == 1 && h->sched == TSLB_SCHED_M && !h->store16))
+    return set_err(TSLB_ESTATE, "peer-memory (IPC) slab transport: single-fluid M steps only");
   int rc;
   if (h->comps == 2 && h->xmode == 1 && nci_on(h)) {
     // two-fluid slab with the near-contact scan: colour moments, phi's
@@ -822,9 +876,11 @@ int enqueue_step(tslb_cuda_sim* h) {
       if (h->xmode == 1) {
         if ((rc = pack_moments(h, h->mo, h->s))) return rc;
         if ((rc = exchange_moments_nccl(h, h->s))) return rc;
+      } else if (h->xmode == 3) {
+        if ((rc = exchange_moments_ipc(h, h->mo, h->s))) return rc;
       }
       h->fimplicit = true;
-    } else if (h->xmode == 1) {
+    } else if (h->xmode == 1 || h->xmode == 3) {
       // slab: the two thin boundary chunks run on the (high-priority) comm
       // stream and write the new boundary planes into the send buffer; the
       // exchange follows them there, while the interior chunk runs on the
@@ -832,17 +888,22 @@ int enqueue_step(tslb_cuda_sim* h) {
       // previous step is complete on both streams; the solver stream joins
       // the exchange before the next step.
       const int b = boundary_planes(h);
+      auto exchange = [&](cudaStream_t st) {
+        if (h->xmode == 3) return exchange_moments_ipc(h, h->mo2, st);
+        if (int r = pack_moments(h, h->mo2, st)) return r;
+        return exchange_moments_nccl(h, st);
+      };
       if (h->nzl <= 2 * b) {
+        if ((rc = ipc_ghosts(h, h->s))) return rc;
         if ((rc = ph_mstep(h, h->s))) return rc;
-        if ((rc = pack_moments(h, h->mo2, h->s))) return rc;
-        if ((rc = exchange_moments_nccl(h, h->s))) return rc;
+        if ((rc = exchange(h->s))) return rc;
       } else {
         CK(cudaEventRecord(h->ev_b, h->s));
         CK(cudaStreamWaitEvent(h->cs, h->ev_b, 0));
+        if ((rc = ipc_ghosts(h, h->cs))) return rc;
         if ((rc = ph_mstep(h, h->cs, 0, b))) return rc;
         if ((rc = ph_mstep(h, h->cs, h->nzl - b, h->nzl))) return rc;
-        if ((rc = pack_moments(h, h->mo2, h->cs))) return rc;
-        if ((rc = exchange_moments_nccl(h, h->cs))) return rc;
+        if ((rc = exchange(h->cs))) return rc;
         CK(cudaEventRecord(h->ev_c, h->cs));
         if ((rc = ph_mstep(h, h->s, b, h->nzl - b))) return rc;
         CK(cudaStreamWaitEvent(h->s, h->ev_c, 0));
@@ -1237,6 +1298,12 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   if (h->s) cudaStreamSynchronize(h->s);
   if (h->cs) cudaStreamSynchronize(h->cs);
   if (h->comm && nccl().CommDestroy) nccl().CommDestroy(h->comm);
+  if (h->ipc_up_mapped) cudaIpcCloseMemHandle(h->ipc_up);
+  if (h->ipc_down_mapped && h->ipc_down != h->ipc_up) cudaIpcCloseMemHandle(h->ipc_down);
+  if (h->ipc_blk) {
+    cudaFree(h->ipc_blk);
+    h->gm = nullptr;  // (it pointed into the block)
+  }
   void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->sx, h->phig, h->two,
                   h->flagg ? h->flagg : h->flag, h->rflag, h->solid, h->slow,
                   h->sbits, h->scratch, h->state_buf, h->mh, h->mh2, h->red, h->dig, h->recv_lo, h->recv_hi};
@@ -2062,6 +2129,83 @@ int tslb_cuda_attach_nccl(tslb_cuda_handle h, const void* id128, int nranks,
   h->up = h->d.mode[ZMax] == kGhost ? (rank + 1) % nranks : -1;
   h->down = h->d.mode[ZMin] == kGhost ? (rank - 1 + nranks) % nranks : -1;
   h->xmode = 1;
+  return 0;
+}
+
+// peer-memory transport (CUDA IPC): export this slab's block of flag words
+// and ghost planes ...
+static int ipc_block(tslb_cuda_sim* h) {
+  if (h->ipc_blk) return 0;
+  const size_t gb = size_t(h->plane()) * 2 * (1 + h->dim + h->np) * h->esz;
+  void* p = nullptr;
+  if (cudaMalloc(&p, kIpcFlags + 2 * gb) != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(TSLB_ENOMEM, "peer-memory transport block (%zu bytes)", kIpcFlags + 2 * gb);
+  }
+  CK(cudaMemset(p, 0, kIpcFlags + 2 * gb));
+  h->ipc_blk = static_cast<char*>(p);
+  h->ipc_gb = gb;
+  h->bytes += kIpcFlags + 2 * gb;
+  return 0;
+}
+
+int tslb_cuda_ipc_handle(tslb_cuda_handle h, void* handle64) {
+  if (!handle64) return set_err(TSLB_EINVAL, "ipc_handle: null output");
+  if (!h->decomposed || h->comps != 1) return set_err(TSLB_ESTATE, "ipc_handle needs a single-fluid slab solver");
+  CK(cudaSetDevice(h->device));
+  if (int rc = ipc_block(h)) return rc;
+  cudaIpcMemHandle_t hd;
+  CK(cudaIpcGetMemHandle(&hd, h->ipc_blk));
+  static_assert(sizeof hd == TSLB_IPC_HANDLE_BYTES, "cudaIpcMemHandle_t size");
+  std::memcpy(handle64, &hd, sizeof hd);
+  return 0;
+}
+
+// ... and map the neighbours' (a face whose neighbour is this rank itself --
+// one rank, periodic -- uses the own block)
+int tslb_cuda_attach_ipc(tslb_cuda_handle h, const void* below64, const void* above64) {
+  if (!h->decomposed || h->comps != 1) return set_err(TSLB_ESTATE, "attach_ipc needs a single-fluid slab solver");
+  if (h->xmode != 0) return set_err(TSLB_ESTATE, "attach_ipc: the slab already has a transport");
+  const bool has_dn = h->d.mode[ZMin] == kGhost, has_up = h->d.mode[ZMax] == kGhost;
+  if ((has_dn && !below64) || (has_up && !above64)) return set_err(TSLB_EINVAL, "attach_ipc: missing neighbour handle");
+  CK(cudaSetDevice(h->device));
+  if (int rc = ipc_block(h)) return rc;
+  cudaIpcMemHandle_t own;
+  CK(cudaIpcGetMemHandle(&own, h->ipc_blk));
+  auto open = [&](const void* hb, char*& ptr, bool& mapped) -> int {
+    if (std::memcmp(hb, &own, sizeof own) == 0) {
+      ptr = h->ipc_blk;
+      return 0;
+    }
+    cudaIpcMemHandle_t hd;
+    std::memcpy(&hd, hb, sizeof hd);
+    void* p = nullptr;
+    const cudaError_t e = cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(TSLB_ECUDA, "cudaIpcOpenMemHandle: %s", cudaGetErrorString(e));
+    }
+    ptr = static_cast<char*>(p);
+    mapped = true;
+    return 0;
+  };
+  if (has_up)
+    if (int rc = open(above64, h->ipc_up, h->ipc_up_mapped)) return rc;
+  if (has_dn) {
+    if (has_up && std::memcmp(below64, above64, sizeof own) == 0) {
+      h->ipc_down = h->ipc_up;  // (two ranks: the same neighbour on both faces)
+    } else if (int rc = open(below64, h->ipc_down, h->ipc_down_mapped)) {
+      return rc;
+    }
+  }
+  // the ghost planes now live in the exported block
+  if (h->gm) {
+    CK(cudaFree(h->gm));
+    h->bytes -= h->ipc_gb;
+  }
+  h->gm = h->ipc_blk + kIpcFlags;
+  h->xcount = 0;
+  h->xmode = 3;
   return 0;
 }
 

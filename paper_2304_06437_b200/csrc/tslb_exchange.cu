@@ -69,4 +69,52 @@ template int launch_unpack<double>(const Dom&, double*, const double*,
                                    const uint8_t*, int, const int*, const int*,
                                    const int*, int, int, cudaStream_t);
 
+// ---------------------------------------------------------------------------
+// Peer-memory halo transport (CUDA IPC, one process per GPU): after a rank
+// has copied its new boundary planes into a neighbour's ghost buffer, one
+// thread publishes the exchange number into the neighbour's flag word (a
+// system-scope release store behind a system fence); before the ghost planes
+// are read, one thread of the consumer's stream waits for the number with
+// acquire loads. A neighbour that never arrives traps after 60 s (a sticky
+// launch failure the host reports) instead of hanging the device.
+__device__ __forceinline__ void st_release_sys(uint64_t* p, uint64_t v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ uint64_t ld_acquire_sys(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void k_ipc_signal(uint64_t* a, uint64_t* b, uint64_t v) {
+  __threadfence_system();
+  if (a) st_release_sys(a, v);
+  if (b) st_release_sys(b, v);
+}
+
+__global__ void k_ipc_wait(const uint64_t* a, const uint64_t* b, uint64_t v) {
+  const uint64_t t0 = global_ns();
+  for (;;) {
+    const bool ok = (!a || ld_acquire_sys(a) >= v) && (!b || ld_acquire_sys(b) >= v);
+    if (ok) return;
+    if (global_ns() - t0 > 60ull * 1000000000ull) __trap();
+    __nanosleep(500);
+  }
+}
+
+int launch_ipc_signal(uint64_t* a, uint64_t* b, uint64_t v, cudaStream_t st) {
+  k_ipc_signal<<<1, 1, 0, st>>>(a, b, v);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
+int launch_ipc_wait(const uint64_t* a, const uint64_t* b, uint64_t v, cudaStream_t st) {
+  k_ipc_wait<<<1, 1, 0, st>>>(a, b, v);
+  return cudaGetLastError() == cudaSuccess ? 0 : 1;
+}
+
 }  // namespace tslb_cuda

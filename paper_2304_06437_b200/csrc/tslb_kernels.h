@@ -159,5 +159,9 @@ template <typename T>
 int launch_unpack(const Dom& d, T* f, const T* recv, const uint8_t* solid,
                   int ndirs, const int* a, const int* cx, const int* cy,
                   int kdst, int ksrc_ghost, cudaStream_t st);
+// peer-memory transport flags: publish / await an exchange number (null
+// words are skipped)
+int launch_ipc_signal(uint64_t* a, uint64_t* b, uint64_t v, cudaStream_t st);
+int launch_ipc_wait(const uint64_t* a, const uint64_t* b, uint64_t v, cudaStream_t st);
 
 }  // namespace tslb_cuda

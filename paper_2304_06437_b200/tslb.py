@@ -482,6 +482,27 @@ class DeviceSolver:
         (1 + D, n) of the storage dtype."""
         self._init_states("tslb_cuda_init_equilibrium", state, 1 + self.lat.dim)
 
+    # peer-memory slab transport (tslb_cuda_ipc_handle / tslb_cuda_attach_ipc)
+    IPC_HANDLE_BYTES = 64
+
+    def ipc_handle(self) -> bytes:
+        """This slab's CUDA IPC handle (ghost planes + flag words), to send
+        to the z neighbours' processes."""
+        buf = (C.c_char * self.IPC_HANDLE_BYTES)()
+        self._call("tslb_cuda_ipc_handle", buf)
+        return bytes(buf)
+
+    def attach_ipc(self, below: bytes | None, above: bytes | None):
+        """Map the neighbours' handles (None for a wall face); the slab then
+        steps with the peer-memory transport."""
+        def arg(b):
+            if b is None:
+                return None
+            if len(b) != self.IPC_HANDLE_BYTES:
+                raise _lib.InvalidArgument(f"attach_ipc: a handle is {self.IPC_HANDLE_BYTES} bytes")
+            return C.create_string_buffer(bytes(b), self.IPC_HANDLE_BYTES)
+        self._call("tslb_cuda_attach_ipc", arg(below), arg(above))
+
     def _init_states(self, fn, state, nm):
         name = fn[len("tslb_cuda_"):]
         if hasattr(state, "data_ptr"):  # a torch tensor (pinned host buffer)
