@@ -384,8 +384,11 @@ def _relaunch(n):
     """`bench.py --gpus N` outside torchrun: re-run this command as N ranks
     (one process per GPU) under torch.distributed.run and return its exit
     code; rank 0 prints the JSON line."""
+    # (torch.distributed.run's parser would take "--n" for an abbreviation of
+    # its own options even after the script path: pass it as "--cube")
+    argv = ["--cube" + a[3:] if a == "--n" or a.startswith("--n=") else a for a in sys.argv[1:]]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *sys.argv[1:]]
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__), *argv]
     env = dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1"))
     return subprocess.run(cmd, env=env).returncode
 
@@ -422,7 +425,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="tgv-d3q19", choices=sorted(WORKLOADS))
-    ap.add_argument("--n", type=int, default=0, help="override the per-GPU cube edge (3D)")
+    ap.add_argument("--n", "--cube", dest="n", type=int, default=0, help="override the per-GPU cube edge (3D)")
     ap.add_argument("--dims", default="", help="override the per-GPU extent nx,ny,nz (3D)")
     ap.add_argument("--math", default="f64", choices=["f64", "f32"])
     ap.add_argument("--schedule", default="auto", choices=["auto", "m", "f1"])
@@ -440,7 +443,15 @@ def main():
                     help="N=1 probe of the multi-GPU step: the GPU's domain is a z slab of a twice-as-tall box on "
                          "a one-rank NCCL communicator (its own up/down neighbour), so every step runs the "
                          "boundary chunks, the NCCL halo exchange on the comm stream and the overlapped interior")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "ipc"],
+                    help="slab halo transport for N > 1 (and the self-exchange probe): NCCL send/recv, or ipc -- "
+                         "the boundary planes copied straight into the neighbours' ghost buffers through CUDA IPC "
+                         "mappings (M single-fluid steps)")
+    ap.add_argument("--ipc-self", action="store_true",
+                    help="like --nccl-self, over the peer-memory transport (the slab's own handle on both faces)")
     args = ap.parse_args()
+    if args.ipc_self:
+        args.nccl_self, args.transport = True, "ipc"
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -464,7 +475,8 @@ def main():
         dims = (dims[0], dims[1], dims[2] // world)
     default = args.workload == "tgv-d3q19" and not args.nccl_self
     scaling = "strong" if strong else "weak"
-    metric = METRIC if default else f"GLUPS ({args.workload}{', NCCL self-exchange probe' if args.nccl_self else ''})"
+    probe = f", {'IPC' if args.transport == 'ipc' else 'NCCL'} self-exchange probe" if args.nccl_self else ""
+    metric = METRIC if default else f"GLUPS ({args.workload}{probe})"
 
     if args.impl == "reference":
         if rank != 0:
@@ -511,11 +523,20 @@ def main():
     from paper_2304_06437_b200 import tslb as T
 
     dist = None
+    # TSLB_BENCH_ONE_GPU=1 (functional checks of the N-rank path on a one-GPU
+    # box; timings meaningless): every rank on device 0, peer-memory transport
+    one_gpu = os.environ.get("TSLB_BENCH_ONE_GPU") == "1"
+    if one_gpu and args.transport != "ipc":
+        raise SystemExit("TSLB_BENCH_ONE_GPU needs --transport ipc (NCCL refuses two ranks on one device)")
+    dev_id = local if world > 1 and not one_gpu else 0
+    backend = "nccl" if args.transport == "nccl" else "gloo"  # (ipc: the process group is control plane only)
     if world > 1:
         import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    dev_id = local if world > 1 else 0
+        torch.cuda.set_device(dev_id)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_id))
+        else:
+            dist.init_process_group("gloo")
     torch.cuda.set_device(dev_id)
 
     lat = T.lattice_of(W["lat"])
@@ -549,7 +570,18 @@ def main():
         sim.set_body_force(8.0 * nu * W["umax"] / float(ny) ** 2, 0.0, 0.0)
     if "force" in W:
         sim.set_body_force(*W["force"])
-    if world > 1 or self_x:
+    if (world > 1 or self_x) and args.transport == "ipc":
+        # peer-memory transport: every rank's handle to every rank
+        own = sim.ipc_handle()
+        hs = [own]
+        if dist:
+            hs = [None] * world
+            dist.all_gather_object(hs, own)
+        zper = spec.faces[T.ZMin].kind == T.FaceKind.Periodic
+        below = hs[(rank - 1) % world] if (rank > 0 or zper) else None
+        above = hs[(rank + 1) % world] if (rank < world - 1 or zper) else None
+        sim.attach_ipc(below, above)
+    elif world > 1 or self_x:
         import ctypes as C
         uid = (C.c_char * 128)()
         if rank == 0:
@@ -587,7 +619,7 @@ def main():
     launches = sim.launch_count() - launches0
     clk = clocks.stop() if clocks else None
     if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda" if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     nodes = nx * ny * nzp * world  # (the self-exchange probe steps one slab)
@@ -697,8 +729,11 @@ def main():
                           **({"solid_fraction": round(float(solid.mean()), 4)} if masked else {}),
                           "node_math": (args.math if W["comps"] == 1 else W["storage"] + " (as the reference)"),
                           "l2": L2_NOTE if nodes > 10 ** 7 else "L2-resident (correctness config)",
-                          "parallelism": f"z-slab x{world}" if world > 1 else
-                          "one z slab on a 1-rank NCCL communicator (self halo exchange)" if self_x
+                          "parallelism": (f"z-slab x{world} ({'NCCL' if args.transport == 'nccl' else 'peer-memory'} "
+                                          f"halos{', all ranks on one device' if one_gpu else ''})") if world > 1 else
+                          ("one z slab on a 1-rank NCCL communicator (self halo exchange)" if args.transport == "nccl"
+                           else "one z slab exchanging with itself over the peer-memory (CUDA IPC) transport")
+                          if self_x
                           else "single GPU"},
                # (how this arm computes the workload; `config` is what both arms run)
                "schedule": ({"m": "M: moment-resident single pass (populations rebuilt in shared "
@@ -709,6 +744,10 @@ def main():
                             else "colour moments + gradient + fused prepare/stream-collide-recolour"),
                "roofline": roof, "gpu_launches": launches, "clocks": clk, "e2e": e2e, "cpu_baseline": cpu}
         print(json.dumps(out), file=out_stream)
+    # (a neighbour may still copy into this rank's buffers until every rank
+    # is done)
+    if dist:
+        dist.barrier()
     sim.close()
     if dist:
         dist.destroy_process_group()

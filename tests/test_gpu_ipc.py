@@ -115,3 +115,22 @@ def test_ipc_processes_equal_oracle(gpu, oracle_port, tmp_path, parts, faces, dt
     assert_bitwise(got["f_mid"], ref_mid, f"IPC x{parts} f({mid})")
     assert_bitwise(got["f"], ref, f"IPC x{parts} f({steps})")
     assert_bitwise(got["m"], rmo, f"IPC x{parts} moments")
+
+
+def test_bench_two_ranks_on_one_device_over_ipc(gpu, tmp_path):
+    """`bench.py --gpus 2 --transport ipc` end to end on a one-GPU box
+    (TSLB_BENCH_ONE_GPU=1: both ranks on device 0; the timing is meaningless,
+    the launch, handle exchange, peer-memory halos and max-over-ranks report
+    are the real N-rank path)."""
+    import json
+    root = os.path.dirname(HERE)
+    env = dict(os.environ, TSLB_BENCH_ONE_GPU="1")
+    env.pop("WORLD_SIZE", None)
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--transport", "ipc",
+                        "--n", "64", "--steps", "4", "--warmup", "3"], env=env, capture_output=True, text=True,
+                       timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert "peer-memory" in line["config"]["parallelism"]
+    assert line["roofline"]["launches_per_step"].get("exchange", 0) > 0
