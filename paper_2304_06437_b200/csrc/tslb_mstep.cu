@@ -80,7 +80,10 @@ void free_mstep_maps(MstepMaps* m) { delete m; }
 namespace mstep {
 
 constexpr int TX = 32;                     // tile width (one warp per row)
-constexpr int TY = 8;                      // tile rows (warps per CTA)
+#ifndef TSLB_TY
+#define TSLB_TY 8
+#endif
+constexpr int TY = TSLB_TY;                // tile rows (warps per CTA; -DTSLB_TY: measurements)
 constexpr int NT = TX * TY;                // threads = tile columns
 constexpr int NH = 2 * TX + 2 * (TY + 2);  // halo ring nodes (x columns include the corners)
 constexpr int TR = TY + 2;                 // staged tile rows (with y halo)
@@ -488,7 +491,7 @@ __global__ void __launch_bounds__(NT, MINB)
       hx = lx;
       hy = side == 0 ? -1 : th;
     }
-  } else if (lx < th + 2) {
+  } else if (side < 4 && lx < th + 2) {  // (warps beyond the eighth have no halo task)
     hnode = 2 * TX + (side - 2) * (TY + 2) + lx;
     hx = side == 2 ? -1 : tw;
     hy = lx - 1;
