@@ -215,9 +215,168 @@ __global__ void __launch_bounds__(32 * WPB)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Temporal blocking for small (latency-bound) domains: one cooperative launch
+// runs the whole step(n); each block owns 32 x 16 tiles and advances a tile
+// K passes at a time in shared memory from its moments plus a K-node halo
+// (the region shrinks by one ring per pass), so the grid barrier and the
+// trip through L2 come once per K passes instead of once per pass. Per pass:
+// (1) every node of the region rebuilds its 9 post-collision populations
+// (same forms as strip_pass, rounded to T); (2) every node whose sources are
+// still valid gathers f_a(x) = pc_a(x - c_a), or -- when x - c_a lies beyond a
+// wall -- the bounce of its own pc_opp(a) (the push x -> x + c_opp crosses that
+// wall, kernels.hpp:178-199), and reduces them to m(t+1) in compute_moments'
+// order. Regions of small periodic domains may hold a node twice; every copy
+// computes the same bits. Same per-node arithmetic as strip_pass: same bits.
+constexpr int TBX = 32, TBY = 16, TBT = 512;  // tile, threads per block
+template <int K>
+struct TbRegion {
+  static constexpr int W = TBX + 2 * K, H = TBY + 2 * K, N = W * H;
+};
+template <typename T, int K>
+constexpr size_t tb_smem() {
+  return size_t(6 + 9) * TbRegion<K>::N * sizeof(T);
+}
+
+template <class L, typename T, typename C, bool WALLS, int K>
+__global__ void __launch_bounds__(TBT, 1)
+    k_mstep2d_tb(Dom d, T* m0, T* m1, C om1, int ngroups, int nsteps, int ntx, int nty) {
+  using Lat = L;
+  using RG = TbRegion<K>;
+  constexpr int W = RG::W, H = RG::H, N = RG::N;
+  extern __shared__ __align__(16) unsigned char tb_raw[];
+  T* mom = reinterpret_cast<T*>(tb_raw);  // [6][N]
+  T* pc = mom + 6 * N;                    // [9][N]
+  cg::grid_group grid = cg::this_grid();
+  const int64_t ms = d.mstride;
+  const int tiles = ntx * nty;
+  // groups of passes: sizes differ by at most one, their count has the
+  // parity of nsteps (the result lands where the per-pass ping-pong would)
+  const T* src = m0;
+  T* dst = m1;
+  int left = nsteps;
+  for (int g = 0; g < ngroups; ++g) {
+    const int ks = (left + (ngroups - g) - 1) / (ngroups - g);
+    left -= ks;
+    for (int tile = int(blockIdx.x); tile < tiles; tile += int(gridDim.x)) {
+      const int ox = (tile % ntx) * TBX - K, oy = (tile / ntx) * TBY - K;  // region origin (global)
+      for (int e = int(threadIdx.x); e < N; e += TBT) {
+        const int gx = wrap_coord(ox + e % W, d.nx, d.mode[XMin], d.mode[XMax]);
+        const int gy = wrap_coord(oy + e / W, d.ny, d.mode[YMin], d.mode[YMax]);
+        if (gx < 0 || gy < 0) continue;  // beyond a wall: no node
+        const int64_t idx = gx + int64_t(d.nx) * gy;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) mom[c * N + e] = __ldcg(src + c * ms + idx);
+      }
+      __syncthreads();
+      for (int s = 0; s < ks; ++s) {
+        // (1) collide the ring [s, W - s) x [s, H - s)
+        {
+          const int w = W - 2 * s, cnt = w * (H - 2 * s);
+          for (int q = int(threadIdx.x); q < cnt; q += TBT) {
+            const int lx = s + q % w, ly = s + q / w, e = lx + W * ly;
+            if (wrap_coord(ox + lx, d.nx, d.mode[XMin], d.mode[XMax]) < 0 ||
+                wrap_coord(oy + ly, d.ny, d.mode[YMin], d.mode[YMax]) < 0)
+              continue;
+            T v[6];
+#pragma unroll
+            for (int c = 0; c < 6; ++c) v[c] = mom[c * N + e];
+            const NodeMoments<C> m = prep<T, C>(v);
+            unroll<9>([&](auto A) {
+              constexpr int a = decltype(A)::value;
+              if constexpr (a == 0) {
+                pc[e] = T(sf_post<Lat, 0, C>(m, om1));
+              } else if constexpr (a & 1) {
+                C ra, rb;
+                sf_pair<Lat, a, C>(m, om1, ra, rb);
+                pc[a * N + e] = T(ra);
+                pc[(a + 1) * N + e] = T(rb);
+              }
+            });
+          }
+        }
+        __syncthreads();
+        // (2) stream + moments on the ring [s + 1, W - s - 1) x [s + 1, H - s - 1)
+        {
+          const int w = W - 2 * (s + 1), cnt = w * (H - 2 * (s + 1));
+          for (int q = int(threadIdx.x); q < cnt; q += TBT) {
+            const int lx = s + 1 + q % w, ly = s + 1 + q / w, e = lx + W * ly;
+            const int gx = ox + lx, gy = oy + ly;
+            if (wrap_coord(gx, d.nx, d.mode[XMin], d.mode[XMax]) < 0 ||
+                wrap_coord(gy, d.ny, d.mode[YMin], d.mode[YMax]) < 0)
+              continue;
+            C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pxy = 0;
+            unroll<9>([&](auto A) {
+              constexpr int a = decltype(A)::value;
+              using dd = Dir<Lat, a>;
+              T fa;
+              if constexpr (a == 0) {
+                fa = pc[e];
+              } else {
+                // the source x - c_a; beyond a wall face it does not exist and
+                // the slot holds the bounce of x's own push along opp(a)
+                bool bx = false, by = false;
+                if constexpr (WALLS) {
+                  const int sx = gx - dd::x, sy = gy - dd::y;
+                  bx = dd::x != 0 && ((sx < 0 && d.mode[XMin] == kWall) || (sx >= d.nx && d.mode[XMax] == kWall));
+                  by = dd::y != 0 && ((sy < 0 && d.mode[YMin] == kWall) || (sy >= d.ny && d.mode[YMax] == kWall));
+                }
+                if (bx || by) {
+                  fa = bounce_value<Lat, dd::opp, T, C>(d, pc[dd::opp * N + e], bx, by, false);
+                } else {
+                  fa = pc[a * N + e - dd::x - W * dd::y];
+                }
+              }
+              const C f = C(fa);
+              r += f;
+              if constexpr (dd::x == 1) jx += f;
+              if constexpr (dd::x == -1) jx -= f;
+              if constexpr (dd::y == 1) jy += f;
+              if constexpr (dd::y == -1) jy -= f;
+              if constexpr (dd::x != 0) pxx += f;
+              if constexpr (dd::y != 0) pyy += f;
+              if constexpr (dd::x * dd::y == 1) pxy += f;
+              if constexpr (dd::x * dd::y == -1) pxy -= f;
+            });
+            force_shift<C>(d, jx, jy, jz);
+            const C c3 = cs2<C>();
+            mom[e] = T(r);
+            mom[N + e] = T(jx);
+            mom[2 * N + e] = T(jy);
+            mom[3 * N + e] = T(pxx - c3 * r - jx * jx);
+            mom[4 * N + e] = T(pyy - c3 * r - jy * jy);
+            mom[5 * N + e] = T(pxy - jx * jy);
+          }
+        }
+        __syncthreads();
+      }
+      // the owned tile (ring K) is exact after ks <= K passes
+      for (int q = int(threadIdx.x); q < TBX * TBY; q += TBT) {
+        const int lx = K + q % TBX, ly = K + q / TBX;
+        const int gx = ox + lx, gy = oy + ly;
+        if (gx >= d.nx || gy >= d.ny) continue;
+        const int64_t idx = gx + int64_t(d.nx) * gy;
+        const int e = lx + W * ly;
+#pragma unroll
+        for (int c = 0; c < 6; ++c) dst[c * ms + idx] = mom[c * N + e];
+      }
+      __syncthreads();
+    }
+    grid.sync();
+    const T* t = src;
+    src = dst;
+    dst = const_cast<T*>(t);
+  }
+}
+
 }  // namespace mstep2d
 
 namespace mstep2d {
+// passes per temporal block (TSLB_TB_K at build time: measurements)
+#ifndef TSLB_TB_K
+#define TSLB_TB_K 4
+#endif
+constexpr int kTbPasses = TSLB_TB_K;
 // rows per warp: 16 measured best at 4096^2 (72.8 GLUPS vs 67.5 at 64 and
 // 71.2 at 8: the two halo rows vs wave quantisation); small domains
 // (launch-bound, e.g. the 256^2 cavity) shorten strips for parallelism:
@@ -296,6 +455,52 @@ int launch_mstep2d_persist(int math, const Dom& d, T* m0, T* m1, double omega, i
     // failure is reported
     return e == cudaErrorCooperativeLaunchTooLarge ? 1 : -int(e);
   };
+  // temporal blocking (TSLB_TB2D=0: the per-pass persistent kernel; read per
+  // call, like TSLB_PERSIST)
+  const char* tbe = std::getenv("TSLB_TB2D");
+  const int tb_env = tbe ? std::atoi(tbe) : 1;
+  constexpr int K = kTbPasses;
+  const int ntx = (d.nx + TBX - 1) / TBX, nty = (d.ny + TBY - 1) / TBY;
+  auto go_tb = [&](auto kern, auto om1) {
+    const size_t smem = tb_smem<T, K>();
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess) {
+      cudaGetLastError();
+      return 1;
+    }
+    int per_sm = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, TBT, smem) != cudaSuccess || per_sm < 1) {
+      cudaGetLastError();
+      return 1;
+    }
+    const int blocks = std::min(ntx * nty, per_sm * sms);
+    // groups of <= K passes whose count has the parity of nsteps
+    int groups = (nsteps + K - 1) / K;
+    if ((groups - nsteps) % 2 != 0) ++groups;
+    Dom dd = d;
+    T *a = m0, *b = m1;
+    int gg = groups, ns = nsteps, x = ntx, y = nty;
+    void* args[] = {&dd, &a, &b, &om1, &gg, &ns, &x, &y};
+    if (const cudaError_t pe = cudaPeekAtLastError(); pe != cudaSuccess) return -int(pe);
+    const cudaError_t e =
+        cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kern), dim3(blocks), dim3(TBT), args, smem, st);
+    if (e == cudaSuccess) return 0;
+    cudaGetLastError();
+    return e == cudaErrorCooperativeLaunchTooLarge ? 1 : -int(e);
+  };
+  // (regions reach at most K nodes past the padded tiles: one wrap suffices)
+  if (tb_env != 0 && nsteps >= 2 && d.nx >= TBX + K && d.ny >= TBY + K) {
+    int r;
+    if (math == kMathDouble) {
+      const double om1 = 1.0 - double(T(omega));
+      r = walls ? go_tb(k_mstep2d_tb<D2Q9, T, double, true, K>, om1)
+                : go_tb(k_mstep2d_tb<D2Q9, T, double, false, K>, om1);
+    } else {
+      const float om1 = 1.0f - float(omega);
+      r = walls ? go_tb(k_mstep2d_tb<D2Q9, T, float, true, K>, om1)
+                : go_tb(k_mstep2d_tb<D2Q9, T, float, false, K>, om1);
+    }
+    if (r <= 0) return r;
+  }
   if (math == kMathDouble) {
     const double om1 = 1.0 - double(T(omega));
     return walls ? go(k_mstep2d_persist<D2Q9, T, double, true>, om1)

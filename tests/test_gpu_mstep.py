@@ -804,3 +804,48 @@ def test_refresh_under_m_is_one_moment_pass(gpu, oracle_port, lat, dims):
         assert_bitwise(dev.download_f(), ref, "f after refresh, moment upload, steps")
     finally:
         dev.close()
+
+
+TB_CASES = [
+    ("lid-256", (256, 256, 1), O.lid_cavity(0.1), None),
+    ("periodic-odd", (100, 70, 1), O.periodic(), None),
+    ("lid-odd", (61, 45, 1), O.lid_cavity(0.05), None),
+    ("ywalls-forced", (96, 40, 1), [("periodic", (0, 0, 0))] * 2 + [("wall", (0, 0, 0))] * 2
+     + [("periodic", (0, 0, 0))] * 2, (2e-5, 0.0, 0.0)),
+]
+
+
+@pytest.mark.parametrize("dtype", DT)
+@pytest.mark.parametrize("nsteps", [2, 5, 9, 33])
+@pytest.mark.parametrize("name,dims,faces,force", TB_CASES, ids=[c[0] for c in TB_CASES])
+def test_mstep2d_temporal_blocking_bitwise(gpu, oracle_port, name, dims, faces, force, nsteps, dtype, monkeypatch):
+    """The persistent 2-D path's temporal blocking (tiles advanced up to K
+    passes in shared memory between grid barriers; group count of the
+    parity of the pass count) == fused_step, bit for bit: walls and the
+    moving lid (bounces gathered from the node's own opposite push),
+    periodic wrap, partial tiles, the body force."""
+    f0 = O.random_state("d2q9", dims, 13, dtype)
+    monkeypatch.setenv("TSLB_PERSIST", "1")
+    monkeypatch.setenv("TSLB_TB2D", "1")
+    dev = T.DeviceSolver("d2q9", T.GridDims(*dims), 1.37, spec_of(faces), dtype)
+    try:
+        if force:
+            dev.set_body_force(*force)
+        dev.upload_f(f0)
+        l0 = dev.launch_count()
+        dev.step(nsteps + 1)  # (the moments pass after the upload, then one launch)
+        assert dev.launch_count() - l0 <= 3
+        mg = _moments(dev, "d2q9")
+        fg = dev.download_f()
+    finally:
+        dev.close()
+    fo = f0.copy()
+    mo = np.zeros((6, fo.shape[1]), dtype)
+    if force:
+        oracle_port.set_body_force(*force)
+    try:
+        oracle_port.single_run("d2q9", dims, 1.37, faces, fo, mo, nsteps + 1, 0)
+    finally:
+        oracle_port.set_body_force(0.0, 0.0, 0.0)
+    assert_bitwise(mg, mo, f"TB {name} moments")
+    assert_bitwise(fg, fo, f"TB {name} f")
