@@ -1301,8 +1301,9 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
   if (h->ipc_up_mapped) cudaIpcCloseMemHandle(h->ipc_up);
   if (h->ipc_down_mapped && h->ipc_down != h->ipc_up) cudaIpcCloseMemHandle(h->ipc_down);
   if (h->ipc_blk) {
+    const char* g = static_cast<const char*>(h->gm);
+    if (g >= h->ipc_blk && g < h->ipc_blk + kIpcFlags + 2 * h->ipc_gb) h->gm = nullptr;  // (inside the block)
     cudaFree(h->ipc_blk);
-    h->gm = nullptr;  // (it pointed into the block)
   }
   void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->sx, h->phig, h->two,
                   h->flagg ? h->flagg : h->flag, h->rflag, h->solid, h->slow,
