@@ -98,12 +98,13 @@ def run_ranks(tmp_path, parts, lat, dims, dtype, steps, mid, faces):
 
 
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
-@pytest.mark.parametrize("parts,faces", [(2, "periodic"), (3, "periodic"), (2, "zwalls")])
-def test_ipc_processes_equal_oracle(gpu, oracle_port, tmp_path, parts, faces, dtype):
+@pytest.mark.parametrize("lat,parts,faces", [("d3q19", 2, "periodic"), ("d3q19", 3, "periodic"),
+                                             ("d3q19", 2, "zwalls"), ("d3q27", 2, "periodic")])
+def test_ipc_processes_equal_oracle(gpu, oracle_port, tmp_path, lat, parts, faces, dtype):
     """`parts` processes, one z slab each, stepping over the peer-memory
     transport == fused_step on the undivided domain, bit for bit (f at the
     mid-run materialisation, f and the moment arrays at the end)."""
-    lat, dims, steps, mid = "d3q19", (32, 16, 12), 6, 2
+    dims, steps, mid = (32, 16, 12), 6, 2
     got = run_ranks(tmp_path, parts, lat, dims, dtype, steps, mid, faces)
     fc = O.periodic() if faces == "periodic" else zwalls_3d()
     f0 = O.random_state(lat, dims, 91, dtype)

@@ -849,3 +849,26 @@ def test_mstep2d_temporal_blocking_bitwise(gpu, oracle_port, name, dims, faces, 
         oracle_port.set_body_force(0.0, 0.0, 0.0)
     assert_bitwise(mg, mo, f"TB {name} moments")
     assert_bitwise(fg, fo, f"TB {name} f")
+
+
+@pytest.mark.parametrize("dtype", DT)
+def test_mstep2d_temporal_blocking_f32_math_equals_per_pass(gpu, dtype, monkeypatch):
+    """fp32 node math (the fused forms every single-fluid kernel shares):
+    the temporally blocked persistent path == one grid barrier per pass,
+    bit for bit."""
+    dims, faces = (200, 120, 1), O.lid_cavity(0.08)
+    f0 = O.random_state("d2q9", dims, 3, dtype)
+    out = {}
+    monkeypatch.setenv("TSLB_PERSIST", "1")
+    for tb in ("1", "0"):
+        monkeypatch.setenv("TSLB_TB2D", tb)
+        dev = T.DeviceSolver("d2q9", T.GridDims(*dims), 1.51, spec_of(faces), dtype)
+        try:
+            dev.set_math(_lib.MATH_F32)
+            dev.upload_f(f0)
+            dev.step(23)
+            out[tb] = (_moments(dev, "d2q9"), dev.download_f())
+        finally:
+            dev.close()
+    assert_bitwise(out["1"][0], out["0"][0], "TB f32 math moments")
+    assert_bitwise(out["1"][1], out["0"][1], "TB f32 math f")
