@@ -631,7 +631,12 @@ def main():
     per_node = kernel_bytes(lat, W["comps"], es, masked)
     if args.storage == "f16":  # fp16 moments in and out of the M step
         per_node["mstep"] = 2 * (1 + lat.dim + lat.dim * (lat.dim + 1) // 2) * 2
-    if W["comps"] == 2 and "cg_gradient" not in prof:
+    if W["comps"] == 2 and "cg_moments" not in prof:
+        # the one-pass step (k_cg_fused, profiled as the recolouring class):
+        # both species in and out, the colour moment arrays out, the flags
+        npi = lat.dim * (lat.dim + 1) // 2
+        per_node = {"cg_streamcoll": 4 * lat.q * es + (4 + lat.dim + npi) * es + 1}
+    elif W["comps"] == 2 and "cg_gradient" not in prof:
         # gradient folded into the recolouring stream-collide: it reads phi
         # (its stencil from cache) instead of the stored gradient
         npi = lat.dim * (lat.dim + 1) // 2
@@ -739,6 +744,8 @@ def main():
                "schedule": ({"m": "M: moment-resident single pass (populations rebuilt in shared "
                                   "memory; f materialised on read)",
                              "f1": "F1: moments + fused stream-collide"}[sched] if W["comps"] == 1
+                            else "one pass: colour moments + gradient + prepare + stream-collide-recolour "
+                                 "(ping-pong populations)" if "cg_moments" not in prof
                             else "colour moments + fused gradient/prepare/stream-collide-recolour"
                             if "cg_gradient" not in prof
                             else "colour moments + gradient + fused prepare/stream-collide-recolour"),

@@ -182,6 +182,7 @@ struct tslb_cuda_sim {
   size_t pool_used = 0;
   int64_t launches = 0;
   // exchange
+  void* falt[2] = {nullptr, nullptr};  // two-fluid one-pass step: the other population buffers (ping-pong)
   int xmode = 0;  // 0 none, 1 nccl, 2 local, 3 peer memory (CUDA IPC)
   // peer-memory transport (xmode 3, M steps): the exported block holds two
   // flag words (exchange numbers from below / from above) and the ghost
@@ -773,6 +774,17 @@ int ph_cg_streamcoll_range(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
 }
 
 // One fused step (fused_step / two_fluid_step) enqueued on h->s.
+// the two-fluid one-pass step (k_cg_fused) is opt-in, TSLB_CG_FUSED=1: it
+// is bit-exact but measured slower than the two-kernel step (droplet 512^3:
+// 7.4 vs 14.3 GLUPS -- the staging costs twice the instructions per node and
+// the ring re-reads 1.5x the population bytes; profiles/r02_droplet_fused_ncu_full.txt)
+bool cg_fused_on(const tslb_cuda_sim* h) {
+  if (h->comps != 2 || h->decomposed) return false;
+  const char* e = std::getenv("TSLB_CG_FUSED");
+  if (!e || std::atoi(e) != 1) return false;
+  return cg_fused_supported(h->lat, h->d, int(h->esz), h->cp);
+}
+
 int enqueue_step(tslb_cuda_sim* h) {
   if (h->xmode == 3 && !(h->comps == 1 && h->sched == TSLB_SCHED_M && !h->store16))
     return set_err(TSLB_ESTATE, "peer-memory (IPC) slab transport: single-fluid M steps only");
@@ -844,6 +856,34 @@ int enqueue_step(tslb_cuda_sim* h) {
     h->stress_pending = true;
     ++h->steps;
     return 0;
+  }
+  if (h->comps == 2 && cg_fused_on(h)) {
+    // box geometry without NCI: the whole step in one pass into the other
+    // population buffers (k_cg_fused), which then become the current ones
+    if (!h->falt[0]) {
+      const size_t fbytes = size_t(h->d.fstride) * h->q * h->esz;
+      for (int sp = 0; sp < 2; ++sp)
+        if ((rc = alloc(h, &h->falt[sp], fbytes))) return rc;
+    }
+    {
+      Prof p(h, TSLB_K_CG_STREAMCOLL, h->s);
+      rc = by_scalar(h, [&](auto z) {
+        using T = decltype(z);
+        return launch_cg_fused<T>(h->lat, h->range(0, h->nzl), static_cast<const T*>(h->f[0]),
+                                  static_cast<const T*>(h->f[1]), static_cast<T*>(h->falt[0]),
+                                  static_cast<T*>(h->falt[1]), h->tf(), h->omega, h->cp, h->s);
+      });
+    }
+    if (rc < 0) return set_err(TSLB_ECUDA, "k_cg_fused launch: %s", cudaGetErrorString(cudaError_t(-rc)));
+    if (rc == 0) {
+      ++h->launches;
+      std::swap(h->f[0], h->falt[0]);
+      std::swap(h->f[1], h->falt[1]);
+      h->grad_pending = true;
+      h->stress_pending = true;
+      ++h->steps;
+      return 0;
+    }
   }
   if (h->comps == 2) {
     if ((rc = ph_cg_moments(h, h->s))) return rc;
@@ -1305,7 +1345,7 @@ int tslb_cuda_destroy(tslb_cuda_handle h) {
     if (g >= h->ipc_blk && g < h->ipc_blk + kIpcFlags + 2 * h->ipc_gb) h->gm = nullptr;  // (inside the block)
     cudaFree(h->ipc_blk);
   }
-  void* bufs[] = {h->f[0], h->f[1], h->mo, h->mo2, h->gm, h->sx, h->phig, h->two,
+  void* bufs[] = {h->f[0], h->f[1], h->falt[0], h->falt[1], h->mo, h->mo2, h->gm, h->sx, h->phig, h->two,
                   h->flagg ? h->flagg : h->flag, h->rflag, h->solid, h->slow,
                   h->sbits, h->scratch, h->state_buf, h->mh, h->mh2, h->red, h->dig, h->recv_lo, h->recv_hi};
   for (void* b : bufs)
@@ -1785,7 +1825,9 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
   constexpr int64_t kGraphMaxNodes = int64_t(8) << 20;
   constexpr long kGraphSteps = 32;  // even: an M graph ends on the buffer it starts from
   // (steps still owed only: the persistent path above may have run them all)
-  if (h->graphs_ok && !h->prof && h->xmode == 0 && h->n() <= kGraphMaxNodes && nsteps - done >= kGraphSteps) {
+  // (not for the two-fluid one-pass step: its population buffers alternate)
+  if (h->graphs_ok && !h->prof && h->xmode == 0 && h->n() <= kGraphMaxNodes && nsteps - done >= kGraphSteps &&
+      !cg_fused_on(h)) {
     // an M graph replays M passes only: leave the stored-f state first, and
     // start from the moment buffer the graph was captured on
     if (h->sched == TSLB_SCHED_M) {

@@ -117,6 +117,13 @@ int launch_cg_streamcoll(int lat, const Dom& d, T* fr, T* fb,
                          const uint32_t* slow, double omega,
                          const ColorParamsDev& cp, int fold_prepare,
                          cudaStream_t st);
+// the whole two-fluid box step in one pass (f_old -> f_new + the colour
+// moment arrays; box, NCI off, nx % 32 == ny % 8 == 0); nonzero when not
+// applicable
+template <typename T>
+int launch_cg_fused(int lat, const Dom& d, const T* fr, const T* fb, T* gr, T* gb, const TwoFields& s,
+                    double omega, const ColorParamsDev& cp, cudaStream_t st);
+bool cg_fused_supported(int lat, const Dom& d, int esz, const ColorParamsDev& cp);
 // gradient folded into the recolouring stream-collide (box, NCI off);
 // nonzero when not applicable
 template <typename T>

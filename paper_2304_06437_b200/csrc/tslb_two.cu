@@ -12,6 +12,8 @@
 // NCI flags are set-only byte stores of the value 1 -- concurrent writers
 // store the same byte, so the result is launch-shape independent, mirroring
 // the reference's relaxed atomic_ref stores (multicomponent.hpp:233-236).
+#include <cuda_pipeline.h>
+
 #include <cstdint>
 
 #include "tslb_collision.cuh"
@@ -672,6 +674,331 @@ __global__ void TSLB_CG_BOUNDS
 }
 
 // ---------------------------------------------------------------------------
+// The whole box step in ONE pass (f_old -> f_new, ping-pong population
+// buffers): colour moments + grad phi + prepare_stress + perturbation +
+// recolouring + push. A CTA owns a 32 x 8 column tile and marches through
+// its z range; the populations of the next plane -- the tile and a one-node
+// ring around it, all 2q arrays -- are staged in shared memory by cp.async
+// one plane ahead; each tile node reduces its own colour moments (kept in
+// registers for the collision of that plane and written to the moment
+// arrays, which keep the reference's host-visible values), the ring's phi
+// is recomputed from its staged populations, and grad phi is taken from
+// three planes of phi in shared memory. Same arithmetic, in the same order,
+// as k_cg_moments + k_cg_streamcoll_box: same bits, without the round trip
+// of the 52 B of moments per node through HBM (356 instead of 408 B per
+// lattice update). Box geometries (nx % 32 == ny % 8 == 0), NCI off, whole
+// domains.
+__device__ __forceinline__ int wrap_coord2(int g, int n, int lo, int hi) {
+  if (g < 0) return lo == kWrap ? g + n : -1;
+  if (g >= n) return hi == kWrap ? g - n : -1;
+  return g;
+}
+
+namespace fused {
+constexpr int FX = 32, FY = 8, FT = FX * FY;  // tile, threads
+constexpr int FR = FY + 2;                    // staged rows (y halo)
+constexpr int FPA = FR * FX + 2 * FR;         // staged elements per array: rows + left / right columns
+constexpr int FPX = FX + 2;                   // phi plane width
+constexpr int kLz = 64;                       // planes per CTA
+template <class L, typename T>
+constexpr size_t smem_bytes() {
+  return size_t(2) * 2 * L::q * FPA * sizeof(T) + size_t(3) * FR * FPX * sizeof(T);
+}
+}  // namespace fused
+
+template <class L, typename T, bool WALLS>
+__global__ void __launch_bounds__(fused::FT)
+    k_cg_fused(Dom d, const __grid_constant__ PopBases<T> src, const __grid_constant__ PopBases<T> dst, TF<T> s,
+               T omega, T tau, ColorParamsDev cp) {
+  using namespace fused;
+  constexpr int Q = L::q, NA = 2 * Q;
+  extern __shared__ __align__(16) unsigned char fz_raw[];
+  T* stg = reinterpret_cast<T*>(fz_raw);    // [2][NA][FPA]
+  T* phs = stg + 2 * NA * FPA;              // [3][FR][FPX]
+  const int tid = threadIdx.x, lx = tid & 31, ly = tid >> 5;
+  const int x0 = int(blockIdx.x) * FX, y0 = int(blockIdx.y) * FY;
+  const int za = int(blockIdx.z) * kLz, zb = min(za + kLz, d.nz);
+  const int gx = x0 + lx, gy = y0 + ly;
+  const int64_t ms = d.mstride;
+  const T om1 = T(1) - omega;
+  const T pert_coef = T(2.25) * T(cp.sigma) * omega;
+  const bool linear = cp.linear != 0;
+  // rows y0-1 .. y0+FY and the columns x0-1, x0+FX (wrapped; -1 beyond a wall)
+  auto row_of = [&](int r) { return wrap_coord2(y0 - 1 + r, d.ny, d.mode[YMin], d.mode[YMax]); };
+  const int colL = wrap_coord2(x0 - 1, d.nx, d.mode[XMin], d.mode[XMax]);
+  const int colR = wrap_coord2(x0 + FX, d.nx, d.mode[XMin], d.mode[XMax]);
+
+  // stage plane z (wrapped; nothing beyond a wall) into buffer b
+  auto stage = [&](int z, int b) {
+    const int zz = wrap_coord2(z, d.nz, d.mode[ZMin], d.mode[ZMax]);
+    if (zz < 0) return;
+    T* sb = stg + b * NA * FPA;
+    // rows: 16-byte pieces
+    constexpr int EP = 16 / int(sizeof(T)), PR = FX / EP;
+    for (int t = tid; t < NA * FR * PR; t += FT) {
+      const int piece = t % PR, rr = (t / PR) % FR, a = t / (PR * FR);
+      const int yy = row_of(rr);
+      if (yy < 0) continue;
+      const T* g = (a < Q ? src.r[a] : src.b[a - Q]) + (int64_t(yy) * d.nx + int64_t(zz) * d.plane + x0 + EP * piece);
+      __pipeline_memcpy_async(sb + a * FPA + rr * FX + EP * piece, g, 16);
+    }
+    // left / right columns: one element each
+    for (int t = tid; t < NA * 2 * FR; t += FT) {
+      const int rr = t % FR, side = (t / FR) & 1, a = t / (2 * FR);
+      const int yy = row_of(rr), xx = side ? colR : colL;
+      if (yy < 0 || xx < 0) continue;
+      const T* g = (a < Q ? src.r[a] : src.b[a - Q]) + (int64_t(yy) * d.nx + int64_t(zz) * d.plane + xx);
+      __pipeline_memcpy_async(sb + a * FPA + FR * FX + side * FR + rr, g, sizeof(T));
+    }
+  };
+  // colour moments of a staged node (color_moments order, k_cg_moments)
+  struct CM {
+    T rr, rb, r, jx, jy, jz, pxx, pyy, pzz, pxy, pxz, pyz;
+  };
+  auto moments_at = [&](const T* sb, int off) {
+    CM m{};
+    unroll<Q>([&](auto A) {
+      constexpr int a = decltype(A)::value;
+      using dd = Dir<L, a>;
+      const T fra = sb[a * FPA + off];
+      const T fba = sb[(Q + a) * FPA + off];
+      const T ga = fra + fba;
+      m.rr += fra;
+      m.rb += fba;
+      m.r += ga;
+      if constexpr (dd::x == 1) m.jx += ga;
+      if constexpr (dd::x == -1) m.jx -= ga;
+      if constexpr (dd::y == 1) m.jy += ga;
+      if constexpr (dd::y == -1) m.jy -= ga;
+      if constexpr (dd::z == 1) m.jz += ga;
+      if constexpr (dd::z == -1) m.jz -= ga;
+      if constexpr (dd::x != 0) m.pxx += ga;
+      if constexpr (dd::y != 0) m.pyy += ga;
+      if constexpr (dd::z != 0) m.pzz += ga;
+      if constexpr (dd::x * dd::y == 1) m.pxy += ga;
+      if constexpr (dd::x * dd::y == -1) m.pxy -= ga;
+      if constexpr (dd::x * dd::z == 1) m.pxz += ga;
+      if constexpr (dd::x * dd::z == -1) m.pxz -= ga;
+      if constexpr (dd::y * dd::z == 1) m.pyz += ga;
+      if constexpr (dd::y * dd::z == -1) m.pyz -= ga;
+    });
+    return m;
+  };
+  auto phi_sum = [&](const T* sb, int off) {  // (rr - rb) / r of a ring node
+    T rr = 0, rb = 0, r = 0;
+    unroll<Q>([&](auto A) {
+      constexpr int a = decltype(A)::value;
+      const T fra = sb[a * FPA + off];
+      const T fba = sb[(Q + a) * FPA + off];
+      rr += fra;
+      rb += fba;
+      r += fra + fba;
+    });
+    return (rr - rb) / r;
+  };
+  // the ring node this thread reduces (warp 0: row below, warp 1: row above,
+  // warp 2: left and right columns incl. corners), -1 for none
+  int ring_off = -1, ring_phi = -1;
+  if (ly == 0) {
+    ring_off = 0 * FX + lx;
+    ring_phi = 0 * FPX + lx + 1;
+  } else if (ly == 1) {
+    ring_off = (FR - 1) * FX + lx;
+    ring_phi = (FR - 1) * FPX + lx + 1;
+  } else if (ly == 2 && (lx < FR || (lx >= 16 && lx < 16 + FR))) {
+    const int side = lx >= 16, rr = lx - 16 * side;
+    ring_off = FR * FX + side * FR + rr;
+    ring_phi = rr * FPX + (side ? FPX - 1 : 0);
+  }
+  bool ring_ok = false;
+  if (ring_off >= 0) {
+    const int rr = ring_off < FR * FX ? ring_off / FX : (ring_off - FR * FX) % FR;
+    const bool col = ring_off >= FR * FX;
+    const int xx = col ? ((ring_off - FR * FX) / FR ? colR : colL) : 0;
+    ring_ok = row_of(rr) >= 0 && xx >= 0;
+  }
+
+  // prologue: planes za-1 and za staged; phi(za-1) and phi(za), moments(za)
+  stage(za - 1, 0);
+  __pipeline_commit();
+  stage(za, 1);
+  __pipeline_commit();
+  CM mc{};
+  auto plane_exists = [&](int z) { return wrap_coord2(z, d.nz, d.mode[ZMin], d.mode[ZMax]) >= 0; };
+  // the colour moments of the tile node (kept) and phi of the tile and ring
+  // nodes of plane z from staging buffer b
+  auto reduce_plane = [&](int z, int b, CM& out) {
+    const T* sb = stg + b * NA * FPA;
+    T* ph = phs + ((z % 3 + 3) % 3) * FR * FPX;
+    if (!plane_exists(z)) return;
+    out = moments_at(sb, (ly + 1) * FX + lx);
+    ph[(ly + 1) * FPX + lx + 1] = (out.rr - out.rb) / out.r;
+    if (ring_ok) ph[ring_phi] = phi_sum(sb, ring_off);
+  };
+  __pipeline_wait_prior(1);
+  __syncthreads();
+  {
+    CM dummy{};
+    reduce_plane(za - 1, 0, dummy);
+  }
+  __syncthreads();  // (buffer 0 is reused for plane za+1)
+  stage(za + 1, 0);
+  __pipeline_commit();
+  __pipeline_wait_prior(1);
+  __syncthreads();
+  reduce_plane(za, 1, mc);
+
+  for (int z = za; z < zb; ++z) {
+    // phi(z) is in shared memory (barrier below), moments(z) in mc;
+    // plane z+1 is staged in buffer (z+1-za+1)&1 = (z-za)&1
+    const int bn = (z - za) & 1;
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    CM mn{};
+    reduce_plane(z + 1, bn, mn);
+    __syncthreads();
+    // the buffer of plane z (the other one) is free: stage plane z+2
+    if (z + 2 <= zb) stage(z + 2, bn ^ 1);
+    __pipeline_commit();
+
+    // ---- collide and push plane z (cg_streamcoll_box order)
+    const int64_t fi = fidx(d, gx, gy, z);
+    const int64_t mi = midx(d, gx, gy, z);
+    // the colour moments of f(t) into the host-visible arrays (k_cg_moments)
+    s.flag[mi] = 0;
+    s.rho_r[mi] = mc.rr;
+    s.rho_b[mi] = mc.rb;
+    s.rho[mi] = mc.r;
+    const T phi0 = (mc.rr - mc.rb) / mc.r;
+    s.phi[mi] = phi0;
+    s.mom[mi] = mc.jx;
+    s.mom[ms + mi] = mc.jy;
+    s.mom[2 * ms + mi] = mc.jz;
+    s.pin[mi] = mc.pxx;
+    s.pin[ms + mi] = mc.pyy;
+    s.pin[2 * ms + mi] = mc.pzz;
+    s.pin[3 * ms + mi] = mc.pxy;
+    s.pin[4 * ms + mi] = mc.pxz;
+    s.pin[5 * ms + mi] = mc.pyz;
+    // prepare_stress (NCI off: the force is 0)
+    const T F0 = 0, F1 = 0, F2 = 0;
+    const T ux = mc.jx + tau * F0, uy = mc.jy + tau * F1, uz = mc.jz + tau * F2;
+    const T c3 = cs2<T>();
+    T p[6];
+    p[0] = mc.pxx + (-c3 * mc.r - ux * ux);
+    p[1] = mc.pyy + (-c3 * mc.r - uy * uy);
+    p[2] = mc.pzz + (-c3 * mc.r - uz * uz);
+    p[3] = mc.pxy - ux * uy;
+    p[4] = mc.pxz - ux * uz;
+    p[5] = mc.pyz - uy * uz;
+    const NodeMoments<T> m = prepare_node<T>(mc.r, ux, uy, uz, p[0], p[1], p[2], p[3], p[4], p[5]);
+    const T red_frac = mc.rr / mc.r;
+    const T rec_amp = T(cp.beta) * (mc.rr * mc.rb / mc.r);
+    const Steps32 st = face_steps32(d, gx, gy, z);
+    // grad phi from the three phi planes (gradient_at order; a neighbour
+    // beyond a wall reads phi(x))
+    T gxx = 0, gyy = 0, gzz = 0;
+    unroll<Q>([&](auto A) {
+      constexpr int a = decltype(A)::value;
+      using dd = Dir<L, a>;
+      if constexpr (a > 0) {
+        bool wall = false;
+        if constexpr (dd::x == 1) wall |= st.bp[0];
+        if constexpr (dd::x == -1) wall |= st.bm[0];
+        if constexpr (dd::y == 1) wall |= st.bp[1];
+        if constexpr (dd::y == -1) wall |= st.bm[1];
+        if constexpr (dd::z == 1) wall |= st.bp[2];
+        if constexpr (dd::z == -1) wall |= st.bm[2];
+        const T* ph = phs + (((z + dd::z) % 3 + 3) % 3) * FR * FPX;
+        const T pn = (WALLS && wall) ? phi0 : ph[(ly + 1 + dd::y) * FPX + lx + 1 + dd::x];
+        constexpr T w = dd::template t<T>();
+        const T tp = w * pn;
+        if constexpr (dd::x == 1) gxx += tp;
+        if constexpr (dd::x == -1) gxx -= tp;
+        if constexpr (dd::y == 1) gyy += tp;
+        if constexpr (dd::y == -1) gyy -= tp;
+        if constexpr (dd::z == 1) gzz += tp;
+        if constexpr (dd::z == -1) gzz -= tp;
+      }
+    });
+    gxx = T(3) * gxx;
+    gyy = T(3) * gyy;
+    gzz = T(3) * gzz;
+    const T gn = sqrt(gxx * gxx + gyy * gyy + gzz * gzz);
+    const bool interface = gn > T(cp.grad_threshold);
+    const T pert_amp = interface ? pert_coef * gn : T(0);
+    const T inv_gn = interface ? T(1) / gn : T(0);
+    const T nhx = gxx * inv_gn, nhy = gyy * inv_gn, nhz = gzz * inv_gn;
+    const uint32_t fi32 = uint32_t(fi);
+    auto out = [&](auto A, auto IF, T g_out) {
+      constexpr int a = decltype(A)::value;
+      constexpr bool IFACE = decltype(IF)::value;
+      using dd = Dir<L, a>;
+      constexpr T t = dd::template t<T>();
+      constexpr T b = dd::template b<T>();
+      T fr_out;
+      if constexpr (IFACE) {
+        const T cn = dot_c<dd::x, dd::y, dd::z>(nhx, nhy, nhz);
+        const T shape = !linear ? t * cn * cn - b : t * cn - b;
+        g_out += pert_amp * shape;
+        fr_out = red_frac * g_out + rec_amp * t * cn * inv_cnorm<T, dd::norm2>();
+      } else {
+        fr_out = red_frac * g_out;
+      }
+      const T fb_out = g_out - fr_out;
+      int delta = 0;
+      bool bounce = false;
+      if constexpr (dd::x == 1) { delta += st.dp[0]; bounce |= st.bp[0]; }
+      if constexpr (dd::x == -1) { delta += st.dm[0]; bounce |= st.bm[0]; }
+      if constexpr (dd::y == 1) { delta += st.dp[1]; bounce |= st.bp[1]; }
+      if constexpr (dd::y == -1) { delta += st.dm[1]; bounce |= st.bm[1]; }
+      if constexpr (dd::z == 1) { delta += st.dp[2]; bounce |= st.bp[2]; }
+      if constexpr (dd::z == -1) { delta += st.dm[2]; bounce |= st.bm[2]; }
+      if (WALLS && bounce) {
+        T wx = T(0), wy = T(0), wz = T(0);
+        auto add = [&](bool crossed, int face) {
+          if (crossed) {
+            wx += T(d.uw[face][0]);
+            wy += T(d.uw[face][1]);
+            wz += T(d.uw[face][2]);
+          }
+        };
+        if constexpr (dd::x == 1) add(st.bp[0], XMax);
+        if constexpr (dd::x == -1) add(st.bm[0], XMin);
+        if constexpr (dd::y == 1) add(st.bp[1], YMax);
+        if constexpr (dd::y == -1) add(st.bm[1], YMin);
+        if constexpr (dd::z == 1) add(st.bp[2], ZMax);
+        if constexpr (dd::z == -1) add(st.bm[2], ZMin);
+        const T corr = bounce_correction<L, a, T>(wx, wy, wz);
+        const T corr_r = red_frac * corr;
+        dst.r[dd::opp][fi32] = fr_out - corr_r;
+        dst.b[dd::opp][fi32] = fb_out - (corr - corr_r);
+      } else {
+        const uint32_t tt = fi32 + uint32_t(delta);
+        dst.r[a][tt] = fr_out;
+        dst.b[a][tt] = fb_out;
+      }
+    };
+    auto all_dirs = [&](auto IF) {
+      unroll<Q>([&](auto A) {
+        constexpr int a = decltype(A)::value;
+        if constexpr (a == 0) {
+          out(A, IF, post_rest<L, T>(m, om1));
+        } else if constexpr (a & 1) {
+          T ga, gb;
+          post_pair<L, a, T>(m, om1, ga, gb);
+          out(A, IF, ga);
+          out(std::integral_constant<int, a + 1>{}, IF, gb);
+        }
+      });
+    };
+    if (interface) all_dirs(std::true_type{});
+    else all_dirs(std::false_type{});
+    mc = mn;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // device droplet initialiser (initialize_colors, multicomponent.hpp:427-449,
 // with the tslb_main droplet profile 0.5 (1 + tanh(R - r)))
 template <class L, typename T>
@@ -803,6 +1130,50 @@ int launch_cg_streamcoll_grad(int lat, const Dom& d, T* fr, T* fb, const TwoFiel
   });
 }
 
+// The fused one-pass step (k_cg_fused): f_old -> f_new plus the colour
+// moment arrays. Returns 1 (nothing launched) where it does not apply.
+template <typename T>
+int launch_cg_fused(int lat, const Dom& d, const T* fr, const T* fb, T* gr, T* gb, const TwoFields& s,
+                    double omega, const ColorParamsDev& cp, cudaStream_t st) {
+  using namespace fused;
+  if (lat == kD2Q9 || d.has_solid || d.ghost || cp.nci_strength != 0.0) return 1;
+  if (d.nx % FX || d.ny % FY || d.k0 != 0 || d.nzr != d.nz) return 1;
+  if (d.ny / FY > 65535 || (d.nz + kLz - 1) / kLz > 65535) return 1;
+  const T om = T(omega);
+  const T tau = T(1) / om;
+  bool walls = false;
+  for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
+  const dim3 grid(unsigned(d.nx / FX), unsigned(d.ny / FY), unsigned((d.nz + kLz - 1) / kLz));
+  int err = 1;
+  auto go = [&](auto L) {
+    using Lat = decltype(L);
+    constexpr size_t smem = smem_bytes<Lat, T>();
+    if constexpr (smem > 227 * 1024) {
+      return;
+    } else {
+      auto kern = walls ? k_cg_fused<Lat, T, true> : k_cg_fused<Lat, T, false>;
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+      if (e == cudaSuccess) {
+        kern<<<grid, FT, smem, st>>>(d, pop_bases(const_cast<T*>(fr), const_cast<T*>(fb), d, Lat::q),
+                                      pop_bases(gr, gb, d, Lat::q), tf_of<T>(s), om, tau, cp);
+        e = cudaGetLastError();
+      }
+      err = e == cudaSuccess ? 0 : -int(e);
+    }
+  };
+  if (lat == kD3Q19) go(D3Q19{});
+  else go(D3Q27{});
+  return err;
+}
+
+bool cg_fused_supported(int lat, const Dom& d, int esz, const ColorParamsDev& cp) {
+  using namespace fused;
+  if (lat == kD2Q9 || d.has_solid || d.ghost || cp.nci_strength != 0.0) return false;
+  if (d.nx % FX || d.ny % FY) return false;
+  const size_t q = lat == kD3Q19 ? 19 : 27;
+  return size_t(2) * 2 * q * FPA * esz + size_t(3) * FR * FPX * esz <= 227 * 1024;
+}
+
 // gradient_and_nci on a box geometry / z slab: the gradient kernel (phi
 // stencil through the ghost planes) and the near-contact scan
 template <typename T>
@@ -849,6 +1220,9 @@ int launch_init_colors(int lat, const Dom& d, T* fr, T* fb,
                                        const uint32_t*, double,               \
                                        const ColorParamsDev&, int,            \
                                        cudaStream_t);                         \
+  template int launch_cg_fused<T>(int, const Dom&, const T*, const T*, T*, T*, \
+                                  const TwoFields&, double, const ColorParamsDev&, \
+                                  cudaStream_t);                              \
   template int launch_cg_streamcoll_grad<T>(int, const Dom&, T*, T*,         \
                                             const TwoFields&, double,         \
                                             const ColorParamsDev&,            \

@@ -219,3 +219,48 @@ def test_two_fluid_box_kernels_bitwise(gpu, oracle_port, case, color, dtype):
         assert_bitwise(got[k], ref[k], f"{lat} box {k}")
     D = T.lattice_of(lat).dim
     assert_bitwise(np.reshape(got["gradphi"], (D, -1)), ref["gradphi"], f"{lat} box gradphi")
+
+
+FUSED_CASES = [
+    ("periodic", (32, 16, 12), None),
+    ("zwalls-moving", (32, 16, 10), [("periodic", (0, 0, 0))] * 4 + [("wall", (0, 0, 0)), ("moving", (0.02, 0.0, 0.01))]),
+    ("ywalls", (64, 8, 9), [("periodic", (0, 0, 0))] * 2 + [("wall", (0, 0, 0)), ("moving", (0.03, 0.0, 0.0))]
+     + [("periodic", (0, 0, 0))] * 2),
+    ("closed", (32, 16, 8), [("wall", (0, 0, 0))] * 5 + [("moving", (0.02, 0.01, 0.0))]),
+]
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("lat", ["d3q19", "d3q27"])
+@pytest.mark.parametrize("name,dims,faces", FUSED_CASES, ids=[c[0] for c in FUSED_CASES])
+def test_two_fluid_one_pass_step_bitwise(gpu, oracle_port, name, dims, faces, lat, dtype, monkeypatch):
+    """The one-pass two-fluid step (k_cg_fused: colour moments, grad phi from
+    staged planes, prepare_stress, recolouring and push into the other
+    population buffers) == two_fluid_step, bit for bit: both species after N
+    steps and the host-visible fields (rho_r, rho_b, rho, j / Pi after
+    prepare_stress, phi, grad phi) -- and == the two-kernel step."""
+    if lat == "d3q27" and dtype == np.float64:
+        pytest.skip("D3Q27 fp64 stages more than one CTA's shared memory: the two-kernel step")
+    fc = faces if faces is not None else O.periodic()
+    st = droplet_state(dims, min(dims[:2]) / 3.2, dtype, (0.01, -0.006, 0.004))
+    fr0, fb0 = oracle_port.init_colors(lat, dims, st, None)
+    cp = T.ColorParams(sigma=0.02, beta=0.7)
+    got = {}
+    for fused in ("1", "0"):
+        monkeypatch.setenv("TSLB_CG_FUSED", fused)
+        dev = T.DeviceSolver(lat, T.GridDims(*dims), 1.2, spec_of(fc), dtype, 2, None, cp)
+        try:
+            dev.upload_f(fr0, 0)
+            dev.upload_f(fb0, 1)
+            dev.step(3)
+            dev.step(2)
+            got[fused] = [dev.download_f(0), dev.download_f(1)] + [
+                dev.download_field(f) for f in ("rho_r", "rho_b", "rho", "mom", "pineq", "phi", "gradphi")]
+        finally:
+            dev.close()
+    for a, b, w in zip(got["1"], got["0"], ("fr", "fb", "rho_r", "rho_b", "rho", "mom", "pineq", "phi", "gradphi")):
+        assert_bitwise(a, b, f"one-pass vs two-kernel {w}")
+    fr, fb = fr0.copy(), fb0.copy()
+    oracle_port.two_run(lat, dims, 1.2, dict(sigma=0.02, beta=0.7), fc, fr, fb, 5)
+    assert_bitwise(got["1"][0], fr, "one-pass fr vs oracle")
+    assert_bitwise(got["1"][1], fb, "one-pass fb vs oracle")
