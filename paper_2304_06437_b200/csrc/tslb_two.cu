@@ -23,7 +23,16 @@
 
 namespace tslb_cuda {
 
-constexpr int BX2 = 128;
+#ifndef TSLB_BX2
+#define TSLB_BX2 256
+#endif
+constexpr int BX2 = TSLB_BX2;  // threads per block = x nodes per block (-DTSLB_BX2: measurements)
+// the domain as the row-tiled two-fluid launches see it (x blocks of BX2)
+inline Dom dx2(const Dom& d) {
+  Dom x = d;
+  x.xblocks = (d.nx + BX2 - 1) / BX2;
+  return x;
+}
 
 template <typename T>
 struct TF {
@@ -1030,7 +1039,7 @@ __global__ void __launch_bounds__(BX2)
 // ---------------------------------------------------------------------------
 namespace {
 inline dim3 grid2(const Dom& d) {
-  return row_grid(d);
+  return row_grid(dx2(d));
 }
 template <class F>
 int with_lat2(int lat, F&& f) {
@@ -1048,7 +1057,7 @@ int launch_cg_moments(int lat, const Dom& d, const T* fr, const T* fb,
                       const TwoFields& s, const uint8_t* solid,
                       cudaStream_t st) {
   return with_lat2(lat, [&](auto L) {
-    k_cg_moments<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), solid);
+    k_cg_moments<decltype(L), T><<<grid2(d), BX2, 0, st>>>(dx2(d), fr, fb, tf_of<T>(s), solid);
   });
 }
 
@@ -1060,11 +1069,11 @@ int launch_cg_gradient(int lat, const Dom& d, const TwoFields& s,
     bool walls = false;
     for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
     if (!d.has_solid && cp.nci_strength == 0.0 && walls)
-      k_cg_gradient_box<decltype(L), T, true><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s));
+      k_cg_gradient_box<decltype(L), T, true><<<grid2(d), BX2, 0, st>>>(dx2(d), tf_of<T>(s));
     else if (!d.has_solid && cp.nci_strength == 0.0)
-      k_cg_gradient_box<decltype(L), T, false><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s));
+      k_cg_gradient_box<decltype(L), T, false><<<grid2(d), BX2, 0, st>>>(dx2(d), tf_of<T>(s));
     else
-      k_cg_gradient<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s), solid, slow, cp);
+      k_cg_gradient<decltype(L), T><<<grid2(d), BX2, 0, st>>>(dx2(d), tf_of<T>(s), solid, slow, cp);
   });
 }
 
@@ -1074,7 +1083,7 @@ int launch_cg_prepare_stress(int lat, const Dom& d, const TwoFields& s,
                              const ColorParamsDev& cp, cudaStream_t st) {
   const T tau = T(1) / T(omega);
   return with_lat2(lat, [&](auto L) {
-    k_cg_prepare<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s), solid, tau, cp);
+    k_cg_prepare<decltype(L), T><<<grid2(d), BX2, 0, st>>>(dx2(d), tf_of<T>(s), solid, tau, cp);
   });
 }
 
@@ -1095,18 +1104,18 @@ int launch_cg_streamcoll(int lat, const Dom& d, T* fr, T* fb,
       for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
       if (walls)
         k_cg_streamcoll_box<decltype(L), T, true, true, false>
-            <<<grid2(d), BX2, 0, st>>>(d, pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
+            <<<grid2(d), BX2, 0, st>>>(dx2(d), pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
       else
         k_cg_streamcoll_box<decltype(L), T, true, false, false>
-            <<<grid2(d), BX2, 0, st>>>(d, pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
+            <<<grid2(d), BX2, 0, st>>>(dx2(d), pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
       return;
     }
     if (fold_prepare)
       k_cg_streamcoll<decltype(L), T, true>
-          <<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), solid, slow, om, tau, cp);
+          <<<grid2(d), BX2, 0, st>>>(dx2(d), fr, fb, tf_of<T>(s), solid, slow, om, tau, cp);
     else
       k_cg_streamcoll<decltype(L), T, false>
-          <<<grid2(d), BX2, 0, st>>>(d, fr, fb, tf_of<T>(s), solid, slow, om, tau, cp);
+          <<<grid2(d), BX2, 0, st>>>(dx2(d), fr, fb, tf_of<T>(s), solid, slow, om, tau, cp);
   });
 }
 
@@ -1123,10 +1132,10 @@ int launch_cg_streamcoll_grad(int lat, const Dom& d, T* fr, T* fb, const TwoFiel
   return with_lat2(lat, [&](auto L) {
     if (walls)
       k_cg_streamcoll_box<decltype(L), T, true, true, true>
-          <<<grid2(d), BX2, 0, st>>>(d, pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
+          <<<grid2(d), BX2, 0, st>>>(dx2(d), pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
     else
       k_cg_streamcoll_box<decltype(L), T, true, false, true>
-          <<<grid2(d), BX2, 0, st>>>(d, pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
+          <<<grid2(d), BX2, 0, st>>>(dx2(d), pop_bases(fr, fb, d, decltype(L)::q), tf_of<T>(s), om, tau, cp);
   });
 }
 
@@ -1183,9 +1192,9 @@ int launch_cg_gradient_nci_box(int lat, const Dom& d, const TwoFields& s, const 
   bool walls = false;
   for (int fc = 0; fc < 6; ++fc) walls |= d.mode[fc] == kWall;
   return with_lat2(lat, [&](auto L) {
-    if (walls) k_cg_gradient_box<decltype(L), T, true><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s));
-    else k_cg_gradient_box<decltype(L), T, false><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s));
-    if (T(cp.nci_strength) != T(0)) k_cg_nci_box<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, tf_of<T>(s), cp);
+    if (walls) k_cg_gradient_box<decltype(L), T, true><<<grid2(d), BX2, 0, st>>>(dx2(d), tf_of<T>(s));
+    else k_cg_gradient_box<decltype(L), T, false><<<grid2(d), BX2, 0, st>>>(dx2(d), tf_of<T>(s));
+    if (T(cp.nci_strength) != T(0)) k_cg_nci_box<decltype(L), T><<<grid2(d), BX2, 0, st>>>(dx2(d), tf_of<T>(s), cp);
   });
 }
 
@@ -1200,7 +1209,7 @@ int launch_init_colors(int lat, const Dom& d, T* fr, T* fb,
                        const uint8_t* solid, const InitSpec& sp,
                        cudaStream_t st) {
   return with_lat2(lat, [&](auto L) {
-    k_init_colors<decltype(L), T><<<grid2(d), BX2, 0, st>>>(d, fr, fb, solid, sp);
+    k_init_colors<decltype(L), T><<<grid2(d), BX2, 0, st>>>(dx2(d), fr, fb, solid, sp);
   });
 }
 
