@@ -89,6 +89,15 @@ def test_gpus_flag_launches_one_rank_per_gpu():
     assert out["n_gpus"] == 2 and out["ranks"] == [0, 1] and out["pids_distinct"]
 
 
+def test_relaunch_passes_the_cube_option_through():
+    """`--n` is an abbreviation torch.distributed.run's own parser would
+    claim (even after the script path): the relaunch passes it as --cube."""
+    import json
+    r = _run_bench(["--gpus", "2", "--n", "64", "--launch-check"])
+    assert r.returncode == 0, r.stderr[-2000:]
+    assert json.loads(r.stdout.strip().splitlines()[-1])["n_gpus"] == 2
+
+
 def test_gpus_flag_must_match_world_size():
     r = _run_bench(["--gpus", "4", "--launch-check"], env={"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
     assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr
