@@ -228,7 +228,12 @@ __global__ void __launch_bounds__(32 * WPB)
 // wall, kernels.hpp:178-199), and reduces them to m(t+1) in compute_moments'
 // order. Regions of small periodic domains may hold a node twice; every copy
 // computes the same bits. Same per-node arithmetic as strip_pass: same bits.
-constexpr int TBX = 32, TBY = 16, TBT = 512;  // tile, threads per block
+#ifndef TSLB_TBX  // (-DTSLB_TBX/TBY/TBT: measurements)
+#define TSLB_TBX 32
+#define TSLB_TBY 16
+#define TSLB_TBT 512
+#endif
+constexpr int TBX = TSLB_TBX, TBY = TSLB_TBY, TBT = TSLB_TBT;  // tile, threads per block
 template <int K>
 struct TbRegion {
   static constexpr int W = TBX + 2 * K, H = TBY + 2 * K, N = W * H;
