@@ -227,11 +227,11 @@ int tslb_cuda_group_step(tslb_cuda_handle* slabs, int count, long nsteps);
  * NCCL): each rank exports a block holding its ghost planes (double
  * buffered by exchange parity) and two flag words as a CUDA IPC handle
  * (TSLB_IPC_HANDLE_BYTES), the ranks swap handles over any host channel, and
- * every rank maps its z neighbours' blocks. A step then copies the new
- * boundary planes straight into the neighbours' ghost buffers (NVLink peer
- * writes between GPUs) and publishes the exchange number in their flag
- * words; the consumer's stream waits for it before the ghost planes are
- * read. A face that wraps onto the rank itself (one rank, periodic) passes
+ * every rank maps its z neighbours' blocks. A step's boundary chunks then
+ * store the new boundary planes straight into the neighbours' ghost buffers
+ * from the M kernel's epilogue (NVLink peer stores between GPUs) and publish
+ * the exchange number in their flag words; the consumer's stream waits for
+ * it before the ghost planes are read. A face that wraps onto the rank itself (one rank, periodic) passes
  * the rank's own handle. TSLB_ESTATE for two-fluid or F1 steps. */
 #define TSLB_IPC_HANDLE_BYTES 64
 int tslb_cuda_ipc_handle(tslb_cuda_handle h, void* handle64);

@@ -375,14 +375,18 @@ int ph_streamcoll(tslb_cuda_sim* h, int k0, int k1, cudaStream_t st) {
 
 // M schedule: m(t) in h->mo -> m(t+1) in h->mo2 for planes [z0, z1) (z1 <= 0:
 // to the end); the caller swaps the buffers once every plane is done.
-int ph_mstep(tslb_cuda_sim* h, cudaStream_t st, int z0 = 0, int z1 = 0) {
+// peer_lo / peer_hi: where the new planes 0 / nzl-1 also go (the z
+// neighbours' ghost buffers, peer-memory transport), or null
+int ph_mstep(tslb_cuda_sim* h, cudaStream_t st, int z0 = 0, int z1 = 0, void* peer_lo = nullptr,
+             void* peer_hi = nullptr) {
   Prof p(h, TSLB_K_MSTEP, st);
   ++h->launches;
   int rc = by_scalar(h, [&](auto z) {
     using T = decltype(z);
     return launch_mstep<T>(h->lat, h->math, h->range(0, h->nzl), static_cast<const T*>(h->mo),
                            static_cast<const T*>(h->gm), static_cast<T*>(h->mo2), h->omega, h->lz, z0, z1, h->mmaps,
-                           h->sbits ? h->sbits + size_t(h->d.ghost) * h->plane() : nullptr, st);
+                           h->sbits ? h->sbits + size_t(h->d.ghost) * h->plane() : nullptr, st,
+                           static_cast<T*>(peer_lo), static_cast<T*>(peer_hi));
   });
   if (rc < 0) return set_err(TSLB_ECUDA, "k_mstep launch: %s", cudaGetErrorString(cudaError_t(-rc)));
   if (rc) return set_err(TSLB_ESTATE, "M step not supported for this domain");
@@ -457,7 +461,9 @@ int exchange_moments_local(tslb_cuda_sim* h, cudaStream_t st) {
 // it has received this rank's next exchange, which is issued after this
 // rank's reads of parity p (stream order).
 constexpr size_t kIpcFlags = 256;
-int exchange_moments_ipc(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
+// copy = false: the M kernel's boundary chunks already wrote the planes into
+// the neighbours' buffers (ipc_targets); only the flags are published
+int exchange_moments_ipc(tslb_cuda_sim* h, const void* buf, cudaStream_t st, bool copy = true) {
   const uint64_t e = ++h->xcount;
   const size_t par = size_t(e & 1) * h->ipc_gb;
   const size_t pb = size_t(h->plane()) * h->esz, blk = moment_plane_block(h);
@@ -465,10 +471,10 @@ int exchange_moments_ipc(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
   const size_t spitch = size_t(h->d.mstride) * h->esz;
   const char* src = static_cast<const char*>(buf);
   Prof p(h, TSLB_K_EXCHANGE, st);
-  if (h->ipc_up)  // top plane -> the up neighbour's "below" ghost planes
+  if (copy && h->ipc_up)  // top plane -> the up neighbour's "below" ghost planes
     CK(cudaMemcpy2DAsync(h->ipc_up + kIpcFlags + par, pb, src + size_t(h->nzl - 1) * pb, spitch, pb, size_t(nm),
                          cudaMemcpyDeviceToDevice, st));
-  if (h->ipc_down)  // bottom plane -> the down neighbour's "above" ghost planes
+  if (copy && h->ipc_down)  // bottom plane -> the down neighbour's "above" ghost planes
     CK(cudaMemcpy2DAsync(h->ipc_down + kIpcFlags + par + blk, pb, src, spitch, pb, size_t(nm),
                          cudaMemcpyDeviceToDevice, st));
   ++h->launches;
@@ -476,6 +482,17 @@ int exchange_moments_ipc(tslb_cuda_sim* h, const void* buf, cudaStream_t st) {
                         h->ipc_down ? reinterpret_cast<uint64_t*>(h->ipc_down) + 1 : nullptr, e, st))
     return set_err(TSLB_ECUDA, "k_ipc_signal launch failed");
   return 0;
+}
+
+// where the M kernel writes this step's boundary planes for the next
+// exchange (plane 0 -> the down neighbour's "above" ghost planes, plane
+// nzl-1 -> the up neighbour's "below" ones, parity of that exchange)
+void ipc_targets(const tslb_cuda_sim* h, void*& lo, void*& hi) {
+  lo = hi = nullptr;
+  if (h->xmode != 3 || h->d.has_solid) return;  // (masked slabs: copies after the chunks)
+  const size_t par = size_t((h->xcount + 1) & 1) * h->ipc_gb;
+  if (h->ipc_down) lo = h->ipc_down + kIpcFlags + par + moment_plane_block(h);
+  if (h->ipc_up) hi = h->ipc_up + kIpcFlags + par;
 }
 
 // before the ghost planes of the current moments are read on `st`: wait for
@@ -928,21 +945,27 @@ int enqueue_step(tslb_cuda_sim* h) {
       // previous step is complete on both streams; the solver stream joins
       // the exchange before the next step.
       const int b = boundary_planes(h);
+      // peer memory: the boundary chunks write their new boundary planes into
+      // the neighbours' ghost buffers themselves, the exchange only
+      // publishes the flags; NCCL: packed send / receive
       auto exchange = [&](cudaStream_t st) {
-        if (h->xmode == 3) return exchange_moments_ipc(h, h->mo2, st);
+        if (h->xmode == 3) return exchange_moments_ipc(h, h->mo2, st, h->d.has_solid);
         if (int r = pack_moments(h, h->mo2, st)) return r;
         return exchange_moments_nccl(h, st);
       };
+      void *plo = nullptr, *phi = nullptr;
       if (h->nzl <= 2 * b) {
         if ((rc = ipc_ghosts(h, h->s))) return rc;
-        if ((rc = ph_mstep(h, h->s))) return rc;
+        ipc_targets(h, plo, phi);
+        if ((rc = ph_mstep(h, h->s, 0, 0, plo, phi))) return rc;
         if ((rc = exchange(h->s))) return rc;
       } else {
         CK(cudaEventRecord(h->ev_b, h->s));
         CK(cudaStreamWaitEvent(h->cs, h->ev_b, 0));
         if ((rc = ipc_ghosts(h, h->cs))) return rc;
-        if ((rc = ph_mstep(h, h->cs, 0, b))) return rc;
-        if ((rc = ph_mstep(h, h->cs, h->nzl - b, h->nzl))) return rc;
+        ipc_targets(h, plo, phi);
+        if ((rc = ph_mstep(h, h->cs, 0, b, plo, nullptr))) return rc;
+        if ((rc = ph_mstep(h, h->cs, h->nzl - b, h->nzl, nullptr, phi))) return rc;
         if ((rc = exchange(h->cs))) return rc;
         CK(cudaEventRecord(h->ev_c, h->cs));
         if ((rc = ph_mstep(h, h->s, b, h->nzl - b))) return rc;

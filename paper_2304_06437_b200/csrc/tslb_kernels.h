@@ -56,7 +56,8 @@ void free_mstep_maps(MstepMaps* maps);
 bool mstep_supported(int lat, const Dom& d, int esz);
 template <typename T>
 int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
-                 int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st);
+                 int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st,
+                 T* peer_lo = nullptr, T* peer_hi = nullptr);
 // mixed-precision M step (tslb_mstep.cu, tslb_store16.cuh): fp16 moments,
 // fp32 populations and arithmetic, whole domains without solids, nx % 8 == 0
 bool mstep16_supported(int lat, const Dom& d);

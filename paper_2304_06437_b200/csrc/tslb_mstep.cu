@@ -447,11 +447,11 @@ __device__ __forceinline__ void finalize(const Dom& d, const Ring<L, T>& rg, con
 // TM: the storage type of the moment arrays (T, or __half: the scaled fp16
 // moments of the mixed-precision mode, tslb_store16.cuh); the populations
 // are rounded to T in the slots either way
-template <class L, typename T, typename C, bool WALLS, bool SOLID, int MINB, typename TM = T>
+template <class L, typename T, typename C, bool WALLS, bool SOLID, int MINB, typename TM = T, bool PEER = false>
 __global__ void __launch_bounds__(NT, MINB)
     k_mstep(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap gmap, Dom d,
             const TM* __restrict__ mi, const TM* __restrict__ gm, TM* __restrict__ mo, C om1, int lz, int zbeg,
-            int zend, const uint32_t* __restrict__ sbits) {
+            int zend, const uint32_t* __restrict__ sbits, TM* __restrict__ peer_lo, TM* __restrict__ peer_hi) {
   static_assert(L::dim == 3, "the M step is 3-D");
   using SM = Smem<L, T, SOLID, TM>;
   using W = typename MStore<TM>::W;
@@ -616,7 +616,21 @@ __global__ void __launch_bounds__(NT, MINB)
     // compute_moments skips solid nodes (their moment arrays keep their values)
     if (active && z - 1 >= za && !(SOLID && solid_prev)) {
       TM* o = mo + col + int64_t(z - 1) * d.plane;
-      finalize<L, T, C>(d, rg, R, [&](int c, T v) { o[c * ms] = MStore<TM>::enc(c, v); });
+      if constexpr (PEER) {
+        // a slab's boundary planes also go straight into the z neighbours'
+        // ghost buffers (peer memory: the halo exchange fused into the
+        // epilogue of the boundary chunks)
+        TM* plo = peer_lo && z - 1 == 0 ? peer_lo + col : nullptr;
+        TM* phi = peer_hi && z - 1 == d.nz - 1 ? peer_hi + col : nullptr;
+        finalize<L, T, C>(d, rg, R, [&](int c, T v) {
+          const TM e = MStore<TM>::enc(c, v);
+          o[c * ms] = e;
+          if (plo) plo[c * d.plane] = e;
+          if (phi) phi[c * d.plane] = e;
+        });
+      } else {
+        finalize<L, T, C>(d, rg, R, [&](int c, T v) { o[c * ms] = MStore<TM>::enc(c, v); });
+      }
     }
     if constexpr (SOLID) solid_prev = (ct.sb & kSelfSolid) != 0;  // (ct.sb: plane z)
     if constexpr (L::rd == 0) __syncthreads();
@@ -815,7 +829,8 @@ int launch_ghost_push(int lat, int math, const Dom& d, T* f, const T* gm, double
 
 template <typename T>
 int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* mo, double omega,
-                 int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st) {
+                 int lz, int z0, int z1, MstepMaps*& maps, const uint32_t* sbits, cudaStream_t st, T* peer_lo,
+                 T* peer_hi) {
   using namespace mstep;
   if (!mstep_supported(lat, d, int(sizeof(T)))) return 1;
   if (d.has_solid && !sbits) return 1;
@@ -853,7 +868,7 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
     auto go = [&](auto kern, auto om1, size_t smem) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e == cudaSuccess) {
-        kern<<<grid, NT, smem, st>>>(*tm, *gmp, d, mi, gm, mo, om1, lz, z0, z1, sbits);
+        kern<<<grid, NT, smem, st>>>(*tm, *gmp, d, mi, gm, mo, om1, lz, z0, z1, sbits, peer_lo, peer_hi);
         e = cudaGetLastError();
       }
       if (e != cudaSuccess) err = -int(e);
@@ -865,11 +880,18 @@ int launch_mstep(int lat, int math, const Dom& d, const T* mi, const T* gm, T* m
     // ILP than the third CTA buys); fp64 storage holds one CTA per SM
     constexpr int MB = sizeof(T) == 4 && Lat::rd == 0 ? 3 : sizeof(T) == 4 ? 2 : 1;
     constexpr int MBD = sizeof(T) == 4 ? 2 : 1;
+    // (peer outputs: slab boundary chunks on the peer-memory transport)
+    const bool peer = (peer_lo || peer_hi) && !d.has_solid;
     if (math == kMathDouble) {
       if (d.has_solid && walls) go(k_mstep<Lat, T, double, true, true, MBD>, om1d, sm1);
       else if (d.has_solid) go(k_mstep<Lat, T, double, false, true, MBD>, om1d, sm1);
+      else if (peer && walls) go(k_mstep<Lat, T, double, true, false, MBD, T, true>, om1d, sm0);
+      else if (peer) go(k_mstep<Lat, T, double, false, false, MBD, T, true>, om1d, sm0);
       else if (walls) go(k_mstep<Lat, T, double, true, false, MBD>, om1d, sm0);
       else go(k_mstep<Lat, T, double, false, false, MBD>, om1d, sm0);
+    } else if (peer) {
+      if (walls) go(k_mstep<Lat, T, float, true, false, MB, T, true>, om1f, sm0);
+      else go(k_mstep<Lat, T, float, false, false, MB, T, true>, om1f, sm0);
     } else {
       if (d.has_solid && walls) go(k_mstep<Lat, T, float, true, true, MB>, om1f, sm1);
       else if (d.has_solid) go(k_mstep<Lat, T, float, false, true, MB>, om1f, sm1);
@@ -907,7 +929,7 @@ int launch_mstep16(int lat, const Dom& d, const __half* mi, __half* mo, double o
     auto go = [&](auto kern) {
       cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
       if (e == cudaSuccess) {
-        kern<<<grid, NT, smem, st>>>(*tm, *tm, d, mi, nullptr, mo, om1, lz, 0, d.nz, nullptr);
+        kern<<<grid, NT, smem, st>>>(*tm, *tm, d, mi, nullptr, mo, om1, lz, 0, d.nz, nullptr, nullptr, nullptr);
         e = cudaGetLastError();
       }
       if (e != cudaSuccess) err = -int(e);
@@ -948,9 +970,9 @@ int launch_moments_codec16(const Dom& d, int nm, float* m32, __half* m16, int to
 }
 
 template int launch_mstep<float>(int, int, const Dom&, const float*, const float*, float*, double, int, int, int,
-                                 MstepMaps*&, const uint32_t*, cudaStream_t);
+                                 MstepMaps*&, const uint32_t*, cudaStream_t, float*, float*);
 template int launch_mstep<double>(int, int, const Dom&, const double*, const double*, double*, double, int, int,
-                                  int, MstepMaps*&, const uint32_t*, cudaStream_t);
+                                  int, MstepMaps*&, const uint32_t*, cudaStream_t, double*, double*);
 template int launch_ghost_push<float>(int, int, const Dom&, float*, const float*, double, int, const uint8_t*,
                                       cudaStream_t);
 template int launch_ghost_push<double>(int, int, const Dom&, double*, const double*, double, int,
