@@ -135,3 +135,32 @@ def test_bench_two_ranks_on_one_device_over_ipc(gpu, tmp_path):
     assert line["n_gpus"] == 2 and line["value"] > 0
     assert "peer-memory" in line["config"]["parallelism"]
     assert line["roofline"]["launches_per_step"].get("exchange", 0) > 0
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_ipc_self_exchange_masked(gpu, dtype, monkeypatch):
+    """A masked M slab on the peer-memory transport (its own neighbour; masked
+    slabs copy their boundary planes after the chunks instead of storing them
+    from the kernel) equals the periodic masked box of the slab's height."""
+    from helpers import random_solid
+    monkeypatch.setenv("TSLB_LZ", "2")
+    lat, nx, ny, nzl = "d3q19", 32, 16, 8
+    mask = random_solid((nx, ny, nzl), 0.15, 9)
+    f0 = O.random_state(lat, (nx, ny, nzl), 6, dtype, mask)
+    spec = spec_of(O.periodic())
+    ref = T.DeviceSolver(lat, T.GridDims(nx, ny, nzl), 1.2, spec, dtype, 1, mask)
+    slab = T.DeviceSolver(lat, T.GridDims(nx, ny, 2 * nzl), 1.2, spec, dtype, 1, np.concatenate([mask, mask]),
+                          slab=(0, nzl))
+    try:
+        assert slab.schedule == "m" and ref.schedule == "m"
+        own = slab.ipc_handle()
+        slab.attach_ipc(own, own)
+        for d in (ref, slab):
+            d.upload_f(f0)
+            d.step(7)
+        assert_bitwise(slab.download_f(), ref.download_f(), "masked IPC self-exchange f")
+        for fld in ("rho", "mom", "pineq"):
+            assert_bitwise(slab.download_field(fld), ref.download_field(fld), f"masked IPC self-exchange {fld}")
+    finally:
+        slab.close()
+        ref.close()
