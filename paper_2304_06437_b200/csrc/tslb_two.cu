@@ -661,8 +661,11 @@ __global__ void TSLB_CG_BOUNDS
       pop.b[dd::opp][fi32] = fb_out - (corr - corr_r);
     } else {
       const uint32_t t = fi32 + uint32_t(delta);
-      pop.r[a][t] = fr_out;
-      pop.b[a][t] = fb_out;
+      // streaming (evict-first) stores: the populations are read back only
+      // by the next step's colour moments, long after L2 has turned over
+      // (r02: 5.34 vs 5.36 ms at 512^3)
+      __stcs(&pop.r[a][t], fr_out);
+      __stcs(&pop.b[a][t], fb_out);
     }
   };
   auto all_dirs = [&](auto IF) {
