@@ -50,8 +50,11 @@ def build(verbose: bool = False, out: str | None = None, defines: tuple = ()) ->
     measurement variant (-D flags) into `out` with its own object directory
     (same-box A/B runs load it through TSLB_LIB; the product .so is untouched)."""
     lib = out or LIB
-    obj_dir = OBJ if not defines else os.path.join(OBJ, "v_" + "_".join(d.replace("=", "-") for d in defines))
-    extra = [f"-D{d}" for d in defines]
+    # (variant builds only: TSLB_NVCC_EXTRA adds raw nvcc flags)
+    raw = os.environ.get("TSLB_NVCC_EXTRA", "").split() if out else []
+    tag = "_".join([d.replace("=", "-") for d in defines] + [str(abs(hash(" ".join(raw))) % 10 ** 8)] * bool(raw))
+    obj_dir = OBJ if not (defines or raw) else os.path.join(OBJ, "v_" + tag)
+    extra = [f"-D{d}" for d in defines] + raw
     os.makedirs(obj_dir, exist_ok=True)
     srcs = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
     hdrs = _headers()
