@@ -164,3 +164,32 @@ def test_ipc_self_exchange_masked(gpu, dtype, monkeypatch):
     finally:
         slab.close()
         ref.close()
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_init_equilibrium_on_an_ipc_slab(gpu, oracle_port, dtype, monkeypatch):
+    """tslb_cuda_init_equilibrium on a slab (rho, u of the local planes; the
+    first step's moments come from the initialiser and go out by copy, every
+    later exchange from the kernel epilogue) over the peer-memory transport
+    == the oracle's initialize_regularized (Pi = 0) + fused_step."""
+    monkeypatch.setenv("TSLB_LZB", "2")
+    lat, nx, ny, nzl = "d3q19", 32, 8, 8
+    n = nx * ny * nzl
+    rng = np.random.default_rng(5)
+    st = np.zeros((10, n))
+    st[:4] = rng.uniform(-0.02, 0.02, (4, n))
+    st[0] += 1.0
+    st = st.astype(dtype)
+    spec = spec_of(O.periodic())
+    slab = T.DeviceSolver(lat, T.GridDims(nx, ny, 2 * nzl), 1.2, spec, dtype, 1, None, slab=(0, nzl))
+    try:
+        own = slab.ipc_handle()
+        slab.attach_ipc(own, own)
+        slab.init_equilibrium(np.ascontiguousarray(st[:4]))
+        slab.step(6)
+        fs = slab.download_f()
+    finally:
+        slab.close()
+    fo = oracle_port.init_regularized(lat, (nx, ny, nzl), st)
+    oracle_port.single_run(lat, (nx, ny, nzl), 1.2, O.periodic(), fo, None, 6, 0)
+    assert_bitwise(fs, fo, "init_equilibrium IPC slab vs oracle f")
