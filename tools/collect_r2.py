@@ -14,9 +14,9 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 NODES = {"mstep_f64": 134217728, "mstep_f32": 134217728, "mstep_f16": 134217728, "droplet_scr": 134217728,
-         "droplet_fused": 134217728,
+         "droplet_fused": 134217728, "cavity_tb": 65536 * 200, "droplet_cgm": 134217728,
          "d3q27_mstep": 134217728}
-ALG = {"mstep_f64": 80, "mstep_f32": 80, "mstep_f16": 40, "droplet_scr": 204, "d3q27_mstep": 80, "droplet_fused": 357}
+ALG = {"mstep_f64": 80, "mstep_f32": 80, "mstep_f16": 40, "droplet_scr": 204, "d3q27_mstep": 80, "droplet_fused": 357, "cavity_tb": 24, "droplet_cgm": 205}
 
 
 def main(tag, prefix="r02", dest=PROF):
