@@ -1816,7 +1816,8 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
   // (tools/micro/tb2d_sizes.py), 256^2 22.3 / 17.5 GLUPS (periodic / lid)
   // persistent vs 17.5 / 16.2 from graphs, 384^2 about equal, 512^2 26.8 vs
   // 37.1 and 1024^2 29.5 vs 52.4 in favour of the graphs
-  constexpr int64_t kPersistMaxNodes = int64_t(3) << 16;
+  const char* pmx = std::getenv("TSLB_PERSIST_MAX");  // (nodes; measurements)
+  const int64_t kPersistMaxNodes = pmx ? std::atoll(pmx) : int64_t(3) << 16;
   const char* pe = std::getenv("TSLB_PERSIST");
   const bool persist = !(pe && std::atoi(pe) == 0);
   if (persist && h->sched == TSLB_SCHED_M && h->dim == 2 && h->comps == 1 && h->xmode == 0 && !h->decomposed &&

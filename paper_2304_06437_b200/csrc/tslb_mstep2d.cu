@@ -240,7 +240,7 @@ struct TbRegion {
 };
 template <typename T, int K>
 constexpr size_t tb_smem() {
-  return size_t(6 + 9) * TbRegion<K>::N * sizeof(T);
+  return size_t(6 + 2 * 9) * TbRegion<K>::N * sizeof(T);
 }
 
 template <class L, typename T, typename C, bool WALLS, int K>
@@ -251,10 +251,30 @@ __global__ void __launch_bounds__(TBT, 1)
   constexpr int W = RG::W, H = RG::H, N = RG::N;
   extern __shared__ __align__(16) unsigned char tb_raw[];
   T* mom = reinterpret_cast<T*>(tb_raw);  // [6][N]
-  T* pc = mom + 6 * N;                    // [9][N]
+  T* pcs = mom + 6 * N;                   // [2][9][N] (double buffered)
   cg::grid_group grid = cg::this_grid();
   const int64_t ms = d.mstride;
   const int tiles = ntx * nty;
+  // the node's 9 post-collision populations from its moments (T values, as
+  // stored), rounded to T, into population buffer pc
+  auto collide = [&](const T (&v)[6], T* pc, int e) {
+    const NodeMoments<C> m = prep<T, C>(v);
+    unroll<9>([&](auto A) {
+      constexpr int a = decltype(A)::value;
+      if constexpr (a == 0) {
+        pc[e] = T(sf_post<Lat, 0, C>(m, om1));
+      } else if constexpr (a & 1) {
+        C ra, rb;
+        sf_pair<Lat, a, C>(m, om1, ra, rb);
+        pc[a * N + e] = T(ra);
+        pc[(a + 1) * N + e] = T(rb);
+      }
+    });
+  };
+  auto exists = [&](int gx, int gy) {
+    return wrap_coord(gx, d.nx, d.mode[XMin], d.mode[XMax]) >= 0 &&
+           wrap_coord(gy, d.ny, d.mode[YMin], d.mode[YMax]) >= 0;
+  };
   // groups of passes: sizes differ by at most one, their count has the
   // parity of nsteps (the result lands where the per-pass ping-pong would)
   const T* src = m0;
@@ -265,92 +285,74 @@ __global__ void __launch_bounds__(TBT, 1)
     left -= ks;
     for (int tile = int(blockIdx.x); tile < tiles; tile += int(gridDim.x)) {
       const int ox = (tile % ntx) * TBX - K, oy = (tile / ntx) * TBY - K;  // region origin (global)
+      // load the region's moments and collide every node of it (pass 0)
       for (int e = int(threadIdx.x); e < N; e += TBT) {
-        const int gx = wrap_coord(ox + e % W, d.nx, d.mode[XMin], d.mode[XMax]);
-        const int gy = wrap_coord(oy + e / W, d.ny, d.mode[YMin], d.mode[YMax]);
-        if (gx < 0 || gy < 0) continue;  // beyond a wall: no node
-        const int64_t idx = gx + int64_t(d.nx) * gy;
+        const int gxr = wrap_coord(ox + e % W, d.nx, d.mode[XMin], d.mode[XMax]);
+        const int gyr = wrap_coord(oy + e / W, d.ny, d.mode[YMin], d.mode[YMax]);
+        if (gxr < 0 || gyr < 0) continue;  // beyond a wall: no node
+        const int64_t idx = gxr + int64_t(d.nx) * gyr;
+        T v[6];
 #pragma unroll
-        for (int c = 0; c < 6; ++c) mom[c * N + e] = __ldcg(src + c * ms + idx);
+        for (int c = 0; c < 6; ++c) v[c] = __ldcg(src + c * ms + idx);
+        collide(v, pcs, e);
       }
       __syncthreads();
+      // pass s: every node of the ring [s + 1, W - s - 1) x [s + 1, H - s - 1)
+      // gathers f_a(x) = pc_a(x - c_a) (or the bounce of its own opposite
+      // push when x - c_a lies beyond a wall), reduces its moments and --
+      // still the same thread, the same node -- collides them for pass s + 1
+      // into the other population buffer: one barrier per pass
       for (int s = 0; s < ks; ++s) {
-        // (1) collide the ring [s, W - s) x [s, H - s)
-        {
-          const int w = W - 2 * s, cnt = w * (H - 2 * s);
-          for (int q = int(threadIdx.x); q < cnt; q += TBT) {
-            const int lx = s + q % w, ly = s + q / w, e = lx + W * ly;
-            if (wrap_coord(ox + lx, d.nx, d.mode[XMin], d.mode[XMax]) < 0 ||
-                wrap_coord(oy + ly, d.ny, d.mode[YMin], d.mode[YMax]) < 0)
-              continue;
-            T v[6];
+        const T* pc = pcs + (s & 1) * 9 * N;
+        T* pn = pcs + ((s + 1) & 1) * 9 * N;
+        const bool last = s + 1 == ks;
+        const int w = W - 2 * (s + 1), cnt = w * (H - 2 * (s + 1));
+        for (int q = int(threadIdx.x); q < cnt; q += TBT) {
+          const int lx = s + 1 + q % w, ly = s + 1 + q / w, e = lx + W * ly;
+          const int gx = ox + lx, gy = oy + ly;
+          if (!exists(gx, gy)) continue;
+          C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pxy = 0;
+          unroll<9>([&](auto A) {
+            constexpr int a = decltype(A)::value;
+            using dd = Dir<Lat, a>;
+            T fa;
+            if constexpr (a == 0) {
+              fa = pc[e];
+            } else {
+              bool bx = false, by = false;
+              if constexpr (WALLS) {
+                const int sx = gx - dd::x, sy = gy - dd::y;
+                bx = dd::x != 0 && ((sx < 0 && d.mode[XMin] == kWall) || (sx >= d.nx && d.mode[XMax] == kWall));
+                by = dd::y != 0 && ((sy < 0 && d.mode[YMin] == kWall) || (sy >= d.ny && d.mode[YMax] == kWall));
+              }
+              if (bx || by) fa = bounce_value<Lat, dd::opp, T, C>(d, pc[dd::opp * N + e], bx, by, false);
+              else fa = pc[a * N + e - dd::x - W * dd::y];
+            }
+            const C f = C(fa);
+            r += f;
+            if constexpr (dd::x == 1) jx += f;
+            if constexpr (dd::x == -1) jx -= f;
+            if constexpr (dd::y == 1) jy += f;
+            if constexpr (dd::y == -1) jy -= f;
+            if constexpr (dd::x != 0) pxx += f;
+            if constexpr (dd::y != 0) pyy += f;
+            if constexpr (dd::x * dd::y == 1) pxy += f;
+            if constexpr (dd::x * dd::y == -1) pxy -= f;
+          });
+          force_shift<C>(d, jx, jy, jz);
+          const C c3 = cs2<C>();
+          T v[6];
+          v[0] = T(r);
+          v[1] = T(jx);
+          v[2] = T(jy);
+          v[3] = T(pxx - c3 * r - jx * jx);
+          v[4] = T(pyy - c3 * r - jy * jy);
+          v[5] = T(pxy - jx * jy);
+          if (last) {
 #pragma unroll
-            for (int c = 0; c < 6; ++c) v[c] = mom[c * N + e];
-            const NodeMoments<C> m = prep<T, C>(v);
-            unroll<9>([&](auto A) {
-              constexpr int a = decltype(A)::value;
-              if constexpr (a == 0) {
-                pc[e] = T(sf_post<Lat, 0, C>(m, om1));
-              } else if constexpr (a & 1) {
-                C ra, rb;
-                sf_pair<Lat, a, C>(m, om1, ra, rb);
-                pc[a * N + e] = T(ra);
-                pc[(a + 1) * N + e] = T(rb);
-              }
-            });
-          }
-        }
-        __syncthreads();
-        // (2) stream + moments on the ring [s + 1, W - s - 1) x [s + 1, H - s - 1)
-        {
-          const int w = W - 2 * (s + 1), cnt = w * (H - 2 * (s + 1));
-          for (int q = int(threadIdx.x); q < cnt; q += TBT) {
-            const int lx = s + 1 + q % w, ly = s + 1 + q / w, e = lx + W * ly;
-            const int gx = ox + lx, gy = oy + ly;
-            if (wrap_coord(gx, d.nx, d.mode[XMin], d.mode[XMax]) < 0 ||
-                wrap_coord(gy, d.ny, d.mode[YMin], d.mode[YMax]) < 0)
-              continue;
-            C r = 0, jx = 0, jy = 0, jz = 0, pxx = 0, pyy = 0, pxy = 0;
-            unroll<9>([&](auto A) {
-              constexpr int a = decltype(A)::value;
-              using dd = Dir<Lat, a>;
-              T fa;
-              if constexpr (a == 0) {
-                fa = pc[e];
-              } else {
-                // the source x - c_a; beyond a wall face it does not exist and
-                // the slot holds the bounce of x's own push along opp(a)
-                bool bx = false, by = false;
-                if constexpr (WALLS) {
-                  const int sx = gx - dd::x, sy = gy - dd::y;
-                  bx = dd::x != 0 && ((sx < 0 && d.mode[XMin] == kWall) || (sx >= d.nx && d.mode[XMax] == kWall));
-                  by = dd::y != 0 && ((sy < 0 && d.mode[YMin] == kWall) || (sy >= d.ny && d.mode[YMax] == kWall));
-                }
-                if (bx || by) {
-                  fa = bounce_value<Lat, dd::opp, T, C>(d, pc[dd::opp * N + e], bx, by, false);
-                } else {
-                  fa = pc[a * N + e - dd::x - W * dd::y];
-                }
-              }
-              const C f = C(fa);
-              r += f;
-              if constexpr (dd::x == 1) jx += f;
-              if constexpr (dd::x == -1) jx -= f;
-              if constexpr (dd::y == 1) jy += f;
-              if constexpr (dd::y == -1) jy -= f;
-              if constexpr (dd::x != 0) pxx += f;
-              if constexpr (dd::y != 0) pyy += f;
-              if constexpr (dd::x * dd::y == 1) pxy += f;
-              if constexpr (dd::x * dd::y == -1) pxy -= f;
-            });
-            force_shift<C>(d, jx, jy, jz);
-            const C c3 = cs2<C>();
-            mom[e] = T(r);
-            mom[N + e] = T(jx);
-            mom[2 * N + e] = T(jy);
-            mom[3 * N + e] = T(pxx - c3 * r - jx * jx);
-            mom[4 * N + e] = T(pyy - c3 * r - jy * jy);
-            mom[5 * N + e] = T(pxy - jx * jy);
+            for (int c = 0; c < 6; ++c) mom[c * N + e] = v[c];
+          } else {
+            collide(v, pn, e);
           }
         }
         __syncthreads();

@@ -27,7 +27,8 @@ def run(n, faces, tb, steps=400, persist=True):
         dev.close()
 
 
-for n in (128, 256, 384, 512, 768, 1024):
+SIZES = [int(v) for v in os.environ.get("TB2D_SIZES", "128,256,384,512,768,1024").split(",")]
+for n in SIZES:
     for faces in ("periodic", "lid"):
         a, b, c = run(n, faces, True), run(n, faces, False), run(n, faces, False, persist=False)
         print(json.dumps({"n": n, "faces": faces, "tb_glups": round(a, 3), "per_pass_glups": round(b, 3),
