@@ -1812,12 +1812,12 @@ int tslb_cuda_step_async(tslb_cuda_handle h, long nsteps) {
   // small 2-D domains under M: the whole run in persistent cooperative
   // launches (temporal blocking: a grid barrier every four passes) -- per-
   // pass launch overhead is most of their step time; TSLB_PERSIST=0 selects
-  // the graph path instead. Up to ~440^2 nodes: measured r02
-  // (tools/micro/tb2d_sizes.py), 256^2 22.3 / 17.5 GLUPS (periodic / lid)
-  // persistent vs 17.5 / 16.2 from graphs, 384^2 about equal, 512^2 26.8 vs
-  // 37.1 and 1024^2 29.5 vs 52.4 in favour of the graphs
+  // the graph path instead. Up to 512^2 nodes: measured r02
+  // (tools/micro/tb2d_sizes.py), 256^2 29.0 / 24.0 GLUPS (periodic / lid)
+  // persistent vs 17.5 / 16.1 from graphs, 512^2 36.7 / 30.9 vs 36.8 / 28.7,
+  // 640^2 39.3 / 33.1 vs 42.7 / 33.5
   const char* pmx = std::getenv("TSLB_PERSIST_MAX");  // (nodes; measurements)
-  const int64_t kPersistMaxNodes = pmx ? std::atoll(pmx) : int64_t(3) << 16;
+  const int64_t kPersistMaxNodes = pmx ? std::atoll(pmx) : int64_t(1) << 18;
   const char* pe = std::getenv("TSLB_PERSIST");
   const bool persist = !(pe && std::atoi(pe) == 0);
   if (persist && h->sched == TSLB_SCHED_M && h->dim == 2 && h->comps == 1 && h->xmode == 0 && !h->decomposed &&

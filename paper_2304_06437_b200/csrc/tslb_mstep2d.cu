@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(32 * WPB)
 #ifndef TSLB_TBX  // (-DTSLB_TBX/TBY/TBT: measurements)
 #define TSLB_TBX 32
 #define TSLB_TBY 16
-#define TSLB_TBT 512
+#define TSLB_TBT 1024
 #endif
 constexpr int TBX = TSLB_TBX, TBY = TSLB_TBY, TBT = TSLB_TBT;  // tile, threads per block
 template <int K>
