@@ -792,6 +792,31 @@ def tgv_state_host(dims, amp, tdt):
     return st
 
 
+def gpu_local_cpus(dev=0):
+    """The host CPUs of the GPU's NUMA node (sysfs), or None (one node, or
+    no information: the single-socket GPU VMs of this pool). On a
+    multi-socket host the e2e loop allocates its pinned buffers from there:
+    pages land on the allocating CPU's node, and DMA from the other socket's
+    memory would cross the socket link."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(dev)
+        addr = f"{int(pr.pci_domain_id):04x}:{int(pr.pci_bus_id):02x}:{int(pr.pci_device_id):02x}.0"
+        with open(f"/sys/bus/pci/devices/{addr}/numa_node") as fh:
+            node = int(fh.read().strip())
+        if node < 0:
+            return None
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as fh:
+            cpus = set()
+            for part in fh.read().strip().split(","):
+                lo, _, hi = part.partition("-")
+                cpus.update(range(int(lo), int(hi or lo) + 1))
+        cpus &= os.sched_getaffinity(0)
+        return cpus or None
+    except Exception:  # (no NUMA information: leave the affinity alone)
+        return None
+
+
 def run_e2e(sim, lat, dims, steps, dtype, amp):
     """The reference driver loop (tslb_main.cpp run_single) through the public
     C-ABI with HOST buffers: the initial rho and u go up from pinned host
@@ -800,16 +825,30 @@ def run_e2e(sim, lat, dims, steps, dtype, amp):
     tslb_main.cpp:115-122 -- chunked upload overlapped with the
     initialisation), `steps` steps each
     followed by a totals() sample read back to the host, then refresh and
-    download rho and u (the output frame). Host wall time around it."""
+    download rho and u (the output frame). Host wall time around it. The
+    host buffers live on the GPU's NUMA node (gpu_local_cpus)."""
+    import torch
+
+    nn = int(np.prod(dims))
+    esz = np.dtype(dtype).itemsize
+    tdt = torch.float32 if esz == 4 else torch.float64
+    nm = 1 + lat.dim
+    saved = os.sched_getaffinity(0)
+    local = gpu_local_cpus()
+    if local:
+        os.sched_setaffinity(0, local)
+    try:
+        return _run_e2e(sim, lat, dims, steps, dtype, amp, nn, esz, tdt, nm, local)
+    finally:
+        os.sched_setaffinity(0, saved)
+
+
+def _run_e2e(sim, lat, dims, steps, dtype, amp, nn, esz, tdt, nm, local):
     import ctypes as C
 
     import torch
 
     from paper_2304_06437_b200 import _lib
-    nn = int(np.prod(dims))
-    esz = np.dtype(dtype).itemsize
-    tdt = torch.float32 if esz == 4 else torch.float64
-    nm = 1 + lat.dim
     try:
         host_state = tgv_state_host(dims, amp, tdt)
         out = torch.empty((1 + lat.dim, nn), dtype=tdt, pin_memory=True)
@@ -837,6 +876,7 @@ def run_e2e(sim, lat, dims, steps, dtype, amp):
     d2h = (1 + lat.dim) * nn * esz + steps * 32
     return {"value": round(nn * steps / t / 1e9, 4), "unit": "GLUPS", "h2d_bytes_per_step": int(h2d / steps),
             "d2h_bytes_per_step": int(d2h / steps), "seconds": round(t, 3), "phase_seconds": phases,
+            "host_cpus": f"{len(local)} on the GPU's NUMA node" if local else "all",
             "loop": "rho, u (pinned) -> init_equilibrium (device initialize_regularized, Pi^neq = 0, upload "
                     "overlapped) -> "
                     "steps x (step + totals readback) -> refresh, download rho,u"}
